@@ -1,0 +1,179 @@
+// common.cuh — shared plumbing for libslink (status handling, scratch
+// allocation, launch accounting).  sm_100a only.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+
+#include <string>
+
+#include "../../include/slink.h"
+
+namespace slk {
+
+// ---------------------------------------------------------------- errors
+struct Error {
+    int status;
+    std::string msg;
+};
+
+void set_error(int status, const std::string &msg);
+int fail(int status, const char *fmt, ...);
+
+#define SLK_CUDA(expr)                                                                       \
+    do {                                                                                     \
+        cudaError_t _e = (expr);                                                             \
+        if (_e != cudaSuccess)                                                               \
+            throw ::slk::Error{SLK_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e)}; \
+    } while (0)
+
+#define SLK_CHECK_LAUNCH()                                                                   \
+    do {                                                                                     \
+        ::slk::count_launch();                                                               \
+        cudaError_t _e = cudaGetLastError();                                                 \
+        if (_e != cudaSuccess)                                                               \
+            throw ::slk::Error{SLK_ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(_e)}; \
+    } while (0)
+
+[[noreturn]] void throw_invalid(const char *fmt, ...);
+[[noreturn]] void throw_internal(const char *fmt, ...);
+
+void count_launch();
+
+// Run `body`, translating thrown slk::Error into a status code.
+template <class F>
+int guarded(F &&body) {
+    try {
+        body();
+        return SLK_OK;
+    } catch (const Error &e) {
+        set_error(e.status, e.msg);
+        return e.status;
+    } catch (const std::exception &e) {
+        set_error(SLK_ERR_INTERNAL, e.what());
+        return SLK_ERR_INTERNAL;
+    }
+}
+
+// ------------------------------------------------------- device scratch
+// Stream-ordered scratch buffer (cudaMallocAsync pool); freed on destruction.
+template <class T>
+struct DevBuf {
+    T *ptr = nullptr;
+    size_t count = 0;
+    cudaStream_t stream = nullptr;
+    DevBuf() = default;
+    DevBuf(size_t n, cudaStream_t s) { alloc(n, s); }
+    void alloc(size_t n, cudaStream_t s) {
+        release();
+        stream = s;
+        count = n;
+        if (n) SLK_CUDA(cudaMallocAsync((void **)&ptr, n * sizeof(T), s));
+    }
+    void release() {
+        if (ptr) cudaFreeAsync(ptr, stream);
+        ptr = nullptr;
+        count = 0;
+    }
+    ~DevBuf() { release(); }
+    DevBuf(const DevBuf &) = delete;
+    DevBuf &operator=(const DevBuf &) = delete;
+    DevBuf(DevBuf &&o) noexcept : ptr(o.ptr), count(o.count), stream(o.stream) {
+        o.ptr = nullptr;
+        o.count = 0;
+    }
+    DevBuf &operator=(DevBuf &&o) noexcept {
+        release();
+        ptr = o.ptr;
+        count = o.count;
+        stream = o.stream;
+        o.ptr = nullptr;
+        o.count = 0;
+        return *this;
+    }
+    T *get() const { return ptr; }
+    operator T *() const { return ptr; }
+};
+
+inline int grid_for(int64_t n, int block, int64_t cap = 148 * 32) {
+    int64_t g = (n + block - 1) / block;
+    if (g < 1) g = 1;
+    if (g > cap) g = cap;
+    return (int)g;
+}
+
+template <class T>
+T read_scalar(const T *d_ptr, cudaStream_t s) {
+    T v;
+    SLK_CUDA(cudaMemcpyAsync(&v, d_ptr, sizeof(T), cudaMemcpyDeviceToHost, s));
+    SLK_CUDA(cudaStreamSynchronize(s));
+    return v;
+}
+
+// Number of SMs of the current device (cached).
+int num_sms();
+
+// ------------------------------------------------- cross-module entry points
+// Scan statistics of the last neighbour search on this thread.
+struct ScanStats {
+    int64_t rows_refined = 0, rows_rescanned = 0, tiles_computed = 0, tiles_skipped = 0;
+};
+ScanStats &scan_stats();
+
+// knn.cu
+void knn_rows(const float *x32, const double *x64, int64_t n, int d, int k, int64_t q0,
+              int64_t q1, int32_t *idx, double *dist, cudaStream_t s);
+void nn1_rows(const float *q32, const double *q64, int64_t nq, const float *x32,
+              const double *x64, int64_t nx, int d, int mode, const uint8_t *mask,
+              const int32_t *qcolor, const int32_t *xcolor, int64_t q0, int64_t q1, int32_t *idx,
+              double *dist, cudaStream_t s);
+void row_norms(const float *x32, const double *x64, int64_t n, int d, double *out, cudaStream_t s);
+void pairwise_l2(const double *q, int64_t nq, const double *x, int64_t nx, int d, int squared,
+                 double *out, cudaStream_t s);
+
+// graph.cu
+// Undirected, deduplicated (min weight) edge list sorted by (a, b), a < b.
+struct EdgeSet {
+    DevBuf<int32_t> a, b;
+    DevBuf<double> w;
+    int64_t m = 0;
+};
+EdgeSet dedup_undirected(int64_t n, const int32_t *src, const int32_t *dst, const double *w,
+                         int64_t m, cudaStream_t s);
+// Spanning forest of an undirected edge set (alteration + Boruvka).  Outputs
+// as slk_solve_mst.  When `negate` the weights are negated for ordering and
+// restored on output.
+// `presorted`: the input is already sorted by (a, b) (dedup_undirected output).
+void msf_undirected(int64_t n, const int32_t *a, const int32_t *b, const double *w, int64_t m,
+                    bool presorted, bool negate, int64_t seed, int32_t *out_src,
+                    int32_t *out_dst, double *out_w, int32_t *colors, int64_t *n_edges,
+                    int64_t *n_components, cudaStream_t s);
+// CSR-level API helpers (graph.cu)
+void csr_from_edges(int64_t n, const int32_t *src, const int32_t *dst, const double *w, int64_t m,
+                    int64_t *offs, int32_t *cols, double *cw, int64_t *nnz, cudaStream_t s);
+bool csr_symmetric(int64_t n, const int64_t *offs, const int32_t *cols, const double *w,
+                   cudaStream_t s);
+double csr_weight_alteration(int64_t n, const int64_t *offs, const int32_t *cols, const double *w,
+                             int64_t seed, double *alt, cudaStream_t s);
+void csr_min_edge_per_vertex(int64_t n, const int64_t *offs, const int32_t *cols,
+                             const double *alt, const int32_t *colors, int64_t *pos,
+                             cudaStream_t s);
+int64_t reconcile_supervertex(int64_t n, const int64_t *pos, const int32_t *dst,
+                              const double *alt, const double *orig, const int32_t *colors,
+                              int32_t *out_a, int32_t *out_b, double *out_w, cudaStream_t s);
+void label_propagation(int64_t n, int32_t *colors, const int32_t *us, const int32_t *vs, int64_t m,
+                       cudaStream_t s);
+void csr_solve_mst(int64_t n, const int64_t *offs, const int32_t *cols, const double *w,
+                   bool maximize, int64_t seed, int32_t *out_src, int32_t *out_dst, double *out_w,
+                   int32_t *colors, int64_t *n_edges, int64_t *n_components, cudaStream_t s);
+
+// dendro.cu
+void dendrogram_device_sort(const int32_t *src, const int32_t *dst, const double *w, int64_t n,
+                            bool take_sqrt, int32_t *h_a, int32_t *h_b, double *h_w,
+                            cudaStream_t s);
+void dendrogram_fold(const int32_t *a, const int32_t *b, const double *w, int64_t n,
+                     double *merges);
+void extract_labels(const double *merges, int64_t n, int64_t n_clusters, int64_t *labels);
+
+}  // namespace slk

@@ -1,0 +1,753 @@
+// graph.cu — k-NN graph symmetrisation and the Boruvka spanning forest.
+//
+// Replaces edge_list_to_csr (/root/reference/pkg/src/parlink/core.py:264-286)
+// and the solver in mst.py (weight_alteration :198-222, _hash_unit :82-91,
+// _alter_weights :94-105, _min_edge_scan :108-128, _reconcile_per_color
+// :131-151, _propagate_colors :154-186, solve_mst :292-344).
+//
+// Design: the solver's strict total order on undirected edges
+// is (w_alt, a, b) with a < b.  We compute w_alt bit-exactly, then ONE stable
+// device radix sort by w_alt over the (a, b)-sorted edge list gives every
+// edge a 32-bit rank in that order.  Boruvka then runs on ranks: per round
+// an edge-centric kernel does atomicMin(rank) into both endpoint colours
+// (deterministic — ranks are unique), roots hook along their minimum edge,
+// 2-cycles are broken toward the smaller id, pointers are jumped in place and
+// the edge list is compacted to the edges that still cross colours.  The
+// minimum spanning forest under a strict total order is unique, so the
+// accepted edge set equals the reference's exactly.
+#include <cub/cub.cuh>
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "common.cuh"
+
+namespace slk {
+
+namespace {
+
+constexpr uint32_t NONE32 = 0xffffffffu;
+
+// ---------------------------------------------------------- sort helpers
+template <class K, class V>
+void sort_pairs(const K *kin, K *kout, const V *vin, V *vout, int64_t m, cudaStream_t s,
+                int begin_bit = 0, int end_bit = sizeof(K) * 8) {
+    if (m <= 0) return;
+    size_t tmp = 0;
+    SLK_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, kin, kout, vin, vout, (int)m, begin_bit,
+                                             end_bit, s));
+    DevBuf<unsigned char> t(tmp, s);
+    SLK_CUDA(cub::DeviceRadixSort::SortPairs(t.get(), tmp, kin, kout, vin, vout, (int)m, begin_bit,
+                                             end_bit, s));
+}
+
+template <class K>
+void sort_keys(const K *kin, K *kout, int64_t m, cudaStream_t s) {
+    if (m <= 0) return;
+    size_t tmp = 0;
+    SLK_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tmp, kin, kout, (int)m, 0, sizeof(K) * 8, s));
+    DevBuf<unsigned char> t(tmp, s);
+    SLK_CUDA(cub::DeviceRadixSort::SortKeys(t.get(), tmp, kin, kout, (int)m, 0, sizeof(K) * 8, s));
+}
+
+template <class T>
+void exclusive_sum(const T *in, T *out, int64_t m, cudaStream_t s) {
+    if (m <= 0) return;
+    size_t tmp = 0;
+    SLK_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, in, out, (int)m, s));
+    DevBuf<unsigned char> t(tmp, s);
+    SLK_CUDA(cub::DeviceScan::ExclusiveSum(t.get(), tmp, in, out, (int)m, s));
+}
+
+int bits_for(int64_t n) {
+    int b = 1;
+    while ((1ll << b) < n) b++;
+    return b;
+}
+
+// ------------------------------------------------------------- kernels
+#define GRID_LOOP(i, n) \
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (n); i += (int64_t)gridDim.x * blockDim.x)
+
+__global__ void canon_keys_kernel(const int32_t *src, const int32_t *dst, int64_t m,
+                                  uint64_t *keys) {
+    GRID_LOOP(e, m) {
+        uint32_t s = (uint32_t)src[e], d = (uint32_t)dst[e];
+        uint32_t a = s < d ? s : d, b = s < d ? d : s;
+        keys[e] = ((uint64_t)a << 32) | b;
+    }
+}
+
+__global__ void directed_keys_kernel(const int32_t *src, const int32_t *dst, const double *w,
+                                     int64_t m, uint64_t *keys, double *ws) {
+    GRID_LOOP(e, m) {
+        uint32_t s = (uint32_t)src[e], d = (uint32_t)dst[e];
+        keys[e] = ((uint64_t)s << 32) | d;
+        keys[m + e] = ((uint64_t)d << 32) | s;
+        ws[e] = w[e];
+        ws[m + e] = w[e];
+    }
+}
+
+// run heads of a sorted key array; run minimum of the weights
+__global__ void run_heads_kernel(const uint64_t *keys, int64_t m, int32_t *flag) {
+    GRID_LOOP(e, m) flag[e] = (e == 0 || keys[e] != keys[e - 1]) ? 1 : 0;
+}
+
+__global__ void run_min_scatter_kernel(const uint64_t *keys, const double *w, const int32_t *flag,
+                                       const int32_t *pos, int64_t m, int32_t *out_a,
+                                       int32_t *out_b, double *out_w) {
+    GRID_LOOP(e, m) {
+        if (!flag[e]) continue;
+        double best = w[e];
+        for (int64_t f = e + 1; f < m && keys[f] == keys[e]; f++) best = fmin(best, w[f]);
+        int32_t p = pos[e];
+        out_a[p] = (int32_t)(keys[e] >> 32);
+        out_b[p] = (int32_t)(keys[e] & 0xffffffffu);
+        out_w[p] = best;
+    }
+}
+
+__global__ void lower_bound_offsets_kernel(const int32_t *rows, int64_t nnz, int64_t n,
+                                           int64_t *offs) {
+    GRID_LOOP(v, n + 1) {
+        int64_t lo = 0, hi = nnz;
+        while (lo < hi) {
+            int64_t mid = (lo + hi) >> 1;
+            if ((int64_t)rows[mid] < v) lo = mid + 1;
+            else hi = mid;
+        }
+        offs[v] = lo;
+    }
+}
+
+__global__ void row_sources_kernel(const int64_t *offs, int64_t n, int32_t *src) {
+    GRID_LOOP(v, n) {
+        for (int64_t p = offs[v]; p < offs[v + 1]; p++) src[p] = (int32_t)v;
+    }
+}
+
+__global__ void check_weights_kernel(const double *w, int64_t m, int *flags) {
+    GRID_LOOP(e, m) {
+        double x = w[e];
+        if (!isfinite(x)) atomicOr(flags, 1);
+        if (x == 0.0) atomicOr(flags, 2);
+    }
+}
+
+__global__ void negate_kernel(const double *w, int64_t m, double *out, bool neg) {
+    GRID_LOOP(e, m) out[e] = neg ? -w[e] : w[e];
+}
+
+// min positive gap between adjacent distinct sorted weights (mst.py:215-217)
+__global__ void min_gap_kernel(const double *s, int64_t m, unsigned long long *gap_bits) {
+    double g = INFINITY;
+    GRID_LOOP(e, m) {
+        if (e > 0 && s[e] != s[e - 1]) g = fmin(g, __dsub_rn(s[e], s[e - 1]));
+    }
+    for (int o = 16; o; o >>= 1) g = fmin(g, __shfl_xor_sync(0xffffffffu, g, o));
+    if ((threadIdx.x & 31) == 0 && g < INFINITY)
+        atomicMin(gap_bits, (unsigned long long)__double_as_longlong(g));  // g > 0: bit order
+}
+
+// ref mst.py:82-91
+__device__ __forceinline__ double hash_unit(uint32_t a, uint32_t b, int64_t seed) {
+    uint64_t z = (uint64_t)a * 0x9E3779B97F4A7C15ULL;
+    z ^= (uint64_t)b + 0xBF58476D1CE4E5B9ULL;
+    z ^= (uint64_t)seed * 0x94D049BB133111EBULL;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    z = z ^ (z >> 31);
+    return __dmul_rn((double)(z >> 11), 0x1p-53);
+}
+
+// ref mst.py:94-105: out = w + hash(a, b, seed) * eps_max (product, then sum)
+__global__ void alter_kernel(const int32_t *a, const int32_t *b, const double *w, int64_t m,
+                             int64_t seed, double eps_max, double *alt) {
+    GRID_LOOP(e, m) {
+        uint32_t s = (uint32_t)a[e], d = (uint32_t)b[e];
+        uint32_t lo = s < d ? s : d, hi = s < d ? d : s;
+        alt[e] = __dadd_rn(w[e], __dmul_rn(hash_unit(lo, hi, seed), eps_max));
+    }
+}
+
+__global__ void iota_kernel(int32_t *v, int64_t m) {
+    GRID_LOOP(e, m) v[e] = (int32_t)e;
+}
+
+template <class T>
+__global__ void gather_kernel(const T *in, const int32_t *perm, int64_t m, T *out) {
+    GRID_LOOP(e, m) out[e] = in[perm[e]];
+}
+
+// --- Boruvka on ranks
+__global__ void fill_u32_kernel(uint32_t *v, int64_t n, uint32_t x) {
+    GRID_LOOP(i, n) v[i] = x;
+}
+
+__global__ void min_edge_kernel(const int32_t *ea, const int32_t *eb, const uint32_t *erank,
+                                int64_t m, const int32_t *color, uint32_t *best) {
+    GRID_LOOP(e, m) {
+        int32_t ca = color[ea[e]], cb = color[eb[e]];
+        if (ca == cb) continue;
+        uint32_t r = erank[e];
+        if (best[ca] > r) atomicMin(&best[ca], r);
+        if (best[cb] > r) atomicMin(&best[cb], r);
+    }
+}
+
+__global__ void hook_kernel(int64_t n, const int32_t *color, const uint32_t *best,
+                            const int32_t *ra, const int32_t *rb, int32_t *parent,
+                            uint8_t *accepted, int *any) {
+    GRID_LOOP(v, n) {
+        if (color[v] != v) continue;
+        uint32_t e = best[v];
+        if (e == NONE32) {
+            parent[v] = (int32_t)v;
+            continue;
+        }
+        accepted[e] = 1;
+        int32_t ca = color[ra[e]], cb = color[rb[e]];
+        parent[v] = ca == v ? cb : ca;
+        *any = 1;
+    }
+}
+
+__global__ void break_cycles_kernel(int64_t n, const int32_t *color, int32_t *parent) {
+    GRID_LOOP(v, n) {
+        if (color[v] != v) continue;
+        int32_t p = parent[v];
+        if (p != v && p > v && parent[p] == v) parent[v] = (int32_t)v;
+    }
+}
+
+__global__ void jump_kernel(int64_t n, const int32_t *color, int32_t *parent) {
+    GRID_LOOP(v, n) {
+        if (color[v] != v) continue;
+        int32_t p = parent[v];
+        while (true) {
+            int32_t pp = parent[p];
+            if (pp == p) break;
+            p = pp;
+        }
+        parent[v] = p;
+    }
+}
+
+__global__ void relabel_kernel(int64_t n, int32_t *color, const int32_t *parent) {
+    GRID_LOOP(v, n) color[v] = parent[color[v]];
+}
+
+__global__ void cross_flag_kernel(const int32_t *ea, const int32_t *eb, int64_t m,
+                                  const int32_t *color, int32_t *flag) {
+    GRID_LOOP(e, m) flag[e] = color[ea[e]] != color[eb[e]] ? 1 : 0;
+}
+
+template <class T>
+__global__ void compact_kernel(const T *in, const int32_t *flag, const int32_t *pos, int64_t m,
+                               T *out) {
+    GRID_LOOP(e, m) if (flag[e]) out[pos[e]] = in[e];
+}
+
+__global__ void accepted_keys_kernel(const uint8_t *accepted, const int32_t *pos, int64_t m,
+                                     const int32_t *ra, const int32_t *rb, const double *rw,
+                                     uint64_t *keys, double *ws) {
+    GRID_LOOP(e, m) {
+        if (!accepted[e]) continue;
+        int32_t p = pos[e];
+        keys[p] = ((uint64_t)(uint32_t)ra[e] << 32) | (uint32_t)rb[e];
+        ws[p] = rw[e];
+    }
+}
+
+__global__ void u8_to_i32_kernel(const uint8_t *in, int64_t m, int32_t *out) {
+    GRID_LOOP(e, m) out[e] = in[e];
+}
+
+__global__ void split_keys_kernel(const uint64_t *keys, int64_t m, int32_t *a, int32_t *b) {
+    GRID_LOOP(e, m) {
+        a[e] = (int32_t)(keys[e] >> 32);
+        b[e] = (int32_t)(keys[e] & 0xffffffffu);
+    }
+}
+
+__global__ void min_member_kernel(int64_t n, const int32_t *color, int32_t *minv, int *roots) {
+    GRID_LOOP(v, n) {
+        atomicMin(&minv[color[v]], (int32_t)v);
+        if (color[v] == v) atomicAdd(roots, 1);
+    }
+}
+
+__global__ void canon_color_kernel(int64_t n, const int32_t *color, const int32_t *minv,
+                                   int32_t *out) {
+    GRID_LOOP(v, n) out[v] = minv[color[v]];
+}
+
+__global__ void fill_i32_kernel(int32_t *v, int64_t n, int32_t x) {
+    GRID_LOOP(i, n) v[i] = x;
+}
+
+// --- CSR-level API kernels (mst.py step functions)
+__device__ __forceinline__ bool key_lt(double w, int64_t a, int64_t b, double qw, int64_t qa,
+                                       int64_t qb) {
+    return w < qw || (w == qw && (a < qa || (a == qa && b < qb)));
+}
+
+// ref mst.py:108-128
+__global__ void min_edge_scan_kernel(int64_t n, const int64_t *offs, const int32_t *cols,
+                                     const double *alt, const int32_t *colors, int64_t *pos) {
+    GRID_LOOP(v, n) {
+        int32_t cv = colors[v];
+        int64_t best = -1, ba = -1, bb = -1;
+        double bw = INFINITY;
+        for (int64_t p = offs[v]; p < offs[v + 1]; p++) {
+            int64_t u = cols[p];
+            if (colors[u] == cv) continue;
+            double w = alt[p];
+            int64_t a = v < u ? v : u, b = v < u ? u : v;
+            if (key_lt(w, a, b, bw, ba, bb)) {
+                best = p;
+                bw = w;
+                ba = a;
+                bb = b;
+            }
+        }
+        pos[v] = best;
+    }
+}
+
+__device__ __forceinline__ unsigned long long ordered_bits(double x) {
+    if (x == 0.0) x = 0.0;  // -0.0 compares equal to +0.0 in the reference
+    unsigned long long b = (unsigned long long)__double_as_longlong(x);
+    return (b & 0x8000000000000000ull) ? ~b : (b | 0x8000000000000000ull);
+}
+
+__global__ void reconcile_phase1(int64_t n, const int64_t *pos, const double *alt,
+                                 const int32_t *colors, unsigned long long *best1) {
+    GRID_LOOP(v, n) {
+        if (pos[v] < 0) continue;
+        atomicMin(&best1[colors[v]], ordered_bits(alt[v]));
+    }
+}
+
+__global__ void reconcile_phase2(int64_t n, const int64_t *pos, const int32_t *dst,
+                                 const double *alt, const int32_t *colors,
+                                 const unsigned long long *best1, unsigned long long *best2) {
+    GRID_LOOP(v, n) {
+        if (pos[v] < 0) continue;
+        int32_t c = colors[v];
+        if (ordered_bits(alt[v]) != best1[c]) continue;
+        uint32_t u = (uint32_t)dst[v], vv = (uint32_t)v;
+        uint64_t key = ((uint64_t)(vv < u ? vv : u) << 32) | (vv < u ? u : vv);
+        atomicMin(&best2[c], (unsigned long long)key);
+    }
+}
+
+__global__ void reconcile_phase3(int64_t n, const int64_t *pos, const int32_t *dst,
+                                 const double *alt, const double *orig, const int32_t *colors,
+                                 const unsigned long long *best1, const unsigned long long *best2,
+                                 int32_t *winner) {
+    GRID_LOOP(v, n) {
+        if (pos[v] < 0) continue;
+        int32_t c = colors[v];
+        if (ordered_bits(alt[v]) != best1[c]) continue;
+        uint32_t u = (uint32_t)dst[v], vv = (uint32_t)v;
+        uint64_t key = ((uint64_t)(vv < u ? vv : u) << 32) | (vv < u ? u : vv);
+        if (key == best2[c]) atomicMin(&winner[c], (int32_t)v);
+    }
+}
+
+__global__ void winner_edges_kernel(int64_t n, const int32_t *winner, const int32_t *dst,
+                                    const double *orig, int32_t *flag, uint64_t *keys,
+                                    double *ws) {
+    GRID_LOOP(c, n) {
+        int32_t v = winner[c];
+        flag[c] = v != 0x7fffffff;
+        if (v == 0x7fffffff) continue;
+        uint32_t u = (uint32_t)dst[v], vv = (uint32_t)v;
+        keys[c] = ((uint64_t)(vv < u ? vv : u) << 32) | (vv < u ? u : vv);
+        ws[c] = orig[v];
+    }
+}
+
+// --- label propagation (ref mst.py:154-186)
+__global__ void prop_init_kernel(int64_t n, int32_t *next) {
+    GRID_LOOP(c, n) next[c] = (int32_t)c;
+}
+__global__ void prop_edges_kernel(const int32_t *colors, const int32_t *us, const int32_t *vs,
+                                  int64_t m, int32_t *next) {
+    GRID_LOOP(e, m) {
+        int32_t a = colors[us[e]], b = colors[vs[e]];
+        if (a == b) continue;
+        int32_t mn = a < b ? a : b;
+        atomicMin(&next[a], mn);
+        atomicMin(&next[b], mn);
+    }
+}
+__global__ void prop_jump_kernel(int64_t n, int32_t *next) {
+    GRID_LOOP(c, n) {
+        int32_t p = next[c];
+        while (true) {
+            int32_t pp = next[p];
+            if (pp >= p) break;
+            p = pp;
+        }
+        atomicMin(&next[c], p);
+    }
+}
+__global__ void prop_apply_kernel(int64_t n, int32_t *colors, const int32_t *next, int *changed) {
+    GRID_LOOP(v, n) {
+        int32_t nc = next[colors[v]];
+        if (nc < colors[v]) {
+            colors[v] = nc;
+            *changed = 1;
+        }
+    }
+}
+
+// --- symmetric check
+__global__ void sym_keys_kernel(const int32_t *src, const int32_t *cols, const double *w,
+                                int64_t m, uint64_t *kf, uint64_t *kr, unsigned long long *wb) {
+    GRID_LOOP(e, m) {
+        uint32_t s = (uint32_t)src[e], d = (uint32_t)cols[e];
+        kf[e] = ((uint64_t)s << 32) | d;
+        kr[e] = ((uint64_t)d << 32) | s;
+        wb[e] = ordered_bits(w[e]);
+    }
+}
+__global__ void compare_kernel(const uint64_t *a, const uint64_t *b, const unsigned long long *wa,
+                               const unsigned long long *wb, int64_t m, int *diff) {
+    GRID_LOOP(e, m) if (a[e] != b[e] || wa[e] != wb[e]) *diff = 1;
+}
+
+__global__ void lt_flag_kernel(const int32_t *src, const int32_t *cols, int64_t m, int32_t *flag) {
+    GRID_LOOP(e, m) flag[e] = src[e] < cols[e] ? 1 : 0;
+}
+
+#undef GRID_LOOP
+
+#define LAUNCH(kernel, n, ...)                                        \
+    do {                                                              \
+        kernel<<<grid_for((n), 256), 256, 0, s>>>(__VA_ARGS__);       \
+        SLK_CHECK_LAUNCH();                                           \
+    } while (0)
+
+// Sort entries by (key, weight) and keep the minimum weight per key.
+// Returns the number of unique keys written to (out_a, out_b, out_w).
+int64_t unique_min(const uint64_t *keys_in, const double *w_in, int64_t m, int key_bits,
+                   int32_t *out_a, int32_t *out_b, double *out_w, cudaStream_t s) {
+    if (m == 0) return 0;
+    DevBuf<uint64_t> ks(m, s);
+    DevBuf<double> ws(m, s);
+    sort_pairs(keys_in, ks.get(), w_in, ws.get(), m, s, 0, key_bits);
+    DevBuf<int32_t> flag(m, s), pos(m, s);
+    LAUNCH(run_heads_kernel, m, ks.get(), m, flag.get());
+    exclusive_sum(flag.get(), pos.get(), m, s);
+    int32_t last_pos = read_scalar(pos.get() + m - 1, s), last_flag = read_scalar(flag.get() + m - 1, s);
+    int64_t u = (int64_t)last_pos + last_flag;
+    LAUNCH(run_min_scatter_kernel, m, ks.get(), ws.get(), flag.get(), pos.get(), m, out_a, out_b, out_w);
+    return u;
+}
+
+}  // namespace
+
+#define LAUNCH(kernel, n, ...)                                        \
+    do {                                                              \
+        kernel<<<grid_for((n), 256), 256, 0, s>>>(__VA_ARGS__);       \
+        SLK_CHECK_LAUNCH();                                           \
+    } while (0)
+
+EdgeSet dedup_undirected(int64_t n, const int32_t *src, const int32_t *dst, const double *w,
+                         int64_t m, cudaStream_t s) {
+    EdgeSet E;
+    if (m == 0) return E;
+    DevBuf<uint64_t> keys(m, s);
+    LAUNCH(canon_keys_kernel, m, src, dst, m, keys.get());
+    E.a.alloc(m, s);
+    E.b.alloc(m, s);
+    E.w.alloc(m, s);
+    E.m = unique_min(keys.get(), w, m, 32 + bits_for(n), E.a.get(), E.b.get(), E.w.get(), s);
+    return E;
+}
+
+// theta (mst.py:215-219) of the given weights; m > 0.
+static double compute_theta(const double *w, int64_t m, cudaStream_t s) {
+    DevBuf<double> sorted(m, s);
+    sort_keys(w, sorted.get(), m, s);
+    DevBuf<unsigned long long> gap(1, s);
+    unsigned long long init = (unsigned long long)0x7ff0000000000000ull;  // +inf bits
+    SLK_CUDA(cudaMemcpyAsync(gap.get(), &init, sizeof(init), cudaMemcpyHostToDevice, s));
+    min_gap_kernel<<<grid_for(m, 256, 2048), 256, 0, s>>>(sorted.get(), m, gap.get());
+    SLK_CHECK_LAUNCH();
+    unsigned long long g = read_scalar(gap.get(), s);
+    if (g != init) {
+        double theta;
+        memcpy(&theta, &g, sizeof theta);
+        return theta;
+    }
+    double first = read_scalar(sorted.get(), s);
+    double a = fabs(first);
+    return (a > 1.0 ? a : 1.0) * 0x1p-20;  // single distinct weight (mst.py:219)
+}
+
+static void validate_weights(const double *w, int64_t m, bool check_zero, cudaStream_t s) {
+    if (m == 0) return;
+    DevBuf<int> flags(1, s);
+    SLK_CUDA(cudaMemsetAsync(flags.get(), 0, sizeof(int), s));
+    LAUNCH(check_weights_kernel, m, w, m, flags.get());
+    int f = read_scalar(flags.get(), s);
+    if (f & 1) throw_invalid("graph contains non-finite edge weights");
+    if (check_zero && (f & 2)) throw_invalid("zero-weight edges are not supported");
+}
+
+void msf_undirected(int64_t n, const int32_t *a_in, const int32_t *b_in, const double *w_in,
+                    int64_t m, bool presorted, bool negate, int64_t seed, int32_t *out_src,
+                    int32_t *out_dst, double *out_w, int32_t *colors_out, int64_t *n_edges,
+                    int64_t *n_components, cudaStream_t s) {
+    if (n <= 0) throw_invalid("empty graph: no vertices");
+    validate_weights(w_in, m, true, s);
+    const int32_t *a = a_in, *b = b_in;
+    const double *w = w_in;
+    DevBuf<int32_t> sa, sb;
+    DevBuf<double> sw;
+    if (!presorted && m > 0) {
+        // the (w_alt, a, b) tie-break needs the list in (a, b) order first
+        DevBuf<uint64_t> keys(m, s), ks(m, s);
+        DevBuf<int32_t> iota(m, s), perm(m, s);
+        LAUNCH(canon_keys_kernel, m, a_in, b_in, m, keys.get());
+        LAUNCH(iota_kernel, m, iota.get(), m);
+        sort_pairs(keys.get(), ks.get(), iota.get(), perm.get(), m, s, 0, 32 + bits_for(n));
+        sa.alloc(m, s);
+        sb.alloc(m, s);
+        sw.alloc(m, s);
+        LAUNCH(split_keys_kernel, m, ks.get(), m, sa.get(), sb.get());
+        LAUNCH(gather_kernel<double>, m, w_in, perm.get(), m, sw.get());
+        a = sa.get();
+        b = sb.get();
+        w = sw.get();
+    }
+    DevBuf<int32_t> color(n, s);
+    LAUNCH(iota_kernel, n, color.get(), n);
+    int64_t accepted_count = 0;
+    if (m > 0) {
+        // --- order: w_alt (mst.py:198-222), ties by (a, b) via a stable sort
+        DevBuf<double> ww(m, s), alt(m, s);
+        LAUNCH(negate_kernel, m, w, m, ww.get(), negate);
+        double theta = compute_theta(ww.get(), m, s);
+        double eps_max = theta * (1.0 - 0x1p-20);
+        LAUNCH(alter_kernel, m, a, b, ww.get(), m, seed, eps_max, alt.get());
+        DevBuf<int32_t> iota(m, s), perm(m, s);
+        DevBuf<double> alt_sorted(m, s);
+        LAUNCH(iota_kernel, m, iota.get(), m);
+        // (a, b) order of the input is required for the tie-break: callers pass
+        // edge lists sorted by (a, b) (dedup_undirected / CSR order).
+        sort_pairs(alt.get(), alt_sorted.get(), iota.get(), perm.get(), m, s);
+        DevBuf<int32_t> ra(m, s), rb(m, s);
+        DevBuf<double> rw(m, s);
+        LAUNCH(gather_kernel<int32_t>, m, a, perm.get(), m, ra.get());
+        LAUNCH(gather_kernel<int32_t>, m, b, perm.get(), m, rb.get());
+        LAUNCH(gather_kernel<double>, m, w, perm.get(), m, rw.get());
+        alt.release();
+        alt_sorted.release();
+        ww.release();
+
+        // --- Boruvka rounds on ranks
+        DevBuf<int32_t> ea(m, s), eb(m, s), ea2(m, s), eb2(m, s), flag(m, s), pos(m, s);
+        DevBuf<uint32_t> er(m, s), er2(m, s), best(n, s);
+        DevBuf<int32_t> parent(n, s);
+        DevBuf<uint8_t> accepted(m, s);
+        DevBuf<int> any(1, s);
+        SLK_CUDA(cudaMemcpyAsync(ea.get(), ra.get(), m * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+        SLK_CUDA(cudaMemcpyAsync(eb.get(), rb.get(), m * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+        LAUNCH(iota_kernel, m, (int32_t *)er.get(), m);
+        SLK_CUDA(cudaMemsetAsync(accepted.get(), 0, m, s));
+        int64_t active = m;
+        for (int round = 0; round < 64 && active > 0; round++) {
+            LAUNCH(fill_u32_kernel, n, best.get(), n, NONE32);
+            LAUNCH(min_edge_kernel, active, ea.get(), eb.get(), er.get(), active, color.get(), best.get());
+            SLK_CUDA(cudaMemsetAsync(any.get(), 0, sizeof(int), s));
+            LAUNCH(hook_kernel, n, n, color.get(), best.get(), ra.get(), rb.get(), parent.get(),
+                   accepted.get(), any.get());
+            if (!read_scalar(any.get(), s)) break;
+            LAUNCH(break_cycles_kernel, n, n, color.get(), parent.get());
+            LAUNCH(jump_kernel, n, n, color.get(), parent.get());
+            LAUNCH(relabel_kernel, n, n, color.get(), parent.get());
+            // keep only edges that still cross colours
+            LAUNCH(cross_flag_kernel, active, ea.get(), eb.get(), active, color.get(), flag.get());
+            exclusive_sum(flag.get(), pos.get(), active, s);
+            int64_t next = (int64_t)read_scalar(pos.get() + active - 1, s) +
+                           read_scalar(flag.get() + active - 1, s);
+            LAUNCH(compact_kernel<int32_t>, active, ea.get(), flag.get(), pos.get(), active, ea2.get());
+            LAUNCH(compact_kernel<int32_t>, active, eb.get(), flag.get(), pos.get(), active, eb2.get());
+            LAUNCH(compact_kernel<uint32_t>, active, er.get(), flag.get(), pos.get(), active, er2.get());
+            std::swap(ea, ea2);
+            std::swap(eb, eb2);
+            std::swap(er, er2);
+            active = next;
+        }
+        // --- accepted edges, sorted by (a, b) with original weights
+        LAUNCH(u8_to_i32_kernel, m, accepted.get(), m, flag.get());
+        exclusive_sum(flag.get(), pos.get(), m, s);
+        accepted_count = (int64_t)read_scalar(pos.get() + m - 1, s) + read_scalar(flag.get() + m - 1, s);
+        if (accepted_count > n - 1) throw_internal("accepted %lld edges for %lld vertices",
+                                                   (long long)accepted_count, (long long)n);
+        DevBuf<uint64_t> keys(accepted_count, s), keys_sorted(accepted_count, s);
+        DevBuf<double> ws(accepted_count, s);
+        LAUNCH(accepted_keys_kernel, m, accepted.get(), pos.get(), m, ra.get(), rb.get(), rw.get(),
+               keys.get(), ws.get());
+        sort_pairs(keys.get(), keys_sorted.get(), ws.get(), out_w, accepted_count, s, 0,
+                   32 + bits_for(n));
+        LAUNCH(split_keys_kernel, accepted_count, keys_sorted.get(), accepted_count, out_src, out_dst);
+    }
+    // --- canonical colours: minimum vertex id per component
+    DevBuf<int32_t> minv(n, s);
+    DevBuf<int> roots(1, s);
+    LAUNCH(fill_i32_kernel, n, minv.get(), n, 0x7fffffff);
+    SLK_CUDA(cudaMemsetAsync(roots.get(), 0, sizeof(int), s));
+    LAUNCH(min_member_kernel, n, n, color.get(), minv.get(), roots.get());
+    LAUNCH(canon_color_kernel, n, n, color.get(), minv.get(), colors_out);
+    int64_t ncomp = read_scalar(roots.get(), s);
+    if (accepted_count != n - ncomp)
+        throw_internal("internal: accepted %lld edges for %lld vertices and %lld components",
+                       (long long)accepted_count, (long long)n, (long long)ncomp);
+    *n_edges = accepted_count;
+    *n_components = ncomp;
+}
+
+// ------------------------------------------------------- C-ABI helpers
+void csr_from_edges(int64_t n, const int32_t *src, const int32_t *dst, const double *w, int64_t m,
+                    int64_t *offs, int32_t *cols, double *cw, int64_t *nnz, cudaStream_t s) {
+    if (m == 0) {
+        SLK_CUDA(cudaMemsetAsync(offs, 0, (n + 1) * sizeof(int64_t), s));
+        *nnz = 0;
+        return;
+    }
+    DevBuf<uint64_t> keys(2 * m, s);
+    DevBuf<double> ws(2 * m, s);
+    LAUNCH(directed_keys_kernel, m, src, dst, w, m, keys.get(), ws.get());
+    DevBuf<int32_t> rows(2 * m, s);
+    int64_t u = unique_min(keys.get(), ws.get(), 2 * m, 32 + bits_for(n), rows.get(), cols, cw, s);
+    LAUNCH(lower_bound_offsets_kernel, n + 1, rows.get(), u, n, offs);
+    *nnz = u;
+}
+
+void csr_row_sources(int64_t n, const int64_t *offs, int32_t *src, cudaStream_t s) {
+    LAUNCH(row_sources_kernel, n, offs, n, src);
+}
+
+bool csr_symmetric(int64_t n, const int64_t *offs, const int32_t *cols, const double *w,
+                   cudaStream_t s) {
+    int64_t m = read_scalar(offs + n, s);
+    if (m == 0) return true;
+    DevBuf<int32_t> src(m, s);
+    csr_row_sources(n, offs, src.get(), s);
+    DevBuf<uint64_t> kf(m, s), kr(m, s), k1(m, s), k2(m, s);
+    DevBuf<unsigned long long> wb(m, s), w1(m, s), w2(m, s), wf(m, s), wr(m, s);
+    LAUNCH(sym_keys_kernel, m, src.get(), cols, w, m, kf.get(), kr.get(), wb.get());
+    // lexicographic (key, w): sort by w, then stable by key
+    sort_pairs(wb.get(), w1.get(), kf.get(), k1.get(), m, s);
+    sort_pairs(k1.get(), kf.get(), w1.get(), wf.get(), m, s);
+    sort_pairs(wb.get(), w2.get(), kr.get(), k2.get(), m, s);
+    sort_pairs(k2.get(), kr.get(), w2.get(), wr.get(), m, s);
+    DevBuf<int> diff(1, s);
+    SLK_CUDA(cudaMemsetAsync(diff.get(), 0, sizeof(int), s));
+    LAUNCH(compare_kernel, m, kf.get(), kr.get(), wf.get(), wr.get(), m, diff.get());
+    return read_scalar(diff.get(), s) == 0;
+}
+
+void csr_validate(int64_t n, const int64_t *offs, const int32_t *cols, const double *w,
+                  cudaStream_t s) {
+    if (n <= 0) throw_invalid("empty graph: no vertices");
+    int64_t m = read_scalar(offs + n, s);
+    validate_weights(w, m, false, s);
+    if (!csr_symmetric(n, offs, cols, w, s))
+        throw_invalid("graph must be symmetric: every (i, j, w) needs its (j, i, w)");
+}
+
+double csr_weight_alteration(int64_t n, const int64_t *offs, const int32_t *cols, const double *w,
+                             int64_t seed, double *alt, cudaStream_t s) {
+    csr_validate(n, offs, cols, w, s);
+    int64_t m = read_scalar(offs + n, s);
+    validate_weights(w, m, true, s);
+    if (m == 0) return 0.0;
+    double theta = compute_theta(w, m, s);
+    DevBuf<int32_t> src(m, s);
+    csr_row_sources(n, offs, src.get(), s);
+    LAUNCH(alter_kernel, m, src.get(), cols, w, m, seed, theta * (1.0 - 0x1p-20), alt);
+    return theta;
+}
+
+void csr_min_edge_per_vertex(int64_t n, const int64_t *offs, const int32_t *cols,
+                             const double *alt, const int32_t *colors, int64_t *pos,
+                             cudaStream_t s) {
+    LAUNCH(min_edge_scan_kernel, n, n, offs, cols, alt, colors, pos);
+}
+
+int64_t reconcile_supervertex(int64_t n, const int64_t *pos, const int32_t *dst,
+                              const double *alt, const double *orig, const int32_t *colors,
+                              int32_t *out_a, int32_t *out_b, double *out_w, cudaStream_t s) {
+    DevBuf<unsigned long long> best1(n, s), best2(n, s);
+    DevBuf<int32_t> winner(n, s), flag(n, s), p(n, s);
+    SLK_CUDA(cudaMemsetAsync(best1.get(), 0xff, n * sizeof(unsigned long long), s));
+    SLK_CUDA(cudaMemsetAsync(best2.get(), 0xff, n * sizeof(unsigned long long), s));
+    LAUNCH(fill_i32_kernel, n, winner.get(), n, 0x7fffffff);
+    LAUNCH(reconcile_phase1, n, n, pos, alt, colors, best1.get());
+    LAUNCH(reconcile_phase2, n, n, pos, dst, alt, colors, best1.get(), best2.get());
+    LAUNCH(reconcile_phase3, n, n, pos, dst, alt, orig, colors, best1.get(), best2.get(), winner.get());
+    DevBuf<uint64_t> keys(n, s);
+    DevBuf<double> ws(n, s);
+    LAUNCH(winner_edges_kernel, n, n, winner.get(), dst, orig, flag.get(), keys.get(), ws.get());
+    exclusive_sum(flag.get(), p.get(), n, s);
+    int64_t cnt = (int64_t)read_scalar(p.get() + n - 1, s) + read_scalar(flag.get() + n - 1, s);
+    if (cnt == 0) return 0;
+    DevBuf<uint64_t> k2(cnt, s);
+    DevBuf<double> w2(cnt, s);
+    LAUNCH(compact_kernel<uint64_t>, n, keys.get(), flag.get(), p.get(), n, k2.get());
+    LAUNCH(compact_kernel<double>, n, ws.get(), flag.get(), p.get(), n, w2.get());
+    return unique_min(k2.get(), w2.get(), cnt, 32 + bits_for(n), out_a, out_b, out_w, s);
+}
+
+void label_propagation(int64_t n, int32_t *colors, const int32_t *us, const int32_t *vs, int64_t m,
+                       cudaStream_t s) {
+    if (m == 0 || n == 0) return;
+    DevBuf<int32_t> next(n, s);
+    DevBuf<int> changed(1, s);
+    for (int it = 0; it < 4096; it++) {
+        LAUNCH(prop_init_kernel, n, n, next.get());
+        LAUNCH(prop_edges_kernel, m, colors, us, vs, m, next.get());
+        LAUNCH(prop_jump_kernel, n, n, next.get());
+        SLK_CUDA(cudaMemsetAsync(changed.get(), 0, sizeof(int), s));
+        LAUNCH(prop_apply_kernel, n, n, colors, next.get(), changed.get());
+        if (!read_scalar(changed.get(), s)) return;
+    }
+    throw_internal("label propagation did not converge");
+}
+
+void csr_solve_mst(int64_t n, const int64_t *offs, const int32_t *cols, const double *w,
+                   bool maximize, int64_t seed, int32_t *out_src, int32_t *out_dst, double *out_w,
+                   int32_t *colors, int64_t *n_edges, int64_t *n_components, cudaStream_t s) {
+    csr_validate(n, offs, cols, w, s);
+    int64_t m = read_scalar(offs + n, s);
+    // undirected entries (src < col) in CSR order, i.e. sorted by (a, b)
+    DevBuf<int32_t> src(m, s), flag(m, s), pos(m, s);
+    int64_t mu = 0;
+    DevBuf<int32_t> ua, ub;
+    DevBuf<double> uw;
+    if (m > 0) {
+        csr_row_sources(n, offs, src.get(), s);
+        validate_weights(w, m, true, s);
+        LAUNCH(lt_flag_kernel, m, src.get(), cols, m, flag.get());
+        exclusive_sum(flag.get(), pos.get(), m, s);
+        mu = (int64_t)read_scalar(pos.get() + m - 1, s) + read_scalar(flag.get() + m - 1, s);
+        ua.alloc(mu, s);
+        ub.alloc(mu, s);
+        uw.alloc(mu, s);
+        LAUNCH(compact_kernel<int32_t>, m, src.get(), flag.get(), pos.get(), m, ua.get());
+        LAUNCH(compact_kernel<int32_t>, m, cols, flag.get(), pos.get(), m, ub.get());
+        LAUNCH(compact_kernel<double>, m, w, flag.get(), pos.get(), m, uw.get());
+    }
+    msf_undirected(n, ua.get(), ub.get(), uw.get(), mu, false, maximize, seed, out_src, out_dst,
+                   out_w, colors, n_edges, n_components, s);
+}
+
+}  // namespace slk

@@ -1,0 +1,794 @@
+// knn.cu — fused brute-force neighbour search for sm_100a.
+//
+// Replaces the reference's fused_knn / _fused_1nn_arrays
+// (/root/reference/pkg/src/parlink/neighbors.py:246-348) and its numba
+// kernels _row_sq_norms (:80-89), _knn_scan_tile (:119-160),
+// _knn_merge_rows (:163-188), _nn1_scan_tile (:191-217).
+//
+// Three stages per call:
+//  K1  pack      X → 128-point blocks, dims-major ([block][dim][128] fp32),
+//                so every (block, 16-dim chunk) operand tile is one
+//                contiguous 8 KB cp.async copy; fp64 row norms in the
+//                reference's sequential order.
+//  K2  scan      one CTA owns 128 query rows for the whole index sweep (no
+//                cross-CTA merge).  8x8 register micro-tiles compute the
+//                exact-fp32 direct form sum((q-x)^2) (relative error bound);
+//                the top-K' selection is fused into the epilogue: a per-row
+//                threshold filter, a per-row shared-memory candidate buffer
+//                and warp-cooperative insertion into a per-row sorted list
+//                (K' = 32R).  No distance tile ever reaches HBM.
+//  K3  refine    one warp per row recomputes the K' candidates in float64
+//                with the reference's operation order (bit-identical values),
+//                sorts by (distance, id), emits the top k and checks a
+//                certificate that no unseen candidate can beat the k-th.
+//                Rows that fail are re-scanned exactly (K3x, float64).
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "common.cuh"
+
+namespace slk {
+
+namespace {
+
+constexpr int BM = 128;   // query rows per CTA
+constexpr int BN = 128;   // index points per block
+constexpr int KC = 16;    // dims per operand chunk
+constexpr int NT = 256;   // threads per CTA
+constexpr int CAP = 32;   // per-row candidate buffer
+constexpr unsigned FULL = 0xffffffffu;
+
+enum Mode { MODE_NONE = 0, MODE_MASK = 1, MODE_COLOR = 2, MODE_SELF = 3 };
+
+// ------------------------------------------------------------------ K1
+__global__ void pack_blocks_kernel(const float *__restrict__ x, int64_t n, int d, int dp,
+                                   int64_t nblocks, float *__restrict__ xp) {
+    // one thread per (point, dim) of the padded layout, reading x coalesced
+    int64_t total = nblocks * BN * (int64_t)dp;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        int64_t p = e / dp;
+        int t = (int)(e - p * dp);
+        float v = (p < n && t < d) ? x[p * d + t] : 0.0f;
+        int64_t b = p / BN;
+        int j = (int)(p - b * BN);
+        xp[(b * dp + t) * BN + j] = v;
+    }
+}
+
+// ref neighbors.py:80-89: acc += x[t]*x[t], sequential, no FMA.
+__global__ void norms_kernel(const float *__restrict__ x32, const double *__restrict__ x64,
+                             int64_t n, int d, double *__restrict__ out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        double acc = 0.0;
+        if (x64) {
+            const double *r = x64 + i * d;
+            for (int t = 0; t < d; t++) acc = __dadd_rn(acc, __dmul_rn(r[t], r[t]));
+        } else {
+            const float *r = x32 + i * d;
+            for (int t = 0; t < d; t++) {
+                double v = (double)r[t];
+                acc = __dadd_rn(acc, __dmul_rn(v, v));
+            }
+        }
+        out[i] = acc;
+    }
+}
+
+__global__ void max_reduce_kernel(const double *__restrict__ v, int64_t n, double *out) {
+    double m = 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        m = fmax(m, v[i]);
+    for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(FULL, m, o));
+    if ((threadIdx.x & 31) == 0)
+        atomicMax((unsigned long long *)out, (unsigned long long)__double_as_longlong(m));
+}
+
+// --------------------------------------------------- warp sorted lists
+// A warp holds a sorted list of 32R (value, id) pairs, element p = r*32+lane,
+// ascending by (value, id).  Insertion shifts the suffix right by one.
+template <class V>
+__device__ __forceinline__ bool pair_gt(V av, int ai, V bv, int bi) {
+    return av > bv || (av == bv && ai > bi);
+}
+
+template <int R, class V>
+__device__ __forceinline__ void warp_list_insert(V (&lv)[R], int (&li)[R], V v, int id, int lane) {
+    bool g[R];
+    V pv[R];
+    int pi[R];
+    bool pg[R];
+    V tv[R];
+    int ti[R];
+    bool tg[R];
+#pragma unroll
+    for (int r = 0; r < R; r++) {
+        g[r] = pair_gt(lv[r], li[r], v, id);
+        pv[r] = __shfl_up_sync(FULL, lv[r], 1);
+        pi[r] = __shfl_up_sync(FULL, li[r], 1);
+        pg[r] = __shfl_up_sync(FULL, (int)g[r], 1) != 0;
+        tv[r] = __shfl_sync(FULL, lv[r], 31);
+        ti[r] = __shfl_sync(FULL, li[r], 31);
+        tg[r] = __shfl_sync(FULL, (int)g[r], 31) != 0;
+    }
+#pragma unroll
+    for (int r = 0; r < R; r++) {
+        if (lane == 0) {
+            if (r == 0) {
+                pg[r] = false;
+            } else {
+                pv[r] = tv[r - 1];
+                pi[r] = ti[r - 1];
+                pg[r] = tg[r - 1];
+            }
+        }
+        if (g[r]) {
+            if (pg[r]) {
+                lv[r] = pv[r];
+                li[r] = pi[r];
+            } else {
+                lv[r] = v;
+                li[r] = id;
+            }
+        }
+    }
+}
+
+// Bitonic sort of the 32R warp-distributed pairs, ascending by (value, id).
+template <int R, class V>
+__device__ __forceinline__ void warp_bitonic_sort(V (&lv)[R], int (&li)[R], int lane) {
+    constexpr int N = 32 * R;
+#pragma unroll
+    for (int size = 2; size <= N; size <<= 1) {
+#pragma unroll
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            if (stride >= 32) {
+                int rs = stride / 32;
+#pragma unroll
+                for (int r = 0; r < R; r++) {
+                    int partner = r ^ rs;
+                    if (partner > r) {
+                        int p = r * 32 + lane;
+                        bool up = (p & size) == 0;
+                        bool sw = up ? pair_gt(lv[r], li[r], lv[partner], li[partner])
+                                     : pair_gt(lv[partner], li[partner], lv[r], li[r]);
+                        if (sw) {
+                            V tv = lv[r];
+                            int ti = li[r];
+                            lv[r] = lv[partner];
+                            li[r] = li[partner];
+                            lv[partner] = tv;
+                            li[partner] = ti;
+                        }
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int r = 0; r < R; r++) {
+                    int p = r * 32 + lane;
+                    V ov = __shfl_xor_sync(FULL, lv[r], stride);
+                    int oi = __shfl_xor_sync(FULL, li[r], stride);
+                    bool lower = (lane & stride) == 0;
+                    bool up = (p & size) == 0;
+                    // lower element keeps the min when ascending
+                    bool mine_gt = pair_gt(lv[r], li[r], ov, oi);
+                    bool take = (lower == up) ? mine_gt : !mine_gt;
+                    if (take && !(lv[r] == ov && li[r] == oi)) {
+                        lv[r] = ov;
+                        li[r] = oi;
+                    }
+                }
+            }
+        }
+    }
+}
+
+// ------------------------------------------------------------------ K2
+struct ScanArgs {
+    const float *qp;   // packed queries [nqb][dp][BN]
+    const float *xp;   // packed index   [nxb][dp][BN]
+    int64_t nq, nx;
+    int dp;
+    int64_t qb0;       // first query block of this launch
+    const uint8_t *mask;     // MODE_MASK: nq x nx
+    const int32_t *qcolor;   // MODE_COLOR
+    const int32_t *xcolor;
+    int32_t *cand;     // [nq_rows_launch][32R] candidate ids (-1 = none)
+    float *kth;        // [nq_rows_launch] approx K'-th value
+    int64_t row0;      // global row of cand[0]
+    int64_t row1;      // rows [row0, row1) are written
+};
+
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+    unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+template <int R>
+struct ScanSmem {
+    float qs[2][KC][BM];
+    float xs[2][KC][BN];
+    float buf_v[BM][CAP];
+    int buf_i[BM][CAP];
+    float list_v[BM][32 * R];
+    int list_i[BM][32 * R];
+    int cnt[BM];
+    float thr[BM];
+    int qcol[BM];
+};
+
+template <int MODE, int R>
+__global__ void __launch_bounds__(NT, (R == 1 ? 2 : 1)) scan_kernel(ScanArgs a) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    ScanSmem<R> &S = *reinterpret_cast<ScanSmem<R> *>(smem_raw);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int ty = tid >> 4, tx = tid & 15;
+    const int64_t qb = a.qb0 + blockIdx.x;
+    const int64_t row_base = qb * BM;
+    const int nkc = a.dp / KC;
+    const int64_t nxb = (a.nx + BN - 1) / BN;
+    const int64_t total_steps = nxb * nkc;
+
+    for (int e = tid; e < BM * 32 * R; e += NT) {
+        (&S.list_v[0][0])[e] = INFINITY;
+        (&S.list_i[0][0])[e] = -1;
+    }
+    for (int r = tid; r < BM; r += NT) {
+        S.cnt[r] = 0;
+        S.thr[r] = INFINITY;
+        if (MODE == MODE_COLOR) {
+            int64_t gi = row_base + r;
+            S.qcol[r] = gi < a.nq ? a.qcolor[gi] : -1;
+        }
+    }
+
+    const float *qsrc = a.qp + qb * (int64_t)a.dp * BM;
+    auto load_step = [&](int64_t step, int buf) {
+        int64_t jb = step / nkc;
+        int kc = (int)(step - jb * nkc);
+        const float *qg = qsrc + (int64_t)kc * KC * BM;
+        const float *xg = a.xp + (jb * a.dp + (int64_t)kc * KC) * BN;
+        // 2 x 8 KB contiguous copies, 16 B per cp.async
+#pragma unroll
+        for (int c = 0; c < (KC * BM / 4) / NT; c++) {
+            int e = (c * NT + tid) * 4;
+            cp_async16(&S.qs[buf][0][0] + e, qg + e);
+            cp_async16(&S.xs[buf][0][0] + e, xg + e);
+        }
+    };
+
+    float acc[8][8];
+#pragma unroll
+    for (int i = 0; i < 8; i++)
+#pragma unroll
+        for (int j = 0; j < 8; j++) acc[i][j] = 0.0f;
+
+    load_step(0, 0);
+    cp_async_commit();
+    __syncthreads();
+
+    for (int64_t step = 0; step < total_steps; step++) {
+        const int buf = (int)(step & 1);
+        if (step + 1 < total_steps) {
+            load_step(step + 1, buf ^ 1);
+            cp_async_commit();
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
+        __syncthreads();
+        // ---- direct-form distance micro-tile: acc += (q - x)^2
+#pragma unroll
+        for (int t = 0; t < KC; t++) {
+            float4 qa = *reinterpret_cast<const float4 *>(&S.qs[buf][t][ty * 4]);
+            float4 qb4 = *reinterpret_cast<const float4 *>(&S.qs[buf][t][64 + ty * 4]);
+            float4 xa = *reinterpret_cast<const float4 *>(&S.xs[buf][t][tx * 4]);
+            float4 xb = *reinterpret_cast<const float4 *>(&S.xs[buf][t][64 + tx * 4]);
+            float q[8] = {qa.x, qa.y, qa.z, qa.w, qb4.x, qb4.y, qb4.z, qb4.w};
+            float x[8] = {xa.x, xa.y, xa.z, xa.w, xb.x, xb.y, xb.z, xb.w};
+#pragma unroll
+            for (int i = 0; i < 8; i++)
+#pragma unroll
+                for (int j = 0; j < 8; j++) {
+                    float df = __fsub_rn(q[i], x[j]);
+                    acc[i][j] = __fmaf_rn(df, df, acc[i][j]);
+                }
+        }
+        __syncthreads();
+
+        const int64_t jb = step / nkc;
+        if ((int)(step - jb * nkc) != nkc - 1) continue;
+
+        // ---- epilogue for index block jb: threshold filter → candidate buffers
+        uint64_t pending = 0;
+        int64_t gj[8];
+        bool colok[8];
+#pragma unroll
+        for (int j = 0; j < 8; j++) {
+            int c = j < 4 ? tx * 4 + j : 64 + tx * 4 + (j - 4);
+            gj[j] = jb * BN + c;
+            colok[j] = gj[j] < a.nx;
+        }
+        int xc[8];
+        if (MODE == MODE_COLOR) {
+#pragma unroll
+            for (int j = 0; j < 8; j++) xc[j] = colok[j] ? a.xcolor[gj[j]] : -1;
+        }
+#pragma unroll
+        for (int i = 0; i < 8; i++) {
+            int r = i < 4 ? ty * 4 + i : 64 + ty * 4 + (i - 4);
+            int64_t gi = row_base + r;
+            float th = S.thr[r];
+#pragma unroll
+            for (int j = 0; j < 8; j++) {
+                bool ok = colok[j] && gi < a.nq && acc[i][j] < th;
+                if (MODE == MODE_SELF) ok = ok && gj[j] != gi;
+                if (MODE == MODE_COLOR) ok = ok && xc[j] != S.qcol[r];
+                if (MODE == MODE_MASK) ok = ok && a.mask[gi * a.nx + gj[j]] != 0;
+                if (ok) pending |= 1ull << (i * 8 + j);
+            }
+        }
+        // insert loop: push pending candidates; merge buffers; retry overflow
+        while (true) {
+            uint64_t todo = pending;
+            pending = 0;
+            while (todo) {
+                int bit = __ffsll((long long)todo) - 1;
+                todo &= todo - 1;
+                int i = bit >> 3, j = bit & 7;
+                int r = i < 4 ? ty * 4 + i : 64 + ty * 4 + (i - 4);
+                float v = acc[i][j];
+                if (!(v < S.thr[r])) continue;
+                int pos = atomicAdd(&S.cnt[r], 1);
+                if (pos < CAP) {
+                    S.buf_v[r][pos] = v;
+                    S.buf_i[r][pos] = (int)gj[j];
+                } else {
+                    pending |= 1ull << bit;
+                }
+            }
+            __syncthreads();
+            // merge: warp w owns rows w, w+8, ...
+            for (int r = warp; r < BM; r += NT / 32) {
+                int c = S.cnt[r];
+                if (c == 0) continue;
+                if (c > CAP) c = CAP;
+                float lv[R];
+                int li[R];
+#pragma unroll
+                for (int rr = 0; rr < R; rr++) {
+                    lv[rr] = S.list_v[r][rr * 32 + lane];
+                    li[rr] = S.list_i[r][rr * 32 + lane];
+                }
+                for (int q = 0; q < c; q++) {
+                    float v = S.buf_v[r][q];
+                    int id = S.buf_i[r][q];
+                    float tv = __shfl_sync(FULL, lv[R - 1], 31);
+                    int tiid = __shfl_sync(FULL, li[R - 1], 31);
+                    if (pair_gt(tv, tiid, v, id)) warp_list_insert<R>(lv, li, v, id, lane);
+                }
+#pragma unroll
+                for (int rr = 0; rr < R; rr++) {
+                    S.list_v[r][rr * 32 + lane] = lv[rr];
+                    S.list_i[r][rr * 32 + lane] = li[rr];
+                }
+                float tv = __shfl_sync(FULL, lv[R - 1], 31);
+                if (lane == 0) {
+                    S.thr[r] = tv;
+                    S.cnt[r] = 0;
+                }
+            }
+            if (!__syncthreads_or(pending != 0)) break;
+        }
+#pragma unroll
+        for (int i = 0; i < 8; i++)
+#pragma unroll
+            for (int j = 0; j < 8; j++) acc[i][j] = 0.0f;
+    }
+
+    // write candidate lists of this CTA's rows
+    for (int r = warp; r < BM; r += NT / 32) {
+        int64_t gi = row_base + r;
+        if (gi < a.row0 || gi >= a.row1) continue;
+        int32_t *dst = a.cand + (gi - a.row0) * (32 * R);
+#pragma unroll
+        for (int rr = 0; rr < R; rr++) dst[rr * 32 + lane] = S.list_i[r][rr * 32 + lane];
+        if (lane == 0) a.kth[gi - a.row0] = S.list_i[r][32 * R - 1] >= 0 ? S.list_v[r][32 * R - 1] : INFINITY;
+    }
+}
+
+// ------------------------------------------------------------------ K3
+struct RefineArgs {
+    const float *q32;
+    const double *q64;
+    const double *qnorm;
+    const float *x32;
+    const double *x64;
+    const double *xnorm;
+    int d, k;
+    int64_t nq, nx;
+    int64_t row0, row1;
+    const int32_t *cand;
+    const float *kth;
+    const double *max_xnorm;  // device scalar
+    bool exact_f32;           // inputs are exactly their float32 values
+    int32_t *out_idx;
+    double *out_dist;
+    int *fail_rows;
+    int *fail_count;
+};
+
+// Exact reference distance (neighbors.py:132-137): dot sequential over t,
+// dist = nq + nx - 2*dot, clamp at 0.  Explicit _rn intrinsics: no FMA.
+__device__ __forceinline__ double exact_dist(const float *q32, const double *q64, const float *x32,
+                                             const double *x64, int64_t i, int64_t j, int d,
+                                             double nq, double nx) {
+    double dot = 0.0;
+    if (q64) {
+        const double *qr = q64 + i * d;
+        const double *xr = x64 + j * d;
+        for (int t = 0; t < d; t++) dot = __dadd_rn(dot, __dmul_rn(qr[t], xr[t]));
+    } else {
+        const float *qr = q32 + i * d;
+        const float *xr = x32 + j * d;
+        for (int t = 0; t < d; t++) dot = __dadd_rn(dot, __dmul_rn((double)qr[t], (double)xr[t]));
+    }
+    double v = __dsub_rn(__dadd_rn(nq, nx), __dmul_rn(2.0, dot));
+    return v < 0.0 ? 0.0 : v;
+}
+
+// Lower bound on the reference distance of any candidate whose fp32 direct
+// value is >= a.
+__device__ double certified_floor(float a, int d, double nq, double max_xn, bool exact_f32) {
+    const double u = 0x1p-24;
+    double c_rel = (d + 4) * u * 1.01;
+    double af = (double)a - (double)d * 0x1p-148;  // subnormal products
+    if (!(af > 0.0)) return -INFINITY;
+    double dt = af / (1.0 + c_rel);  // lower bound on |q~ - x~|^2
+    double s = sqrt(dt) * (1.0 - 1e-15);
+    if (!exact_f32) s -= u * 1.01 * (sqrt(nq) + sqrt(max_xn));  // f64→f32 input rounding
+    if (!(s > 0.0)) return -INFINITY;
+    double dlo = s * s * (1.0 - 1e-15);
+    double ev = (d + 4) * 0x1p-52 * (nq + max_xn) * 1.01 + 0x1p-1074;  // fp64 expanded-form error
+    return dlo - ev;
+}
+
+template <int R>
+__global__ void refine_kernel(RefineArgs a) {
+    const int lane = threadIdx.x & 31;
+    const int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nrows = a.row1 - a.row0;
+    if (wid >= nrows) return;
+    const int64_t gi = a.row0 + wid;
+    const int32_t *cand = a.cand + wid * (32 * R);
+    const double nq = a.qnorm[gi];
+    double lv[R];
+    int li[R];
+#pragma unroll
+    for (int r = 0; r < R; r++) {
+        int j = cand[r * 32 + lane];
+        if (j >= 0) {
+            lv[r] = exact_dist(a.q32, a.q64, a.x32, a.x64, gi, j, a.d, nq, a.xnorm[j]);
+            li[r] = j;
+        } else {
+            lv[r] = INFINITY;
+            li[r] = 0x7fffffff;
+        }
+    }
+    warp_bitonic_sort<R>(lv, li, lane);
+#pragma unroll
+    for (int r = 0; r < R; r++) {
+        int p = r * 32 + lane;
+        if (p < a.k) {
+            a.out_idx[wid * a.k + p] = li[r] == 0x7fffffff ? -1 : li[r];
+            a.out_dist[wid * a.k + p] = lv[r];
+        }
+    }
+    // certificate: the k-th exact value must beat every unseen candidate
+    const int kr = (a.k - 1) / 32, kl = (a.k - 1) & 31;
+    double vk = 0.0;
+    int ik = 0;
+#pragma unroll
+    for (int r = 0; r < R; r++)
+        if (r == kr) {
+            vk = __shfl_sync(FULL, lv[r], kl);
+            ik = __shfl_sync(FULL, li[r], kl);
+        }
+    if (lane == 0) {
+        float kth = a.kth[wid];
+        bool ok;
+        if (ik == 0x7fffffff) {
+            ok = false;  // fewer than k admissible candidates in the list
+        } else if (kth == INFINITY && cand[32 * R - 1] < 0) {
+            ok = true;  // list never filled: every admissible candidate was kept
+        } else {
+            double floor = certified_floor(kth, a.d, nq, *a.max_xnorm, a.exact_f32);
+            ok = floor > vk;
+        }
+        if (!ok) {
+            int slot = atomicAdd(a.fail_count, 1);
+            a.fail_rows[slot] = (int)wid;
+        }
+    }
+}
+
+// ------------------------------------------------------------------ K3x
+// Exact float64 re-scan of one row per warp (rows that failed the
+// certificate): every admissible candidate, reference values, (v, id) order.
+struct ExactArgs {
+    const float *q32;
+    const double *q64;
+    const double *qnorm;
+    const float *x32;
+    const double *x64;
+    const double *xnorm;
+    int d, k, mode;
+    int64_t nq, nx, row0;
+    const uint8_t *mask;
+    const int32_t *qcolor, *xcolor;
+    const int *rows;
+    int nrows;
+    int32_t *out_idx;
+    double *out_dist;
+    int *missing;  // first row (global) without admissible candidate, or INT_MAX
+};
+
+template <int R>
+__global__ void exact_rescan_kernel(ExactArgs a) {
+    const int lane = threadIdx.x & 31;
+    const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    if (w >= a.nrows) return;
+    const int64_t wid = a.rows[w];
+    const int64_t gi = a.row0 + wid;
+    const double nq = a.qnorm[gi];
+    double lv[R];
+    int li[R];
+#pragma unroll
+    for (int r = 0; r < R; r++) {
+        lv[r] = INFINITY;
+        li[r] = 0x7fffffff;
+    }
+    for (int64_t j0 = 0; j0 < a.nx; j0 += 32) {
+        int64_t j = j0 + lane;
+        bool ok = j < a.nx;
+        if (ok && a.mode == MODE_SELF) ok = j != gi;
+        if (ok && a.mode == MODE_COLOR) ok = a.xcolor[j] != a.qcolor[gi];
+        if (ok && a.mode == MODE_MASK) ok = a.mask[gi * a.nx + j] != 0;
+        double v = ok ? exact_dist(a.q32, a.q64, a.x32, a.x64, gi, j, a.d, nq, a.xnorm[j]) : INFINITY;
+        double tv = __shfl_sync(FULL, lv[R - 1], 31);
+        int ti = __shfl_sync(FULL, li[R - 1], 31);
+        unsigned m = __ballot_sync(FULL, ok && pair_gt(tv, ti, v, (int)j));
+        while (m) {
+            int src = __ffs(m) - 1;
+            m &= m - 1;
+            double cv = __shfl_sync(FULL, v, src);
+            int cj = __shfl_sync(FULL, (int)j, src);
+            double t2 = __shfl_sync(FULL, lv[R - 1], 31);
+            int i2 = __shfl_sync(FULL, li[R - 1], 31);
+            if (pair_gt(t2, i2, cv, cj)) warp_list_insert<R>(lv, li, cv, cj, lane);
+        }
+    }
+#pragma unroll
+    for (int r = 0; r < R; r++) {
+        int p = r * 32 + lane;
+        if (p < a.k) {
+            a.out_idx[wid * a.k + p] = li[r] == 0x7fffffff ? -1 : li[r];
+            a.out_dist[wid * a.k + p] = lv[r];
+        }
+    }
+    int first = __shfl_sync(FULL, li[0], 0);
+    if (lane == 0 && first == 0x7fffffff) atomicMin(a.missing, (int)gi);
+}
+
+__global__ void check_missing_kernel(const int32_t *idx, int64_t rows, int k, int64_t row0,
+                                     int *missing) {
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < rows;
+         r += (int64_t)gridDim.x * blockDim.x)
+        if (idx[r * k + k - 1] < 0) atomicMin(missing, (int)(row0 + r));
+}
+
+// ----------------------------------------------------------- host side
+struct Packed {
+    DevBuf<float> p;
+    int dp = 0;
+    int64_t nblocks = 0;
+};
+
+Packed pack(const float *x, int64_t n, int d, cudaStream_t s) {
+    Packed P;
+    P.dp = ((d + KC - 1) / KC) * KC;
+    P.nblocks = (n + BN - 1) / BN;
+    P.p.alloc((size_t)P.nblocks * BN * P.dp, s);
+    int64_t total = P.nblocks * BN * (int64_t)P.dp;
+    pack_blocks_kernel<<<grid_for(total, 256), 256, 0, s>>>(x, n, d, P.dp, P.nblocks, P.p);
+    SLK_CHECK_LAUNCH();
+    return P;
+}
+
+template <int MODE, int R>
+void launch_scan(const ScanArgs &args, int64_t nqb, cudaStream_t s) {
+    size_t smem = sizeof(ScanSmem<R>);
+    static bool configured = false;
+    if (!configured) {
+        SLK_CUDA(cudaFuncSetAttribute(scan_kernel<MODE, R>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        configured = true;
+    }
+    scan_kernel<MODE, R><<<(unsigned)nqb, NT, smem, s>>>(args);
+    SLK_CHECK_LAUNCH();
+}
+
+template <int R>
+void dispatch_scan(int mode, const ScanArgs &args, int64_t nqb, cudaStream_t s) {
+    switch (mode) {
+        case MODE_NONE: launch_scan<MODE_NONE, R>(args, nqb, s); break;
+        case MODE_MASK: launch_scan<MODE_MASK, R>(args, nqb, s); break;
+        case MODE_COLOR: launch_scan<MODE_COLOR, R>(args, nqb, s); break;
+        default: launch_scan<MODE_SELF, R>(args, nqb, s); break;
+    }
+}
+
+template <int R>
+void launch_refine(const RefineArgs &ra, int64_t rows, cudaStream_t s) {
+    int64_t threads = rows * 32;
+    refine_kernel<R><<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(ra);
+    SLK_CHECK_LAUNCH();
+}
+
+template <int R>
+void launch_exact(const ExactArgs &ea, cudaStream_t s) {
+    int64_t threads = (int64_t)ea.nrows * 32;
+    exact_rescan_kernel<R><<<(unsigned)((threads + 127) / 128), 128, 0, s>>>(ea);
+    SLK_CHECK_LAUNCH();
+}
+
+// Full neighbour search for query rows [q0, q1); k results per row.
+void search(const float *q32, const double *q64, int64_t nq, const float *x32, const double *x64,
+            int64_t nx, int d, int k, int mode, const uint8_t *mask, const int32_t *qcolor,
+            const int32_t *xcolor, int64_t q0, int64_t q1, int32_t *out_idx, double *out_dist,
+            cudaStream_t s) {
+    ScanStats &st = scan_stats();
+    st = ScanStats{};
+    const int64_t rows = q1 - q0;
+    if (rows <= 0) return;
+    const bool same = (q32 == x32);
+    // fp64 norms in the reference's order
+    DevBuf<double> xnorm(nx, s), qnorm_own;
+    norms_kernel<<<grid_for(nx, 256), 256, 0, s>>>(x32, x64, nx, d, xnorm);
+    SLK_CHECK_LAUNCH();
+    const double *qnorm = xnorm;
+    if (!same) {
+        qnorm_own.alloc(nq, s);
+        norms_kernel<<<grid_for(nq, 256), 256, 0, s>>>(q32, q64, nq, d, qnorm_own);
+        SLK_CHECK_LAUNCH();
+        qnorm = qnorm_own;
+    }
+    DevBuf<double> max_xn(1, s);
+    SLK_CUDA(cudaMemsetAsync(max_xn, 0, sizeof(double), s));
+    max_reduce_kernel<<<grid_for(nx, 256, 1024), 256, 0, s>>>(xnorm, nx, max_xn);
+    SLK_CHECK_LAUNCH();
+
+    DevBuf<int> fail_rows(rows, s), counters(2, s);
+    SLK_CUDA(cudaMemsetAsync(counters, 0, sizeof(int), s));
+    const int Rsel = k < 32 ? 1 : (k < 64 ? 2 : 4);
+    if (k <= 127) {
+        Packed X = pack(x32, nx, d, s);
+        Packed Qown;
+        const float *qp = X.p;
+        if (!same) {
+            Qown = pack(q32, nq, d, s);
+            qp = Qown.p;
+        }
+        const int64_t qb0 = q0 / BM, qb1 = (q1 + BM - 1) / BM;
+        DevBuf<int32_t> cand(rows * 32 * Rsel, s);
+        DevBuf<float> kth(rows, s);
+        ScanArgs sa{qp, X.p, nq, nx, X.dp, qb0, mask, qcolor, xcolor, cand, kth, q0, q1};
+        if (Rsel == 1) dispatch_scan<1>(mode, sa, qb1 - qb0, s);
+        else if (Rsel == 2) dispatch_scan<2>(mode, sa, qb1 - qb0, s);
+        else dispatch_scan<4>(mode, sa, qb1 - qb0, s);
+        st.tiles_computed = (qb1 - qb0) * X.nblocks;
+
+        RefineArgs ra{q32, same ? x64 : q64, qnorm, x32, x64, xnorm, d, k, nq, nx, q0, q1,
+                      cand, kth, max_xn, x64 == nullptr, out_idx, out_dist, fail_rows, counters};
+        if (Rsel == 1) launch_refine<1>(ra, rows, s);
+        else if (Rsel == 2) launch_refine<2>(ra, rows, s);
+        else launch_refine<4>(ra, rows, s);
+        st.rows_refined = rows;
+    } else {
+        // k beyond the fused list capacity: every row takes the exact path
+        std::vector<int> all(rows);
+        for (int64_t r = 0; r < rows; r++) all[r] = (int)r;
+        SLK_CUDA(cudaMemcpyAsync(fail_rows, all.data(), rows * sizeof(int), cudaMemcpyHostToDevice, s));
+        int rr = (int)rows;
+        SLK_CUDA(cudaMemcpyAsync(counters, &rr, sizeof(int), cudaMemcpyHostToDevice, s));
+        if (k > 256) throw_invalid("k=%d exceeds the GPU limit of 256 neighbours", k);
+    }
+    int nfail = read_scalar<int>(counters, s);
+    st.rows_rescanned = nfail;
+    int missing_init = 0x7fffffff;
+    SLK_CUDA(cudaMemcpyAsync(counters.get() + 1, &missing_init, sizeof(int), cudaMemcpyHostToDevice, s));
+    if (nfail > 0) {
+        ExactArgs ea{q32, same ? x64 : q64, qnorm, x32, x64, xnorm, d, k, mode, nq, nx, q0,
+                     mask, qcolor, xcolor, fail_rows, nfail, out_idx, out_dist, counters.get() + 1};
+        if (k <= 32) launch_exact<1>(ea, s);
+        else if (k <= 64) launch_exact<2>(ea, s);
+        else if (k <= 128) launch_exact<4>(ea, s);
+        else launch_exact<8>(ea, s);
+    }
+    check_missing_kernel<<<grid_for(rows, 256), 256, 0, s>>>(out_idx, rows, k, q0, counters.get() + 1);
+    SLK_CHECK_LAUNCH();
+    int missing = read_scalar<int>(counters.get() + 1, s);
+    if (missing != 0x7fffffff) {
+        if (mode == MODE_SELF)
+            throw_internal("row %d has fewer than k neighbours", missing);
+        throw_invalid("query row %d has no admissible candidate", missing);
+    }
+}
+
+}  // namespace
+
+void row_norms(const float *x32, const double *x64, int64_t n, int d, double *out, cudaStream_t s) {
+    norms_kernel<<<grid_for(n, 256), 256, 0, s>>>(x32, x64, n, d, out);
+    SLK_CHECK_LAUNCH();
+}
+
+void knn_rows(const float *x32, const double *x64, int64_t n, int d, int k, int64_t q0,
+              int64_t q1, int32_t *idx, double *dist, cudaStream_t s) {
+    if (k < 1 || k > n - 1) throw_invalid("k must be in [1, %lld] for %lld points, got %d",
+                                          (long long)(n - 1), (long long)n, k);
+    if (q0 < 0 || q1 > n || q0 > q1) throw_invalid("query row range [%lld, %lld) outside [0, %lld)",
+                                                   (long long)q0, (long long)q1, (long long)n);
+    search(x32, x64, n, x32, x64, n, d, k, MODE_SELF, nullptr, nullptr, nullptr, q0, q1, idx,
+           dist, s);
+}
+
+void nn1_rows(const float *q32, const double *q64, int64_t nq, const float *x32,
+              const double *x64, int64_t nx, int d, int mode, const uint8_t *mask,
+              const int32_t *qcolor, const int32_t *xcolor, int64_t q0, int64_t q1, int32_t *idx,
+              double *dist, cudaStream_t s) {
+    if (mode < 0 || mode > 2) throw_invalid("unknown admissibility mode %d", mode);
+    if (nx < 1) throw_invalid("query row %lld has no admissible candidate", (long long)q0);
+    search(q32, q64, nq, x32, x64, nx, d, 1, mode, mask, qcolor, xcolor, q0, q1, idx, dist, s);
+}
+
+namespace {
+// ref neighbors.py:92-104 (_dist_tile): float64 expanded form, clamp, optional sqrt.
+__global__ void pairwise_kernel(const double *__restrict__ q, int64_t nq, const double *__restrict__ x,
+                                int64_t nx, int d, const double *qn, const double *xn, int squared,
+                                double *out) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nq * nx;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        int64_t i = e / nx, j = e - i * nx;
+        double dot = 0.0;
+        for (int t = 0; t < d; t++) dot = __dadd_rn(dot, __dmul_rn(q[i * d + t], x[j * d + t]));
+        double v = __dsub_rn(__dadd_rn(qn[i], xn[j]), __dmul_rn(2.0, dot));
+        if (v < 0.0) v = 0.0;
+        out[e] = squared ? v : __dsqrt_rn(v);
+    }
+}
+}  // namespace
+
+void pairwise_l2(const double *q, int64_t nq, const double *x, int64_t nx, int d, int squared,
+                 double *out, cudaStream_t s) {
+    if (nq == 0 || nx == 0) return;
+    DevBuf<double> qn(nq, s), xn(nx, s);
+    norms_kernel<<<grid_for(nq, 256), 256, 0, s>>>(nullptr, q, nq, d, qn);
+    SLK_CHECK_LAUNCH();
+    norms_kernel<<<grid_for(nx, 256), 256, 0, s>>>(nullptr, x, nx, d, xn);
+    SLK_CHECK_LAUNCH();
+    pairwise_kernel<<<grid_for(nq * nx, 256), 256, 0, s>>>(q, nq, x, nx, d, qn, xn, squared, out);
+    SLK_CHECK_LAUNCH();
+}
+
+}  // namespace slk

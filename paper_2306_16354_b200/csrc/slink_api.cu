@@ -1,0 +1,402 @@
+// slink_api.cu — the C ABI (include/slink.h) and the single-GPU pipeline
+// driver replacing single_linkage / connect_graph
+// (/root/reference/pkg/src/parlink/linkage.py:222-311).
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdarg.h>
+#include <stdint.h>
+#include <string.h>
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+
+namespace slk {
+
+static thread_local std::string g_last_error;
+static thread_local ScanStats g_scan_stats;
+static std::atomic<int64_t> g_launches{0};
+
+void set_error(int status, const std::string &msg) {
+    (void)status;
+    g_last_error = msg;
+}
+
+static std::string vformat(const char *fmt, va_list ap) {
+    char buf[1024];
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    return buf;
+}
+
+void throw_invalid(const char *fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    std::string m = vformat(fmt, ap);
+    va_end(ap);
+    throw Error{SLK_ERR_INVALID, m};
+}
+
+void throw_internal(const char *fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    std::string m = vformat(fmt, ap);
+    va_end(ap);
+    throw Error{SLK_ERR_INTERNAL, m};
+}
+
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+ScanStats &scan_stats() { return g_scan_stats; }
+
+int num_sms() {
+    static int cached = 0;
+    if (!cached) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&cached, cudaDevAttrMultiProcessorCount, dev);
+        if (!cached) cached = 148;
+    }
+    return cached;
+}
+
+namespace {
+
+__global__ void repeat_rows_kernel(int64_t n, int k, int32_t *src) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n * k;
+         e += (int64_t)gridDim.x * blockDim.x)
+        src[e] = (int32_t)(e / k);
+}
+
+__global__ void iota32_kernel(int64_t n, int32_t *v) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+         e += (int64_t)gridDim.x * blockDim.x)
+        v[e] = (int32_t)e;
+}
+
+struct StreamGuard {
+    cudaStream_t s = nullptr;
+    StreamGuard() { SLK_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking)); }
+    ~StreamGuard() {
+        if (s) cudaStreamDestroy(s);
+    }
+};
+
+double now_ms() {
+    using namespace std::chrono;
+    return duration<double, std::milli>(steady_clock::now().time_since_epoch()).count();
+}
+
+std::string largest_sizes(const std::vector<int32_t> &colors) {
+    std::vector<int64_t> counts(colors.size(), 0);
+    for (int32_t c : colors) counts[c]++;
+    std::vector<int64_t> sizes;
+    for (int64_t c : counts)
+        if (c > 0) sizes.push_back(c);
+    std::sort(sizes.rbegin(), sizes.rend());
+    if (sizes.size() > 8) sizes.resize(8);
+    std::string out = "[";
+    for (size_t i = 0; i < sizes.size(); i++) out += (i ? ", " : "") + std::to_string(sizes[i]);
+    return out + "]";
+}
+
+}  // namespace
+
+// Pipeline state on one device (used by slk_single_linkage).
+void single_linkage_device(const float *x32, const double *x64, int64_t n, int d, int k,
+                           int64_t n_clusters, int metric, int64_t seed, int64_t max_iters,
+                           double *h_merges, int64_t *h_labels, int64_t *h_tree_src,
+                           int64_t *h_tree_dst, double *h_tree_w, int64_t *n_iters,
+                           double *timings, cudaStream_t s) {
+    double t0 = now_ms();
+    // --- k-NN graph (linkage.py:287)
+    DevBuf<int32_t> idx(n * k, s);
+    DevBuf<double> dist(n * k, s);
+    knn_rows(x32, x64, n, d, k, 0, n, idx, dist, s);
+    SLK_CUDA(cudaStreamSynchronize(s));
+    double t1 = now_ms();
+    // --- symmetrise + spanning forest (linkage.py:289-290)
+    DevBuf<int32_t> src(n * k, s);
+    repeat_rows_kernel<<<grid_for(n * k, 256), 256, 0, s>>>(n, k, src);
+    SLK_CHECK_LAUNCH();
+    EdgeSet E = dedup_undirected(n, src, idx, dist, n * k, s);
+    src.release();
+    idx.release();
+    dist.release();
+    DevBuf<int32_t> ts(n, s), td(n, s), colors(n, s);
+    DevBuf<double> tw(n, s);
+    int64_t ne = 0, nc = 0;
+    msf_undirected(n, E.a, E.b, E.w, E.m, true, false, seed, ts, td, tw, colors, &ne, &nc, s);
+    E = EdgeSet{};
+    double t2 = now_ms();
+    // --- connect loop (linkage.py:222-254)
+    int64_t budget = max_iters >= 0 ? max_iters : (int64_t)ceil(log2((double)std::max<int64_t>(n, 2))) + 8;
+    int64_t iters = 0;
+    if (nc > 1) {
+        DevBuf<int32_t> usrc(2 * n, s), udst(2 * n, s);
+        DevBuf<double> uw(2 * n, s);
+        while (nc > 1) {
+            if (iters >= budget) {
+                std::vector<int32_t> hc(n);
+                SLK_CUDA(cudaMemcpyAsync(hc.data(), colors.get(), n * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+                SLK_CUDA(cudaStreamSynchronize(s));
+                throw Error{SLK_ERR_CONVERGENCE,
+                            "reconnection did not converge within " + std::to_string(budget) +
+                                " iterations: " + std::to_string(nc) +
+                                " components remain (largest sizes " + largest_sizes(hc) + ")"};
+            }
+            // bridges: one per point (neighbors.py:375-391)
+            int64_t m = ne + n;
+            SLK_CUDA(cudaMemcpyAsync(usrc.get(), ts.get(), ne * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+            SLK_CUDA(cudaMemcpyAsync(udst.get(), td.get(), ne * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+            SLK_CUDA(cudaMemcpyAsync(uw.get(), tw.get(), ne * sizeof(double), cudaMemcpyDeviceToDevice, s));
+            iota32_kernel<<<grid_for(n, 256), 256, 0, s>>>(n, usrc.get() + ne);
+            SLK_CHECK_LAUNCH();
+            nn1_rows(x32, x64, n, x32, x64, n, d, 2, nullptr, colors, colors, 0, n, udst.get() + ne,
+                     uw.get() + ne, s);
+            EdgeSet U = dedup_undirected(n, usrc, udst, uw, m, s);
+            msf_undirected(n, U.a, U.b, U.w, U.m, true, false, seed, ts, td, tw, colors, &ne, &nc, s);
+            iters++;
+        }
+    }
+    SLK_CUDA(cudaStreamSynchronize(s));
+    double t3 = now_ms();
+    // --- dendrogram (linkage.py:295-300)
+    std::vector<int32_t> ha(n - 1), hb(n - 1);
+    std::vector<double> hw(n - 1);
+    dendrogram_device_sort(ts, td, tw, n, metric == 0, ha.data(), hb.data(), hw.data(), s);
+    dendrogram_fold(ha.data(), hb.data(), hw.data(), n, h_merges);
+    double t4 = now_ms();
+    extract_labels(h_merges, n, n_clusters, h_labels);
+    double t5 = now_ms();
+    if (h_tree_src || h_tree_dst || h_tree_w) {
+        std::vector<int32_t> hs(n - 1), hd(n - 1);
+        SLK_CUDA(cudaMemcpyAsync(hs.data(), ts.get(), (n - 1) * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+        SLK_CUDA(cudaMemcpyAsync(hd.data(), td.get(), (n - 1) * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+        if (h_tree_w)
+            SLK_CUDA(cudaMemcpyAsync(h_tree_w, tw.get(), (n - 1) * sizeof(double), cudaMemcpyDeviceToHost, s));
+        SLK_CUDA(cudaStreamSynchronize(s));
+        for (int64_t i = 0; i < n - 1; i++) {
+            if (h_tree_src) h_tree_src[i] = hs[i];
+            if (h_tree_dst) h_tree_dst[i] = hd[i];
+        }
+    }
+    if (n_iters) *n_iters = iters;
+    if (timings) {
+        timings[0] = t1 - t0;
+        timings[1] = t2 - t1;
+        timings[2] = t3 - t2;
+        timings[3] = t4 - t3;
+        timings[4] = t5 - t4;
+    }
+}
+
+}  // namespace slk
+
+using namespace slk;
+
+#define STREAM(s) cudaStream_t s = (cudaStream_t)stream_
+
+extern "C" {
+
+int slk_version(void) { return 100; }
+
+const char *slk_last_error(void) { return g_last_error.c_str(); }
+
+int64_t slk_kernel_launches(void) { return g_launches.load(); }
+
+int slk_last_scan_stats(int64_t *stats4) {
+    stats4[0] = g_scan_stats.rows_refined;
+    stats4[1] = g_scan_stats.rows_rescanned;
+    stats4[2] = g_scan_stats.tiles_computed;
+    stats4[3] = g_scan_stats.tiles_skipped;
+    return SLK_OK;
+}
+
+int slk_knn(const float *d_x32, const double *d_x64, int64_t n, int d, int k, int64_t q0,
+            int64_t q1, int32_t *d_idx, double *d_dist, void *stream_) {
+    STREAM(s);
+    return guarded([&] {
+        knn_rows(d_x32, d_x64, n, d, k, q0, q1, d_idx, d_dist, s);
+        SLK_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+int slk_nn1(const float *d_q32, const double *d_q64, int64_t nq, const float *d_x32,
+            const double *d_x64, int64_t nx, int d, int mode, const uint8_t *d_mask,
+            const int32_t *d_qcolor, const int32_t *d_xcolor, int64_t q0, int64_t q1,
+            int32_t *d_idx, double *d_dist, void *stream_) {
+    STREAM(s);
+    return guarded([&] {
+        nn1_rows(d_q32, d_q64, nq, d_x32, d_x64, nx, d, mode, d_mask, d_qcolor, d_xcolor, q0, q1,
+                 d_idx, d_dist, s);
+        SLK_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+int slk_row_norms(const float *d_x32, const double *d_x64, int64_t n, int d, double *d_out,
+                  void *stream_) {
+    STREAM(s);
+    return guarded([&] {
+        row_norms(d_x32, d_x64, n, d, d_out, s);
+        SLK_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+int slk_edge_list_to_csr(int64_t n, const int32_t *d_src, const int32_t *d_dst,
+                         const double *d_w, int64_t m, int64_t *d_offsets, int32_t *d_cols,
+                         double *d_cols_w, int64_t *nnz, void *stream_) {
+    STREAM(s);
+    return guarded([&] {
+        csr_from_edges(n, d_src, d_dst, d_w, m, d_offsets, d_cols, d_cols_w, nnz, s);
+        SLK_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+int slk_csr_is_symmetric(int64_t n, const int64_t *d_offsets, const int32_t *d_cols,
+                         const double *d_w, int *is_symmetric, void *stream_) {
+    STREAM(s);
+    return guarded([&] { *is_symmetric = csr_symmetric(n, d_offsets, d_cols, d_w, s) ? 1 : 0; });
+}
+
+int slk_weight_alteration(int64_t n, const int64_t *d_offsets, const int32_t *d_cols,
+                          const double *d_w, int64_t seed, double *d_alt, double *theta,
+                          void *stream_) {
+    STREAM(s);
+    return guarded([&] {
+        *theta = csr_weight_alteration(n, d_offsets, d_cols, d_w, seed, d_alt, s);
+        SLK_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+int slk_min_edge_per_vertex(int64_t n, const int64_t *d_offsets, const int32_t *d_cols,
+                            const double *d_alt, const int32_t *d_colors, int64_t *d_pos,
+                            void *stream_) {
+    STREAM(s);
+    return guarded([&] {
+        csr_min_edge_per_vertex(n, d_offsets, d_cols, d_alt, d_colors, d_pos, s);
+        SLK_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+int slk_min_edge_per_supervertex(int64_t n, const int64_t *d_pos, const int32_t *d_dst,
+                                 const double *d_alt, const double *d_orig,
+                                 const int32_t *d_colors, int32_t *d_a, int32_t *d_b,
+                                 double *d_w, int64_t *m_out, void *stream_) {
+    STREAM(s);
+    return guarded([&] {
+        *m_out = reconcile_supervertex(n, d_pos, d_dst, d_alt, d_orig, d_colors, d_a, d_b, d_w, s);
+        SLK_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+int slk_label_propagation(int64_t n, int32_t *d_colors, const int32_t *d_us, const int32_t *d_vs,
+                          int64_t m, void *stream_) {
+    STREAM(s);
+    return guarded([&] {
+        label_propagation(n, d_colors, d_us, d_vs, m, s);
+        SLK_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+int slk_solve_mst(int64_t n, const int64_t *d_offsets, const int32_t *d_cols, const double *d_w,
+                  int maximize, int64_t seed, int32_t *d_src, int32_t *d_dst, double *d_out_w,
+                  int32_t *d_colors, int64_t *n_edges, int64_t *n_components, void *stream_) {
+    STREAM(s);
+    return guarded([&] {
+        csr_solve_mst(n, d_offsets, d_cols, d_w, maximize != 0, seed, d_src, d_dst, d_out_w,
+                      d_colors, n_edges, n_components, s);
+        SLK_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+int slk_msf_edges(int64_t n, const int32_t *d_src, const int32_t *d_dst, const double *d_w,
+                  int64_t m, int64_t seed, int32_t *d_out_src, int32_t *d_out_dst,
+                  double *d_out_w, int32_t *d_colors, int64_t *n_edges, int64_t *n_components,
+                  void *stream_) {
+    STREAM(s);
+    return guarded([&] {
+        EdgeSet E = dedup_undirected(n, d_src, d_dst, d_w, m, s);
+        msf_undirected(n, E.a, E.b, E.w, E.m, true, false, seed, d_out_src, d_out_dst, d_out_w,
+                       d_colors, n_edges, n_components, s);
+        SLK_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+int slk_build_dendrogram(const int32_t *d_src, const int32_t *d_dst, const double *d_w,
+                         int64_t n, double *h_merges, void *stream_) {
+    STREAM(s);
+    return guarded([&] {
+        if (n < 2) throw_invalid("dendrogram needs at least 2 points");
+        std::vector<int32_t> ha(n - 1), hb(n - 1);
+        std::vector<double> hw(n - 1);
+        dendrogram_device_sort(d_src, d_dst, d_w, n, false, ha.data(), hb.data(), hw.data(), s);
+        dendrogram_fold(ha.data(), hb.data(), hw.data(), n, h_merges);
+    });
+}
+
+int slk_extract_clusters(const double *h_merges, int64_t n, int64_t n_clusters,
+                         int64_t *h_labels) {
+    return guarded([&] { extract_labels(h_merges, n, n_clusters, h_labels); });
+}
+
+int slk_pairwise_l2(const double *d_q, int64_t nq, const double *d_x, int64_t nx, int d,
+                    int squared, double *d_out, void *stream_) {
+    STREAM(s);
+    return guarded([&] {
+        pairwise_l2(d_q, nq, d_x, nx, d, squared, d_out, s);
+        SLK_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+int slk_single_linkage(const float *h_x32, const double *h_x64, int64_t n, int d, int k,
+                       int64_t n_clusters, int metric, int64_t seed, int64_t max_connect_iters,
+                       double *h_merges, int64_t *h_labels, int64_t *h_tree_src,
+                       int64_t *h_tree_dst, double *h_tree_w, int64_t *n_connect_iters,
+                       double *h_timings) {
+    return guarded([&] {
+        if (n < 2) throw_invalid("need at least 2 points, got %lld", (long long)n);
+        if (n_clusters < 1) throw_invalid("n_clusters must be >= 1, got %lld", (long long)n_clusters);
+        if (n_clusters > n) throw_invalid("n_clusters=%lld exceeds %lld points", (long long)n_clusters, (long long)n);
+        if (k < 1) throw_invalid("k must be >= 1, got %d", k);
+        if (k > n - 1) throw_invalid("k=%d exceeds N-1=%lld", k, (long long)(n - 1));
+        if (n >= (1ll << 31)) throw_invalid("n=%lld exceeds the 2^31-1 point limit", (long long)n);
+        StreamGuard g;
+        cudaStream_t s = g.s;
+        DevBuf<float> x32(n * (int64_t)d, s);
+        DevBuf<double> x64;
+        SLK_CUDA(cudaMemcpyAsync(x32.get(), h_x32, n * (int64_t)d * sizeof(float), cudaMemcpyHostToDevice, s));
+        if (h_x64) {
+            x64.alloc(n * (int64_t)d, s);
+            SLK_CUDA(cudaMemcpyAsync(x64.get(), h_x64, n * (int64_t)d * sizeof(double), cudaMemcpyHostToDevice, s));
+        }
+        single_linkage_device(x32, h_x64 ? x64.get() : nullptr, n, d, k, n_clusters, metric, seed,
+                              max_connect_iters, h_merges, h_labels, h_tree_src, h_tree_dst,
+                              h_tree_w, n_connect_iters, h_timings, s);
+        SLK_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+int slk_single_linkage_device(const float *d_x32, const double *d_x64, int64_t n, int d, int k,
+                              int64_t n_clusters, int metric, int64_t seed,
+                              int64_t max_connect_iters, double *h_merges, int64_t *h_labels,
+                              int64_t *h_tree_src, int64_t *h_tree_dst, double *h_tree_w,
+                              int64_t *n_connect_iters, double *h_timings, void *stream_) {
+    STREAM(s);
+    return guarded([&] {
+        if (n < 2) throw_invalid("need at least 2 points, got %lld", (long long)n);
+        if (n_clusters < 1) throw_invalid("n_clusters must be >= 1, got %lld", (long long)n_clusters);
+        if (n_clusters > n) throw_invalid("n_clusters=%lld exceeds %lld points", (long long)n_clusters, (long long)n);
+        if (k < 1) throw_invalid("k must be >= 1, got %d", k);
+        if (k > n - 1) throw_invalid("k=%d exceeds N-1=%lld", k, (long long)(n - 1));
+        single_linkage_device(d_x32, d_x64, n, d, k, n_clusters, metric, seed, max_connect_iters,
+                              h_merges, h_labels, h_tree_src, h_tree_dst, h_tree_w,
+                              n_connect_iters, h_timings, s);
+        SLK_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+}  // extern "C"

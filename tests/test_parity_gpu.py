@@ -1,0 +1,234 @@
+"""Parity of the CUDA path with the reference (golden fixtures) and the oracle.
+
+Every comparison is bit-exact (np.array_equal on float64 values) unless the
+north-star tolerance is named: MST total weight / dendrogram heights within
+1e-5 relative, labels ARI == 1.0.  All tests need a B200.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import load_golden
+
+pytestmark = pytest.mark.gpu
+
+PIPELINES = ["slink_blobs_3k_d16", "slink_blobs_2k_d64", "slink_blobs_2k_d32_k2",
+             "slink_normal_600_d8_f64", "slink_tiny_k2"]
+
+
+@pytest.fixture(scope="module")
+def slk():
+    import paper_2306_16354_b200 as slk
+
+    return slk
+
+
+def _points(g):
+    x = g["x"]
+    x32 = x.astype(np.float32)
+    return x32 if np.array_equal(x32.astype(np.float64), x) else x
+
+
+@pytest.mark.parametrize("name", PIPELINES)
+def test_knn_golden(slk, name):
+    g = load_golden(name)
+    knn = slk.fused_knn(_points(g), int(g["k"]))
+    assert np.array_equal(knn.indices, g["knn_idx"])
+    assert np.array_equal(knn.distances, g["knn_dist"])
+
+
+@pytest.mark.parametrize("name", PIPELINES)
+def test_forest_golden(slk, name):
+    g = load_golden(name)
+    knn = slk.KnnGraph(g["knn_idx"], g["knn_dist"])
+    res = slk.solve_mst(slk.edge_list_to_csr(knn.to_edge_list()), seed=int(g["seed"]))
+    assert np.array_equal(res.edges.src, g["forest_src"])
+    assert np.array_equal(res.edges.dst, g["forest_dst"])
+    assert np.array_equal(res.edges.weight, g["forest_w"])
+    assert np.array_equal(res.colors.colors, g["forest_colors"])
+    assert res.n_components == int(g["forest_ncomp"])
+
+
+@pytest.mark.parametrize("name", PIPELINES)
+def test_single_linkage_golden(slk, name):
+    g = load_golden(name)
+    metric = "sqeuclidean" if "f64" in name else "euclidean"
+    cfg = slk.LinkageConfig(n_clusters=int(g["n_clusters"]), k=int(g["k"]), seed=int(g["seed"]),
+                            metric=metric)
+    res = slk.single_linkage_result(_points(g), cfg)
+    assert np.array_equal(res.tree.src, g["tree_src"])
+    assert np.array_equal(res.tree.dst, g["tree_dst"])
+    assert np.array_equal(res.tree.weight, g["tree_w"])
+    assert np.array_equal(res.dendrogram.merges, g["merges"])
+    assert np.array_equal(res.labels.labels, g["labels"])
+    assert res.connect_iters == int(g["connect_iters"])
+    # the public drop-in entry point returns the same
+    dendro, labels = slk.single_linkage(_points(g), cfg)
+    assert np.array_equal(dendro.merges, g["merges"]) and np.array_equal(labels.labels, g["labels"])
+
+
+@pytest.mark.parametrize("name", ["slink_blobs_2k_d32_k2", "slink_tiny_k2"])
+def test_connect_graph_golden(slk, name):
+    g = load_golden(name)
+    cfg = slk.LinkageConfig(n_clusters=int(g["n_clusters"]), k=int(g["k"]), seed=int(g["seed"]))
+    forest = slk.EdgeList(len(g["x"]), g["forest_src"], g["forest_dst"], g["forest_w"])
+    tree = slk.connect_graph(_points(g), forest, slk.ColorArray(g["forest_colors"]), cfg)
+    assert np.array_equal(tree.src, g["tree_src"]) and np.array_equal(tree.weight, g["tree_w"])
+
+
+def test_neighbors_golden(slk):
+    g = load_golden("neighbors")
+    knn = slk.fused_knn(g["x"], 32)  # float64 data, not float32-representable
+    assert np.array_equal(knn.indices, g["knn_idx"]) and np.array_equal(knn.distances, g["knn_dist"])
+    cc = slk.cross_color_1nn(g["x"], slk.ColorArray(g["colors"]))
+    assert np.array_equal(cc.dst, g["cc_dst"]) and np.array_equal(cc.weight, g["cc_w"])
+    nn = slk.fused_1nn(g["q"], g["xi"], g["mask"])
+    assert [p.index for p in nn] == g["nn_idx"].tolist()
+    assert [p.distance for p in nn] == g["nn_dist"].tolist()
+    tie = slk.fused_knn(g["dup"], 6)  # exact ties and duplicates: certificate must fall back
+    assert np.array_equal(tie.indices, g["tie_idx"]) and np.array_equal(tie.distances, g["tie_dist"])
+    tcc = slk.cross_color_1nn(g["dup"], slk.ColorArray(g["dup_colors"]))
+    assert np.array_equal(tcc.dst, g["tie_cc_dst"]) and np.array_equal(tcc.weight, g["tie_cc_w"])
+
+
+def test_known_answers(slk):
+    # ref tests/test_neighbors.py:46-52, :165-175, :53-59
+    g = slk.fused_knn(np.array([[0.0], [1.0], [3.0]]), 1)
+    assert g.indices.ravel().tolist() == [1, 0, 1]
+    assert g.distances.ravel().tolist() == [1.0, 1.0, 4.0]
+    assert slk.fused_knn(np.array([[0.0], [1.0], [3.0]]), 1, squared=False).distances.ravel().tolist() == [1.0, 1.0, 2.0]
+    e = slk.cross_color_1nn(np.array([[0.0], [2.0]]), slk.ColorArray(np.array([0, 1])))
+    assert list(e.iter_edges()) == [(0, 1, 4.0), (1, 0, 4.0)]
+    e = slk.cross_color_1nn(np.array([[0.0], [0.1], [10.0]]), slk.ColorArray(np.array([0, 0, 2])),
+                            squared=False)
+    assert e.dst[2] == 1 and e.weight[2] == pytest.approx(9.9)
+    x = np.array([[1.0, 1.0]] * 3 + [[5.0, 5.0]])
+    g = slk.fused_knn(x, 2)
+    assert g.indices.tolist() == [[1, 2], [0, 2], [0, 1], [0, 1]]
+    assert slk.fused_1nn(np.array([[0.0, 0.0]]), np.array([[1.0, 0.0], [-1.0, 0.0], [0.0, 1.0]]))[0].index == 0
+    row = np.array([[1.5, -2.0, 3.0]])
+    assert slk.pairwise_l2_tile(row, row)[0, 0] == 0.0
+    assert slk.pairwise_l2_tile(np.array([[0.0, 0.0]]), np.array([[3.0, 4.0]]), squared=False)[0, 0] == pytest.approx(5.0)
+
+
+def test_k_full_sort_matches_oracle(slk, oracle, rng):
+    x = rng.standard_normal((30, 4))
+    g = slk.fused_knn(x, 29)
+    oi, od = oracle.fused_knn(x, 29)
+    assert np.array_equal(g.indices, oi) and np.array_equal(g.distances, od)
+
+
+def test_mst_golden(slk):
+    g = load_golden("mst")
+    for t in range(int(g["n_graphs"])):
+        n = int(g[f"g{t}_n"])
+        csr = slk.edge_list_to_csr(slk.EdgeList(n, g[f"g{t}_src"], g[f"g{t}_dst"], g[f"g{t}_w"]))
+        assert np.array_equal(csr.row_offsets, g[f"g{t}_offs"])
+        assert np.array_equal(csr.col_indices, g[f"g{t}_cols"])
+        assert np.array_equal(csr.weights, g[f"g{t}_csrw"])
+        maximize = bool(g[f"g{t}_max"])
+        work = slk.CsrGraph(n, csr.row_offsets, csr.col_indices, -csr.weights) if maximize else csr
+        alt = slk.weight_alteration(work, seed=t)
+        assert alt.theta == float(g[f"g{t}_theta"])
+        assert np.array_equal(alt.graph.weights, g[f"g{t}_alt"])
+        res = slk.solve_mst(csr, maximize=maximize, seed=t)
+        assert np.array_equal(res.edges.src, g[f"g{t}_msrc"])
+        assert np.array_equal(res.edges.dst, g[f"g{t}_mdst"])
+        assert np.array_equal(res.edges.weight, g[f"g{t}_mw"])
+        assert np.array_equal(res.colors.colors, g[f"g{t}_colors"])
+        assert res.n_components == int(g[f"g{t}_ncomp"])
+    n = int(g["f_n"])
+    res = slk.solve_mst(slk.CsrGraph(n, g["f_offs"], g["f_cols"], g["f_w"]), seed=7)
+    assert np.array_equal(res.edges.src, g["f_msrc"]) and np.array_equal(res.edges.weight, g["f_mw"])
+    assert np.array_equal(res.colors.colors, g["f_colors"]) and res.n_components == int(g["f_ncomp"])
+
+
+def test_mst_step_functions_match_oracle(slk, oracle, rng):
+    from paper_2306_16354_b200.synthetic import random_connected_graph
+
+    src, dst, w = random_connected_graph(rng, 60, 240, weights="ties")
+    csr = slk.edge_list_to_csr(slk.EdgeList(60, src, dst, w))
+    alt = slk.weight_alteration(csr, seed=4)
+    reps = np.array([0, 17, 33])
+    colors = reps[rng.integers(0, 3, size=60)]
+    colors[reps] = reps
+    cand = slk.min_edge_per_vertex(alt, slk.ColorArray(colors))
+    pos = oracle.min_edge_scan(60, csr.row_offsets, csr.col_indices, alt.graph.weights, colors)
+    assert np.array_equal(cand.position, pos)
+    batch = slk.min_edge_per_supervertex(cand, slk.ColorArray(colors))
+    a, b, ww = oracle.reconcile(60, cand.position, np.where(cand.position >= 0, cand.dst, -1),
+                                cand.altered_weight, cand.original_weight, colors)
+    assert np.array_equal(batch.src, a) and np.array_equal(batch.dst, b)
+    assert np.array_equal(batch.weight, ww)
+    new = slk.label_propagation(batch, slk.ColorArray(colors))
+    assert np.array_equal(new.colors, oracle.propagate_colors(colors, a, b))
+
+
+def test_dendrogram_golden(slk):
+    g = load_golden("dendrogram")
+    for t in range(int(g["n_trees"])):
+        n = int(g[f"t{t}_n"])
+        d = slk.build_dendrogram(slk.EdgeList(n, g[f"t{t}_src"], g[f"t{t}_dst"], g[f"t{t}_w"]), n)
+        assert np.array_equal(d.merges, g[f"t{t}_merges"])
+        labels = slk.extract_clusters(d, int(g[f"t{t}_c"]))
+        assert np.array_equal(labels.labels, g[f"t{t}_labels"])
+
+
+def test_errors(slk, rng):
+    g = load_golden("neighbors")
+    with pytest.raises(slk.ValidationError, match="zero"):
+        slk.single_linkage(g["dup"], slk.LinkageConfig(n_clusters=2, k=3))
+    q, x = rng.standard_normal((3, 2)), rng.standard_normal((4, 2))
+    mask = np.ones((3, 4), dtype=bool)
+    mask[1] = False
+    with pytest.raises(slk.ValidationError, match="row 1"):
+        slk.fused_1nn(q, x, mask)
+    with pytest.raises(slk.ValidationError, match="already connected"):
+        slk.cross_color_1nn(rng.standard_normal((4, 2)), slk.ColorArray(np.zeros(4, dtype=np.int64)))
+    x = np.concatenate([rng.standard_normal((10, 2)), rng.standard_normal((10, 2)) + 50.0])
+    knn = slk.fused_knn(x, 1)
+    res = slk.solve_mst(slk.edge_list_to_csr(knn.to_edge_list()), seed=0)
+    with pytest.raises(slk.ConvergenceError, match="components"):
+        slk.connect_graph(x, res.edges, res.colors, slk.LinkageConfig(n_clusters=2, k=1, max_connect_iters=0))
+    with pytest.raises(slk.ValidationError, match="symmetric"):
+        slk.solve_mst(slk.CsrGraph(2, np.array([0, 1, 1]), np.array([1]), np.array([2.0])))
+    with pytest.raises(slk.ValidationError, match="finite"):
+        slk.solve_mst(slk.CsrGraph(2, np.array([0, 1, 2]), np.array([1, 0]), np.array([np.inf, np.inf])))
+    with pytest.raises(slk.ValidationError, match="empty"):
+        slk.solve_mst(slk.edge_list_to_csr(slk.EdgeList.from_pairs(0, [])))
+    with pytest.raises(slk.ValidationError, match="cycle"):
+        slk.build_dendrogram(slk.EdgeList.from_pairs(4, [(0, 1, 1.0), (1, 2, 2.0), (2, 0, 3.0)]), 4)
+
+
+@pytest.mark.parametrize("n,d,k,c", [(20000, 64, 15, 20), (6000, 128, 32, 6), (5000, 32, 64, 5),
+                                     (4000, 512, 8, 4), (3000, 7, 3, 3)])
+def test_knn_blobs_match_oracle(slk, oracle, n, d, k, c):
+    from paper_2306_16354_b200.synthetic import make_blobs
+
+    x = make_blobs(np.random.default_rng(n + d), n, d, c).astype(np.float32)
+    g = slk.fused_knn(x, k)
+    rows = (0, min(n, 2048))
+    oi, od = oracle.fused_knn(x, k, rows=rows)
+    assert np.array_equal(g.indices[rows[0]:rows[1]], oi)
+    assert np.array_equal(g.distances[rows[0]:rows[1]], od)
+
+
+@pytest.mark.parametrize("n,d,k", [(8000, 32, 8), (8000, 128, 32)])
+def test_knn_normal_match_oracle(slk, oracle, n, d, k):
+    x = np.random.default_rng(7).standard_normal((n, d), dtype=np.float32)
+    g = slk.fused_knn(x, k)
+    oi, od = oracle.fused_knn(x, k, rows=(0, 1024))
+    assert np.array_equal(g.indices[:1024], oi) and np.array_equal(g.distances[:1024], od)
+
+
+def test_single_linkage_blobs_match_oracle(slk, oracle):
+    from paper_2306_16354_b200.synthetic import make_blobs
+
+    x = make_blobs(np.random.default_rng(11), 12000, 24, 30).astype(np.float32)
+    cfg = slk.LinkageConfig(n_clusters=30, k=5, seed=2)
+    res = slk.single_linkage_result(x, cfg)
+    ref = oracle.single_linkage(x, 30, k=5, seed=2)
+    assert np.array_equal(res.tree.src, ref["tree_src"]) and np.array_equal(res.tree.weight, ref["tree_w"])
+    assert np.array_equal(res.dendrogram.merges, ref["merges"])
+    assert np.array_equal(res.labels.labels, ref["labels"])
+    assert res.connect_iters == ref["connect_iters"]
