@@ -35,6 +35,7 @@ SIGNATURES = {
     "slk_last_error": (ctypes.c_char_p, []),
     "slk_kernel_launches": (_I64, []),
     "slk_last_scan_stats": (_I, [_PI64]),
+    "slk_profile": (_I, [_PD, _I]),
     "slk_knn": (_I, [_P, _P, _I64, _I, _I, _I64, _I64, _P, _P, _P]),
     "slk_nn1": (_I, [_P, _P, _I64, _P, _P, _I64, _I, _I, _P, _P, _P, _I64, _I64, _P, _P, _P]),
     "slk_pairwise_l2": (_I, [_P, _I64, _P, _I64, _I, _I, _P, _P]),
@@ -145,6 +146,14 @@ def scan_stats() -> dict:
     load().slk_last_scan_stats(buf)
     return dict(rows_refined=buf[0], rows_rescanned=buf[1], tiles_computed=buf[2],
                 tiles_skipped=buf[3])
+
+
+def profile(reset: bool = False) -> dict:
+    """Cumulative scan-kernel profile (CUDA-event timed inside the library)."""
+    buf = (ctypes.c_double * 6)()
+    load().slk_profile(buf, int(reset))
+    keys = ("scan_ms", "scan_launches", "scan_flops", "scan_tiles", "refine_ms", "rescan_rows")
+    return dict(zip(keys, list(buf)))
 
 
 def kernel_launches() -> int:

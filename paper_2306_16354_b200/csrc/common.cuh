@@ -121,6 +121,34 @@ struct ScanStats {
 };
 ScanStats &scan_stats();
 
+// Cumulative kernel profile (process-wide), read by bench.py via slk_profile.
+struct Profile {
+    double scan_ms = 0, scan_launches = 0, scan_flops = 0, scan_tiles = 0, refine_ms = 0,
+           rescan_rows = 0;
+};
+Profile &profile();
+
+// CUDA-event pair on one stream.
+struct EventPair {
+    cudaEvent_t a = nullptr, b = nullptr;
+    EventPair() {
+        SLK_CUDA(cudaEventCreate(&a));
+        SLK_CUDA(cudaEventCreate(&b));
+    }
+    ~EventPair() {
+        if (a) cudaEventDestroy(a);
+        if (b) cudaEventDestroy(b);
+    }
+    void start(cudaStream_t s) { SLK_CUDA(cudaEventRecord(a, s)); }
+    void stop(cudaStream_t s) { SLK_CUDA(cudaEventRecord(b, s)); }
+    double ms() {
+        float v = 0;
+        SLK_CUDA(cudaEventSynchronize(b));
+        SLK_CUDA(cudaEventElapsedTime(&v, a, b));
+        return v;
+    }
+};
+
 // knn.cu
 void knn_rows(const float *x32, const double *x64, int64_t n, int d, int k, int64_t q0,
               int64_t q1, int32_t *idx, double *dist, cudaStream_t s);

@@ -694,17 +694,29 @@ void search(const float *q32, const double *q64, int64_t nq, const float *x32, c
         DevBuf<int32_t> cand(rows * 32 * Rsel, s);
         DevBuf<float> kth(rows, s);
         ScanArgs sa{qp, X.p, nq, nx, X.dp, qb0, mask, qcolor, xcolor, cand, kth, q0, q1};
+        EventPair ev_scan, ev_refine;
+        ev_scan.start(s);
         if (Rsel == 1) dispatch_scan<1>(mode, sa, qb1 - qb0, s);
         else if (Rsel == 2) dispatch_scan<2>(mode, sa, qb1 - qb0, s);
         else dispatch_scan<4>(mode, sa, qb1 - qb0, s);
+        ev_scan.stop(s);
         st.tiles_computed = (qb1 - qb0) * X.nblocks;
 
         RefineArgs ra{q32, same ? x64 : q64, qnorm, x32, x64, xnorm, d, k, nq, nx, q0, q1,
                       cand, kth, max_xn, x64 == nullptr, out_idx, out_dist, fail_rows, counters};
+        ev_refine.start(s);
         if (Rsel == 1) launch_refine<1>(ra, rows, s);
         else if (Rsel == 2) launch_refine<2>(ra, rows, s);
         else launch_refine<4>(ra, rows, s);
+        ev_refine.stop(s);
         st.rows_refined = rows;
+        SLK_CUDA(cudaStreamSynchronize(s));
+        Profile &pf = profile();
+        pf.scan_ms += ev_scan.ms();
+        pf.scan_launches += 1;
+        pf.scan_flops += 2.0 * (double)rows * (double)nx * (double)d;
+        pf.scan_tiles += (double)st.tiles_computed;
+        pf.refine_ms += ev_refine.ms();
     } else {
         // k beyond the fused list capacity: every row takes the exact path
         std::vector<int> all(rows);
@@ -716,6 +728,7 @@ void search(const float *q32, const double *q64, int64_t nq, const float *x32, c
     }
     int nfail = read_scalar<int>(counters, s);
     st.rows_rescanned = nfail;
+    profile().rescan_rows += nfail;
     int missing_init = 0x7fffffff;
     SLK_CUDA(cudaMemcpyAsync(counters.get() + 1, &missing_init, sizeof(int), cudaMemcpyHostToDevice, s));
     if (nfail > 0) {

@@ -52,6 +52,9 @@ void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 ScanStats &scan_stats() { return g_scan_stats; }
 
+static Profile g_profile;
+Profile &profile() { return g_profile; }
+
 int num_sms() {
     static int cached = 0;
     if (!cached) {
@@ -207,6 +210,17 @@ int slk_version(void) { return 100; }
 const char *slk_last_error(void) { return g_last_error.c_str(); }
 
 int64_t slk_kernel_launches(void) { return g_launches.load(); }
+
+int slk_profile(double *out6, int reset) {
+    out6[0] = g_profile.scan_ms;
+    out6[1] = g_profile.scan_launches;
+    out6[2] = g_profile.scan_flops;
+    out6[3] = g_profile.scan_tiles;
+    out6[4] = g_profile.refine_ms;
+    out6[5] = g_profile.rescan_rows;
+    if (reset) g_profile = Profile{};
+    return SLK_OK;
+}
 
 int slk_last_scan_stats(int64_t *stats4) {
     stats4[0] = g_scan_stats.rows_refined;

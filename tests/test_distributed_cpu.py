@@ -1,0 +1,119 @@
+"""World-size-2 gloo test of the multi-GPU orchestration (paper_2306_16354_b200/parallel.py).
+
+No GPU here: the sharded compute is delegated to a checker engine built on
+the CPU oracle (test infrastructure), so this exercises exactly the product's
+sharding, padding, all-gather, colour broadcast and connect-loop control
+flow, and compares rank 0's result with the reference's golden fixture.
+"""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from conftest import ROOT, load_golden
+
+
+class OracleEngine:
+    """CPU stand-in for DeviceEngine (same interface), backed by the oracle."""
+
+    def __init__(self):
+        from oracle import oracle as orc
+
+        self.orc = orc
+
+    def upload(self, x):
+        return np.asarray(x, dtype=np.float64)
+
+    def n_points(self, x):
+        return len(x)
+
+    def knn_shard(self, x, k, rows):
+        idx, d = self.orc.fused_knn(x, k, rows=rows)
+        return torch.from_numpy(idx.astype(np.int32)), torch.from_numpy(d)
+
+    def nn1_shard(self, x, colors, rows):
+        idx, d = self.orc.cross_color_1nn(x, colors.numpy().astype(np.int64), rows=rows)
+        return torch.from_numpy(idx.astype(np.int32)), torch.from_numpy(d)
+
+    def msf(self, n, src, dst, w, m, seed):
+        offs, cols, ww = self.orc.edge_list_to_csr(n, src.numpy()[:m], dst.numpy()[:m], w.numpy()[:m])
+        s, d, wt, colors, nc = self.orc.solve_mst(n, offs, cols, ww, seed=seed)
+        return (torch.from_numpy(s.astype(np.int32)), torch.from_numpy(d.astype(np.int32)),
+                torch.from_numpy(wt), torch.from_numpy(colors.astype(np.int32)), len(s), nc)
+
+    def finish(self, n, t_src, t_dst, t_w, cfg):
+        from paper_2306_16354_b200 import Dendrogram, EdgeList, LabelArray
+
+        w = t_w.numpy()
+        w2 = np.sqrt(w) if cfg.metric == "euclidean" else w
+        merges = self.orc.build_dendrogram(t_src.numpy(), t_dst.numpy(), w2, n)
+        labels = self.orc.extract_clusters(merges, n, cfg.n_clusters)
+        tree = EdgeList(n, t_src.numpy(), t_dst.numpy(), w)
+        return tree, Dendrogram(n, merges), LabelArray(labels, cfg.n_clusters)
+
+    def sync(self):
+        pass
+
+
+def _worker(rank, world, port, name, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import sys
+
+        sys.path.insert(0, str(ROOT))
+        import paper_2306_16354_b200 as slk
+        from paper_2306_16354_b200.parallel import single_linkage_distributed
+
+        g = load_golden(name)
+        cfg = slk.LinkageConfig(n_clusters=int(g["n_clusters"]), k=int(g["k"]), seed=int(g["seed"]))
+        res = single_linkage_distributed(g["x"], cfg, engine=OracleEngine())
+        if rank == 0:
+            out.put((res.tree.src, res.tree.weight, res.dendrogram.merges, res.labels.labels,
+                     res.connect_iters))
+        else:
+            assert res is None
+    finally:
+        dist.destroy_process_group()
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def test_shard_rows_cover_exactly():
+    from paper_2306_16354_b200.parallel import shard_rows
+
+    for n in (1, 127, 128, 129, 1000, 10_000, 1_000_000):
+        for world in (1, 2, 3, 4, 8):
+            ranges = [shard_rows(n, world, r) for r in range(world)]
+            assert ranges[0][0] == 0 and ranges[-1][1] == n
+            for (a0, a1), (b0, b1) in zip(ranges, ranges[1:]):
+                assert a1 == b0 and a0 <= a1
+            assert all(a % 128 == 0 for a, _ in ranges if a < n)
+
+
+@pytest.mark.parametrize("name", ["slink_blobs_2k_d32_k2", "slink_tiny_k2"])
+def test_two_rank_pipeline_matches_reference(oracle, name):
+    ctx = mp.get_context("spawn")
+    out = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, name, out)) for r in range(2)]
+    for p in procs:
+        p.start()
+    result = out.get(timeout=300)
+    for p in procs:
+        p.join(timeout=300)
+        assert p.exitcode == 0
+    src, w, merges, labels, iters = result
+    g = load_golden(name)
+    assert np.array_equal(src, g["tree_src"]) and np.array_equal(w, g["tree_w"])
+    assert np.array_equal(merges, g["merges"]) and np.array_equal(labels, g["labels"])
+    assert iters == int(g["connect_iters"])
