@@ -276,7 +276,8 @@ def run_gpu(args, c, cfg_name):
         return
     clocks = clk.summary()
     sm_mhz = clocks["sm_mhz"] or 1965.0
-    achieved = prof["scan_flops"] / (prof["scan_ms"] / 1e3) / 1e12 if prof["scan_ms"] else None
+    # achieved: FLOP of the tiles the kernel actually computed (pruned tiles excluded)
+    achieved = prof["scan_flops_done"] / (prof["scan_ms"] / 1e3) / 1e12 if prof["scan_ms"] else None
     peak = SM_COUNT * FP32_LANES * 2 * sm_mhz * 1e6 / 1e12
     traffic = load_traffic()
     roofline = {
@@ -287,7 +288,10 @@ def run_gpu(args, c, cfg_name):
         "peak_note": (f"FP32 FFMA peak 148 SM x 128 lanes x 2 x {sm_mhz:.0f} MHz (median SM clock "
                       "under load); MEASURED_PEAKS.json has no FP32 figure. The direct form "
                       "sum((q-x)^2) issues 2 FP32 ops per 2 algorithmic FLOP, so 0.5 is its ceiling."),
-        "algorithmic_flop_per_step": prof["scan_flops"] / max(args.steps, 1),
+        "algorithmic_flop_per_step": prof["scan_flops_done"] / max(args.steps, 1),
+        "brute_force_flop_per_step": prof["scan_flops"] / max(args.steps, 1),
+        "tiles_computed_frac": prof["scan_tiles"] / max(prof["scan_tiles_total"], 1),
+        "visit_order_ms_per_step": prof["order_ms"] / max(args.steps, 1),
         "scan_ms_per_step": prof["scan_ms"] / max(args.steps, 1),
         "scan_launches_per_step": prof["scan_launches"] / max(args.steps, 1),
         "rows_rescanned_per_step": prof["rescan_rows"] / max(args.steps, 1),

@@ -199,12 +199,15 @@ int slk_msf_edges(int64_t n, const int32_t *d_src, const int32_t *d_dst, const d
  * re-scanned exactly, [2] index tiles computed, [3] index tiles skipped. */
 int slk_last_scan_stats(int64_t *stats4);
 
-/* Process-wide kernel profile since the last reset: out6[0] distance-scan
+/* Process-wide kernel profile since the last reset: out[0] distance-scan
  * kernel milliseconds (CUDA events on the launching stream), [1] scan
- * launches, [2] algorithmic FLOP of those launches (2 * rows * n_index * d),
- * [3] 128x128 tiles computed, [4] refine-kernel milliseconds, [5] rows
- * re-scanned exactly.  reset != 0 zeroes the counters after reading. */
-int slk_profile(double *out6, int reset);
+ * launches, [2] algorithmic FLOP of those launches (2 * rows * n_index * d,
+ * brute force), [3] 128x128 tiles computed, [4] refine-kernel milliseconds,
+ * [5] rows re-scanned exactly, [6] visit-order (bounds + segmented sort)
+ * milliseconds, [7] FLOP of the tiles actually computed (2*128*128*d each),
+ * [8] tiles a brute-force scan would compute.  reset != 0 zeroes the counters
+ * after reading.  out must hold 9 doubles. */
+int slk_profile(double *out, int reset);
 
 #ifdef __cplusplus
 }

@@ -150,9 +150,10 @@ def scan_stats() -> dict:
 
 def profile(reset: bool = False) -> dict:
     """Cumulative scan-kernel profile (CUDA-event timed inside the library)."""
-    buf = (ctypes.c_double * 6)()
+    buf = (ctypes.c_double * 9)()
     load().slk_profile(buf, int(reset))
-    keys = ("scan_ms", "scan_launches", "scan_flops", "scan_tiles", "refine_ms", "rescan_rows")
+    keys = ("scan_ms", "scan_launches", "scan_flops", "scan_tiles", "refine_ms", "rescan_rows",
+            "order_ms", "scan_flops_done", "scan_tiles_total")
     return dict(zip(keys, list(buf)))
 
 

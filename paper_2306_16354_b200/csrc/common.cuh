@@ -6,6 +6,7 @@
 #include <stdint.h>
 #include <stdio.h>
 
+#include <memory>
 #include <string>
 
 #include "../../include/slink.h"
@@ -57,6 +58,10 @@ int guarded(F &&body) {
 }
 
 // ------------------------------------------------------- device scratch
+// Keep freed scratch in the device's stream-ordered pool instead of returning
+// it to the driver at every synchronisation (default release threshold 0).
+void ensure_pool();
+
 // Stream-ordered scratch buffer (cudaMallocAsync pool); freed on destruction.
 template <class T>
 struct DevBuf {
@@ -69,7 +74,10 @@ struct DevBuf {
         release();
         stream = s;
         count = n;
-        if (n) SLK_CUDA(cudaMallocAsync((void **)&ptr, n * sizeof(T), s));
+        if (n) {
+            ensure_pool();
+            SLK_CUDA(cudaMallocAsync((void **)&ptr, n * sizeof(T), s));
+        }
     }
     void release() {
         if (ptr) cudaFreeAsync(ptr, stream);
@@ -124,7 +132,7 @@ ScanStats &scan_stats();
 // Cumulative kernel profile (process-wide), read by bench.py via slk_profile.
 struct Profile {
     double scan_ms = 0, scan_launches = 0, scan_flops = 0, scan_tiles = 0, refine_ms = 0,
-           rescan_rows = 0;
+           rescan_rows = 0, order_ms = 0, scan_flops_done = 0, scan_tiles_total = 0;
 };
 Profile &profile();
 
@@ -150,6 +158,23 @@ struct EventPair {
 };
 
 // knn.cu
+// A point matrix prepared for the scans: dims-major 128-point blocks, fp64
+// norms (reference order), max norm, and per-block bounding spheres.
+struct PointSet {
+    const float *x32 = nullptr;
+    const double *x64 = nullptr;
+    int64_t n = 0, nb = 0, nsb = 0;
+    int d = 0, dp = 0;
+    DevBuf<float> packed, centroid, radius, sb_centroid, sb_radius;
+    DevBuf<double> norms, maxn;
+};
+std::shared_ptr<PointSet> make_pointset(const float *x32, const double *x64, int64_t n, int d,
+                                        cudaStream_t s);
+void knn_ps(const PointSet &X, int k, int64_t q0, int64_t q1, int32_t *idx, double *dist,
+            cudaStream_t s);
+void nn1_ps(const PointSet &Q, const PointSet &X, int mode, const uint8_t *mask,
+            const int32_t *qcolor, const int32_t *xcolor, int64_t q0, int64_t q1, int32_t *idx,
+            double *dist, cudaStream_t s);
 void knn_rows(const float *x32, const double *x64, int64_t n, int d, int k, int64_t q0,
               int64_t q1, int32_t *idx, double *dist, cudaStream_t s);
 void nn1_rows(const float *q32, const double *q64, int64_t nq, const float *x32,

@@ -26,7 +26,10 @@
 #include <math.h>
 #include <stdint.h>
 
+#include <cub/cub.cuh>
+
 #include <algorithm>
+#include <memory>
 #include <vector>
 
 #include "common.cuh"
@@ -203,6 +206,53 @@ struct ScanArgs {
     float *kth;        // [nq_rows_launch] approx K'-th value
     int64_t row0;      // global row of cand[0]
     int64_t row1;      // rows [row0, row1) are written
+    // visit order: per query block of the launch, the
+    // superblocks (32 index blocks) sorted by a lower bound on the squared
+    // distance between any of their points and any query point of the block,
+    // plus the per-block bounds; +inf = never admissible (same colour).
+    const int32_t *sb_order;  // [nqb_launch][nsb]
+    const float *sb_lb;       // [nqb_launch][nsb] ascending
+    const float *blk_lb;      // [nqb_launch][nxb]
+    int64_t nsb;
+    unsigned long long *tiles_done;
+};
+
+// Iterates the index blocks a query block must visit: superblocks in
+// ascending bound order, members in index order, skipping every block whose
+// bound exceeds the current threshold; stops at the first superblock whose
+// bound exceeds it (member bounds are >= their superblock's).  Every thread
+// runs it redundantly and gets the same answer (warp-uniform ballots).
+struct BlockVisitor {
+    const int32_t *sb_order;
+    const float *sb_lb;
+    const float *blk_lb;
+    int64_t nsb, nxb;
+    int64_t s = -1, sb = 0;
+    unsigned mask = 0;
+    float my_lb = INFINITY;
+
+    __device__ int64_t next(float thr_max, int lane) {
+        while (true) {
+            if (mask == 0) {
+                if (++s >= nsb) return -1;
+                float l = sb_lb[s];
+                if (l == INFINITY || l > thr_max) {
+                    s = nsb;
+                    return -1;
+                }
+                sb = sb_order[s];
+                int64_t b = sb * 32 + lane;
+                my_lb = b < nxb ? blk_lb[b] : INFINITY;
+                mask = __ballot_sync(0xffffffffu, my_lb != INFINITY && !(my_lb > thr_max));
+                continue;
+            }
+            int m = __ffs(mask) - 1;
+            mask &= mask - 1;
+            float l = __shfl_sync(0xffffffffu, my_lb, m);
+            if (l > thr_max) continue;
+            return sb * 32 + m;
+        }
+    }
 };
 
 __device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
@@ -226,6 +276,7 @@ struct ScanSmem {
     int cnt[BM];
     float thr[BM];
     int qcol[BM];
+    float part[4];
 };
 
 template <int MODE, int R>
@@ -238,7 +289,8 @@ __global__ void __launch_bounds__(NT, (R == 1 ? 2 : 1)) scan_kernel(ScanArgs a) 
     const int64_t row_base = qb * BM;
     const int nkc = a.dp / KC;
     const int64_t nxb = (a.nx + BN - 1) / BN;
-    const int64_t total_steps = nxb * nkc;
+    BlockVisitor vis{a.sb_order + (int64_t)blockIdx.x * a.nsb, a.sb_lb + (int64_t)blockIdx.x * a.nsb,
+                     a.blk_lb + (int64_t)blockIdx.x * nxb, a.nsb, nxb};
 
     for (int e = tid; e < BM * 32 * R; e += NT) {
         (&S.list_v[0][0])[e] = INFINITY;
@@ -252,11 +304,12 @@ __global__ void __launch_bounds__(NT, (R == 1 ? 2 : 1)) scan_kernel(ScanArgs a) 
             S.qcol[r] = gi < a.nq ? a.qcolor[gi] : -1;
         }
     }
+    // largest per-row threshold of the block's valid rows; a block whose
+    // lower bound exceeds it cannot improve any row (thresholds only shrink)
+    float thr_max = INFINITY;
 
     const float *qsrc = a.qp + qb * (int64_t)a.dp * BM;
-    auto load_step = [&](int64_t step, int buf) {
-        int64_t jb = step / nkc;
-        int kc = (int)(step - jb * nkc);
+    auto load_step = [&](int64_t jb, int kc, int buf) {
         const float *qg = qsrc + (int64_t)kc * KC * BM;
         const float *xg = a.xp + (jb * a.dp + (int64_t)kc * KC) * BN;
         // 2 x 8 KB contiguous copies, 16 B per cp.async
@@ -274,14 +327,28 @@ __global__ void __launch_bounds__(NT, (R == 1 ? 2 : 1)) scan_kernel(ScanArgs a) 
 #pragma unroll
         for (int j = 0; j < 8; j++) acc[i][j] = 0.0f;
 
-    load_step(0, 0);
-    cp_async_commit();
+    int kc = 0;
+    int64_t jb = vis.next(thr_max, lane);
+    bool have = jb >= 0;
+    if (have) {
+        load_step(jb, 0, 0);
+        cp_async_commit();
+    }
     __syncthreads();
-
-    for (int64_t step = 0; step < total_steps; step++) {
-        const int buf = (int)(step & 1);
-        if (step + 1 < total_steps) {
-            load_step(step + 1, buf ^ 1);
+    int buf = 0;
+    int64_t computed = 0;
+    while (have) {
+        // ---- decide and prefetch the next (block, chunk) step
+        int64_t njb = jb;
+        int nkc_ = kc + 1;
+        bool has_next = true;
+        if (nkc_ == nkc) {
+            nkc_ = 0;
+            njb = vis.next(thr_max, lane);
+            has_next = njb >= 0;
+        }
+        if (has_next) {
+            load_step(njb, nkc_, buf ^ 1);
             cp_async_commit();
             cp_async_wait<1>();
         } else {
@@ -290,11 +357,11 @@ __global__ void __launch_bounds__(NT, (R == 1 ? 2 : 1)) scan_kernel(ScanArgs a) 
         __syncthreads();
         // ---- direct-form distance micro-tile: acc += (q - x)^2
 #pragma unroll
-        for (int t = 0; t < KC; t++) {
-            float4 qa = *reinterpret_cast<const float4 *>(&S.qs[buf][t][ty * 4]);
-            float4 qb4 = *reinterpret_cast<const float4 *>(&S.qs[buf][t][64 + ty * 4]);
-            float4 xa = *reinterpret_cast<const float4 *>(&S.xs[buf][t][tx * 4]);
-            float4 xb = *reinterpret_cast<const float4 *>(&S.xs[buf][t][64 + tx * 4]);
+        for (int tt = 0; tt < KC; tt++) {
+            float4 qa = *reinterpret_cast<const float4 *>(&S.qs[buf][tt][ty * 4]);
+            float4 qb4 = *reinterpret_cast<const float4 *>(&S.qs[buf][tt][64 + ty * 4]);
+            float4 xa = *reinterpret_cast<const float4 *>(&S.xs[buf][tt][tx * 4]);
+            float4 xb = *reinterpret_cast<const float4 *>(&S.xs[buf][tt][64 + tx * 4]);
             float q[8] = {qa.x, qa.y, qa.z, qa.w, qb4.x, qb4.y, qb4.z, qb4.w};
             float x[8] = {xa.x, xa.y, xa.z, xa.w, xb.x, xb.y, xb.z, xb.w};
 #pragma unroll
@@ -307,95 +374,98 @@ __global__ void __launch_bounds__(NT, (R == 1 ? 2 : 1)) scan_kernel(ScanArgs a) 
         }
         __syncthreads();
 
-        const int64_t jb = step / nkc;
-        if ((int)(step - jb * nkc) != nkc - 1) continue;
-
-        // ---- epilogue for index block jb: threshold filter → candidate buffers
-        uint64_t pending = 0;
-        int64_t gj[8];
-        bool colok[8];
+        if (kc == nkc - 1) {
+            computed++;
+            // ---- epilogue for index block jb: threshold filter → candidate buffers
+            uint64_t pending = 0;
+            const int64_t col0 = jb * BN;
 #pragma unroll
-        for (int j = 0; j < 8; j++) {
-            int c = j < 4 ? tx * 4 + j : 64 + tx * 4 + (j - 4);
-            gj[j] = jb * BN + c;
-            colok[j] = gj[j] < a.nx;
-        }
-        int xc[8];
-        if (MODE == MODE_COLOR) {
-#pragma unroll
-            for (int j = 0; j < 8; j++) xc[j] = colok[j] ? a.xcolor[gj[j]] : -1;
-        }
-#pragma unroll
-        for (int i = 0; i < 8; i++) {
-            int r = i < 4 ? ty * 4 + i : 64 + ty * 4 + (i - 4);
-            int64_t gi = row_base + r;
-            float th = S.thr[r];
-#pragma unroll
-            for (int j = 0; j < 8; j++) {
-                bool ok = colok[j] && gi < a.nq && acc[i][j] < th;
-                if (MODE == MODE_SELF) ok = ok && gj[j] != gi;
-                if (MODE == MODE_COLOR) ok = ok && xc[j] != S.qcol[r];
-                if (MODE == MODE_MASK) ok = ok && a.mask[gi * a.nx + gj[j]] != 0;
-                if (ok) pending |= 1ull << (i * 8 + j);
-            }
-        }
-        // insert loop: push pending candidates; merge buffers; retry overflow
-        while (true) {
-            uint64_t todo = pending;
-            pending = 0;
-            while (todo) {
-                int bit = __ffsll((long long)todo) - 1;
-                todo &= todo - 1;
-                int i = bit >> 3, j = bit & 7;
+            for (int i = 0; i < 8; i++) {
                 int r = i < 4 ? ty * 4 + i : 64 + ty * 4 + (i - 4);
-                float v = acc[i][j];
-                if (!(v < S.thr[r])) continue;
-                int pos = atomicAdd(&S.cnt[r], 1);
-                if (pos < CAP) {
-                    S.buf_v[r][pos] = v;
-                    S.buf_i[r][pos] = (int)gj[j];
-                } else {
-                    pending |= 1ull << bit;
+                int64_t gi = row_base + r;
+                float th = S.thr[r];
+#pragma unroll
+                for (int j = 0; j < 8; j++) {
+                    int64_t gj = col0 + (j < 4 ? tx * 4 + j : 64 + tx * 4 + (j - 4));
+                    bool ok = gj < a.nx && gi < a.nq && acc[i][j] < th;
+                    if (MODE == MODE_SELF) ok = ok && gj != gi;
+                    if (MODE == MODE_COLOR) ok = ok && a.xcolor[gj] != S.qcol[r];
+                    if (MODE == MODE_MASK) ok = ok && a.mask[gi * a.nx + gj] != 0;
+                    if (ok) pending |= 1ull << (i * 8 + j);
                 }
+            }
+            // insert loop: push pending candidates; merge buffers; retry overflow
+            while (true) {
+                uint64_t todo = pending;
+                pending = 0;
+                while (todo) {
+                    int bit = __ffsll((long long)todo) - 1;
+                    todo &= todo - 1;
+                    int i = bit >> 3, j = bit & 7;
+                    int r = i < 4 ? ty * 4 + i : 64 + ty * 4 + (i - 4);
+                    float v = acc[i][j];
+                    if (!(v < S.thr[r])) continue;
+                    int pos = atomicAdd(&S.cnt[r], 1);
+                    if (pos < CAP) {
+                        S.buf_v[r][pos] = v;
+                        S.buf_i[r][pos] = (int)(col0 + (j < 4 ? tx * 4 + j : 64 + tx * 4 + (j - 4)));
+                    } else {
+                        pending |= 1ull << bit;
+                    }
+                }
+                __syncthreads();
+                // merge: warp w owns rows w, w+8, ...
+                for (int r = warp; r < BM; r += NT / 32) {
+                    int c = S.cnt[r];
+                    if (c == 0) continue;
+                    if (c > CAP) c = CAP;
+                    float lv[R];
+                    int li[R];
+#pragma unroll
+                    for (int rr = 0; rr < R; rr++) {
+                        lv[rr] = S.list_v[r][rr * 32 + lane];
+                        li[rr] = S.list_i[r][rr * 32 + lane];
+                    }
+                    for (int q = 0; q < c; q++) {
+                        float v = S.buf_v[r][q];
+                        int id = S.buf_i[r][q];
+                        float tv = __shfl_sync(FULL, lv[R - 1], 31);
+                        int tiid = __shfl_sync(FULL, li[R - 1], 31);
+                        if (pair_gt(tv, tiid, v, id)) warp_list_insert<R>(lv, li, v, id, lane);
+                    }
+#pragma unroll
+                    for (int rr = 0; rr < R; rr++) {
+                        S.list_v[r][rr * 32 + lane] = lv[rr];
+                        S.list_i[r][rr * 32 + lane] = li[rr];
+                    }
+                    float tv = __shfl_sync(FULL, lv[R - 1], 31);
+                    if (lane == 0) {
+                        S.thr[r] = tv;
+                        S.cnt[r] = 0;
+                    }
+                }
+                if (!__syncthreads_or(pending != 0)) break;
+            }
+            // block-wide max threshold over valid rows (pruning bound)
+            if (warp < BM / 32) {
+                int r = warp * 32 + lane;
+                float v = (row_base + r < a.nq) ? S.thr[r] : -INFINITY;
+                for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(FULL, v, o));
+                if (lane == 0) S.part[warp] = v;
             }
             __syncthreads();
-            // merge: warp w owns rows w, w+8, ...
-            for (int r = warp; r < BM; r += NT / 32) {
-                int c = S.cnt[r];
-                if (c == 0) continue;
-                if (c > CAP) c = CAP;
-                float lv[R];
-                int li[R];
+            thr_max = fmaxf(fmaxf(S.part[0], S.part[1]), fmaxf(S.part[2], S.part[3]));
 #pragma unroll
-                for (int rr = 0; rr < R; rr++) {
-                    lv[rr] = S.list_v[r][rr * 32 + lane];
-                    li[rr] = S.list_i[r][rr * 32 + lane];
-                }
-                for (int q = 0; q < c; q++) {
-                    float v = S.buf_v[r][q];
-                    int id = S.buf_i[r][q];
-                    float tv = __shfl_sync(FULL, lv[R - 1], 31);
-                    int tiid = __shfl_sync(FULL, li[R - 1], 31);
-                    if (pair_gt(tv, tiid, v, id)) warp_list_insert<R>(lv, li, v, id, lane);
-                }
+            for (int i = 0; i < 8; i++)
 #pragma unroll
-                for (int rr = 0; rr < R; rr++) {
-                    S.list_v[r][rr * 32 + lane] = lv[rr];
-                    S.list_i[r][rr * 32 + lane] = li[rr];
-                }
-                float tv = __shfl_sync(FULL, lv[R - 1], 31);
-                if (lane == 0) {
-                    S.thr[r] = tv;
-                    S.cnt[r] = 0;
-                }
-            }
-            if (!__syncthreads_or(pending != 0)) break;
+                for (int j = 0; j < 8; j++) acc[i][j] = 0.0f;
         }
-#pragma unroll
-        for (int i = 0; i < 8; i++)
-#pragma unroll
-            for (int j = 0; j < 8; j++) acc[i][j] = 0.0f;
+        if (!has_next) break;
+        jb = njb;
+        kc = nkc_;
+        buf ^= 1;
     }
+    if (tid == 0 && a.tiles_done) atomicAdd(a.tiles_done, (unsigned long long)computed);
 
     // write candidate lists of this CTA's rows
     for (int r = warp; r < BM; r += NT / 32) {
@@ -406,6 +476,159 @@ __global__ void __launch_bounds__(NT, (R == 1 ? 2 : 1)) scan_kernel(ScanArgs a) 
         for (int rr = 0; rr < R; rr++) dst[rr * 32 + lane] = S.list_i[r][rr * 32 + lane];
         if (lane == 0) a.kth[gi - a.row0] = S.list_i[r][32 * R - 1] >= 0 ? S.list_v[r][32 * R - 1] : INFINITY;
     }
+}
+
+// ------------------------------------------------------------ K2 visit order
+// Bounding sphere of each 128-point block (from the float32 operand values):
+// centroid (float, dims-major [dp][nb]) and radius rounded up, computed in
+// float64 so the bound is rigorous for the values the scan sees.
+__global__ void block_sphere_kernel(const float *__restrict__ xp, int64_t n, int d, int dp,
+                                    int64_t nb, float *__restrict__ centroid,
+                                    float *__restrict__ radius) {
+    const int lane = threadIdx.x & 31;
+    const int64_t b = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    if (b >= nb) return;
+    const int cnt = (int)(n - b * BN < BN ? n - b * BN : BN);
+    const float *blk = xp + b * (int64_t)dp * BN;
+    for (int t = 0; t < d; t++) {
+        double s = 0.0;
+        for (int j = lane; j < cnt; j += 32) s += (double)blk[(int64_t)t * BN + j];
+        for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(FULL, s, o);
+        if (lane == 0) centroid[(int64_t)t * nb + b] = (float)(s / cnt);
+    }
+    __syncwarp();
+    double r2 = 0.0;
+    for (int j = lane; j < cnt; j += 32) {
+        double acc = 0.0;
+        for (int t = 0; t < d; t++) {
+            double df = (double)blk[(int64_t)t * BN + j] - (double)centroid[(int64_t)t * nb + b];
+            acc += df * df;
+        }
+        r2 = fmax(r2, acc);
+    }
+    for (int o = 16; o; o >>= 1) r2 = fmax(r2, __shfl_xor_sync(FULL, r2, o));
+    if (lane == 0) radius[b] = (float)(sqrt(r2) * (1.0 + 1e-6)) + 1e-30f;
+}
+
+__global__ void block_color_range_kernel(const int32_t *__restrict__ color, int64_t n, int64_t nb,
+                                         int2 *__restrict__ range) {
+    const int lane = threadIdx.x & 31;
+    const int64_t b = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    if (b >= nb) return;
+    int lo = 0x7fffffff, hi = -1;
+    for (int64_t j = b * BN + lane; j < (n < (b + 1) * BN ? n : (b + 1) * BN); j += 32) {
+        int c = color[j];
+        lo = min(lo, c);
+        hi = max(hi, c);
+    }
+    for (int o = 16; o; o >>= 1) {
+        lo = min(lo, __shfl_xor_sync(FULL, lo, o));
+        hi = max(hi, __shfl_xor_sync(FULL, hi, o));
+    }
+    if (lane == 0) range[b] = make_int2(lo, hi);
+}
+
+// Lower bound on the squared distance between any point of query block q and
+// any point of a sphere (c, r): (|c_q - c| - r_q - r)^2 by the triangle
+// inequality, rounded down.
+__device__ __forceinline__ float sphere_lb(const float *qc, const float *qr, int64_t nqb_total,
+                                           int64_t q, const float *xc, const float *xr,
+                                           int64_t nx_total, int64_t b, int d) {
+    double s = 0.0;
+    for (int t = 0; t < d; t++) {
+        double df = (double)qc[(int64_t)t * nqb_total + q] - (double)xc[(int64_t)t * nx_total + b];
+        s += df * df;
+    }
+    double g = sqrt(s) * (1.0 - 1e-12) - (double)qr[q] - (double)xr[b];
+    return g > 0.0 ? (float)(g * g * (1.0 - 1e-6)) : 0.0f;
+}
+
+__device__ __forceinline__ bool same_colour(const int2 *qcol, const int2 *xcol, int64_t q, int64_t b) {
+    if (!qcol) return false;
+    int2 a = qcol[q], c = xcol[b];
+    return a.x == a.y && c.x == c.y && a.x == c.x;
+}
+
+// per (query block, index block): bound, +inf when every pair is same-coloured
+__global__ void block_lb_kernel(const float *__restrict__ qc, const float *__restrict__ qr,
+                                int64_t nqb_total, const float *__restrict__ xc,
+                                const float *__restrict__ xr, int64_t nxb, int d, int64_t qb0,
+                                int64_t nqb, const int2 *__restrict__ qcol,
+                                const int2 *__restrict__ xcol, float *__restrict__ lb) {
+    const int64_t total = nqb * nxb;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        int64_t ql = e / nxb, b = e - ql * nxb, q = qb0 + ql;
+        lb[e] = same_colour(qcol, xcol, q, b) ? INFINITY
+                                              : sphere_lb(qc, qr, nqb_total, q, xc, xr, nxb, b, d);
+    }
+}
+
+// per (query block, superblock): bound + ids + segment offsets for the sort
+__global__ void superblock_lb_kernel(const float *__restrict__ qc, const float *__restrict__ qr,
+                                     int64_t nqb_total, const float *__restrict__ sc,
+                                     const float *__restrict__ sr, int64_t nsb, int d, int64_t qb0,
+                                     int64_t nqb, const int2 *__restrict__ qcol,
+                                     const int2 *__restrict__ scol, float *__restrict__ lb,
+                                     int32_t *__restrict__ ids, int32_t *__restrict__ seg) {
+    const int64_t total = nqb * nsb;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        int64_t ql = e / nsb, b = e - ql * nsb, q = qb0 + ql;
+        lb[e] = same_colour(qcol, scol, q, b) ? INFINITY
+                                              : sphere_lb(qc, qr, nqb_total, q, sc, sr, nsb, b, d);
+        ids[e] = (int32_t)b;
+        if (b == 0) seg[ql] = (int32_t)(ql * nsb);
+        if (e == total - 1) seg[nqb] = (int32_t)total;
+    }
+}
+
+// Superblock spheres from their (up to 32) member block spheres:
+// centre = mean of member centres, radius = max(|c_sb - c_b| + r_b), rounded up.
+__global__ void superblock_sphere_kernel(const float *__restrict__ bc, const float *__restrict__ br,
+                                         int64_t nb, int d, int64_t nsb, float *__restrict__ sc,
+                                         float *__restrict__ sr) {
+    const int lane = threadIdx.x & 31;
+    const int64_t sb = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    if (sb >= nsb) return;
+    const int64_t b = sb * 32 + lane;
+    const bool valid = b < nb;
+    const int cnt = __popc(__ballot_sync(FULL, valid));
+    for (int t = 0; t < d; t++) {
+        double v = valid ? (double)bc[(int64_t)t * nb + b] : 0.0;
+        for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+        if (lane == 0) sc[(int64_t)t * nsb + sb] = (float)(v / cnt);
+    }
+    __syncwarp();
+    double r = 0.0;
+    if (valid) {
+        double s2 = 0.0;
+        for (int t = 0; t < d; t++) {
+            double df = (double)bc[(int64_t)t * nb + b] - (double)sc[(int64_t)t * nsb + sb];
+            s2 += df * df;
+        }
+        r = sqrt(s2) + (double)br[b];
+    }
+    for (int o = 16; o; o >>= 1) r = fmax(r, __shfl_xor_sync(FULL, r, o));
+    if (lane == 0) sr[sb] = (float)(r * (1.0 + 1e-6)) + 1e-30f;
+}
+
+__global__ void superblock_color_kernel(const int2 *__restrict__ brange, int64_t nb, int64_t nsb,
+                                        int2 *__restrict__ srange) {
+    const int lane = threadIdx.x & 31;
+    const int64_t sb = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    if (sb >= nsb) return;
+    const int64_t b = sb * 32 + lane;
+    int lo = 0x7fffffff, hi = -1;
+    if (b < nb) {
+        lo = brange[b].x;
+        hi = brange[b].y;
+    }
+    for (int o = 16; o; o >>= 1) {
+        lo = min(lo, __shfl_xor_sync(FULL, lo, o));
+        hi = max(hi, __shfl_xor_sync(FULL, hi, o));
+    }
+    if (lane == 0) srange[sb] = make_int2(lo, hi);
 }
 
 // ------------------------------------------------------------------ K3
@@ -599,32 +822,11 @@ __global__ void check_missing_kernel(const int32_t *idx, int64_t rows, int k, in
 }
 
 // ----------------------------------------------------------- host side
-struct Packed {
-    DevBuf<float> p;
-    int dp = 0;
-    int64_t nblocks = 0;
-};
-
-Packed pack(const float *x, int64_t n, int d, cudaStream_t s) {
-    Packed P;
-    P.dp = ((d + KC - 1) / KC) * KC;
-    P.nblocks = (n + BN - 1) / BN;
-    P.p.alloc((size_t)P.nblocks * BN * P.dp, s);
-    int64_t total = P.nblocks * BN * (int64_t)P.dp;
-    pack_blocks_kernel<<<grid_for(total, 256), 256, 0, s>>>(x, n, d, P.dp, P.nblocks, P.p);
-    SLK_CHECK_LAUNCH();
-    return P;
-}
-
 template <int MODE, int R>
 void launch_scan(const ScanArgs &args, int64_t nqb, cudaStream_t s) {
     size_t smem = sizeof(ScanSmem<R>);
-    static bool configured = false;
-    if (!configured) {
-        SLK_CUDA(cudaFuncSetAttribute(scan_kernel<MODE, R>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        configured = true;
-    }
+    SLK_CUDA(cudaFuncSetAttribute(scan_kernel<MODE, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)smem));
     scan_kernel<MODE, R><<<(unsigned)nqb, NT, smem, s>>>(args);
     SLK_CHECK_LAUNCH();
 }
@@ -653,78 +855,115 @@ void launch_exact(const ExactArgs &ea, cudaStream_t s) {
     SLK_CHECK_LAUNCH();
 }
 
-// Full neighbour search for query rows [q0, q1); k results per row.
-void search(const float *q32, const double *q64, int64_t nq, const float *x32, const double *x64,
-            int64_t nx, int d, int k, int mode, const uint8_t *mask, const int32_t *qcolor,
-            const int32_t *xcolor, int64_t q0, int64_t q1, int32_t *out_idx, double *out_dist,
-            cudaStream_t s) {
+// Per query block of [qb0, qb0 + nqb): superblocks sorted by lower bound, and
+// the per-block bounds.
+struct VisitOrder {
+    DevBuf<int32_t> sb_order;
+    DevBuf<float> sb_lb, blk_lb;
+};
+
+VisitOrder visit_order(const PointSet &Q, const PointSet &X, int64_t qb0, int64_t nqb,
+                       const int32_t *qcolor, const int32_t *xcolor, cudaStream_t s) {
+    const int64_t nxb = X.nb, nsb = X.nsb, total = nqb * nxb, stotal = nqb * nsb;
+    if (stotal >= (1ll << 31)) throw_invalid("too many (query block, superblock) pairs: %lld", (long long)stotal);
+    DevBuf<int2> qrange, xrange, srange;
+    if (qcolor) {
+        qrange.alloc(Q.nb, s);
+        xrange.alloc(X.nb, s);
+        srange.alloc(nsb, s);
+        block_color_range_kernel<<<(unsigned)((Q.nb * 32 + 255) / 256), 256, 0, s>>>(qcolor, Q.n, Q.nb, qrange);
+        SLK_CHECK_LAUNCH();
+        block_color_range_kernel<<<(unsigned)((X.nb * 32 + 255) / 256), 256, 0, s>>>(xcolor, X.n, X.nb, xrange);
+        SLK_CHECK_LAUNCH();
+        superblock_color_kernel<<<(unsigned)((nsb * 32 + 255) / 256), 256, 0, s>>>(xrange, X.nb, nsb, srange);
+        SLK_CHECK_LAUNCH();
+    }
+    VisitOrder V;
+    V.blk_lb.alloc(total, s);
+    block_lb_kernel<<<grid_for(total, 256), 256, 0, s>>>(Q.centroid, Q.radius, Q.nb, X.centroid,
+                                                         X.radius, nxb, Q.d, qb0, nqb, qrange.get(),
+                                                         xrange.get(), V.blk_lb);
+    SLK_CHECK_LAUNCH();
+    DevBuf<float> lb(stotal, s);
+    DevBuf<int32_t> ids(stotal, s), seg(nqb + 1, s);
+    superblock_lb_kernel<<<grid_for(stotal, 256), 256, 0, s>>>(
+        Q.centroid, Q.radius, Q.nb, X.sb_centroid, X.sb_radius, nsb, Q.d, qb0, nqb, qrange.get(),
+        srange.get(), lb, ids, seg);
+    SLK_CHECK_LAUNCH();
+    V.sb_order.alloc(stotal, s);
+    V.sb_lb.alloc(stotal, s);
+    size_t tmp = 0;
+    SLK_CUDA(cub::DeviceSegmentedRadixSort::SortPairs(nullptr, tmp, lb.get(), V.sb_lb.get(), ids.get(),
+                                                      V.sb_order.get(), (int)stotal, (int)nqb, seg.get(),
+                                                      seg.get() + 1, 0, 32, s));
+    DevBuf<unsigned char> t(tmp, s);
+    SLK_CUDA(cub::DeviceSegmentedRadixSort::SortPairs(t.get(), tmp, lb.get(), V.sb_lb.get(), ids.get(),
+                                                      V.sb_order.get(), (int)stotal, (int)nqb, seg.get(),
+                                                      seg.get() + 1, 0, 32, s));
+    return V;
+}
+
+// Full neighbour search for query rows [q0, q1) of Q against X; k results per row.
+void search(const PointSet &Q, const PointSet &X, int k, int mode, const uint8_t *mask,
+            const int32_t *qcolor, const int32_t *xcolor, int64_t q0, int64_t q1,
+            int32_t *out_idx, double *out_dist, cudaStream_t s) {
     ScanStats &st = scan_stats();
     st = ScanStats{};
     const int64_t rows = q1 - q0;
     if (rows <= 0) return;
-    const bool same = (q32 == x32);
-    // fp64 norms in the reference's order
-    DevBuf<double> xnorm(nx, s), qnorm_own;
-    norms_kernel<<<grid_for(nx, 256), 256, 0, s>>>(x32, x64, nx, d, xnorm);
-    SLK_CHECK_LAUNCH();
-    const double *qnorm = xnorm;
-    if (!same) {
-        qnorm_own.alloc(nq, s);
-        norms_kernel<<<grid_for(nq, 256), 256, 0, s>>>(q32, q64, nq, d, qnorm_own);
-        SLK_CHECK_LAUNCH();
-        qnorm = qnorm_own;
-    }
-    DevBuf<double> max_xn(1, s);
-    SLK_CUDA(cudaMemsetAsync(max_xn, 0, sizeof(double), s));
-    max_reduce_kernel<<<grid_for(nx, 256, 1024), 256, 0, s>>>(xnorm, nx, max_xn);
-    SLK_CHECK_LAUNCH();
-
+    const int d = X.d;
+    const int64_t nq = Q.n, nx = X.n;
     DevBuf<int> fail_rows(rows, s), counters(2, s);
     SLK_CUDA(cudaMemsetAsync(counters, 0, sizeof(int), s));
     const int Rsel = k < 32 ? 1 : (k < 64 ? 2 : 4);
     if (k <= 127) {
-        Packed X = pack(x32, nx, d, s);
-        Packed Qown;
-        const float *qp = X.p;
-        if (!same) {
-            Qown = pack(q32, nq, d, s);
-            qp = Qown.p;
-        }
         const int64_t qb0 = q0 / BM, qb1 = (q1 + BM - 1) / BM;
         DevBuf<int32_t> cand(rows * 32 * Rsel, s);
         DevBuf<float> kth(rows, s);
-        ScanArgs sa{qp, X.p, nq, nx, X.dp, qb0, mask, qcolor, xcolor, cand, kth, q0, q1};
-        EventPair ev_scan, ev_refine;
+        DevBuf<unsigned long long> tiles(1, s);
+        SLK_CUDA(cudaMemsetAsync(tiles, 0, sizeof(unsigned long long), s));
+        EventPair ev_order, ev_scan, ev_refine;
+        ev_order.start(s);
+        VisitOrder V = visit_order(Q, X, qb0, qb1 - qb0, mode == MODE_COLOR ? qcolor : nullptr,
+                                   xcolor, s);
+        ev_order.stop(s);
+        ScanArgs sa{Q.packed, X.packed, nq, nx, X.dp, qb0, mask, qcolor, xcolor, cand, kth,
+                    q0, q1, V.sb_order, V.sb_lb, V.blk_lb, X.nsb, tiles};
         ev_scan.start(s);
         if (Rsel == 1) dispatch_scan<1>(mode, sa, qb1 - qb0, s);
         else if (Rsel == 2) dispatch_scan<2>(mode, sa, qb1 - qb0, s);
         else dispatch_scan<4>(mode, sa, qb1 - qb0, s);
         ev_scan.stop(s);
-        st.tiles_computed = (qb1 - qb0) * X.nblocks;
 
-        RefineArgs ra{q32, same ? x64 : q64, qnorm, x32, x64, xnorm, d, k, nq, nx, q0, q1,
-                      cand, kth, max_xn, x64 == nullptr, out_idx, out_dist, fail_rows, counters};
+        RefineArgs ra{Q.x32, Q.x64, Q.norms, X.x32, X.x64, X.norms, d, k, nq, nx, q0, q1,
+                      cand, kth, X.maxn, X.x64 == nullptr && Q.x64 == nullptr, out_idx, out_dist,
+                      fail_rows, counters};
         ev_refine.start(s);
         if (Rsel == 1) launch_refine<1>(ra, rows, s);
         else if (Rsel == 2) launch_refine<2>(ra, rows, s);
         else launch_refine<4>(ra, rows, s);
         ev_refine.stop(s);
         st.rows_refined = rows;
-        SLK_CUDA(cudaStreamSynchronize(s));
+        unsigned long long done = read_scalar(tiles.get(), s);
+        st.tiles_computed = (int64_t)done;
+        st.tiles_skipped = (qb1 - qb0) * X.nb - (int64_t)done;
         Profile &pf = profile();
         pf.scan_ms += ev_scan.ms();
+        pf.order_ms += ev_order.ms();
         pf.scan_launches += 1;
         pf.scan_flops += 2.0 * (double)rows * (double)nx * (double)d;
-        pf.scan_tiles += (double)st.tiles_computed;
+        pf.scan_flops_done += 2.0 * (double)done * BM * BN * (double)d;
+        pf.scan_tiles += (double)done;
+        pf.scan_tiles_total += (double)((qb1 - qb0) * X.nb);
         pf.refine_ms += ev_refine.ms();
     } else {
         // k beyond the fused list capacity: every row takes the exact path
+        if (k > 256) throw_invalid("k=%d exceeds the GPU limit of 256 neighbours", k);
         std::vector<int> all(rows);
         for (int64_t r = 0; r < rows; r++) all[r] = (int)r;
         SLK_CUDA(cudaMemcpyAsync(fail_rows, all.data(), rows * sizeof(int), cudaMemcpyHostToDevice, s));
         int rr = (int)rows;
         SLK_CUDA(cudaMemcpyAsync(counters, &rr, sizeof(int), cudaMemcpyHostToDevice, s));
-        if (k > 256) throw_invalid("k=%d exceeds the GPU limit of 256 neighbours", k);
     }
     int nfail = read_scalar<int>(counters, s);
     st.rows_rescanned = nfail;
@@ -732,7 +971,7 @@ void search(const float *q32, const double *q64, int64_t nq, const float *x32, c
     int missing_init = 0x7fffffff;
     SLK_CUDA(cudaMemcpyAsync(counters.get() + 1, &missing_init, sizeof(int), cudaMemcpyHostToDevice, s));
     if (nfail > 0) {
-        ExactArgs ea{q32, same ? x64 : q64, qnorm, x32, x64, xnorm, d, k, mode, nq, nx, q0,
+        ExactArgs ea{Q.x32, Q.x64, Q.norms, X.x32, X.x64, X.norms, d, k, mode, nq, nx, q0,
                      mask, qcolor, xcolor, fail_rows, nfail, out_idx, out_dist, counters.get() + 1};
         if (k <= 32) launch_exact<1>(ea, s);
         else if (k <= 64) launch_exact<2>(ea, s);
@@ -756,23 +995,80 @@ void row_norms(const float *x32, const double *x64, int64_t n, int d, double *ou
     SLK_CHECK_LAUNCH();
 }
 
-void knn_rows(const float *x32, const double *x64, int64_t n, int d, int k, int64_t q0,
-              int64_t q1, int32_t *idx, double *dist, cudaStream_t s) {
+std::shared_ptr<PointSet> make_pointset(const float *x32, const double *x64, int64_t n, int d,
+                                        cudaStream_t s) {
+    auto P = std::make_shared<PointSet>();
+    P->x32 = x32;
+    P->x64 = x64;
+    P->n = n;
+    P->d = d;
+    P->dp = ((d + KC - 1) / KC) * KC;
+    P->nb = (n + BN - 1) / BN;
+    P->packed.alloc((size_t)P->nb * BN * P->dp, s);
+    int64_t total = P->nb * BN * (int64_t)P->dp;
+    pack_blocks_kernel<<<grid_for(total, 256), 256, 0, s>>>(x32, n, d, P->dp, P->nb, P->packed);
+    SLK_CHECK_LAUNCH();
+    P->norms.alloc(n, s);
+    norms_kernel<<<grid_for(n, 256), 256, 0, s>>>(x32, x64, n, d, P->norms);
+    SLK_CHECK_LAUNCH();
+    P->maxn.alloc(1, s);
+    SLK_CUDA(cudaMemsetAsync(P->maxn, 0, sizeof(double), s));
+    max_reduce_kernel<<<grid_for(n, 256, 1024), 256, 0, s>>>(P->norms, n, P->maxn);
+    SLK_CHECK_LAUNCH();
+    P->centroid.alloc((size_t)P->dp * P->nb, s);
+    P->radius.alloc(P->nb, s);
+    block_sphere_kernel<<<(unsigned)((P->nb * 32 + 255) / 256), 256, 0, s>>>(
+        P->packed, n, d, P->dp, P->nb, P->centroid, P->radius);
+    SLK_CHECK_LAUNCH();
+    P->nsb = (P->nb + 31) / 32;
+    P->sb_centroid.alloc((size_t)P->dp * P->nsb, s);
+    P->sb_radius.alloc(P->nsb, s);
+    superblock_sphere_kernel<<<(unsigned)((P->nsb * 32 + 255) / 256), 256, 0, s>>>(
+        P->centroid, P->radius, P->nb, d, P->nsb, P->sb_centroid, P->sb_radius);
+    SLK_CHECK_LAUNCH();
+    return P;
+}
+
+void knn_ps(const PointSet &X, int k, int64_t q0, int64_t q1, int32_t *idx, double *dist,
+            cudaStream_t s) {
+    const int64_t n = X.n;
     if (k < 1 || k > n - 1) throw_invalid("k must be in [1, %lld] for %lld points, got %d",
                                           (long long)(n - 1), (long long)n, k);
     if (q0 < 0 || q1 > n || q0 > q1) throw_invalid("query row range [%lld, %lld) outside [0, %lld)",
                                                    (long long)q0, (long long)q1, (long long)n);
-    search(x32, x64, n, x32, x64, n, d, k, MODE_SELF, nullptr, nullptr, nullptr, q0, q1, idx,
-           dist, s);
+    search(X, X, k, MODE_SELF, nullptr, nullptr, nullptr, q0, q1, idx, dist, s);
+}
+
+void nn1_ps(const PointSet &Q, const PointSet &X, int mode, const uint8_t *mask,
+            const int32_t *qcolor, const int32_t *xcolor, int64_t q0, int64_t q1, int32_t *idx,
+            double *dist, cudaStream_t s) {
+    if (mode < 0 || mode > 2) throw_invalid("unknown admissibility mode %d", mode);
+    if (X.n < 1) throw_invalid("query row %lld has no admissible candidate", (long long)q0);
+    if (q0 < 0 || q1 > Q.n || q0 > q1) throw_invalid("query row range [%lld, %lld) outside [0, %lld)",
+                                                     (long long)q0, (long long)q1, (long long)Q.n);
+    search(Q, X, 1, mode, mask, qcolor, xcolor, q0, q1, idx, dist, s);
+}
+
+void knn_rows(const float *x32, const double *x64, int64_t n, int d, int k, int64_t q0,
+              int64_t q1, int32_t *idx, double *dist, cudaStream_t s) {
+    if (k < 1 || k > n - 1) throw_invalid("k must be in [1, %lld] for %lld points, got %d",
+                                          (long long)(n - 1), (long long)n, k);
+    auto X = make_pointset(x32, x64, n, d, s);
+    knn_ps(*X, k, q0, q1, idx, dist, s);
 }
 
 void nn1_rows(const float *q32, const double *q64, int64_t nq, const float *x32,
               const double *x64, int64_t nx, int d, int mode, const uint8_t *mask,
               const int32_t *qcolor, const int32_t *xcolor, int64_t q0, int64_t q1, int32_t *idx,
               double *dist, cudaStream_t s) {
-    if (mode < 0 || mode > 2) throw_invalid("unknown admissibility mode %d", mode);
     if (nx < 1) throw_invalid("query row %lld has no admissible candidate", (long long)q0);
-    search(q32, q64, nq, x32, x64, nx, d, 1, mode, mask, qcolor, xcolor, q0, q1, idx, dist, s);
+    auto X = make_pointset(x32, x64, nx, d, s);
+    if (q32 == x32 && nq == nx) {
+        nn1_ps(*X, *X, mode, mask, qcolor, xcolor, q0, q1, idx, dist, s);
+    } else {
+        auto Q = make_pointset(q32, q64, nq, d, s);
+        nn1_ps(*Q, *X, mode, mask, qcolor, xcolor, q0, q1, idx, dist, s);
+    }
 }
 
 namespace {

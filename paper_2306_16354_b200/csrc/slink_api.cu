@@ -48,6 +48,18 @@ void throw_internal(const char *fmt, ...) {
     throw Error{SLK_ERR_INTERNAL, m};
 }
 
+void ensure_pool() {
+    static bool done[64] = {};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64 || done[dev]) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t keep = ~0ull;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    done[dev] = true;
+}
+
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 ScanStats &scan_stats() { return g_scan_stats; }
@@ -116,9 +128,10 @@ void single_linkage_device(const float *x32, const double *x64, int64_t n, int d
                            double *timings, cudaStream_t s) {
     double t0 = now_ms();
     // --- k-NN graph (linkage.py:287)
+    auto P = make_pointset(x32, x64, n, d, s);
     DevBuf<int32_t> idx(n * k, s);
     DevBuf<double> dist(n * k, s);
-    knn_rows(x32, x64, n, d, k, 0, n, idx, dist, s);
+    knn_ps(*P, k, 0, n, idx, dist, s);
     SLK_CUDA(cudaStreamSynchronize(s));
     double t1 = now_ms();
     // --- symmetrise + spanning forest (linkage.py:289-290)
@@ -158,8 +171,7 @@ void single_linkage_device(const float *x32, const double *x64, int64_t n, int d
             SLK_CUDA(cudaMemcpyAsync(uw.get(), tw.get(), ne * sizeof(double), cudaMemcpyDeviceToDevice, s));
             iota32_kernel<<<grid_for(n, 256), 256, 0, s>>>(n, usrc.get() + ne);
             SLK_CHECK_LAUNCH();
-            nn1_rows(x32, x64, n, x32, x64, n, d, 2, nullptr, colors, colors, 0, n, udst.get() + ne,
-                     uw.get() + ne, s);
+            nn1_ps(*P, *P, 2, nullptr, colors, colors, 0, n, udst.get() + ne, uw.get() + ne, s);
             EdgeSet U = dedup_undirected(n, usrc, udst, uw, m, s);
             msf_undirected(n, U.a, U.b, U.w, U.m, true, false, seed, ts, td, tw, colors, &ne, &nc, s);
             iters++;
@@ -211,13 +223,16 @@ const char *slk_last_error(void) { return g_last_error.c_str(); }
 
 int64_t slk_kernel_launches(void) { return g_launches.load(); }
 
-int slk_profile(double *out6, int reset) {
-    out6[0] = g_profile.scan_ms;
-    out6[1] = g_profile.scan_launches;
-    out6[2] = g_profile.scan_flops;
-    out6[3] = g_profile.scan_tiles;
-    out6[4] = g_profile.refine_ms;
-    out6[5] = g_profile.rescan_rows;
+int slk_profile(double *out, int reset) {
+    out[0] = g_profile.scan_ms;
+    out[1] = g_profile.scan_launches;
+    out[2] = g_profile.scan_flops;
+    out[3] = g_profile.scan_tiles;
+    out[4] = g_profile.refine_ms;
+    out[5] = g_profile.rescan_rows;
+    out[6] = g_profile.order_ms;
+    out[7] = g_profile.scan_flops_done;
+    out[8] = g_profile.scan_tiles_total;
     if (reset) g_profile = Profile{};
     return SLK_OK;
 }
