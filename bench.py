@@ -295,6 +295,8 @@ def run_gpu(args, c, cfg_name):
         "scan_ms_per_step": prof["scan_ms"] / max(args.steps, 1),
         "scan_launches_per_step": prof["scan_launches"] / max(args.steps, 1),
         "rows_rescanned_per_step": prof["rescan_rows"] / max(args.steps, 1),
+        "profile_per_step": {k: v / max(args.steps, 1) for k, v in prof.items()},
+        "scan_engine": os.environ.get("SLK_SCAN", "auto"),
     }
     cpu = None
     if not args.no_cpu_baseline and world == 1:

@@ -195,9 +195,11 @@ int slk_msf_edges(int64_t n, const int32_t *d_src, const int32_t *d_dst, const d
                   void *stream);
 
 /* Scan-kernel statistics of the last slk_knn / slk_nn1 call on this thread:
- * stats[0] rows refined, [1] rows that failed the certificate and were
- * re-scanned exactly, [2] index tiles computed, [3] index tiles skipped. */
-int slk_last_scan_stats(int64_t *stats4);
+ * stats[0] rows refined, [1] rows re-scanned exactly in float64, [2] index
+ * tiles computed, [3] index tiles skipped by the bounds, [4] rows the
+ * tensor-core pass could not certify (redone by the exact-fp32 scan).
+ * stats must hold 5 values. */
+int slk_last_scan_stats(int64_t *stats);
 
 /* Process-wide kernel profile since the last reset: out[0] distance-scan
  * kernel milliseconds (CUDA events on the launching stream), [1] scan
@@ -205,8 +207,10 @@ int slk_last_scan_stats(int64_t *stats4);
  * brute force), [3] 128x128 tiles computed, [4] refine-kernel milliseconds,
  * [5] rows re-scanned exactly, [6] visit-order (bounds + segmented sort)
  * milliseconds, [7] FLOP of the tiles actually computed (2*128*128*d each),
- * [8] tiles a brute-force scan would compute.  reset != 0 zeroes the counters
- * after reading.  out must hold 9 doubles. */
+ * [8] tiles a brute-force scan would compute, [9] tensor-core scan kernel
+ * milliseconds, [10] FLOP of the tiles it computed, [11] rows it could not
+ * certify.  reset != 0 zeroes the counters after reading.  out must hold 12
+ * doubles. */
 int slk_profile(double *out, int reset);
 
 #ifdef __cplusplus

@@ -142,18 +142,19 @@ def ids_to_device(ids: np.ndarray):
 
 
 def scan_stats() -> dict:
-    buf = (ctypes.c_int64 * 4)()
+    buf = (ctypes.c_int64 * 5)()
     load().slk_last_scan_stats(buf)
     return dict(rows_refined=buf[0], rows_rescanned=buf[1], tiles_computed=buf[2],
-                tiles_skipped=buf[3])
+                tiles_skipped=buf[3], rows_uncertified=buf[4])
 
 
 def profile(reset: bool = False) -> dict:
     """Cumulative scan-kernel profile (CUDA-event timed inside the library)."""
-    buf = (ctypes.c_double * 9)()
+    buf = (ctypes.c_double * 12)()
     load().slk_profile(buf, int(reset))
     keys = ("scan_ms", "scan_launches", "scan_flops", "scan_tiles", "refine_ms", "rescan_rows",
-            "order_ms", "scan_flops_done", "scan_tiles_total")
+            "order_ms", "scan_flops_done", "scan_tiles_total", "tc_ms", "tc_flops_done",
+            "tc_uncertified")
     return dict(zip(keys, list(buf)))
 
 

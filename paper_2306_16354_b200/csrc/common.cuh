@@ -125,14 +125,16 @@ int num_sms();
 // ------------------------------------------------- cross-module entry points
 // Scan statistics of the last neighbour search on this thread.
 struct ScanStats {
-    int64_t rows_refined = 0, rows_rescanned = 0, tiles_computed = 0, tiles_skipped = 0;
+    int64_t rows_refined = 0, rows_rescanned = 0, tiles_computed = 0, tiles_skipped = 0,
+            rows_uncertified = 0;
 };
 ScanStats &scan_stats();
 
 // Cumulative kernel profile (process-wide), read by bench.py via slk_profile.
 struct Profile {
     double scan_ms = 0, scan_launches = 0, scan_flops = 0, scan_tiles = 0, refine_ms = 0,
-           rescan_rows = 0, order_ms = 0, scan_flops_done = 0, scan_tiles_total = 0;
+           rescan_rows = 0, order_ms = 0, scan_flops_done = 0, scan_tiles_total = 0, tc_ms = 0,
+           tc_flops_done = 0, tc_uncertified = 0;
 };
 Profile &profile();
 
@@ -165,6 +167,7 @@ struct PointSet {
     const double *x64 = nullptr;
     int64_t n = 0, nb = 0, nsb = 0;
     int d = 0, dp = 0;
+    float maxabs = 0.0f;  // max |x| of the float32 values (tensor-path scaling)
     DevBuf<float> packed, centroid, radius, sb_centroid, sb_radius;
     DevBuf<double> norms, maxn;
 };

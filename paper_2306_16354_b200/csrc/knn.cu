@@ -25,6 +25,8 @@
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
 
 #include <cub/cub.cuh>
 
@@ -33,19 +35,13 @@
 #include <vector>
 
 #include "common.cuh"
+#include "scan_common.cuh"
+#include "tc_scan.cuh"
 
 namespace slk {
 
 namespace {
-
-constexpr int BM = 128;   // query rows per CTA
-constexpr int BN = 128;   // index points per block
-constexpr int KC = 16;    // dims per operand chunk
-constexpr int NT = 256;   // threads per CTA
-constexpr int CAP = 32;   // per-row candidate buffer
-constexpr unsigned FULL = 0xffffffffu;
-
-enum Mode { MODE_NONE = 0, MODE_MASK = 1, MODE_COLOR = 2, MODE_SELF = 3 };
+using namespace scan;
 
 // ------------------------------------------------------------------ K1
 __global__ void pack_blocks_kernel(const float *__restrict__ x, int64_t n, int d, int dp,
@@ -83,6 +79,21 @@ __global__ void norms_kernel(const float *__restrict__ x32, const double *__rest
     }
 }
 
+__global__ void maxabs_kernel(const float *__restrict__ x, int64_t m, unsigned int *out) {
+    float v = 0.0f;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
+         i += (int64_t)gridDim.x * blockDim.x)
+        v = fmaxf(v, fabsf(x[i]));
+    for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(FULL, v, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(out, __float_as_uint(v));  // v >= 0: bit order
+}
+
+inline float __uint_as_float_host(unsigned int b) {
+    float f;
+    memcpy(&f, &b, sizeof f);
+    return f;
+}
+
 __global__ void max_reduce_kernel(const double *__restrict__ v, int64_t n, double *out) {
     double m = 0.0;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
@@ -91,105 +102,6 @@ __global__ void max_reduce_kernel(const double *__restrict__ v, int64_t n, doubl
     for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(FULL, m, o));
     if ((threadIdx.x & 31) == 0)
         atomicMax((unsigned long long *)out, (unsigned long long)__double_as_longlong(m));
-}
-
-// --------------------------------------------------- warp sorted lists
-// A warp holds a sorted list of 32R (value, id) pairs, element p = r*32+lane,
-// ascending by (value, id).  Insertion shifts the suffix right by one.
-template <class V>
-__device__ __forceinline__ bool pair_gt(V av, int ai, V bv, int bi) {
-    return av > bv || (av == bv && ai > bi);
-}
-
-template <int R, class V>
-__device__ __forceinline__ void warp_list_insert(V (&lv)[R], int (&li)[R], V v, int id, int lane) {
-    bool g[R];
-    V pv[R];
-    int pi[R];
-    bool pg[R];
-    V tv[R];
-    int ti[R];
-    bool tg[R];
-#pragma unroll
-    for (int r = 0; r < R; r++) {
-        g[r] = pair_gt(lv[r], li[r], v, id);
-        pv[r] = __shfl_up_sync(FULL, lv[r], 1);
-        pi[r] = __shfl_up_sync(FULL, li[r], 1);
-        pg[r] = __shfl_up_sync(FULL, (int)g[r], 1) != 0;
-        tv[r] = __shfl_sync(FULL, lv[r], 31);
-        ti[r] = __shfl_sync(FULL, li[r], 31);
-        tg[r] = __shfl_sync(FULL, (int)g[r], 31) != 0;
-    }
-#pragma unroll
-    for (int r = 0; r < R; r++) {
-        if (lane == 0) {
-            if (r == 0) {
-                pg[r] = false;
-            } else {
-                pv[r] = tv[r - 1];
-                pi[r] = ti[r - 1];
-                pg[r] = tg[r - 1];
-            }
-        }
-        if (g[r]) {
-            if (pg[r]) {
-                lv[r] = pv[r];
-                li[r] = pi[r];
-            } else {
-                lv[r] = v;
-                li[r] = id;
-            }
-        }
-    }
-}
-
-// Bitonic sort of the 32R warp-distributed pairs, ascending by (value, id).
-template <int R, class V>
-__device__ __forceinline__ void warp_bitonic_sort(V (&lv)[R], int (&li)[R], int lane) {
-    constexpr int N = 32 * R;
-#pragma unroll
-    for (int size = 2; size <= N; size <<= 1) {
-#pragma unroll
-        for (int stride = size >> 1; stride > 0; stride >>= 1) {
-            if (stride >= 32) {
-                int rs = stride / 32;
-#pragma unroll
-                for (int r = 0; r < R; r++) {
-                    int partner = r ^ rs;
-                    if (partner > r) {
-                        int p = r * 32 + lane;
-                        bool up = (p & size) == 0;
-                        bool sw = up ? pair_gt(lv[r], li[r], lv[partner], li[partner])
-                                     : pair_gt(lv[partner], li[partner], lv[r], li[r]);
-                        if (sw) {
-                            V tv = lv[r];
-                            int ti = li[r];
-                            lv[r] = lv[partner];
-                            li[r] = li[partner];
-                            lv[partner] = tv;
-                            li[partner] = ti;
-                        }
-                    }
-                }
-            } else {
-#pragma unroll
-                for (int r = 0; r < R; r++) {
-                    int p = r * 32 + lane;
-                    V ov = __shfl_xor_sync(FULL, lv[r], stride);
-                    int oi = __shfl_xor_sync(FULL, li[r], stride);
-                    bool lower = (lane & stride) == 0;
-                    bool up = (p & size) == 0;
-                    // lower element keeps the min when ascending
-                    bool mine_gt = pair_gt(lv[r], li[r], ov, oi);
-                    bool take = (lower == up) ? mine_gt : !mine_gt;
-                    if (take && !(lv[r] == ov && li[r] == oi)) {
-                        lv[r] = ov;
-                        li[r] = oi;
-                    }
-                }
-            }
-        }
-    }
 }
 
 // ------------------------------------------------------------------ K2
@@ -215,55 +127,8 @@ struct ScanArgs {
     const float *blk_lb;      // [nqb_launch][nxb]
     int64_t nsb;
     unsigned long long *tiles_done;
+    const int32_t *qid;  // query row -> id in the index (gathered queries), or null
 };
-
-// Iterates the index blocks a query block must visit: superblocks in
-// ascending bound order, members in index order, skipping every block whose
-// bound exceeds the current threshold; stops at the first superblock whose
-// bound exceeds it (member bounds are >= their superblock's).  Every thread
-// runs it redundantly and gets the same answer (warp-uniform ballots).
-struct BlockVisitor {
-    const int32_t *sb_order;
-    const float *sb_lb;
-    const float *blk_lb;
-    int64_t nsb, nxb;
-    int64_t s = -1, sb = 0;
-    unsigned mask = 0;
-    float my_lb = INFINITY;
-
-    __device__ int64_t next(float thr_max, int lane) {
-        while (true) {
-            if (mask == 0) {
-                if (++s >= nsb) return -1;
-                float l = sb_lb[s];
-                if (l == INFINITY || l > thr_max) {
-                    s = nsb;
-                    return -1;
-                }
-                sb = sb_order[s];
-                int64_t b = sb * 32 + lane;
-                my_lb = b < nxb ? blk_lb[b] : INFINITY;
-                mask = __ballot_sync(0xffffffffu, my_lb != INFINITY && !(my_lb > thr_max));
-                continue;
-            }
-            int m = __ffs(mask) - 1;
-            mask &= mask - 1;
-            float l = __shfl_sync(0xffffffffu, my_lb, m);
-            if (l > thr_max) continue;
-            return sb * 32 + m;
-        }
-    }
-};
-
-__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
-    unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-    asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
-}
 
 template <int R>
 struct ScanSmem {
@@ -388,7 +253,7 @@ __global__ void __launch_bounds__(NT, (R == 1 ? 2 : 1)) scan_kernel(ScanArgs a) 
                 for (int j = 0; j < 8; j++) {
                     int64_t gj = col0 + (j < 4 ? tx * 4 + j : 64 + tx * 4 + (j - 4));
                     bool ok = gj < a.nx && gi < a.nq && acc[i][j] < th;
-                    if (MODE == MODE_SELF) ok = ok && gj != gi;
+                    if (MODE == MODE_SELF) ok = ok && gj != (a.qid ? (int64_t)a.qid[gi] : gi);
                     if (MODE == MODE_COLOR) ok = ok && a.xcolor[gj] != S.qcol[r];
                     if (MODE == MODE_MASK) ok = ok && a.mask[gi * a.nx + gj] != 0;
                     if (ok) pending |= 1ull << (i * 8 + j);
@@ -650,6 +515,9 @@ struct RefineArgs {
     double *out_dist;
     int *fail_rows;
     int *fail_count;
+    // tensor-core scan (tc_scan.cu): kth in scaled units, |q^|^2 per row
+    const float *qhat;        // nullptr for the exact-fp32 scan
+    double scale;             // power of two applied after centring
 };
 
 // Exact reference distance (neighbors.py:132-137): dot sequential over t,
@@ -684,6 +552,35 @@ __device__ double certified_floor(float a, int d, double nq, double max_xn, bool
     if (!(s > 0.0)) return -INFINITY;
     double dlo = s * s * (1.0 - 1e-15);
     double ev = (d + 4) * 0x1p-52 * (nq + max_xn) * 1.01 + 0x1p-1074;  // fp64 expanded-form error
+    return dlo - ev;
+}
+
+// Same bound for the tensor-core scan.  a: approximate value
+// in scaled units, a = |q^|^2 + |x^|^2 - 2<q^,x^> of the centred, scaled,
+// fp16-rounded points, with fp32 norms and tensor-core fp32 accumulation.
+//   |a - D^| <= g (|q^| + |x^|)^2,   g = (2d + 8) 2^-23   (all fp32 roundings)
+//   |x^| <= |q^| + sqrt(D^)                               (triangle)
+// gives the smallest sqrt(D^) compatible with a >= A; then
+//   sqrt(D) >= sqrt(D^) - eta (|q'| + |x'|) - 2 sqrt(d) 2^-25
+// (eta: fp32 centring + fp16 rounding, 2^-25: fp16 subnormal spacing / 2).
+__device__ double certified_floor_tc(float a, float qhat2, double scale, int d, double nq,
+                                     double max_xn, bool exact_f32) {
+    const double A = (double)a;
+    if (!(A > 0.0) || !(A < INFINITY)) return -INFINITY;
+    const double r = sqrt((double)qhat2) * (1.0 + 1e-12);
+    const double g = (2.0 * d + 8.0) * 0x1p-23;
+    const double ca = 1.0 + g, cb = 4.0 * g * r, cc = 4.0 * g * r * r - A;
+    const double disc = cb * cb - 4.0 * ca * cc;
+    if (!(disc > 0.0)) return -INFINITY;
+    double sh = (-cb + sqrt(disc)) / (2.0 * ca) * (1.0 - 1e-12);  // min sqrt(D^), scaled
+    const double eta = 0x1p-11 * 1.01;
+    const double etap = eta * (1.0 + 2.0 * eta);
+    double sd = sh * (1.0 - etap) - 2.0 * etap * r - 2.0 * sqrt((double)d) * 0x1p-25;
+    sd = sd / scale;  // back to data units (scale is a power of two)
+    if (!exact_f32) sd -= 0x1p-24 * 1.01 * (sqrt(nq) + sqrt(max_xn));
+    if (!(sd > 0.0)) return -INFINITY;
+    double dlo = sd * sd * (1.0 - 1e-15);
+    double ev = (d + 4) * 0x1p-52 * (nq + max_xn) * 1.01 + 0x1p-1074;
     return dlo - ev;
 }
 
@@ -736,7 +633,9 @@ __global__ void refine_kernel(RefineArgs a) {
         } else if (kth == INFINITY && cand[32 * R - 1] < 0) {
             ok = true;  // list never filled: every admissible candidate was kept
         } else {
-            double floor = certified_floor(kth, a.d, nq, *a.max_xnorm, a.exact_f32);
+            double floor = a.qhat ? certified_floor_tc(kth, a.qhat[wid], a.scale, a.d, nq,
+                                                       *a.max_xnorm, a.exact_f32)
+                                  : certified_floor(kth, a.d, nq, *a.max_xnorm, a.exact_f32);
             ok = floor > vk;
         }
         if (!ok) {
@@ -765,6 +664,7 @@ struct ExactArgs {
     int32_t *out_idx;
     double *out_dist;
     int *missing;  // first row (global) without admissible candidate, or INT_MAX
+    const int32_t *qid;  // query row -> id in the index (gathered queries), or null
 };
 
 template <int R>
@@ -785,7 +685,7 @@ __global__ void exact_rescan_kernel(ExactArgs a) {
     for (int64_t j0 = 0; j0 < a.nx; j0 += 32) {
         int64_t j = j0 + lane;
         bool ok = j < a.nx;
-        if (ok && a.mode == MODE_SELF) ok = j != gi;
+        if (ok && a.mode == MODE_SELF) ok = j != (a.qid ? (int64_t)a.qid[gi] : gi);
         if (ok && a.mode == MODE_COLOR) ok = a.xcolor[j] != a.qcolor[gi];
         if (ok && a.mode == MODE_MASK) ok = a.mask[gi * a.nx + j] != 0;
         double v = ok ? exact_dist(a.q32, a.q64, a.x32, a.x64, gi, j, a.d, nq, a.xnorm[j]) : INFINITY;
@@ -903,14 +803,85 @@ VisitOrder visit_order(const PointSet &Q, const PointSet &X, int64_t qb0, int64_
     return V;
 }
 
-// Full neighbour search for query rows [q0, q1) of Q against X; k results per row.
-void search(const PointSet &Q, const PointSet &X, int k, int mode, const uint8_t *mask,
-            const int32_t *qcolor, const int32_t *xcolor, int64_t q0, int64_t q1,
-            int32_t *out_idx, double *out_dist, cudaStream_t s) {
+__global__ void gather_rows_kernel(const float *x32, const double *x64, const int32_t *rows,
+                                   int64_t m, int d, float *o32, double *o64) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m * d;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        int64_t r = e / d, t = e - r * d, src = (int64_t)rows[r] * d + t;
+        o32[e] = x32[src];
+        if (o64) o64[e] = x64[src];
+    }
+}
+
+__global__ void gather_meta_kernel(const int32_t *rows, int64_t m, const int32_t *qcolor,
+                                   const uint8_t *mask, int64_t nx, int32_t *qcolor_g,
+                                   uint8_t *mask_g) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m * (mask ? nx : 1);
+         e += (int64_t)gridDim.x * blockDim.x) {
+        if (mask) {
+            int64_t r = e / nx, j = e - r * nx;
+            mask_g[e] = mask[(int64_t)rows[r] * nx + j];
+            if (j == 0 && qcolor) qcolor_g[r] = qcolor[rows[r]];
+        } else if (qcolor) {
+            qcolor_g[e] = qcolor[rows[e]];
+        }
+    }
+}
+
+__global__ void to_global_rows_kernel(const int *rel, int64_t m, int64_t q0, int32_t *glob) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m;
+         e += (int64_t)gridDim.x * blockDim.x)
+        glob[e] = (int32_t)(q0 + rel[e]);
+}
+
+__global__ void scatter_rows_kernel(const int32_t *idx_g, const double *dist_g, const int *rel,
+                                    int64_t m, int k, int32_t *out_idx, double *out_dist) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m * k;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        int64_t r = e / k, c = e - r * k, dst = (int64_t)rel[r] * k + c;
+        out_idx[dst] = idx_g[e];
+        out_dist[dst] = dist_g[e];
+    }
+}
+
+enum class Engine { Auto, Ffma, Tensor };
+
+Engine engine_choice() {
+    const char *e = getenv("SLK_SCAN");
+    if (e && !strcmp(e, "ffma")) return Engine::Ffma;
+    if (e && !strcmp(e, "tc")) return Engine::Tensor;
+    return Engine::Auto;
+}
+
+void record_profile(const EventPair &ev_order, const EventPair &ev_scan, const EventPair &ev_refine,
+                    int64_t rows, int64_t nx, int d, unsigned long long done, int64_t tiles_total,
+                    bool tensor) {
+    Profile &pf = profile();
+    double scan_ms = const_cast<EventPair &>(ev_scan).ms();
+    pf.scan_ms += scan_ms;
+    pf.order_ms += const_cast<EventPair &>(ev_order).ms();
+    pf.scan_launches += 1;
+    pf.scan_flops += 2.0 * (double)rows * (double)nx * (double)d;
+    pf.scan_flops_done += 2.0 * (double)done * BM * BN * (double)d;
+    pf.scan_tiles += (double)done;
+    pf.scan_tiles_total += (double)tiles_total;
+    pf.refine_ms += const_cast<EventPair &>(ev_refine).ms();
+    if (tensor) {
+        pf.tc_ms += scan_ms;
+        pf.tc_flops_done += 2.0 * (double)done * BM * BN * (double)d;
+    }
+}
+
+// Exact-fp32 scan → refine → exact re-scan for uncertified rows.  Queries are
+// rows [q0, q1) of Q; `qid` (nullable) maps a query row to its id in X for
+// self-exclusion (gathered queries).  Returns the first query row without an
+// admissible candidate, or -1.
+int64_t search_ffma(const PointSet &Q, const PointSet &X, const int32_t *qid, int k, int mode,
+                    const uint8_t *mask, const int32_t *qcolor, const int32_t *xcolor, int64_t q0,
+                    int64_t q1, int32_t *out_idx, double *out_dist, cudaStream_t s) {
     ScanStats &st = scan_stats();
-    st = ScanStats{};
     const int64_t rows = q1 - q0;
-    if (rows <= 0) return;
+    if (rows <= 0) return -1;
     const int d = X.d;
     const int64_t nq = Q.n, nx = X.n;
     DevBuf<int> fail_rows(rows, s), counters(2, s);
@@ -928,34 +899,25 @@ void search(const PointSet &Q, const PointSet &X, int k, int mode, const uint8_t
                                    xcolor, s);
         ev_order.stop(s);
         ScanArgs sa{Q.packed, X.packed, nq, nx, X.dp, qb0, mask, qcolor, xcolor, cand, kth,
-                    q0, q1, V.sb_order, V.sb_lb, V.blk_lb, X.nsb, tiles};
+                    q0, q1, V.sb_order, V.sb_lb, V.blk_lb, X.nsb, tiles, qid};
         ev_scan.start(s);
         if (Rsel == 1) dispatch_scan<1>(mode, sa, qb1 - qb0, s);
         else if (Rsel == 2) dispatch_scan<2>(mode, sa, qb1 - qb0, s);
         else dispatch_scan<4>(mode, sa, qb1 - qb0, s);
         ev_scan.stop(s);
-
         RefineArgs ra{Q.x32, Q.x64, Q.norms, X.x32, X.x64, X.norms, d, k, nq, nx, q0, q1,
                       cand, kth, X.maxn, X.x64 == nullptr && Q.x64 == nullptr, out_idx, out_dist,
-                      fail_rows, counters};
+                      fail_rows, counters, nullptr, 1.0};
         ev_refine.start(s);
         if (Rsel == 1) launch_refine<1>(ra, rows, s);
         else if (Rsel == 2) launch_refine<2>(ra, rows, s);
         else launch_refine<4>(ra, rows, s);
         ev_refine.stop(s);
-        st.rows_refined = rows;
         unsigned long long done = read_scalar(tiles.get(), s);
-        st.tiles_computed = (int64_t)done;
-        st.tiles_skipped = (qb1 - qb0) * X.nb - (int64_t)done;
-        Profile &pf = profile();
-        pf.scan_ms += ev_scan.ms();
-        pf.order_ms += ev_order.ms();
-        pf.scan_launches += 1;
-        pf.scan_flops += 2.0 * (double)rows * (double)nx * (double)d;
-        pf.scan_flops_done += 2.0 * (double)done * BM * BN * (double)d;
-        pf.scan_tiles += (double)done;
-        pf.scan_tiles_total += (double)((qb1 - qb0) * X.nb);
-        pf.refine_ms += ev_refine.ms();
+        st.rows_refined += rows;
+        st.tiles_computed += (int64_t)done;
+        st.tiles_skipped += (qb1 - qb0) * X.nb - (int64_t)done;
+        record_profile(ev_order, ev_scan, ev_refine, rows, nx, d, done, (qb1 - qb0) * X.nb, false);
     } else {
         // k beyond the fused list capacity: every row takes the exact path
         if (k > 256) throw_invalid("k=%d exceeds the GPU limit of 256 neighbours", k);
@@ -966,13 +928,14 @@ void search(const PointSet &Q, const PointSet &X, int k, int mode, const uint8_t
         SLK_CUDA(cudaMemcpyAsync(counters, &rr, sizeof(int), cudaMemcpyHostToDevice, s));
     }
     int nfail = read_scalar<int>(counters, s);
-    st.rows_rescanned = nfail;
+    st.rows_rescanned += nfail;
     profile().rescan_rows += nfail;
     int missing_init = 0x7fffffff;
     SLK_CUDA(cudaMemcpyAsync(counters.get() + 1, &missing_init, sizeof(int), cudaMemcpyHostToDevice, s));
     if (nfail > 0) {
         ExactArgs ea{Q.x32, Q.x64, Q.norms, X.x32, X.x64, X.norms, d, k, mode, nq, nx, q0,
-                     mask, qcolor, xcolor, fail_rows, nfail, out_idx, out_dist, counters.get() + 1};
+                     mask, qcolor, xcolor, fail_rows, nfail, out_idx, out_dist, counters.get() + 1,
+                     qid};
         if (k <= 32) launch_exact<1>(ea, s);
         else if (k <= 64) launch_exact<2>(ea, s);
         else if (k <= 128) launch_exact<4>(ea, s);
@@ -981,10 +944,121 @@ void search(const PointSet &Q, const PointSet &X, int k, int mode, const uint8_t
     check_missing_kernel<<<grid_for(rows, 256), 256, 0, s>>>(out_idx, rows, k, q0, counters.get() + 1);
     SLK_CHECK_LAUNCH();
     int missing = read_scalar<int>(counters.get() + 1, s);
-    if (missing != 0x7fffffff) {
-        if (mode == MODE_SELF)
-            throw_internal("row %d has fewer than k neighbours", missing);
-        throw_invalid("query row %d has no admissible candidate", missing);
+    return missing == 0x7fffffff ? -1 : missing;
+}
+
+// Power-of-two scale putting the centred operands in fp16's range: |x| s <= 2^13.
+bool tensor_scale(const PointSet &Q, const PointSet &X, float *scale, float *inv_scale2) {
+    float m = fmaxf(Q.maxabs, X.maxabs);
+    if (!(m > 0.0f)) m = 1.0f;
+    int e = 13 - (int)ceilf(log2f(m));
+    if (e < -50 || e > 50) return false;
+    *scale = ldexpf(1.0f, e);
+    *inv_scale2 = ldexpf(1.0f, -2 * e);
+    return true;
+}
+
+// Full neighbour search for query rows [q0, q1) of Q against X; k results per row.
+void search(const PointSet &Q, const PointSet &X, int k, int mode, const uint8_t *mask,
+            const int32_t *qcolor, const int32_t *xcolor, int64_t q0, int64_t q1,
+            int32_t *out_idx, double *out_dist, cudaStream_t s) {
+    ScanStats &st = scan_stats();
+    st = ScanStats{};
+    const int64_t rows = q1 - q0;
+    if (rows <= 0) return;
+    const int d = X.d;
+    const int Rsel = k < 32 ? 1 : (k < 64 ? 2 : 4);
+    const Engine eng = engine_choice();
+    float scale = 1.0f, inv_scale2 = 1.0f;
+    const bool use_tc = eng != Engine::Ffma && k <= 127 && tc::supported(d, Rsel) &&
+                        tensor_scale(Q, X, &scale, &inv_scale2);
+    int64_t missing = -1;
+    if (!use_tc) {
+        missing = search_ffma(Q, X, nullptr, k, mode, mask, qcolor, xcolor, q0, q1, out_idx,
+                              out_dist, s);
+    } else {
+        const int64_t nq = Q.n, nx = X.n;
+        const int64_t qb0 = q0 / BM, qb1 = (q1 + BM - 1) / BM;
+        DevBuf<int32_t> cand(rows * 32 * Rsel, s);
+        DevBuf<float> kth(rows, s), qhat(rows, s);
+        DevBuf<unsigned long long> tiles(1, s);
+        DevBuf<int> fail_rows(rows, s), counters(1, s);
+        SLK_CUDA(cudaMemsetAsync(tiles, 0, sizeof(unsigned long long), s));
+        SLK_CUDA(cudaMemsetAsync(counters, 0, sizeof(int), s));
+        EventPair ev_order, ev_scan, ev_refine;
+        ev_order.start(s);
+        VisitOrder V = visit_order(Q, X, qb0, qb1 - qb0, mode == MODE_COLOR ? qcolor : nullptr,
+                                   xcolor, s);
+        ev_order.stop(s);
+        tc::TcArgs ta{Q.packed, X.packed, nq, nx, d, X.dp, ((d + 15) / 16) * 16, qb0, Q.centroid,
+                      Q.nb, scale, inv_scale2, mask, qcolor, xcolor, cand, kth, qhat, q0, q1,
+                      V.sb_order, V.sb_lb, V.blk_lb, X.nsb, tiles};
+        ev_scan.start(s);
+        tc::launch(mode, Rsel, ta, qb1 - qb0, s);
+        ev_scan.stop(s);
+        RefineArgs ra{Q.x32, Q.x64, Q.norms, X.x32, X.x64, X.norms, d, k, nq, nx, q0, q1,
+                      cand, kth, X.maxn, X.x64 == nullptr && Q.x64 == nullptr, out_idx, out_dist,
+                      fail_rows, counters, qhat, (double)scale};
+        ev_refine.start(s);
+        if (Rsel == 1) launch_refine<1>(ra, rows, s);
+        else if (Rsel == 2) launch_refine<2>(ra, rows, s);
+        else launch_refine<4>(ra, rows, s);
+        ev_refine.stop(s);
+        unsigned long long done = read_scalar(tiles.get(), s);
+        st.rows_refined += rows;
+        st.tiles_computed += (int64_t)done;
+        st.tiles_skipped += (qb1 - qb0) * X.nb - (int64_t)done;
+        record_profile(ev_order, ev_scan, ev_refine, rows, nx, d, done, (qb1 - qb0) * X.nb, true);
+        const int nfail = read_scalar<int>(counters, s);
+        st.rows_uncertified += nfail;
+        profile().tc_uncertified += nfail;
+        if (nfail > 0) {
+            // uncertified rows: exact-fp32 scan of the gathered rows (sorted, so
+            // gathered query blocks stay spatially coherent for pruning)
+            DevBuf<int> sorted(nfail, s);
+            size_t tmp = 0;
+            SLK_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tmp, fail_rows.get(), sorted.get(), nfail, 0, 32, s));
+            DevBuf<unsigned char> t(tmp, s);
+            SLK_CUDA(cub::DeviceRadixSort::SortKeys(t.get(), tmp, fail_rows.get(), sorted.get(), nfail, 0, 32, s));
+            DevBuf<int32_t> glob(nfail, s);
+            to_global_rows_kernel<<<grid_for(nfail, 256), 256, 0, s>>>(sorted, nfail, q0, glob);
+            SLK_CHECK_LAUNCH();
+            DevBuf<float> g32((int64_t)nfail * d, s);
+            DevBuf<double> g64;
+            if (Q.x64) g64.alloc((int64_t)nfail * d, s);
+            gather_rows_kernel<<<grid_for((int64_t)nfail * d, 256), 256, 0, s>>>(
+                Q.x32, Q.x64, glob, nfail, d, g32, g64.get());
+            SLK_CHECK_LAUNCH();
+            DevBuf<int32_t> gcol;
+            DevBuf<uint8_t> gmask;
+            if (mode == MODE_COLOR) gcol.alloc(nfail, s);
+            if (mode == MODE_MASK) gmask.alloc((int64_t)nfail * nx, s);
+            if (mode == MODE_COLOR || mode == MODE_MASK) {
+                int64_t work = mode == MODE_MASK ? (int64_t)nfail * nx : nfail;
+                gather_meta_kernel<<<grid_for(work, 256), 256, 0, s>>>(
+                    glob, nfail, mode == MODE_COLOR ? qcolor : nullptr,
+                    mode == MODE_MASK ? mask : nullptr, nx, gcol.get(), gmask.get());
+                SLK_CHECK_LAUNCH();
+            }
+            auto G = make_pointset(g32, g64.get(), nfail, d, s);
+            DevBuf<int32_t> gidx((int64_t)nfail * k, s);
+            DevBuf<double> gdist((int64_t)nfail * k, s);
+            int64_t gm = search_ffma(*G, X, glob, k, mode, gmask.get(), gcol.get(), xcolor, 0, nfail,
+                                     gidx, gdist, s);
+            if (gm >= 0) {
+                int32_t orig = 0;
+                SLK_CUDA(cudaMemcpyAsync(&orig, glob.get() + gm, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+                SLK_CUDA(cudaStreamSynchronize(s));
+                missing = orig;
+            }
+            scatter_rows_kernel<<<grid_for((int64_t)nfail * k, 256), 256, 0, s>>>(
+                gidx, gdist, sorted, nfail, k, out_idx, out_dist);
+            SLK_CHECK_LAUNCH();
+        }
+    }
+    if (missing >= 0) {
+        if (mode == MODE_SELF) throw_internal("row %lld has fewer than k neighbours", (long long)missing);
+        throw_invalid("query row %lld has no admissible candidate", (long long)missing);
     }
 }
 
@@ -1015,6 +1089,14 @@ std::shared_ptr<PointSet> make_pointset(const float *x32, const double *x64, int
     SLK_CUDA(cudaMemsetAsync(P->maxn, 0, sizeof(double), s));
     max_reduce_kernel<<<grid_for(n, 256, 1024), 256, 0, s>>>(P->norms, n, P->maxn);
     SLK_CHECK_LAUNCH();
+    {
+        DevBuf<unsigned int> mx(1, s);
+        SLK_CUDA(cudaMemsetAsync(mx, 0, sizeof(unsigned int), s));
+        maxabs_kernel<<<grid_for(n * (int64_t)d, 256, 2048), 256, 0, s>>>(x32, n * (int64_t)d, mx);
+        SLK_CHECK_LAUNCH();
+        unsigned int bits = read_scalar(mx.get(), s);
+        P->maxabs = __uint_as_float_host(bits);
+    }
     P->centroid.alloc((size_t)P->dp * P->nb, s);
     P->radius.alloc(P->nb, s);
     block_sphere_kernel<<<(unsigned)((P->nb * 32 + 255) / 256), 256, 0, s>>>(
@@ -1101,3 +1183,31 @@ void pairwise_l2(const double *q, int64_t nq, const double *x, int64_t nx, int d
 }
 
 }  // namespace slk
+
+namespace slk {
+// Diagnostic: run only the tensor-core scan (kNN mode) and return its raw
+// candidate lists, K'-th values (scaled units), |q^|^2 and the scale.
+void debug_tc_scan(const float *x32, int64_t n, int d, int k, int32_t *cand, float *kth,
+                   float *qhat, float *scale_out, cudaStream_t s) {
+    auto P = make_pointset(x32, nullptr, n, d, s);
+    const int R = k < 32 ? 1 : (k < 64 ? 2 : 4);
+    float scale = 1, inv2 = 1;
+    if (!tensor_scale(*P, *P, &scale, &inv2)) throw_invalid("no tensor scale");
+    const int64_t nqb = P->nb;
+    VisitOrder V = visit_order(*P, *P, 0, nqb, nullptr, nullptr, s);
+    DevBuf<unsigned long long> tiles(1, s);
+    SLK_CUDA(cudaMemsetAsync(tiles, 0, sizeof(unsigned long long), s));
+    tc::TcArgs ta{P->packed, P->packed, n, n, d, P->dp, ((d + 15) / 16) * 16, 0, P->centroid,
+                  P->nb, scale, inv2, nullptr, nullptr, nullptr, cand, kth, qhat, 0, n,
+                  V.sb_order, V.sb_lb, V.blk_lb, P->nsb, tiles};
+    tc::launch(scan::MODE_SELF, R, ta, nqb, s);
+    SLK_CUDA(cudaStreamSynchronize(s));
+    *scale_out = scale;
+}
+}  // namespace slk
+
+extern "C" int slk_debug_tc_scan(const float *d_x32, int64_t n, int d, int k, int32_t *d_cand,
+                                 float *d_kth, float *d_qhat, float *scale, void *stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    return slk::guarded([&] { slk::debug_tc_scan(d_x32, n, d, k, d_cand, d_kth, d_qhat, scale, s); });
+}

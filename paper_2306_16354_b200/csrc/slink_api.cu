@@ -233,6 +233,9 @@ int slk_profile(double *out, int reset) {
     out[6] = g_profile.order_ms;
     out[7] = g_profile.scan_flops_done;
     out[8] = g_profile.scan_tiles_total;
+    out[9] = g_profile.tc_ms;
+    out[10] = g_profile.tc_flops_done;
+    out[11] = g_profile.tc_uncertified;
     if (reset) g_profile = Profile{};
     return SLK_OK;
 }
@@ -242,6 +245,7 @@ int slk_last_scan_stats(int64_t *stats4) {
     stats4[1] = g_scan_stats.rows_rescanned;
     stats4[2] = g_scan_stats.tiles_computed;
     stats4[3] = g_scan_stats.tiles_skipped;
+    stats4[4] = g_scan_stats.rows_uncertified;
     return SLK_OK;
 }
 
