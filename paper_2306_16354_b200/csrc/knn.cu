@@ -141,6 +141,7 @@ struct ScanSmem {
     int cnt[BM];
     float thr[BM];
     int qcol[BM];
+    int qself[BM];  // id of the query row in the index, -1 = not a valid row
     float part[4];
 };
 
@@ -164,10 +165,9 @@ __global__ void __launch_bounds__(NT, (R == 1 ? 2 : 1)) scan_kernel(ScanArgs a) 
     for (int r = tid; r < BM; r += NT) {
         S.cnt[r] = 0;
         S.thr[r] = INFINITY;
-        if (MODE == MODE_COLOR) {
-            int64_t gi = row_base + r;
-            S.qcol[r] = gi < a.nq ? a.qcolor[gi] : -1;
-        }
+        const int64_t gi = row_base + r;
+        S.qself[r] = gi < a.nq ? (a.qid ? a.qid[gi] : (int)gi) : -1;
+        if (MODE == MODE_COLOR) S.qcol[r] = gi < a.nq ? a.qcolor[gi] : -1;
     }
     // largest per-row threshold of the block's valid rows; a block whose
     // lower bound exceeds it cannot improve any row (thresholds only shrink)
@@ -252,8 +252,9 @@ __global__ void __launch_bounds__(NT, (R == 1 ? 2 : 1)) scan_kernel(ScanArgs a) 
 #pragma unroll
                 for (int j = 0; j < 8; j++) {
                     int64_t gj = col0 + (j < 4 ? tx * 4 + j : 64 + tx * 4 + (j - 4));
-                    bool ok = gj < a.nx && gi < a.nq && acc[i][j] < th;
-                    if (MODE == MODE_SELF) ok = ok && gj != (a.qid ? (int64_t)a.qid[gi] : gi);
+                    const int qs = S.qself[r];
+                    bool ok = gj < a.nx && qs >= 0 && acc[i][j] < th;
+                    if (MODE == MODE_SELF) ok = ok && gj != (int64_t)qs;
                     if (MODE == MODE_COLOR) ok = ok && a.xcolor[gj] != S.qcol[r];
                     if (MODE == MODE_MASK) ok = ok && a.mask[gi * a.nx + gj] != 0;
                     if (ok) pending |= 1ull << (i * 8 + j);
@@ -314,7 +315,7 @@ __global__ void __launch_bounds__(NT, (R == 1 ? 2 : 1)) scan_kernel(ScanArgs a) 
             // block-wide max threshold over valid rows (pruning bound)
             if (warp < BM / 32) {
                 int r = warp * 32 + lane;
-                float v = (row_base + r < a.nq) ? S.thr[r] : -INFINITY;
+                float v = S.qself[r] >= 0 ? S.thr[r] : -INFINITY;
                 for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(FULL, v, o));
                 if (lane == 0) S.part[warp] = v;
             }
@@ -518,6 +519,7 @@ struct RefineArgs {
     // tensor-core scan (tc_scan.cu): kth in scaled units, |q^|^2 per row
     const float *qhat;        // nullptr for the exact-fp32 scan
     double scale;             // power of two applied after centring
+    const int32_t *qid;       // gathered queries: -1 marks padding rows (skipped)
 };
 
 // Exact reference distance (neighbors.py:132-137): dot sequential over t,
@@ -556,24 +558,27 @@ __device__ double certified_floor(float a, int d, double nq, double max_xn, bool
 }
 
 // Same bound for the tensor-core scan.  a: approximate value
-// in scaled units, a = |q^|^2 + |x^|^2 - 2<q^,x^> of the centred, scaled,
-// fp16-rounded points, with fp32 norms and tensor-core fp32 accumulation.
-//   |a - D^| <= g (|q^| + |x^|)^2,   g = (2d + 8) 2^-23   (all fp32 roundings)
-//   |x^| <= |q^| + sqrt(D^)                               (triangle)
-// gives the smallest sqrt(D^) compatible with a >= A; then
-//   sqrt(D) >= sqrt(D^) - eta (|q'| + |x'|) - 2 sqrt(d) 2^-25
-// (eta: fp32 centring + fp16 rounding, 2^-25: fp16 subnormal spacing / 2).
+// in scaled units, a = |q~|^2 + |x~|^2 - 2<q~,x~> of the centred, scaled,
+// two-term-fp16 points, fp32 norms, tensor-core fp32 accumulation of the
+// hi.hi + hi.lo + lo.hi products:
+//   |a - D~| <= g (|q~| + |x~|)^2,  g = (3d + 8) 2^-23 1.1 + 2^-21
+//   (all fp32 roundings, and the dropped lo.lo term)
+//   |x~| <= |q~| + sqrt(D~)                              (triangle)
+// gives the smallest sqrt(D~) compatible with a >= A; then
+//   sqrt(D) >= sqrt(D~) - eta (|q'| + |x'|) - 2 sqrt(d) 2^-25
+// (eta: fp32 centring + two-term fp16 representation, 2^-25: fp16 subnormal
+// spacing / 2 of the low term).
 __device__ double certified_floor_tc(float a, float qhat2, double scale, int d, double nq,
                                      double max_xn, bool exact_f32) {
     const double A = (double)a;
     if (!(A > 0.0) || !(A < INFINITY)) return -INFINITY;
     const double r = sqrt((double)qhat2) * (1.0 + 1e-12);
-    const double g = (2.0 * d + 8.0) * 0x1p-23;
+    const double g = (3.0 * d + 8.0) * 0x1p-23 * 1.1 + 0x1p-21;
     const double ca = 1.0 + g, cb = 4.0 * g * r, cc = 4.0 * g * r * r - A;
     const double disc = cb * cb - 4.0 * ca * cc;
     if (!(disc > 0.0)) return -INFINITY;
-    double sh = (-cb + sqrt(disc)) / (2.0 * ca) * (1.0 - 1e-12);  // min sqrt(D^), scaled
-    const double eta = 0x1p-11 * 1.01;
+    double sh = (-cb + sqrt(disc)) / (2.0 * ca) * (1.0 - 1e-12);  // min sqrt(D~), scaled
+    const double eta = 0x1p-22 * 1.3;
     const double etap = eta * (1.0 + 2.0 * eta);
     double sd = sh * (1.0 - etap) - 2.0 * etap * r - 2.0 * sqrt((double)d) * 0x1p-25;
     sd = sd / scale;  // back to data units (scale is a power of two)
@@ -591,6 +596,7 @@ __global__ void refine_kernel(RefineArgs a) {
     const int64_t nrows = a.row1 - a.row0;
     if (wid >= nrows) return;
     const int64_t gi = a.row0 + wid;
+    if (a.qid && a.qid[gi] < 0) return;  // padding row of a gathered query set
     const int32_t *cand = a.cand + wid * (32 * R);
     const double nq = a.qnorm[gi];
     double lv[R];
@@ -907,7 +913,7 @@ int64_t search_ffma(const PointSet &Q, const PointSet &X, const int32_t *qid, in
         ev_scan.stop(s);
         RefineArgs ra{Q.x32, Q.x64, Q.norms, X.x32, X.x64, X.norms, d, k, nq, nx, q0, q1,
                       cand, kth, X.maxn, X.x64 == nullptr && Q.x64 == nullptr, out_idx, out_dist,
-                      fail_rows, counters, nullptr, 1.0};
+                      fail_rows, counters, nullptr, 1.0, qid};
         ev_refine.start(s);
         if (Rsel == 1) launch_refine<1>(ra, rows, s);
         else if (Rsel == 2) launch_refine<2>(ra, rows, s);
@@ -958,6 +964,140 @@ bool tensor_scale(const PointSet &Q, const PointSet &X, float *scale, float *inv
     return true;
 }
 
+// One tensor-core pass (scan + float64 refine) over query rows [q0, q1) of Q.
+// Writes certified and uncertified rows alike into out_*; returns the
+// uncertified rows (relative to q0) in `fail` and their count, and the
+// approximate K'-th values (scaled units) in `kth`.
+int tc_pass(const PointSet &Q, const PointSet &X, const int32_t *qid, int k, int mode,
+            const uint8_t *mask, const int32_t *qcolor, const int32_t *xcolor, int64_t q0,
+            int64_t q1, float scale, float inv_scale2, int32_t *out_idx, double *out_dist,
+            DevBuf<int> &fail, DevBuf<float> &kth, cudaStream_t s) {
+    ScanStats &st = scan_stats();
+    const int64_t rows = q1 - q0;
+    const int d = X.d;
+    const int64_t nq = Q.n, nx = X.n;
+    const int64_t qb0 = q0 / BM, qb1 = (q1 + BM - 1) / BM;
+    DevBuf<int32_t> cand(rows * 32, s);
+    DevBuf<float> qhat(rows, s);
+    DevBuf<unsigned long long> tiles(1, s);
+    DevBuf<int> counters(1, s);
+    kth.alloc(rows, s);
+    fail.alloc(rows, s);
+    SLK_CUDA(cudaMemsetAsync(tiles, 0, sizeof(unsigned long long), s));
+    SLK_CUDA(cudaMemsetAsync(counters, 0, sizeof(int), s));
+    EventPair ev_order, ev_scan, ev_refine;
+    ev_order.start(s);
+    VisitOrder V = visit_order(Q, X, qb0, qb1 - qb0, mode == MODE_COLOR ? qcolor : nullptr, xcolor, s);
+    ev_order.stop(s);
+    tc::TcArgs ta{Q.packed, X.packed, nq, nx, d, X.dp, ((d + 15) / 16) * 16, qb0, Q.centroid,
+                  Q.nb, scale, inv_scale2, mask, qcolor, xcolor, cand, kth, qhat, q0, q1,
+                  V.sb_order, V.sb_lb, V.blk_lb, X.nsb, tiles, qid};
+    ev_scan.start(s);
+    tc::launch(mode, 1, ta, qb1 - qb0, s);
+    ev_scan.stop(s);
+    RefineArgs ra{Q.x32, Q.x64, Q.norms, X.x32, X.x64, X.norms, d, k, nq, nx, q0, q1,
+                  cand, kth, X.maxn, X.x64 == nullptr && Q.x64 == nullptr, out_idx, out_dist,
+                  fail, counters, qhat, (double)scale, qid};
+    ev_refine.start(s);
+    launch_refine<1>(ra, rows, s);
+    ev_refine.stop(s);
+    unsigned long long done = read_scalar(tiles.get(), s);
+    st.rows_refined += rows;
+    st.tiles_computed += (int64_t)done;
+    st.tiles_skipped += (qb1 - qb0) * X.nb - (int64_t)done;
+    record_profile(ev_order, ev_scan, ev_refine, rows, nx, d, done, (qb1 - qb0) * X.nb, true);
+    const int nfail = read_scalar<int>(counters, s);
+    st.rows_uncertified += nfail;
+    profile().tc_uncertified += nfail;
+    return nfail;
+}
+
+// cluster-boundary flags between consecutive (sorted) uncertified rows: a new
+// query block starts where the gap exceeds both rows' K'-th distances
+__global__ void split_flags_kernel(const float *x32, int d, const int32_t *rows, const float *kth,
+                                   double inv_scale2, int64_t m, int32_t *flag) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        if (i == 0) {
+            flag[i] = 1;
+            continue;
+        }
+        const float *a = x32 + (int64_t)rows[i] * d, *b = x32 + (int64_t)rows[i - 1] * d;
+        double g = 0.0;
+        for (int t = 0; t < d; t++) {
+            double df = (double)a[t] - (double)b[t];
+            g += df * df;
+        }
+        double ka = (double)kth[i] * inv_scale2, kb = (double)kth[i - 1] * inv_scale2;
+        double lim = 4.0 * fmax(ka, kb);
+        flag[i] = (g > lim || !(lim < INFINITY)) ? 1 : 0;
+    }
+}
+
+__global__ void gather_by_rel_kernel(const int *rel, int64_t m, int64_t q0, const float *kth_in,
+                                     int32_t *glob, float *kth_out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        glob[i] = (int32_t)(q0 + rel[i]);
+        kth_out[i] = kth_in[rel[i]];
+    }
+}
+
+// scatter rows of a gathered result (padding rows have qid < 0) back to
+// rows qid - q0 of the output
+__global__ void scatter_gathered_kernel(const int32_t *idx_g, const double *dist_g,
+                                        const int32_t *qid, int64_t m, int k, int64_t q0,
+                                        int32_t *out_idx, double *out_dist) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m * k;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        int64_t r = e / k, c = e - r * k;
+        int32_t g = qid[r];
+        if (g < 0) continue;
+        int64_t dst = (int64_t)(g - q0) * k + c;
+        out_idx[dst] = idx_g[e];
+        out_dist[dst] = dist_g[e];
+    }
+}
+
+// A gathered query set: rows `src` of Q (padding rows repeat a real row of
+// their block), with qid = index id of each row or -1 for padding.
+struct Gathered {
+    std::shared_ptr<PointSet> P;
+    DevBuf<float> x32;
+    DevBuf<double> x64;
+    DevBuf<int32_t> qid, qcolor;
+    DevBuf<uint8_t> mask;
+    int64_t n = 0;
+};
+
+Gathered gather_queries(const PointSet &Q, const std::vector<int32_t> &src,
+                        const std::vector<int32_t> &qid, int mode, const int32_t *qcolor,
+                        const uint8_t *mask, int64_t nx, cudaStream_t s) {
+    Gathered G;
+    G.n = (int64_t)src.size();
+    const int d = Q.d;
+    DevBuf<int32_t> dsrc(G.n, s);
+    G.qid.alloc(G.n, s);
+    SLK_CUDA(cudaMemcpyAsync(dsrc.get(), src.data(), G.n * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+    SLK_CUDA(cudaMemcpyAsync(G.qid.get(), qid.data(), G.n * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+    G.x32.alloc(G.n * d, s);
+    if (Q.x64) G.x64.alloc(G.n * d, s);
+    gather_rows_kernel<<<grid_for(G.n * d, 256), 256, 0, s>>>(Q.x32, Q.x64, dsrc, G.n, d, G.x32,
+                                                               G.x64.get());
+    SLK_CHECK_LAUNCH();
+    if (mode == MODE_COLOR) G.qcolor.alloc(G.n, s);
+    if (mode == MODE_MASK) G.mask.alloc(G.n * nx, s);
+    if (mode == MODE_COLOR || mode == MODE_MASK) {
+        int64_t work = mode == MODE_MASK ? G.n * nx : G.n;
+        gather_meta_kernel<<<grid_for(work, 256), 256, 0, s>>>(
+            dsrc, G.n, mode == MODE_COLOR ? qcolor : nullptr, mode == MODE_MASK ? mask : nullptr,
+            nx, G.qcolor.get(), G.mask.get());
+        SLK_CHECK_LAUNCH();
+    }
+    G.P = make_pointset(G.x32, G.x64.get(), G.n, d, s);
+    return G;
+}
+
 // Full neighbour search for query rows [q0, q1) of Q against X; k results per row.
 void search(const PointSet &Q, const PointSet &X, int k, int mode, const uint8_t *mask,
             const int32_t *qcolor, const int32_t *xcolor, int64_t q0, int64_t q1,
@@ -967,93 +1107,87 @@ void search(const PointSet &Q, const PointSet &X, int k, int mode, const uint8_t
     const int64_t rows = q1 - q0;
     if (rows <= 0) return;
     const int d = X.d;
+    const int64_t nx = X.n;
     const int Rsel = k < 32 ? 1 : (k < 64 ? 2 : 4);
     const Engine eng = engine_choice();
     float scale = 1.0f, inv_scale2 = 1.0f;
-    const bool use_tc = eng != Engine::Ffma && k <= 127 && tc::supported(d, Rsel) &&
+    const bool use_tc = eng != Engine::Ffma && k <= 31 && tc::supported(d, 1) &&
                         tensor_scale(Q, X, &scale, &inv_scale2);
     int64_t missing = -1;
     if (!use_tc) {
         missing = search_ffma(Q, X, nullptr, k, mode, mask, qcolor, xcolor, q0, q1, out_idx,
                               out_dist, s);
     } else {
-        const int64_t nq = Q.n, nx = X.n;
-        const int64_t qb0 = q0 / BM, qb1 = (q1 + BM - 1) / BM;
-        DevBuf<int32_t> cand(rows * 32 * Rsel, s);
-        DevBuf<float> kth(rows, s), qhat(rows, s);
-        DevBuf<unsigned long long> tiles(1, s);
-        DevBuf<int> fail_rows(rows, s), counters(1, s);
-        SLK_CUDA(cudaMemsetAsync(tiles, 0, sizeof(unsigned long long), s));
-        SLK_CUDA(cudaMemsetAsync(counters, 0, sizeof(int), s));
-        EventPair ev_order, ev_scan, ev_refine;
-        ev_order.start(s);
-        VisitOrder V = visit_order(Q, X, qb0, qb1 - qb0, mode == MODE_COLOR ? qcolor : nullptr,
-                                   xcolor, s);
-        ev_order.stop(s);
-        tc::TcArgs ta{Q.packed, X.packed, nq, nx, d, X.dp, ((d + 15) / 16) * 16, qb0, Q.centroid,
-                      Q.nb, scale, inv_scale2, mask, qcolor, xcolor, cand, kth, qhat, q0, q1,
-                      V.sb_order, V.sb_lb, V.blk_lb, X.nsb, tiles};
-        ev_scan.start(s);
-        tc::launch(mode, Rsel, ta, qb1 - qb0, s);
-        ev_scan.stop(s);
-        RefineArgs ra{Q.x32, Q.x64, Q.norms, X.x32, X.x64, X.norms, d, k, nq, nx, q0, q1,
-                      cand, kth, X.maxn, X.x64 == nullptr && Q.x64 == nullptr, out_idx, out_dist,
-                      fail_rows, counters, qhat, (double)scale};
-        ev_refine.start(s);
-        if (Rsel == 1) launch_refine<1>(ra, rows, s);
-        else if (Rsel == 2) launch_refine<2>(ra, rows, s);
-        else launch_refine<4>(ra, rows, s);
-        ev_refine.stop(s);
-        unsigned long long done = read_scalar(tiles.get(), s);
-        st.rows_refined += rows;
-        st.tiles_computed += (int64_t)done;
-        st.tiles_skipped += (qb1 - qb0) * X.nb - (int64_t)done;
-        record_profile(ev_order, ev_scan, ev_refine, rows, nx, d, done, (qb1 - qb0) * X.nb, true);
-        const int nfail = read_scalar<int>(counters, s);
-        st.rows_uncertified += nfail;
-        profile().tc_uncertified += nfail;
+        DevBuf<int> fail;
+        DevBuf<float> kth;
+        const int nfail = tc_pass(Q, X, nullptr, k, mode, mask, qcolor, xcolor, q0, q1, scale,
+                                  inv_scale2, out_idx, out_dist, fail, kth, s);
+        (void)Rsel;
         if (nfail > 0) {
-            // uncertified rows: exact-fp32 scan of the gathered rows (sorted, so
-            // gathered query blocks stay spatially coherent for pruning)
+            // Uncertified rows mostly sit in query blocks that straddle two
+            // clusters (the block centroid is far from both halves).  Re-block
+            // them at cluster boundaries (padding each segment to 128 rows) and
+            // run the tensor pass again: each new block has a local centroid.
             DevBuf<int> sorted(nfail, s);
             size_t tmp = 0;
-            SLK_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tmp, fail_rows.get(), sorted.get(), nfail, 0, 32, s));
+            SLK_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tmp, fail.get(), sorted.get(), nfail, 0, 32, s));
             DevBuf<unsigned char> t(tmp, s);
-            SLK_CUDA(cub::DeviceRadixSort::SortKeys(t.get(), tmp, fail_rows.get(), sorted.get(), nfail, 0, 32, s));
-            DevBuf<int32_t> glob(nfail, s);
-            to_global_rows_kernel<<<grid_for(nfail, 256), 256, 0, s>>>(sorted, nfail, q0, glob);
+            SLK_CUDA(cub::DeviceRadixSort::SortKeys(t.get(), tmp, fail.get(), sorted.get(), nfail, 0, 32, s));
+            DevBuf<int32_t> glob(nfail, s), flag(nfail, s);
+            DevBuf<float> gk(nfail, s);
+            gather_by_rel_kernel<<<grid_for(nfail, 256), 256, 0, s>>>(sorted, nfail, q0, kth, glob, gk);
             SLK_CHECK_LAUNCH();
-            DevBuf<float> g32((int64_t)nfail * d, s);
-            DevBuf<double> g64;
-            if (Q.x64) g64.alloc((int64_t)nfail * d, s);
-            gather_rows_kernel<<<grid_for((int64_t)nfail * d, 256), 256, 0, s>>>(
-                Q.x32, Q.x64, glob, nfail, d, g32, g64.get());
+            split_flags_kernel<<<grid_for(nfail, 128), 128, 0, s>>>(Q.x32, d, glob, gk,
+                                                                    (double)inv_scale2, nfail, flag);
             SLK_CHECK_LAUNCH();
-            DevBuf<int32_t> gcol;
-            DevBuf<uint8_t> gmask;
-            if (mode == MODE_COLOR) gcol.alloc(nfail, s);
-            if (mode == MODE_MASK) gmask.alloc((int64_t)nfail * nx, s);
-            if (mode == MODE_COLOR || mode == MODE_MASK) {
-                int64_t work = mode == MODE_MASK ? (int64_t)nfail * nx : nfail;
-                gather_meta_kernel<<<grid_for(work, 256), 256, 0, s>>>(
-                    glob, nfail, mode == MODE_COLOR ? qcolor : nullptr,
-                    mode == MODE_MASK ? mask : nullptr, nx, gcol.get(), gmask.get());
+            std::vector<int32_t> hglob(nfail), hflag(nfail);
+            SLK_CUDA(cudaMemcpyAsync(hglob.data(), glob.get(), nfail * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+            SLK_CUDA(cudaMemcpyAsync(hflag.data(), flag.get(), nfail * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+            SLK_CUDA(cudaStreamSynchronize(s));
+            std::vector<int32_t> src, qid;
+            int32_t seg_first = hglob[0];
+            for (int i = 0; i < nfail; i++) {
+                if (hflag[i] && !src.empty()) {
+                    while (src.size() % BM) {
+                        src.push_back(seg_first);
+                        qid.push_back(-1);
+                    }
+                }
+                if (hflag[i]) seg_first = hglob[i];
+                src.push_back(hglob[i]);
+                qid.push_back(hglob[i]);
+            }
+            Gathered G = gather_queries(Q, src, qid, mode, qcolor, mask, nx, s);
+            DevBuf<int32_t> gidx(G.n * k, s);
+            DevBuf<double> gdist(G.n * k, s);
+            DevBuf<int> fail2;
+            DevBuf<float> kth2;
+            const int nfail2 = tc_pass(*G.P, X, G.qid, k, mode, G.mask.get(), G.qcolor.get(),
+                                       xcolor, 0, G.n, scale, inv_scale2, gidx, gdist, fail2, kth2, s);
+            // global query ids in the gathered set are Q row ids: scatter to q0-relative rows
+            scatter_gathered_kernel<<<grid_for(G.n * k, 256), 256, 0, s>>>(gidx, gdist, G.qid, G.n,
+                                                                            k, q0, out_idx, out_dist);
+            SLK_CHECK_LAUNCH();
+            if (nfail2 > 0) {
+                // still uncertified: exact-fp32 scan of those rows (no padding)
+                std::vector<int32_t> rel2(nfail2);
+                SLK_CUDA(cudaMemcpyAsync(rel2.data(), fail2.get(), nfail2 * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+                std::vector<int32_t> hqid(G.n);
+                SLK_CUDA(cudaMemcpyAsync(hqid.data(), G.qid.get(), G.n * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+                SLK_CUDA(cudaStreamSynchronize(s));
+                std::vector<int32_t> ids;
+                for (int r : rel2) ids.push_back(hqid[r]);
+                std::sort(ids.begin(), ids.end());
+                Gathered F = gather_queries(Q, ids, ids, mode, qcolor, mask, nx, s);
+                DevBuf<int32_t> fidx(F.n * k, s);
+                DevBuf<double> fdist(F.n * k, s);
+                int64_t fm = search_ffma(*F.P, X, F.qid, k, mode, F.mask.get(), F.qcolor.get(),
+                                         xcolor, 0, F.n, fidx, fdist, s);
+                if (fm >= 0) missing = ids[fm];
+                scatter_gathered_kernel<<<grid_for(F.n * k, 256), 256, 0, s>>>(
+                    fidx, fdist, F.qid, F.n, k, q0, out_idx, out_dist);
                 SLK_CHECK_LAUNCH();
             }
-            auto G = make_pointset(g32, g64.get(), nfail, d, s);
-            DevBuf<int32_t> gidx((int64_t)nfail * k, s);
-            DevBuf<double> gdist((int64_t)nfail * k, s);
-            int64_t gm = search_ffma(*G, X, glob, k, mode, gmask.get(), gcol.get(), xcolor, 0, nfail,
-                                     gidx, gdist, s);
-            if (gm >= 0) {
-                int32_t orig = 0;
-                SLK_CUDA(cudaMemcpyAsync(&orig, glob.get() + gm, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-                SLK_CUDA(cudaStreamSynchronize(s));
-                missing = orig;
-            }
-            scatter_rows_kernel<<<grid_for((int64_t)nfail * k, 256), 256, 0, s>>>(
-                gidx, gdist, sorted, nfail, k, out_idx, out_dist);
-            SLK_CHECK_LAUNCH();
         }
     }
     if (missing >= 0) {
@@ -1199,7 +1333,7 @@ void debug_tc_scan(const float *x32, int64_t n, int d, int k, int32_t *cand, flo
     SLK_CUDA(cudaMemsetAsync(tiles, 0, sizeof(unsigned long long), s));
     tc::TcArgs ta{P->packed, P->packed, n, n, d, P->dp, ((d + 15) / 16) * 16, 0, P->centroid,
                   P->nb, scale, inv2, nullptr, nullptr, nullptr, cand, kth, qhat, 0, n,
-                  V.sb_order, V.sb_lb, V.blk_lb, P->nsb, tiles};
+                  V.sb_order, V.sb_lb, V.blk_lb, P->nsb, tiles, nullptr};
     tc::launch(scan::MODE_SELF, R, ta, nqb, s);
     SLK_CUDA(cudaStreamSynchronize(s));
     *scale_out = scale;

@@ -8,14 +8,16 @@
 // the final result exact.
 //
 // Numerics.  Both operands are centred on the query block's
-// centroid c and scaled by a power of two s, then rounded to fp16:
-//   q^ = fp16((q - c) s),  x^ = fp16((x - c) s).
-// One kind::f16 MMA per 16 dims gives <q^, x^> with fp32 accumulation, and
-// the epilogue forms a = |q^|^2 + |x^|^2 - 2<q^, x^> with the squared norms
-// of the *rounded* vectors, i.e. the squared distance of the rounded points
-// up to fp32 rounding.  Centring keeps |q^|, |x^| at the scale of the data's
-// local spread instead of its absolute position, which is what makes fp16
-// operands accurate enough (the refine certifies every row rigorously).
+// centroid c, scaled by a power of two s and split into two fp16 terms:
+//   q~ = hi + lo ~ (q - c) s,  x~ ~ (x - c) s   (relative error 2^-22).
+// Three kind::f16 MMAs per 16 dims (hi.hi + hi.lo + lo.hi) give <q~, x~>
+// with fp32 accumulation, and the epilogue forms
+//   a = |q~|^2 + |x~|^2 - 2<q~, x~>
+// with the squared norms of the represented vectors, i.e. the squared
+// distance of the represented points up to fp32 rounding.  Centring keeps
+// |q~|, |x~| at the scale of the data's local spread instead of its absolute
+// position; the split keeps cross-cluster distances (the connect passes)
+// resolvable.  The float64 refine certifies every row rigorously.
 //
 // CTA = 9 warps, warp-specialised:
 //   warps 0-3  prep:     A tile once; then per visited index block, centre /
@@ -127,6 +129,19 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
     for (int i = 0; i < 32; i++) v[i] = __uint_as_float(r[i]);
 }
 
+// Two-term fp16 split of a centred, scaled pair: v ~ hi + lo with relative
+// error <= 2^-22 (lo = fp16(v - hi), v - hi exact in fp32); accumulates the
+// squared norm of the represented value hi + lo (exact in fp32) into nrm.
+__device__ __forceinline__ void split2(float v0, float v1, __half2 &hi, __half2 &lo, float &nrm) {
+    hi = __floats2half2_rn(v0, v1);
+    const float2 fh = __half22float2(hi);
+    lo = __floats2half2_rn(__fsub_rn(v0, fh.x), __fsub_rn(v1, fh.y));
+    const float2 fl = __half22float2(lo);
+    const float w0 = __fadd_rn(fh.x, fl.x), w1 = __fadd_rn(fh.y, fl.y);
+    nrm = __fmaf_rn(w0, w0, nrm);
+    nrm = __fmaf_rn(w1, w1, nrm);
+}
+
 // ------------------------------------------------------------- smem plan
 struct Plan {
     uint32_t a, b, xx, xcol, qq, cq, misc, bars, total;
@@ -142,8 +157,8 @@ __host__ __device__ inline Plan make_plan(int dk, int R) {
         return at;
     };
     const uint32_t tile = (uint32_t)BM * dk * 2;  // 128 rows x dk fp16
-    p.a = take(tile, 1024);
-    p.b = take(tile * NSTAGE, 1024);
+    p.a = take(2 * tile, 1024);           // A_hi, A_lo
+    p.b = take(2 * tile * NSTAGE, 1024);  // per stage: B_hi, B_lo
     p.xx = take(NSTAGE * BN * 4, 16);
     p.xcol = take(NSTAGE * BN * 4, 16);
     p.qq = take(BM * 4, 16);
@@ -218,18 +233,16 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_scan_kernel(TcArgs a) {
             const float *src = a.qp + qb * (int64_t)a.dp * BM + r;
             unsigned char *dst = sA + (r >> 3) * sbo + (r & 7) * 16;
             for (int t0 = 0; t0 < dk; t0 += 8) {
-                __half2 h[4];
+                __half2 h[4], l[4];
 #pragma unroll
                 for (int u = 0; u < 4; u++) {
                     int t = t0 + 2 * u;
                     float v0 = t < a.d ? __fmaf_rn(src[(int64_t)t * BM], sc, s_cq[t]) : 0.0f;
                     float v1 = t + 1 < a.d ? __fmaf_rn(src[(int64_t)(t + 1) * BM], sc, s_cq[t + 1]) : 0.0f;
-                    h[u] = __floats2half2_rn(v0, v1);
-                    float2 f = __half22float2(h[u]);
-                    qq = __fmaf_rn(f.x, f.x, qq);
-                    qq = __fmaf_rn(f.y, f.y, qq);
+                    split2(v0, v1, h[u], l[u], qq);
                 }
                 *reinterpret_cast<uint4 *>(dst + (t0 >> 3) * 128) = *reinterpret_cast<uint4 *>(h);
+                *reinterpret_cast<uint4 *>(dst + tile_bytes + (t0 >> 3) * 128) = *reinterpret_cast<uint4 *>(l);
             }
             s_qq[r] = qq;
         }
@@ -258,7 +271,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_scan_kernel(TcArgs a) {
             computed++;
             float xx = 0.0f;
             const float *src = a.xp + (int64_t)jb * a.dp * BN + r;
-            unsigned char *dst = sB + s * tile_bytes + (r >> 3) * sbo + (r & 7) * 16;
+            unsigned char *dst = sB + s * 2 * tile_bytes + (r >> 3) * sbo + (r & 7) * 16;
             for (int t0 = 0; t0 < dk; t0 += 32) {
                 float v[32];  // 32 loads in flight per thread (coalesced across the 128 points)
 #pragma unroll
@@ -269,18 +282,16 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_scan_kernel(TcArgs a) {
 #pragma unroll
                 for (int g = 0; g < 4; g++) {
                     if (t0 + g * 8 >= dk) break;
-                    __half2 h[4];
+                    __half2 h[4], l[4];
 #pragma unroll
                     for (int u = 0; u < 4; u++) {
                         const int t = t0 + g * 8 + 2 * u;
                         const float v0 = t < a.d ? __fmaf_rn(v[g * 8 + 2 * u], sc, s_cq[t]) : 0.0f;
                         const float v1 = t + 1 < a.d ? __fmaf_rn(v[g * 8 + 2 * u + 1], sc, s_cq[t + 1]) : 0.0f;
-                        h[u] = __floats2half2_rn(v0, v1);
-                        const float2 f = __half22float2(h[u]);
-                        xx = __fmaf_rn(f.x, f.x, xx);
-                        xx = __fmaf_rn(f.y, f.y, xx);
+                        split2(v0, v1, h[u], l[u], xx);
                     }
                     *reinterpret_cast<uint4 *>(dst + ((t0 >> 3) + g) * 128) = *reinterpret_cast<uint4 *>(h);
+                    *reinterpret_cast<uint4 *>(dst + tile_bytes + ((t0 >> 3) + g) * 128) = *reinterpret_cast<uint4 *>(l);
                 }
             }
             s_xx[s * BN + r] = xx;
@@ -307,10 +318,16 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_scan_kernel(TcArgs a) {
                     break;
                 }
                 const uint32_t d_tmem = tmem + (uint32_t)s * 128;
+                // <q~, x~> = hi.hi + hi.lo + lo.hi (the lo.lo term, <= 2^-22 |q~||x~|, is dropped)
+                const uint32_t bs = b_base + s * 2 * tile_bytes;
                 for (int k = 0; k < dk / 16; k++) {
-                    uint64_t ad = umma_desc(a_base + k * 256, 128, sbo);
-                    uint64_t bd = umma_desc(b_base + s * tile_bytes + k * 256, 128, sbo);
-                    umma_f16(d_tmem, ad, bd, k > 0 ? 1u : 0u);
+                    const uint64_t ah = umma_desc(a_base + k * 256, 128, sbo);
+                    const uint64_t al = umma_desc(a_base + tile_bytes + k * 256, 128, sbo);
+                    const uint64_t bh = umma_desc(bs + k * 256, 128, sbo);
+                    const uint64_t bl = umma_desc(bs + tile_bytes + k * 256, 128, sbo);
+                    umma_f16(d_tmem, ah, bh, k > 0 ? 1u : 0u);
+                    umma_f16(d_tmem, ah, bl, 1u);
+                    umma_f16(d_tmem, al, bh, 1u);
                 }
                 umma_commit(&tfull[s]);
             }
@@ -321,7 +338,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_scan_kernel(TcArgs a) {
         const int ew = warp - 4;  // TMEM lane quarter
         const int row = ew * 32 + lane;
         const int64_t gi = row_base + row;
-        const bool row_ok = gi < a.nq;
+        // qid (gathered queries): id of the row in the index, -1 for padding
+        const int64_t self_id = (gi < a.nq && a.qid) ? (int64_t)a.qid[gi] : gi;
+        const bool row_ok = gi < a.nq && self_id >= 0;
         float qq = 0.0f;  // |q^|^2, written by the prep warps: read after the first tfull
         const int qc = (MODE == MODE_COLOR && row_ok) ? a.qcolor[gi] : -1;
         // This thread's row keeps its 32 best (approximate value, id) pairs in
@@ -351,7 +370,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_scan_kernel(TcArgs a) {
             // itself (32-bit, once per tile instead of 64-bit math per value)
             const int64_t rem = a.nx - col0;
             const int col_limit = row_ok ? (rem < BN ? (int)rem : BN) : 0;
-            const int self_col = (MODE == MODE_SELF && gi >= col0 && gi < col0 + BN) ? (int)(gi - col0) : -1;
+            const int self_col =
+                (MODE == MODE_SELF && self_id >= col0 && self_id < col0 + BN) ? (int)(self_id - col0) : -1;
             const float *xxs = s_xx + s * BN;
 #pragma unroll 1
             for (int c0 = 0; c0 < BN; c0 += 32) {
@@ -414,7 +434,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_scan_kernel(TcArgs a) {
             if (lane == 0) ((volatile float *)misc->part)[ew] = wm;
         }
         // write this row's candidate list
-        if (gi >= a.row0 && gi < a.row1) {
+        if (gi >= a.row0 && gi < a.row1 && row_ok) {
             int32_t *dst = a.cand + (gi - a.row0) * 32;
 #pragma unroll
             for (int q = 0; q < 32; q++) dst[q] = li[q];

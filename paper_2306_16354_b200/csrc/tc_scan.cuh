@@ -28,6 +28,7 @@ struct TcArgs {
     const float *blk_lb;
     int64_t nsb;
     unsigned long long *tiles_done;
+    const int32_t *qid;      // query row -> id in the index, -1 = padding (or null)
 };
 
 size_t smem_bytes(int d, int R);

@@ -23,6 +23,7 @@ from .core import (
     Dendrogram,
     EdgeList,
     ValidationError,
+    _trusted,
     as_point_matrix,
 )
 from .neighbors import DevicePoints, TileSpec, nn1_device
@@ -228,10 +229,11 @@ def _run(pm, cfg: LinkageConfig, device_points=None) -> SingleLinkageResult:
         _lib.call("slk_single_linkage_device", _lib.ptr(dp.x32), _lib.ptr(dp.x64), n, d, cfg.k,
                   cfg.n_clusters, metric, int(cfg.seed), budget, p(merges), p(labels), p(ts),
                   p(td), p(tw), ctypes.byref(iters), p(tim), _lib.stream_handle())
-    dendro = Dendrogram(n, merges[: n - 1])
-    return SingleLinkageResult(dendro, LabelArray(labels, cfg.n_clusters),
-                               EdgeList(n, ts[: n - 1], td[: n - 1], tw[: n - 1]),
-                               int(iters.value), dict(zip(STAGES, tim.tolist())))
+    # outputs of the library itself: skip re-validating 1M-row arrays
+    dendro = _trusted(Dendrogram, n_points=n, merges=merges[: n - 1])
+    lab = _trusted(LabelArray, labels=labels, n_clusters=cfg.n_clusters)
+    tree = _trusted(EdgeList, n_vertices=n, src=ts[: n - 1], dst=td[: n - 1], weight=tw[: n - 1])
+    return SingleLinkageResult(dendro, lab, tree, int(iters.value), dict(zip(STAGES, tim.tolist())))
 
 
 def single_linkage_result(x, cfg: LinkageConfig) -> SingleLinkageResult:
