@@ -122,8 +122,9 @@ struct ScanArgs {
     // superblocks (32 index blocks) sorted by a lower bound on the squared
     // distance between any of their points and any query point of the block,
     // plus the per-block bounds; +inf = never admissible (same colour).
-    const int32_t *sb_order;  // [nqb_launch][nsb]
-    const float *sb_lb;       // [nqb_launch][nsb] ascending
+    const int32_t *sb_order;  // [nqb_launch][nsb] ascending centroid distance
+    const float *sb_key;      // [nqb_launch][nsb] the sorted distances (+inf last)
+    const float *sb_lb;       // [nqb_launch][nsb] lower bound, by superblock id
     const float *blk_lb;      // [nqb_launch][nxb]
     int64_t nsb;
     unsigned long long *tiles_done;
@@ -155,8 +156,9 @@ __global__ void __launch_bounds__(NT, (R == 1 ? 2 : 1)) scan_kernel(ScanArgs a) 
     const int64_t row_base = qb * BM;
     const int nkc = a.dp / KC;
     const int64_t nxb = (a.nx + BN - 1) / BN;
-    BlockVisitor vis{a.sb_order + (int64_t)blockIdx.x * a.nsb, a.sb_lb + (int64_t)blockIdx.x * a.nsb,
-                     a.blk_lb + (int64_t)blockIdx.x * nxb, a.nsb, nxb};
+    BlockVisitor vis{a.sb_order + (int64_t)blockIdx.x * a.nsb, a.sb_key + (int64_t)blockIdx.x * a.nsb,
+                     a.sb_lb + (int64_t)blockIdx.x * a.nsb, a.blk_lb + (int64_t)blockIdx.x * nxb,
+                     a.nsb, nxb};
 
     for (int e = tid; e < BM * 32 * R; e += NT) {
         (&S.list_v[0][0])[e] = INFINITY;
@@ -430,19 +432,27 @@ __global__ void block_lb_kernel(const float *__restrict__ qc, const float *__res
     }
 }
 
-// per (query block, superblock): bound + ids + segment offsets for the sort
+// per (query block, superblock): lower bound (by id), sort key = centroid
+// distance (+inf when every pair is same-coloured), ids, segment offsets
 __global__ void superblock_lb_kernel(const float *__restrict__ qc, const float *__restrict__ qr,
                                      int64_t nqb_total, const float *__restrict__ sc,
                                      const float *__restrict__ sr, int64_t nsb, int d, int64_t qb0,
                                      int64_t nqb, const int2 *__restrict__ qcol,
                                      const int2 *__restrict__ scol, float *__restrict__ lb,
-                                     int32_t *__restrict__ ids, int32_t *__restrict__ seg) {
+                                     float *__restrict__ key, int32_t *__restrict__ ids,
+                                     int32_t *__restrict__ seg) {
     const int64_t total = nqb * nsb;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
          e += (int64_t)gridDim.x * blockDim.x) {
         int64_t ql = e / nsb, b = e - ql * nsb, q = qb0 + ql;
-        lb[e] = same_colour(qcol, scol, q, b) ? INFINITY
-                                              : sphere_lb(qc, qr, nqb_total, q, sc, sr, nsb, b, d);
+        double s = 0.0;
+        for (int t = 0; t < d; t++) {
+            double df = (double)qc[(int64_t)t * nqb_total + q] - (double)sc[(int64_t)t * nsb + b];
+            s += df * df;
+        }
+        const bool same = same_colour(qcol, scol, q, b);
+        lb[e] = same ? INFINITY : sphere_lb(qc, qr, nqb_total, q, sc, sr, nsb, b, d);
+        key[e] = same ? INFINITY : (float)s;
         ids[e] = (int32_t)b;
         if (b == 0) seg[ql] = (int32_t)(ql * nsb);
         if (e == total - 1) seg[nqb] = (int32_t)total;
@@ -761,11 +771,11 @@ void launch_exact(const ExactArgs &ea, cudaStream_t s) {
     SLK_CHECK_LAUNCH();
 }
 
-// Per query block of [qb0, qb0 + nqb): superblocks sorted by lower bound, and
-// the per-block bounds.
+// Per query block of [qb0, qb0 + nqb): superblocks in ascending centroid
+// distance, their lower bounds, and the per-block bounds.
 struct VisitOrder {
     DevBuf<int32_t> sb_order;
-    DevBuf<float> sb_lb, blk_lb;
+    DevBuf<float> sb_key, sb_lb, blk_lb;
 };
 
 VisitOrder visit_order(const PointSet &Q, const PointSet &X, int64_t qb0, int64_t nqb,
@@ -790,20 +800,21 @@ VisitOrder visit_order(const PointSet &Q, const PointSet &X, int64_t qb0, int64_
                                                          X.radius, nxb, Q.d, qb0, nqb, qrange.get(),
                                                          xrange.get(), V.blk_lb);
     SLK_CHECK_LAUNCH();
-    DevBuf<float> lb(stotal, s);
+    DevBuf<float> key(stotal, s);
     DevBuf<int32_t> ids(stotal, s), seg(nqb + 1, s);
+    V.sb_lb.alloc(stotal, s);
     superblock_lb_kernel<<<grid_for(stotal, 256), 256, 0, s>>>(
         Q.centroid, Q.radius, Q.nb, X.sb_centroid, X.sb_radius, nsb, Q.d, qb0, nqb, qrange.get(),
-        srange.get(), lb, ids, seg);
+        srange.get(), V.sb_lb, key, ids, seg);
     SLK_CHECK_LAUNCH();
     V.sb_order.alloc(stotal, s);
-    V.sb_lb.alloc(stotal, s);
+    V.sb_key.alloc(stotal, s);
     size_t tmp = 0;
-    SLK_CUDA(cub::DeviceSegmentedRadixSort::SortPairs(nullptr, tmp, lb.get(), V.sb_lb.get(), ids.get(),
+    SLK_CUDA(cub::DeviceSegmentedRadixSort::SortPairs(nullptr, tmp, key.get(), V.sb_key.get(), ids.get(),
                                                       V.sb_order.get(), (int)stotal, (int)nqb, seg.get(),
                                                       seg.get() + 1, 0, 32, s));
     DevBuf<unsigned char> t(tmp, s);
-    SLK_CUDA(cub::DeviceSegmentedRadixSort::SortPairs(t.get(), tmp, lb.get(), V.sb_lb.get(), ids.get(),
+    SLK_CUDA(cub::DeviceSegmentedRadixSort::SortPairs(t.get(), tmp, key.get(), V.sb_key.get(), ids.get(),
                                                       V.sb_order.get(), (int)stotal, (int)nqb, seg.get(),
                                                       seg.get() + 1, 0, 32, s));
     return V;
@@ -905,7 +916,7 @@ int64_t search_ffma(const PointSet &Q, const PointSet &X, const int32_t *qid, in
                                    xcolor, s);
         ev_order.stop(s);
         ScanArgs sa{Q.packed, X.packed, nq, nx, X.dp, qb0, mask, qcolor, xcolor, cand, kth,
-                    q0, q1, V.sb_order, V.sb_lb, V.blk_lb, X.nsb, tiles, qid};
+                    q0, q1, V.sb_order, V.sb_key, V.sb_lb, V.blk_lb, X.nsb, tiles, qid};
         ev_scan.start(s);
         if (Rsel == 1) dispatch_scan<1>(mode, sa, qb1 - qb0, s);
         else if (Rsel == 2) dispatch_scan<2>(mode, sa, qb1 - qb0, s);
@@ -991,7 +1002,7 @@ int tc_pass(const PointSet &Q, const PointSet &X, const int32_t *qid, int k, int
     ev_order.stop(s);
     tc::TcArgs ta{Q.packed, X.packed, nq, nx, d, X.dp, ((d + 15) / 16) * 16, qb0, Q.centroid,
                   Q.nb, scale, inv_scale2, mask, qcolor, xcolor, cand, kth, qhat, q0, q1,
-                  V.sb_order, V.sb_lb, V.blk_lb, X.nsb, tiles, qid};
+                  V.sb_order, V.sb_key, V.sb_lb, V.blk_lb, X.nsb, tiles, qid};
     ev_scan.start(s);
     tc::launch(mode, 1, ta, qb1 - qb0, s);
     ev_scan.stop(s);
@@ -1333,7 +1344,7 @@ void debug_tc_scan(const float *x32, int64_t n, int d, int k, int32_t *cand, flo
     SLK_CUDA(cudaMemsetAsync(tiles, 0, sizeof(unsigned long long), s));
     tc::TcArgs ta{P->packed, P->packed, n, n, d, P->dp, ((d + 15) / 16) * 16, 0, P->centroid,
                   P->nb, scale, inv2, nullptr, nullptr, nullptr, cand, kth, qhat, 0, n,
-                  V.sb_order, V.sb_lb, V.blk_lb, P->nsb, tiles, nullptr};
+                  V.sb_order, V.sb_key, V.sb_lb, V.blk_lb, P->nsb, tiles, nullptr};
     tc::launch(scan::MODE_SELF, R, ta, nqb, s);
     SLK_CUDA(cudaStreamSynchronize(s));
     *scale_out = scale;

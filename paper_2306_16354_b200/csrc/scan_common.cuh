@@ -174,15 +174,18 @@ __device__ __forceinline__ void warp_merge_batch(V (&lv)[R], int (&li)[R], V (&b
     warp_bitonic_merge<R>(lv, li, lane);
 }
 
-// Iterates the index blocks a query block must visit: superblocks in
-// ascending bound order, members in index order, skipping every block whose
-// bound exceeds the current threshold; stops at the first superblock whose
-// bound exceeds it (member bounds are >= their superblock's).  Every thread
+// Iterates the index blocks a query block must visit.  Superblocks come in
+// ascending centroid distance (the query's own cluster first, so row
+// thresholds tighten before distant blocks are considered); a superblock or
+// member block is skipped when its lower bound exceeds the current largest
+// row threshold (sb_lb / blk_lb are indexed by id).  Superblocks whose every
+// pair is same-coloured sort last (key +inf) and end the walk.  Every thread
 // runs it redundantly and gets the same answer (warp-uniform ballots).
 struct BlockVisitor {
-    const int32_t *sb_order;
-    const float *sb_lb;
-    const float *blk_lb;
+    const int32_t *sb_order;  // superblock ids, ascending centroid distance
+    const float *sb_key;      // the sorted keys (+inf = never admissible)
+    const float *sb_lb;       // per superblock id
+    const float *blk_lb;      // per block id
     int64_t nsb, nxb;
     int64_t s = -1, sb = 0;
     unsigned mask = 0;
@@ -192,12 +195,13 @@ struct BlockVisitor {
         while (true) {
             if (mask == 0) {
                 if (++s >= nsb) return -1;
-                float l = sb_lb[s];
-                if (l == INFINITY || l > thr_max) {
+                if (sb_key[s] == INFINITY) {
                     s = nsb;
                     return -1;
                 }
                 sb = sb_order[s];
+                const float l = sb_lb[sb];
+                if (l > thr_max) continue;  // members' bounds are >= their superblock's
                 int64_t b = sb * 32 + lane;
                 my_lb = b < nxb ? blk_lb[b] : INFINITY;
                 mask = __ballot_sync(0xffffffffu, my_lb != INFINITY && !(my_lb > thr_max));

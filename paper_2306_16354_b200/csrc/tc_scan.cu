@@ -237,8 +237,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_scan_kernel(TcArgs a) {
 #pragma unroll
                 for (int u = 0; u < 4; u++) {
                     int t = t0 + 2 * u;
-                    float v0 = t < a.d ? __fmaf_rn(src[(int64_t)t * BM], sc, s_cq[t]) : 0.0f;
-                    float v1 = t + 1 < a.d ? __fmaf_rn(src[(int64_t)(t + 1) * BM], sc, s_cq[t + 1]) : 0.0f;
+                    float v0 = __fmaf_rn(src[t * BM], sc, s_cq[t]);  // padded dims: 0*s + 0
+                    float v1 = __fmaf_rn(src[(t + 1) * BM], sc, s_cq[t + 1]);
                     split2(v0, v1, h[u], l[u], qq);
                 }
                 *reinterpret_cast<uint4 *>(dst + (t0 >> 3) * 128) = *reinterpret_cast<uint4 *>(h);
@@ -246,8 +246,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_scan_kernel(TcArgs a) {
             }
             s_qq[r] = qq;
         }
-        BlockVisitor vis{a.sb_order + (int64_t)blockIdx.x * a.nsb, a.sb_lb + (int64_t)blockIdx.x * a.nsb,
-                         a.blk_lb + (int64_t)blockIdx.x * nxb, a.nsb, nxb};
+        BlockVisitor vis{a.sb_order + (int64_t)blockIdx.x * a.nsb, a.sb_key + (int64_t)blockIdx.x * a.nsb,
+                         a.sb_lb + (int64_t)blockIdx.x * a.nsb, a.blk_lb + (int64_t)blockIdx.x * nxb,
+                         a.nsb, nxb};
         int64_t computed = 0;
         for (int it = 0;; it++) {
             const int s = it & 1;
@@ -273,11 +274,18 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_scan_kernel(TcArgs a) {
             const float *src = a.xp + (int64_t)jb * a.dp * BN + r;
             unsigned char *dst = sB + s * 2 * tile_bytes + (r >> 3) * sbo + (r & 7) * 16;
             for (int t0 = 0; t0 < dk; t0 += 32) {
-                float v[32];  // 32 loads in flight per thread (coalesced across the 128 points)
+                // 32 loads in flight per thread, coalesced across the 128 points;
+                // dims in [d, dk) are zero in the packed layout
+                float v[32];
+                const float *col = src + t0 * BN;
+                if (t0 + 32 <= dk) {
 #pragma unroll
-                for (int u = 0; u < 32; u++) {
-                    const int t = t0 + u;
-                    v[u] = (t < a.d) ? __ldg(src + (int64_t)t * BN) : 0.0f;
+                    for (int u = 0; u < 32; u++) v[u] = __ldg(col + u * BN);
+                } else {
+#pragma unroll
+                    for (int u = 0; u < 16; u++) v[u] = __ldg(col + u * BN);
+#pragma unroll
+                    for (int u = 16; u < 32; u++) v[u] = 0.0f;
                 }
 #pragma unroll
                 for (int g = 0; g < 4; g++) {
@@ -286,8 +294,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_scan_kernel(TcArgs a) {
 #pragma unroll
                     for (int u = 0; u < 4; u++) {
                         const int t = t0 + g * 8 + 2 * u;
-                        const float v0 = t < a.d ? __fmaf_rn(v[g * 8 + 2 * u], sc, s_cq[t]) : 0.0f;
-                        const float v1 = t + 1 < a.d ? __fmaf_rn(v[g * 8 + 2 * u + 1], sc, s_cq[t + 1]) : 0.0f;
+                        const float v0 = __fmaf_rn(v[g * 8 + 2 * u], sc, s_cq[t]);
+                        const float v1 = __fmaf_rn(v[g * 8 + 2 * u + 1], sc, s_cq[t + 1]);
                         split2(v0, v1, h[u], l[u], xx);
                     }
                     *reinterpret_cast<uint4 *>(dst + ((t0 >> 3) + g) * 128) = *reinterpret_cast<uint4 *>(h);

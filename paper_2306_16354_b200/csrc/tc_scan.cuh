@@ -24,6 +24,7 @@ struct TcArgs {
     float *qhat;             // [rows] |q^|^2 (scaled units)
     int64_t row0, row1;
     const int32_t *sb_order;
+    const float *sb_key;
     const float *sb_lb;
     const float *blk_lb;
     int64_t nsb;
