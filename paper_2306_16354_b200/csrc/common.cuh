@@ -228,8 +228,10 @@ void csr_solve_mst(int64_t n, const int64_t *offs, const int32_t *cols, const do
 void dendrogram_device_sort(const int32_t *src, const int32_t *dst, const double *w, int64_t n,
                             bool take_sqrt, int32_t *h_a, int32_t *h_b, double *h_w,
                             cudaStream_t s);
+// labels (optional): the flat cut for n_clusters, taken during the fold
 void dendrogram_fold(const int32_t *a, const int32_t *b, const double *w, int64_t n,
-                     double *merges);
+                     double *merges, int64_t n_clusters = 0, int64_t *labels = nullptr,
+                     double *extract_ms = nullptr);
 void extract_labels(const double *merges, int64_t n, int64_t n_clusters, int64_t *labels);
 
 }  // namespace slk

@@ -183,10 +183,10 @@ void single_linkage_device(const float *x32, const double *x64, int64_t n, int d
     std::vector<int32_t> ha(n - 1), hb(n - 1);
     std::vector<double> hw(n - 1);
     dendrogram_device_sort(ts, td, tw, n, metric == 0, ha.data(), hb.data(), hw.data(), s);
-    dendrogram_fold(ha.data(), hb.data(), hw.data(), n, h_merges);
-    double t4 = now_ms();
-    extract_labels(h_merges, n, n_clusters, h_labels);
+    double extract_ms = 0.0;
+    dendrogram_fold(ha.data(), hb.data(), hw.data(), n, h_merges, n_clusters, h_labels, &extract_ms);
     double t5 = now_ms();
+    double t4 = t5 - extract_ms;  // the cut is taken inside the fold
     if (h_tree_src || h_tree_dst || h_tree_w) {
         std::vector<int32_t> hs(n - 1), hd(n - 1);
         SLK_CUDA(cudaMemcpyAsync(hs.data(), ts.get(), (n - 1) * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
