@@ -195,6 +195,68 @@ def load_traffic():
     return None
 
 
+def measured_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    try:
+        return json.loads(p.read_text()), "of measured"
+    except (OSError, json.JSONDecodeError):
+        return {"bf16_tflops": 1590.0, "hbm_gbs": 6650.0}, "of fallback"
+
+
+def make_roofline(prof, steps, d, sm_mhz):
+    """Roofline of the dominant kernel (the fused distance + top-K' scan).
+
+    achieved = algorithmic FLOP of the distance tiles the kernel computed
+    (2*128*128*d per computed 128x128 tile; pruned tiles excluded) / its
+    CUDA-event time inside the library (events on the launching stream).
+    Tensor-core kernel (tc_scan_kernel): bound "tensor", peak = measured dense
+    bf16 GEMM throughput (kind::f16 runs at the bf16 rate).  Exact-fp32 FFMA
+    kernel (scan_kernel, fallback): peak = 148 SM x 128 lanes x 2 x clock.
+    """
+    steps = max(steps, 1)
+    peaks, peak_src = measured_peaks()
+    tc = prof.get("tc_ms", 0.0) > 0
+    if tc:
+        ms, flops = prof["tc_ms"], prof["tc_flops_done"]
+        peak = float(peaks["bf16_tflops"])
+        dk = (d + 15) // 16 * 16
+        issued = flops / d * dk * 3  # three fp16 MMAs (hi.hi, hi.lo, lo.hi) over dk padded dims
+        kernel = "tc_scan_kernel (tcgen05 kind::f16 distance tiles + fused top-K' select)"
+        note = (f"peak = dense bf16/fp16 tensor throughput, burst, {peak_src} (MEASURED_PEAKS.json). "
+                "achieved counts 2*128*128*d FLOP per computed tile; the kernel issues 3 fp16 MMAs "
+                "per product (two-term split) over d padded to 16, see issued_tensor_frac. The kernel "
+                "is bound by its SIMT epilogue (threshold filter + top-K' insertion), not the tensor "
+                "pipe: DESIGN.md section 3.6.")
+    else:
+        ms, flops = prof["scan_ms"], prof["scan_flops_done"]
+        peak = SM_COUNT * FP32_LANES * 2 * sm_mhz * 1e6 / 1e12
+        issued = None
+        kernel = "scan_kernel (exact-fp32 FFMA distance tiles + fused top-K' select)"
+        note = (f"FP32 FFMA peak 148 SM x 128 lanes x 2 x {sm_mhz:.0f} MHz (median SM clock under "
+                "load); the direct form sum((q-x)^2) issues 2 FP32 ops per 2 algorithmic FLOP.")
+    achieved = flops / (ms / 1e3) / 1e12 if ms else None
+    traffic = load_traffic()
+    return {
+        "kernel": kernel, "bound": "tensor" if tc else "fp32",
+        "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+        "frac": achieved / peak if achieved else None,
+        "traffic": traffic.get("dram_bytes_per_launch") if traffic else None,
+        "traffic_note": traffic.get("note") if traffic else None,
+        "peak_note": note,
+        "issued_tensor_frac": (issued / (ms / 1e3) / 1e12 / peak) if (issued and ms) else None,
+        "algorithmic_flop_per_step": flops / steps,
+        "brute_force_flop_per_step": prof["scan_flops"] / steps,
+        "tiles_computed_frac": prof["scan_tiles"] / max(prof["scan_tiles_total"], 1),
+        "scan_ms_per_step": ms / steps,
+        "scan_launches_per_step": prof["scan_launches"] / steps,
+        "visit_order_ms_per_step": prof["order_ms"] / steps,
+        "refine_ms_per_step": prof["refine_ms"] / steps,
+        "rows_uncertified_per_step": prof.get("tc_uncertified", 0.0) / steps,
+        "rows_rescanned_per_step": prof["rescan_rows"] / steps,
+        "scan_engine": os.environ.get("SLK_SCAN", "auto"),
+    }
+
+
 def run_gpu(args, c, cfg_name):
     import torch
     import torch.distributed as dist
@@ -276,28 +338,7 @@ def run_gpu(args, c, cfg_name):
         return
     clocks = clk.summary()
     sm_mhz = clocks["sm_mhz"] or 1965.0
-    # achieved: FLOP of the tiles the kernel actually computed (pruned tiles excluded)
-    achieved = prof["scan_flops_done"] / (prof["scan_ms"] / 1e3) / 1e12 if prof["scan_ms"] else None
-    peak = SM_COUNT * FP32_LANES * 2 * sm_mhz * 1e6 / 1e12
-    traffic = load_traffic()
-    roofline = {
-        "kernel": "scan_kernel (fused exact-fp32 distance + top-K' select)",
-        "bound": "fp32", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-        "frac": achieved / peak if achieved else None,
-        "traffic": traffic.get("dram_bytes_per_launch") if traffic else None,
-        "peak_note": (f"FP32 FFMA peak 148 SM x 128 lanes x 2 x {sm_mhz:.0f} MHz (median SM clock "
-                      "under load); MEASURED_PEAKS.json has no FP32 figure. The direct form "
-                      "sum((q-x)^2) issues 2 FP32 ops per 2 algorithmic FLOP, so 0.5 is its ceiling."),
-        "algorithmic_flop_per_step": prof["scan_flops_done"] / max(args.steps, 1),
-        "brute_force_flop_per_step": prof["scan_flops"] / max(args.steps, 1),
-        "tiles_computed_frac": prof["scan_tiles"] / max(prof["scan_tiles_total"], 1),
-        "visit_order_ms_per_step": prof["order_ms"] / max(args.steps, 1),
-        "scan_ms_per_step": prof["scan_ms"] / max(args.steps, 1),
-        "scan_launches_per_step": prof["scan_launches"] / max(args.steps, 1),
-        "rows_rescanned_per_step": prof["rescan_rows"] / max(args.steps, 1),
-        "profile_per_step": {k: v / max(args.steps, 1) for k, v in prof.items()},
-        "scan_engine": os.environ.get("SLK_SCAN", "auto"),
-    }
+    roofline = make_roofline(prof, args.steps, c["d"], sm_mhz)
     cpu = None
     if not args.no_cpu_baseline and world == 1:
         b = cpu_slab_seconds(x, c, args.cpu_rows, cpu_cores(), n_iters=max(res.connect_iters, 1)
