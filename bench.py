@@ -317,6 +317,7 @@ def run_gpu(args, c, cfg_name):
 
     for _ in range(args.warmup):
         value_step()
+        e2e_step()  # the host-buffer path too: pinned staging and pool growth happen here
     barrier()
     _lib.profile(reset=True)
     launches0 = _lib.kernel_launches()
@@ -359,7 +360,8 @@ def run_gpu(args, c, cfg_name):
                    "connect_iters": getattr(res, "connect_iters", None),
                    "stage_ms": getattr(res, "timings", None)},
         "e2e": {"value": e2e, "unit": "s", "h2d_bytes_per_step": int(h2d),
-                "d2h_bytes_per_step": int(d2h)},
+                "d2h_bytes_per_step": int(d2h), "steps_s": [round(t, 5) for t in e2e_times]},
+        "value_steps_s": [round(t, 5) for t in times],
         "gpu_launches": int(launches),
         "roofline": roofline,
         "cpu_baseline": cpu,

@@ -170,6 +170,8 @@ struct PointSet {
     float maxabs = 0.0f;  // max |x| of the float32 values (tensor-path scaling)
     DevBuf<float> packed, centroid, radius, sb_centroid, sb_radius;
     DevBuf<double> norms, maxn;
+    // tensor-core scan operand layout (knn.cu:tcpack_kernel), built on first use
+    mutable DevBuf<float> tcpack;
 };
 std::shared_ptr<PointSet> make_pointset(const float *x32, const double *x64, int64_t n, int d,
                                         cudaStream_t s);

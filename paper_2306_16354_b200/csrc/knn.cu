@@ -59,6 +59,30 @@ __global__ void pack_blocks_kernel(const float *__restrict__ x, int64_t n, int d
     }
 }
 
+// Tensor-scan operand layout: block b is one contiguous run of 128 x dk
+// floats (dk = d rounded up to 16, zero padded) laid out so that the bytes of
+// point r, dims 8g..8g+3 sit at the fp16 "hi" core-matrix row of (r, g) and
+// dims 8g+4..8g+7 at the "lo" one (K-major, no swizzle: row group r>>3 every
+// dk*16 bytes, core matrix g every 128 bytes, row r&7 every 16 bytes).  One
+// bulk copy brings a block into shared memory and each thread converts its
+// own point in place (tc_scan.cu:convert_tile).
+__global__ void tcpack_kernel(const float *__restrict__ x, int64_t n, int d, int dk, int64_t nblocks,
+                              float *__restrict__ out) {
+    const int64_t total = nblocks * BN * (int64_t)dk;
+    const int64_t half = (int64_t)BN * dk / 2;  // floats per fp16 tile half
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t p = e / dk;
+        const int t = (int)(e - p * dk);
+        const float v = (p < n && t < d) ? x[p * d + t] : 0.0f;
+        const int64_t b = p / BN;
+        const int r = (int)(p - b * BN);
+        const int g = t >> 3, w = t & 7;
+        const int64_t off = (int64_t)(r >> 3) * (dk * 4) + g * 32 + (r & 7) * 4 + (w & 3);
+        out[b * BN * dk + (w >> 2) * half + off] = v;
+    }
+}
+
 // ref neighbors.py:80-89: acc += x[t]*x[t], sequential, no FMA.
 __global__ void norms_kernel(const float *__restrict__ x32, const double *__restrict__ x64,
                              int64_t n, int d, double *__restrict__ out) {
@@ -964,6 +988,20 @@ int64_t search_ffma(const PointSet &Q, const PointSet &X, const int32_t *qid, in
     return missing == 0x7fffffff ? -1 : missing;
 }
 
+// Candidates the tensor scan keeps per row: the smallest of 8 / 16 / 32 that
+// is at least 2k (the certificate compares the K'-th approximate value with
+// the k-th exact one, so K' = k + 1 leaves no slack for near-ties; measured
+// at C3: K' = 16 for k = 15 leaves 12 % of the rows uncertified, K' = 32
+// 0.5 %).  SLK_TC_KP overrides (it must exceed k).
+int tc_kp(int k) {
+    int kp = 2 * k <= 8 ? 8 : (2 * k <= 16 ? 16 : 32);
+    if (const char *e = getenv("SLK_TC_KP")) {
+        int v = atoi(e);
+        if (v > k && v <= 32) kp = v <= 8 ? 8 : (v <= 16 ? 16 : 32);
+    }
+    return kp;
+}
+
 // Power-of-two scale putting the centred operands in fp16's range: |x| s <= 2^13.
 bool tensor_scale(const PointSet &Q, const PointSet &X, float *scale, float *inv_scale2) {
     float m = fmaxf(Q.maxabs, X.maxabs);
@@ -973,6 +1011,17 @@ bool tensor_scale(const PointSet &Q, const PointSet &X, float *scale, float *inv
     *scale = ldexpf(1.0f, e);
     *inv_scale2 = ldexpf(1.0f, -2 * e);
     return true;
+}
+
+const float *ensure_tcpack(const PointSet &P, cudaStream_t s) {
+    if (!P.tcpack) {
+        const int dk = ((P.d + 15) / 16) * 16;
+        P.tcpack.alloc((size_t)P.nb * BN * dk, s);
+        tcpack_kernel<<<grid_for(P.nb * BN * (int64_t)dk, 256), 256, 0, s>>>(P.x32, P.n, P.d, dk, P.nb,
+                                                                            P.tcpack);
+        SLK_CHECK_LAUNCH();
+    }
+    return P.tcpack;
 }
 
 // One tensor-core pass (scan + float64 refine) over query rows [q0, q1) of Q.
@@ -1000,11 +1049,20 @@ int tc_pass(const PointSet &Q, const PointSet &X, const int32_t *qid, int k, int
     ev_order.start(s);
     VisitOrder V = visit_order(Q, X, qb0, qb1 - qb0, mode == MODE_COLOR ? qcolor : nullptr, xcolor, s);
     ev_order.stop(s);
-    tc::TcArgs ta{Q.packed, X.packed, nq, nx, d, X.dp, ((d + 15) / 16) * 16, qb0, Q.centroid,
-                  Q.nb, scale, inv_scale2, mask, qcolor, xcolor, cand, kth, qhat, q0, q1,
+    // colours of the index padded to whole blocks (one bulk copy per block)
+    DevBuf<int32_t> xcolp;
+    if (mode == MODE_COLOR) {
+        xcolp.alloc((size_t)X.nb * BN, s);
+        SLK_CUDA(cudaMemsetAsync(xcolp, 0xff, (size_t)X.nb * BN * sizeof(int32_t), s));
+        SLK_CUDA(cudaMemcpyAsync(xcolp, xcolor, (size_t)nx * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+    }
+    const float *qtc = ensure_tcpack(Q, s), *xtc = ensure_tcpack(X, s);
+    tc::TcArgs ta{qtc, xtc, nq, nx, d, X.dp, ((d + 15) / 16) * 16, qb0, Q.centroid,
+                  Q.nb, scale, inv_scale2, mask, qcolor, mode == MODE_COLOR ? xcolp.get() : xcolor,
+                  cand, kth, qhat, q0, q1,
                   V.sb_order, V.sb_key, V.sb_lb, V.blk_lb, X.nsb, tiles, qid};
     ev_scan.start(s);
-    tc::launch(mode, 1, ta, qb1 - qb0, s);
+    tc::launch(mode, tc_kp(k), ta, qb1 - qb0, s);
     ev_scan.stop(s);
     RefineArgs ra{Q.x32, Q.x64, Q.norms, X.x32, X.x64, X.norms, d, k, nq, nx, q0, q1,
                   cand, kth, X.maxn, X.x64 == nullptr && Q.x64 == nullptr, out_idx, out_dist,
@@ -1122,7 +1180,7 @@ void search(const PointSet &Q, const PointSet &X, int k, int mode, const uint8_t
     const int Rsel = k < 32 ? 1 : (k < 64 ? 2 : 4);
     const Engine eng = engine_choice();
     float scale = 1.0f, inv_scale2 = 1.0f;
-    const bool use_tc = eng != Engine::Ffma && k <= 31 && tc::supported(d, 1) &&
+    const bool use_tc = eng != Engine::Ffma && k <= 31 && tc::supported(d) &&
                         tensor_scale(Q, X, &scale, &inv_scale2);
     int64_t missing = -1;
     if (!use_tc) {
@@ -1335,17 +1393,17 @@ namespace slk {
 void debug_tc_scan(const float *x32, int64_t n, int d, int k, int32_t *cand, float *kth,
                    float *qhat, float *scale_out, cudaStream_t s) {
     auto P = make_pointset(x32, nullptr, n, d, s);
-    const int R = k < 32 ? 1 : (k < 64 ? 2 : 4);
     float scale = 1, inv2 = 1;
     if (!tensor_scale(*P, *P, &scale, &inv2)) throw_invalid("no tensor scale");
     const int64_t nqb = P->nb;
     VisitOrder V = visit_order(*P, *P, 0, nqb, nullptr, nullptr, s);
     DevBuf<unsigned long long> tiles(1, s);
     SLK_CUDA(cudaMemsetAsync(tiles, 0, sizeof(unsigned long long), s));
-    tc::TcArgs ta{P->packed, P->packed, n, n, d, P->dp, ((d + 15) / 16) * 16, 0, P->centroid,
+    const float *tcp = ensure_tcpack(*P, s);
+    tc::TcArgs ta{tcp, tcp, n, n, d, P->dp, ((d + 15) / 16) * 16, 0, P->centroid,
                   P->nb, scale, inv2, nullptr, nullptr, nullptr, cand, kth, qhat, 0, n,
                   V.sb_order, V.sb_key, V.sb_lb, V.blk_lb, P->nsb, tiles, nullptr};
-    tc::launch(scan::MODE_SELF, R, ta, nqb, s);
+    tc::launch(scan::MODE_SELF, tc_kp(k), ta, nqb, s);
     SLK_CUDA(cudaStreamSynchronize(s));
     *scale_out = scale;
 }

@@ -3,37 +3,41 @@
 // Same contract as the exact-fp32 scan in knn.cu (replaces the reference's
 // _knn_scan_tile / _nn1_scan_tile, /root/reference/pkg/src/parlink/
 // neighbors.py:119-160,191-217): one CTA owns 128 query rows for the whole
-// (pruned) index sweep and leaves, per row, the K' = 32R best candidates by
-// an approximate distance; the float64 refine + certificate in knn.cu makes
-// the final result exact.
+// (pruned) index sweep and leaves, per row, the K' best candidates by an
+// approximate distance; the float64 refine + certificate in knn.cu makes the
+// final result exact.
 //
 // Numerics.  Both operands are centred on the query block's
 // centroid c, scaled by a power of two s and split into two fp16 terms:
 //   q~ = hi + lo ~ (q - c) s,  x~ ~ (x - c) s   (relative error 2^-22).
 // Three kind::f16 MMAs per 16 dims (hi.hi + hi.lo + lo.hi) give <q~, x~>
-// with fp32 accumulation, and the epilogue forms
-//   a = |q~|^2 + |x~|^2 - 2<q~, x~>
-// with the squared norms of the represented vectors, i.e. the squared
-// distance of the represented points up to fp32 rounding.  Centring keeps
-// |q~|, |x~| at the scale of the data's local spread instead of its absolute
-// position; the split keeps cross-cluster distances (the connect passes)
-// resolvable.  The float64 refine certifies every row rigorously.
+// with fp32 accumulation; the epilogue forms b = |x~|^2 - 2<q~,x~> and the
+// row constant |q~|^2 is added once per row (a = |q~|^2 + b).  Centring keeps
+// |q~|, |x~| at the scale of the data's local spread; the split keeps
+// cross-cluster distances (the connect passes) resolvable.
 //
-// CTA = 9 warps, warp-specialised:
-//   warps 0-3  prep:     A tile once; then per visited index block, centre /
-//                        scale / round the 128 points into the canonical
-//                        K-major no-swizzle smem layout + their |x^|^2;
-//                        warp 0 also runs the pruning visitor.
-//   warp  8    MMA:      one elected thread issues tcgen05.mma (M=128,
-//                        N=128, K=16) into a TMEM accumulator stage and
-//                        tcgen05.commit's it to an mbarrier.
-//   warps 4-7  epilogue: tcgen05.ld one accumulator row per thread (thread
-//                        = query row), threshold filter (bit mask per 32
-//                        columns), branch-free shift-insertion into the
-//                        row's 32-entry register list.  No distance tile
-//                        ever reaches HBM.
-// Two pipeline stages (B tile + TMEM accumulator) overlap prep(t+1), MMA and
-// epilogue(t).
+// Operand staging.  The index is stored once per call in a "tc-packed" fp32
+// layout (tcpack_kernel in knn.cu): block jb is one contiguous 128 x dk x 4 B
+// run whose bytes sit exactly where the converted fp16 hi/lo UMMA tiles of
+// the same points go (point r, dims 8g..8g+3 at the hi core-matrix row of
+// (r, g), dims 8g+4..8g+7 at the lo one).  A block therefore arrives with
+// ONE cp.async.bulk (TMA bulk copy, mbarrier complete_tx) and is converted
+// in place, each thread touching only its own point's bytes.
+//
+// CTA = 10 warps, warp-specialised, all hand-offs on mbarriers:
+//   warp  9    producer: walks the pruned visit order (32 superblocks per
+//              step, ballots), issues the bulk copies of raw blocks (and their
+//              colours) into a ring of NB stages, NB - 1 blocks ahead.
+//   warps 0-3  convert:  centre / scale / split the stage in place into the
+//              canonical K-major no-swizzle layout + |x~|^2 per point.
+//   warp  8    MMA:      one elected thread issues tcgen05.mma (M=128, N=128,
+//              K=16) into one of NT TMEM accumulator stages, then commits to
+//              the stage's "B empty" and the accumulator's "full" barriers.
+//   warps 4-7  epilogue: tcgen05.ld one accumulator row per thread (thread =
+//              query row), chunk minimum vs the row threshold (fast path), and
+//              only for chunks with a hit: exact pass mask, staging of the 32
+//              values in smem, shift-insertion into the row's K'-entry
+//              register list.  No distance tile ever reaches HBM.
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -44,12 +48,9 @@
 
 namespace slk {
 namespace tc {
+namespace {
 
 using namespace scan;
-
-constexpr int NTHREADS = 288;
-constexpr int NSTAGE = 2;
-constexpr uint32_t TMEM_COLS = 256;  // 2 stages x 128 fp32 columns
 
 // ------------------------------------------------------------ PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
@@ -142,12 +143,22 @@ __device__ __forceinline__ void split2(float v0, float v1, __half2 &hi, __half2 
     nrm = __fmaf_rn(w1, w1, nrm);
 }
 
+
 // ------------------------------------------------------------- smem plan
+constexpr int NTHREADS = 320;
+constexpr int NT = 2;        // TMEM accumulator stages (128 fp32 columns each)
+constexpr int MAX_NB = 6;    // B operand stages
+constexpr int NMETA = MAX_NB + NT;  // per-tile metadata ring (see producer)
+constexpr uint32_t TMEM_COLS = NT * 128;
+constexpr int STG_STRIDE = 36;  // per-row chunk staging (36 floats: conflict-free STS.128)
+constexpr uint32_t SMEM_LIMIT = 227 * 1024;
+
 struct Plan {
-    uint32_t a, b, xx, xcol, qq, cq, misc, bars, total;
+    uint32_t a, b, xx, xcol, qq, cq, stg, misc, bars, total;
+    int nb;  // B stages that fit
 };
 
-__host__ __device__ inline Plan make_plan(int dk, int R) {
+__host__ __device__ inline Plan make_plan(int dk) {
     Plan p{};
     uint32_t off = 0;
     auto take = [&](uint32_t bytes, uint32_t align) {
@@ -156,56 +167,156 @@ __host__ __device__ inline Plan make_plan(int dk, int R) {
         off += bytes;
         return at;
     };
-    const uint32_t tile = (uint32_t)BM * dk * 2;  // 128 rows x dk fp16
-    p.a = take(2 * tile, 1024);           // A_hi, A_lo
-    p.b = take(2 * tile * NSTAGE, 1024);  // per stage: B_hi, B_lo
-    p.xx = take(NSTAGE * BN * 4, 16);
-    p.xcol = take(NSTAGE * BN * 4, 16);
+    const uint32_t stage = (uint32_t)BM * dk * 4;  // hi + lo fp16 tiles = raw fp32 block
+    p.a = take(stage, 1024);
+    p.xx = take(NMETA * BN * 4, 16);
+    p.xcol = take(NMETA * BN * 4, 16);
     p.qq = take(BM * 4, 16);
     p.cq = take(dk * 4, 16);
-    p.misc = take(64, 16);  // part[4] float, next block, stage blocks[2], tmem base
-    p.bars = take(8 * 3 * NSTAGE, 8);
+    p.stg = take(BM * STG_STRIDE * 4, 16);
+    p.misc = take(128, 16);
+    p.bars = take(8 * (4 * MAX_NB + 2 * NT + 1), 8);
+    off = (off + 1023) / 1024 * 1024;
+    int nb = off >= SMEM_LIMIT ? 0 : (int)((SMEM_LIMIT - off) / stage);
+    p.nb = nb > MAX_NB ? MAX_NB : nb;
+    p.b = take(stage * (p.nb > 0 ? p.nb : 0), 1024);
     p.total = off;
     return p;
 }
 
 struct Misc {
-    float part[4];
-    int next_blk;
-    int stage_blk[NSTAGE];
+    float part[4];            // per epilogue warp: largest row threshold (a units)
     uint32_t tmem_base;
+    int meta_blk[NMETA];      // block id of tile t at slot t % NMETA (-1 = end)
 };
 
-template <int MODE, int R>
+// ------------------------------------------------------------ PTX: TMA bulk
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+// Converts one 128-point operand tile in place (raw tc-packed fp32 -> fp16
+// hi/lo canonical layout); thread r owns point r.  Returns |x~|^2 of the
+// represented point.
+__device__ __forceinline__ float convert_tile(unsigned char *tile, int r, int dk, float sc,
+                                              const float *s_cq) {
+    const uint32_t half_bytes = (uint32_t)BM * dk * 2;
+    unsigned char *row = tile + (r >> 3) * (dk * 16) + (r & 7) * 16;
+    float nrm = 0.0f;
+#pragma unroll 2
+    for (int g = 0; g < dk / 8; g++) {
+        float4 *ph = reinterpret_cast<float4 *>(row + g * 128);
+        float4 *pl = reinterpret_cast<float4 *>(row + half_bytes + g * 128);
+        const float4 u = *ph, w = *pl;
+        const float4 c0 = *reinterpret_cast<const float4 *>(s_cq + 8 * g);
+        const float4 c1 = *reinterpret_cast<const float4 *>(s_cq + 8 * g + 4);
+        const float v[8] = {__fmaf_rn(u.x, sc, c0.x), __fmaf_rn(u.y, sc, c0.y), __fmaf_rn(u.z, sc, c0.z),
+                            __fmaf_rn(u.w, sc, c0.w), __fmaf_rn(w.x, sc, c1.x), __fmaf_rn(w.y, sc, c1.y),
+                            __fmaf_rn(w.z, sc, c1.z), __fmaf_rn(w.w, sc, c1.w)};
+        __half2 h[4], l[4];
+#pragma unroll
+        for (int q = 0; q < 4; q++) split2(v[2 * q], v[2 * q + 1], h[q], l[q], nrm);
+        *reinterpret_cast<uint4 *>(ph) = *reinterpret_cast<uint4 *>(h);
+        *reinterpret_cast<uint4 *>(pl) = *reinterpret_cast<uint4 *>(l);
+    }
+    return nrm;
+}
+
+// Pruned visit order of one query block, 32 superblocks per step: lanes load
+// the next 32 sorted superblock ids/keys and their bounds, a ballot keeps the
+// admissible ones, then each admissible superblock's 32 member bounds are
+// loaded at once.  Bounds are re-checked against the current threshold at
+// every step (thresholds only fall, so skipping stays exact).  Keys are
+// sorted with +inf (never admissible: every pair same-coloured) last.
+struct Visitor {
+    const int32_t *sb_order;
+    const float *sb_key, *sb_lb, *blk_lb;
+    int64_t nsb, nxb;
+    int64_t base = 0;
+    bool done = false;
+    unsigned sbmask = 0, bmask = 0;
+    int my_sb = 0, cur_sb = 0;
+    float my_sblb = INFINITY, my_blb = INFINITY;
+
+    __device__ int64_t next(float thr, int lane) {
+        while (true) {
+            if (bmask) {
+                const int m = __ffs(bmask) - 1;
+                bmask &= bmask - 1;
+                if (__shfl_sync(FULL, my_blb, m) > thr) continue;
+                return (int64_t)cur_sb * 32 + m;
+            }
+            if (sbmask) {
+                const int i = __ffs(sbmask) - 1;
+                sbmask &= sbmask - 1;
+                if (__shfl_sync(FULL, my_sblb, i) > thr) continue;
+                cur_sb = __shfl_sync(FULL, my_sb, i);
+                const int64_t b = (int64_t)cur_sb * 32 + lane;
+                my_blb = b < nxb ? __ldg(blk_lb + b) : INFINITY;
+                bmask = __ballot_sync(FULL, my_blb != INFINITY && !(my_blb > thr));
+                continue;
+            }
+            if (done) return -1;
+            const int64_t pos = base + lane;
+            const float key = pos < nsb ? __ldg(sb_key + pos) : INFINITY;
+            my_sb = pos < nsb ? __ldg(sb_order + pos) : 0;
+            my_sblb = key != INFINITY ? __ldg(sb_lb + my_sb) : INFINITY;
+            sbmask = __ballot_sync(FULL, key != INFINITY && !(my_sblb > thr));
+            base += 32;
+            if (base >= nsb || __ballot_sync(FULL, key == INFINITY)) done = true;
+        }
+    }
+};
+
+template <int MODE, int KP>
 __global__ void __launch_bounds__(NTHREADS, 1) tc_scan_kernel(TcArgs a) {
     extern __shared__ __align__(1024) unsigned char smem[];
     const int dk = a.dk;
-    const Plan P = make_plan(dk, R);
+    const Plan P = make_plan(dk);
+    const int nb = P.nb;
     unsigned char *sA = smem + P.a;
     unsigned char *sB = smem + P.b;
     float *s_xx = reinterpret_cast<float *>(smem + P.xx);
     int *s_xcol = reinterpret_cast<int *>(smem + P.xcol);
     float *s_qq = reinterpret_cast<float *>(smem + P.qq);
     float *s_cq = reinterpret_cast<float *>(smem + P.cq);
+    float *s_stg = reinterpret_cast<float *>(smem + P.stg);
     Misc *misc = reinterpret_cast<Misc *>(smem + P.misc);
-    uint64_t *bfull = reinterpret_cast<uint64_t *>(smem + P.bars);
-    uint64_t *tfull = bfull + NSTAGE;
-    uint64_t *sfree = tfull + NSTAGE;
+    uint64_t *rawfull = reinterpret_cast<uint64_t *>(smem + P.bars);  // producer -> convert
+    uint64_t *bfull = rawfull + MAX_NB;                                 // convert -> MMA
+    uint64_t *bempty = bfull + MAX_NB;                                  // MMA commit -> producer
+    uint64_t *tfull = bempty + MAX_NB;                                  // MMA commit -> epilogue
+    uint64_t *tempty = tfull + NT;                                      // epilogue -> MMA
+    uint64_t *afull = tempty + NT;                                      // A tile landed
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int64_t qb = a.qb0 + blockIdx.x;
     const int64_t row_base = qb * BM;
     const int64_t nxb = (a.nx + BN - 1) / BN;
-    const uint32_t tile_bytes = (uint32_t)BM * dk * 2;
+    const uint32_t stage_bytes = (uint32_t)BM * dk * 4;
+    const uint32_t half_bytes = (uint32_t)BM * dk * 2;
     const uint32_t sbo = (uint32_t)dk * 16;  // (dk/8) core matrices of 128 B per 8-row group
 
-    // ---- setup: barriers, TMEM, per-row state
+    // ---- setup: barriers, TMEM, centring constants
     if (tid == 0) {
-        for (int s = 0; s < NSTAGE; s++) {
+        for (int s = 0; s < MAX_NB; s++) {
+            mbar_init(&rawfull[s], 1);
             mbar_init(&bfull[s], 128);
-            mbar_init(&tfull[s], 1);
-            mbar_init(&sfree[s], 128);
+            mbar_init(&bempty[s], 1);
         }
+        for (int s = 0; s < NT; s++) {
+            mbar_init(&tfull[s], 1);
+            mbar_init(&tempty[s], 128);
+        }
+        mbar_init(afull, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         for (int i = 0; i < 4; i++) misc->part[i] = INFINITY;
     }
@@ -216,7 +327,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_scan_kernel(TcArgs a) {
                      : "memory");
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     }
-    // s_cq[t] = -c_t * s (exact: s is a power of two), so x^ = fp16(fma(x, s, s_cq[t]))
+    // s_cq[t] = -c_t * s (exact: s is a power of two), so x~ = fma(x, s, s_cq[t])
     for (int t = tid; t < dk; t += NTHREADS)
         s_cq[t] = t < a.d ? -a.qcentroid[(int64_t)t * a.nqb_total + qb] * a.scale : 0.0f;
     tc_fence_before();
@@ -224,205 +335,196 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_scan_kernel(TcArgs a) {
     tc_fence_after();
     const uint32_t tmem = misc->tmem_base;
 
-    if (warp < 4) {
-        // ===================== prep warps: A once, then B per visited block
-        const int r = tid;  // 0..127: query row (A) / index point (B)
-        const float sc = a.scale;
-        {
-            float qq = 0.0f;
-            const float *src = a.qp + qb * (int64_t)a.dp * BM + r;
-            unsigned char *dst = sA + (r >> 3) * sbo + (r & 7) * 16;
-            for (int t0 = 0; t0 < dk; t0 += 8) {
-                __half2 h[4], l[4];
-#pragma unroll
-                for (int u = 0; u < 4; u++) {
-                    int t = t0 + 2 * u;
-                    float v0 = __fmaf_rn(src[t * BM], sc, s_cq[t]);  // padded dims: 0*s + 0
-                    float v1 = __fmaf_rn(src[(t + 1) * BM], sc, s_cq[t + 1]);
-                    split2(v0, v1, h[u], l[u], qq);
-                }
-                *reinterpret_cast<uint4 *>(dst + (t0 >> 3) * 128) = *reinterpret_cast<uint4 *>(h);
-                *reinterpret_cast<uint4 *>(dst + tile_bytes + (t0 >> 3) * 128) = *reinterpret_cast<uint4 *>(l);
-            }
-            s_qq[r] = qq;
+    if (warp == 9) {
+        // ===================== producer: visit order + bulk copies
+        if (lane == 0) {
+            mbar_expect_tx(afull, stage_bytes);
+            bulk_g2s(sA, a.qp + qb * (int64_t)dk * BM, stage_bytes, afull);
         }
-        BlockVisitor vis{a.sb_order + (int64_t)blockIdx.x * a.nsb, a.sb_key + (int64_t)blockIdx.x * a.nsb,
-                         a.sb_lb + (int64_t)blockIdx.x * a.nsb, a.blk_lb + (int64_t)blockIdx.x * nxb,
-                         a.nsb, nxb};
+        Visitor vis{a.sb_order + (int64_t)blockIdx.x * a.nsb, a.sb_key + (int64_t)blockIdx.x * a.nsb,
+                    a.sb_lb + (int64_t)blockIdx.x * a.nsb, a.blk_lb + (int64_t)blockIdx.x * nxb,
+                    a.nsb, nxb};
         int64_t computed = 0;
         for (int it = 0;; it++) {
-            const int s = it & 1;
-            const uint32_t use = (uint32_t)(it >> 1);
-            // pruning decision by warp 0, broadcast to the 4 prep warps
-            if (warp == 0) {
-                volatile float *part = misc->part;
-                float thr_max = fmaxf(fmaxf(part[0], part[1]), fmaxf(part[2], part[3])) * a.inv_scale2;
-                int64_t jb = vis.next(thr_max, lane);
-                if (lane == 0) misc->next_blk = (int)jb;
-            }
-            asm volatile("bar.sync 1, 128;" ::: "memory");
-            const int jb = misc->next_blk;
-            asm volatile("bar.sync 2, 128;" ::: "memory");  // next_blk consumed before rewrite
-            mbar_wait(&sfree[s], (use & 1) ^ 1);
-            if (jb < 0) {
-                if (tid == 0) misc->stage_blk[s] = -1;
-                mbar_arrive(&bfull[s]);
-                break;
-            }
-            computed++;
-            float xx = 0.0f;
-            const float *src = a.xp + (int64_t)jb * a.dp * BN + r;
-            unsigned char *dst = sB + s * 2 * tile_bytes + (r >> 3) * sbo + (r & 7) * 16;
-            for (int t0 = 0; t0 < dk; t0 += 32) {
-                // 32 loads in flight per thread, coalesced across the 128 points;
-                // dims in [d, dk) are zero in the packed layout
-                float v[32];
-                const float *col = src + t0 * BN;
-                if (t0 + 32 <= dk) {
-#pragma unroll
-                    for (int u = 0; u < 32; u++) v[u] = __ldg(col + u * BN);
+            const int s = it % nb;
+            const uint32_t ph = (uint32_t)(it / nb) & 1u;
+            volatile float *part = misc->part;
+            const float thr = fmaxf(fmaxf(part[0], part[1]), fmaxf(part[2], part[3])) * a.inv_scale2;
+            const int64_t jb = vis.next(thr, lane);
+            if (lane == 0) {
+                mbar_wait(&bempty[s], ph ^ 1u);
+                misc->meta_blk[it % NMETA] = (int)jb;
+                if (jb < 0) {
+                    mbar_arrive(&rawfull[s]);
                 } else {
-#pragma unroll
-                    for (int u = 0; u < 16; u++) v[u] = __ldg(col + u * BN);
-#pragma unroll
-                    for (int u = 16; u < 32; u++) v[u] = 0.0f;
-                }
-#pragma unroll
-                for (int g = 0; g < 4; g++) {
-                    if (t0 + g * 8 >= dk) break;
-                    __half2 h[4], l[4];
-#pragma unroll
-                    for (int u = 0; u < 4; u++) {
-                        const int t = t0 + g * 8 + 2 * u;
-                        const float v0 = __fmaf_rn(v[g * 8 + 2 * u], sc, s_cq[t]);
-                        const float v1 = __fmaf_rn(v[g * 8 + 2 * u + 1], sc, s_cq[t + 1]);
-                        split2(v0, v1, h[u], l[u], xx);
-                    }
-                    *reinterpret_cast<uint4 *>(dst + ((t0 >> 3) + g) * 128) = *reinterpret_cast<uint4 *>(h);
-                    *reinterpret_cast<uint4 *>(dst + tile_bytes + ((t0 >> 3) + g) * 128) = *reinterpret_cast<uint4 *>(l);
+                    const bool col = MODE == MODE_COLOR;
+                    mbar_expect_tx(&rawfull[s], stage_bytes + (col ? BN * 4 : 0));
+                    bulk_g2s(sB + (size_t)s * stage_bytes, a.xp + jb * (int64_t)dk * BN, stage_bytes,
+                             &rawfull[s]);
+                    if (col)
+                        bulk_g2s(s_xcol + (it % NMETA) * BN, a.xcolor + jb * BN, BN * 4, &rawfull[s]);
+                    computed++;
                 }
             }
-            s_xx[s * BN + r] = xx;
-            if (MODE == MODE_COLOR) {
-                int64_t gj = (int64_t)jb * BN + r;
-                s_xcol[s * BN + r] = gj < a.nx ? a.xcolor[gj] : -1;
-            }
-            if (tid == 0) misc->stage_blk[s] = jb;
-            fence_async_smem();  // generic-proxy smem writes → visible to the tensor core
-            mbar_arrive(&bfull[s]);
+            if (jb < 0) break;
         }
-        if (tid == 0 && a.tiles_done) atomicAdd(a.tiles_done, (unsigned long long)computed);
+        if (lane == 0 && a.tiles_done) atomicAdd(a.tiles_done, (unsigned long long)computed);
+    } else if (warp < 4) {
+        // ===================== convert warps: A once, then every B stage in place
+        const int r = tid;  // 0..127: query row (A) / index point (B)
+        const float sc = a.scale;
+        mbar_wait(afull, 0);
+        s_qq[r] = convert_tile(sA, r, dk, sc, s_cq);
+        for (int it = 0;; it++) {
+            const int s = it % nb;
+            const uint32_t ph = (uint32_t)(it / nb) & 1u;
+            mbar_wait(&rawfull[s], ph);
+            const int jb = misc->meta_blk[it % NMETA];
+            if (jb >= 0) {
+                s_xx[(it % NMETA) * BN + r] = convert_tile(sB + (size_t)s * stage_bytes, r, dk, sc, s_cq);
+                fence_async_smem();  // generic-proxy smem writes -> visible to the tensor core
+            }
+            mbar_arrive(&bfull[s]);
+            if (jb < 0) break;
+        }
     } else if (warp == 8) {
         // ===================== MMA issuer (one elected thread)
         if (lane == 0) {
             const uint32_t a_base = smem_u32(sA), b_base = smem_u32(sB);
             for (int it = 0;; it++) {
-                const int s = it & 1;
-                const uint32_t use = (uint32_t)(it >> 1);
-                mbar_wait(&bfull[s], use & 1);
-                tc_fence_after();
-                if (misc->stage_blk[s] < 0) {
-                    mbar_arrive(&tfull[s]);
+                const int s = it % nb;
+                const uint32_t ph = (uint32_t)(it / nb) & 1u;
+                const int ts = it % NT;
+                const uint32_t tph = (uint32_t)(it / NT) & 1u;
+                mbar_wait(&bfull[s], ph);
+                // the accumulator stage must be drained even for the end marker:
+                // two completions of tfull[ts] ahead of the epilogue would alias
+                // its phase parity
+                mbar_wait(&tempty[ts], tph ^ 1u);
+                if (misc->meta_blk[it % NMETA] < 0) {
+                    mbar_arrive(&tfull[ts]);
                     break;
                 }
-                const uint32_t d_tmem = tmem + (uint32_t)s * 128;
+                tc_fence_after();
+                const uint32_t d_tmem = tmem + (uint32_t)ts * 128;
                 // <q~, x~> = hi.hi + hi.lo + lo.hi (the lo.lo term, <= 2^-22 |q~||x~|, is dropped)
-                const uint32_t bs = b_base + s * 2 * tile_bytes;
+                const uint32_t bs = b_base + s * stage_bytes;
                 for (int k = 0; k < dk / 16; k++) {
                     const uint64_t ah = umma_desc(a_base + k * 256, 128, sbo);
-                    const uint64_t al = umma_desc(a_base + tile_bytes + k * 256, 128, sbo);
+                    const uint64_t al = umma_desc(a_base + half_bytes + k * 256, 128, sbo);
                     const uint64_t bh = umma_desc(bs + k * 256, 128, sbo);
-                    const uint64_t bl = umma_desc(bs + tile_bytes + k * 256, 128, sbo);
+                    const uint64_t bl = umma_desc(bs + half_bytes + k * 256, 128, sbo);
                     umma_f16(d_tmem, ah, bh, k > 0 ? 1u : 0u);
                     umma_f16(d_tmem, ah, bl, 1u);
                     umma_f16(d_tmem, al, bh, 1u);
                 }
-                umma_commit(&tfull[s]);
+                umma_commit(&bempty[s]);  // operands consumed: the producer may refill stage s
+                umma_commit(&tfull[ts]);  // accumulator ready
             }
         }
         __syncwarp();
     } else {
-        // ===================== epilogue warps: one query row per thread
+        // ===================== epilogue warps (4-7): one query row per thread
         const int ew = warp - 4;  // TMEM lane quarter
         const int row = ew * 32 + lane;
         const int64_t gi = row_base + row;
         // qid (gathered queries): id of the row in the index, -1 for padding
         const int64_t self_id = (gi < a.nq && a.qid) ? (int64_t)a.qid[gi] : gi;
         const bool row_ok = gi < a.nq && self_id >= 0;
-        float qq = 0.0f;  // |q^|^2, written by the prep warps: read after the first tfull
+        float qq = 0.0f;  // |q~|^2, written by the convert warps: read after the first tfull
         const int qc = (MODE == MODE_COLOR && row_ok) ? a.qcolor[gi] : -1;
-        // This thread's row keeps its 32 best (approximate value, id) pairs in
-        // registers, ascending; thr = the 32nd.  Ties may be ordered either
-        // way: the certificate only needs every dropped candidate >= thr.
-        float lv[32];
-        int li[32];
+        float *stg = s_stg + row * STG_STRIDE;
+        // This thread's row keeps its KP best (b, id) pairs in registers,
+        // ascending, where b = |x~|^2 - 2<q~,x~> (a = |q~|^2 + b).  thr = the
+        // KP-th b; padding rows use -inf so they never take a candidate.  Ties
+        // may be ordered either way: the certificate only needs every dropped
+        // b >= thr.
+        float lv[KP];
+        int li[KP];
 #pragma unroll
-        for (int p = 0; p < 32; p++) {
+        for (int p = 0; p < KP; p++) {
             lv[p] = INFINITY;
             li[p] = -1;
         }
-        float thr = INFINITY;
+        float thr = row_ok ? INFINITY : -INFINITY;
 
         for (int it = 0;; it++) {
-            const int s = it & 1;
-            const uint32_t use = (uint32_t)(it >> 1);
-            mbar_wait(&tfull[s], use & 1);
+            const int ts = it % NT;
+            const uint32_t tph = (uint32_t)(it / NT) & 1u;
+            mbar_wait(&tfull[ts], tph);
             tc_fence_after();
-            // bfull (prep done with A and this B) happened before tfull
+            // the convert warps wrote A (and |q~|^2) before their first bfull arrive
             if (it == 0) qq = s_qq[row];
-            const int jb = misc->stage_blk[s];
+            const int slot = it % NMETA;
+            const int jb = misc->meta_blk[slot];
             if (jb < 0) break;
             const int64_t col0 = (int64_t)jb * BN;
-            const uint32_t taddr = tmem + ((uint32_t)(ew * 32) << 16) + (uint32_t)s * 128;
-            // columns this row may take from this block: inside the index, not
-            // itself (32-bit, once per tile instead of 64-bit math per value)
+            const uint32_t taddr = tmem + ((uint32_t)(ew * 32) << 16) + (uint32_t)ts * 128;
+            // columns this row may take from this block: inside the index, not itself
             const int64_t rem = a.nx - col0;
             const int col_limit = row_ok ? (rem < BN ? (int)rem : BN) : 0;
             const int self_col =
                 (MODE == MODE_SELF && self_id >= col0 && self_id < col0 + BN) ? (int)(self_id - col0) : -1;
-            const float *xxs = s_xx + s * BN;
+            const float *xxs = s_xx + slot * BN;
+            const int *xcs = s_xcol + slot * BN;
 #pragma unroll 1
             for (int c0 = 0; c0 < BN; c0 += 32) {
                 float dot[32];
                 tmem_ld32(taddr + c0, dot);
-                uint32_t valid = c0 >= col_limit ? 0u : (col_limit - c0 >= 32 ? 0xffffffffu : ((1u << (col_limit - c0)) - 1u));
-                if (self_col >= c0 && self_col < c0 + 32) valid &= ~(1u << (self_col - c0));
-                uint32_t pass = 0;
+                // fast path: b = fma(-2, dot, |x~|^2) and the chunk minimum
                 float av[32];
 #pragma unroll
                 for (int i = 0; i < 32; i += 4) {
                     const float4 x4 = *reinterpret_cast<const float4 *>(xxs + c0 + i);
-                    av[i + 0] = __fmaf_rn(-2.0f, dot[i + 0], __fadd_rn(qq, x4.x));
-                    av[i + 1] = __fmaf_rn(-2.0f, dot[i + 1], __fadd_rn(qq, x4.y));
-                    av[i + 2] = __fmaf_rn(-2.0f, dot[i + 2], __fadd_rn(qq, x4.z));
-                    av[i + 3] = __fmaf_rn(-2.0f, dot[i + 3], __fadd_rn(qq, x4.w));
-                    pass |= (av[i + 0] < thr ? 1u : 0u) << (i + 0);
-                    pass |= (av[i + 1] < thr ? 1u : 0u) << (i + 1);
-                    pass |= (av[i + 2] < thr ? 1u : 0u) << (i + 2);
-                    pass |= (av[i + 3] < thr ? 1u : 0u) << (i + 3);
+                    av[i + 0] = __fmaf_rn(-2.0f, dot[i + 0], x4.x);
+                    av[i + 1] = __fmaf_rn(-2.0f, dot[i + 1], x4.y);
+                    av[i + 2] = __fmaf_rn(-2.0f, dot[i + 2], x4.z);
+                    av[i + 3] = __fmaf_rn(-2.0f, dot[i + 3], x4.w);
                 }
-                pass &= valid;
-                if (MODE == MODE_COLOR && pass) {
+                float m16[16];
 #pragma unroll
-                    for (int i = 0; i < 32; i++)
-                        if (s_xcol[s * BN + c0 + i] == qc) pass &= ~(1u << i);
-                }
-                if (MODE == MODE_MASK && pass) {
-                    for (int i = 0; i < 32; i++)
-                        if (((pass >> i) & 1u) && a.mask[gi * a.nx + col0 + c0 + i] == 0) pass &= ~(1u << i);
+                for (int i = 0; i < 16; i++) m16[i] = fminf(av[i], av[i + 16]);
+#pragma unroll
+                for (int w = 8; w; w >>= 1)
+#pragma unroll
+                    for (int i = 0; i < w; i++) m16[i] = fminf(m16[i], m16[i + w]);
+                const bool hit = m16[0] < thr;
+                if (!__any_sync(FULL, hit)) continue;  // warp-uniform: nothing to insert
+                uint32_t pass = 0;
+                if (hit) {
+#pragma unroll
+                    for (int i = 0; i < 32; i++) pass |= (av[i] < thr ? 1u : 0u) << i;
+                    uint32_t valid = c0 >= col_limit ? 0u
+                                     : (col_limit - c0 >= 32 ? 0xffffffffu : ((1u << (col_limit - c0)) - 1u));
+                    if (self_col >= c0 && self_col < c0 + 32) valid &= ~(1u << (self_col - c0));
+                    pass &= valid;
+                    if (MODE == MODE_COLOR && pass) {
+#pragma unroll
+                        for (int i = 0; i < 32; i++)
+                            if (xcs[c0 + i] == qc) pass &= ~(1u << i);
+                    }
+                    if (MODE == MODE_MASK && pass) {
+                        for (int i = 0; i < 32; i++)
+                            if (((pass >> i) & 1u) && a.mask[gi * a.nx + col0 + c0 + i] == 0) pass &= ~(1u << i);
+                    }
+                    if (pass) {
+                        // stage the chunk: a passing value is one LDS away (no
+                        // dynamic register indexing)
+#pragma unroll
+                        for (int i = 0; i < 32; i += 4)
+                            *reinterpret_cast<float4 *>(stg + i) = make_float4(av[i], av[i + 1], av[i + 2], av[i + 3]);
+                    }
                 }
                 while (pass) {
                     const int i = __ffs(pass) - 1;
                     pass &= pass - 1;
-                    float v = av[0];
-#pragma unroll
-                    for (int u = 1; u < 32; u++) v = (i == u) ? av[u] : v;
+                    const float v = stg[i];
                     if (!(v < thr)) continue;  // the threshold may have dropped
                     const int id = (int)(col0 + c0 + i);
                     // shift-insert: new[p] = v < old[p-1] ? old[p-1] : (v < old[p] ? v : old[p])
-                    bool c_next = v < lv[31];
+                    bool c_next = v < lv[KP - 1];
 #pragma unroll
-                    for (int p = 31; p > 0; p--) {
+                    for (int p = KP - 1; p > 0; p--) {
                         const bool c_prev = v < lv[p - 1];
                         lv[p] = c_prev ? lv[p - 1] : (c_next ? v : lv[p]);
                         li[p] = c_prev ? li[p - 1] : (c_next ? id : li[p]);
@@ -432,21 +534,23 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_scan_kernel(TcArgs a) {
                         lv[0] = v;
                         li[0] = id;
                     }
-                    thr = lv[31];
+                    thr = lv[KP - 1];
                 }
             }
             tc_fence_before();
-            mbar_arrive(&sfree[s]);  // TMEM stage, B tile and xx of stage s are free
-            float wm = row_ok ? thr : -INFINITY;
+            mbar_arrive(&tempty[ts]);  // accumulator stage free (xx/xcol slots: see NMETA)
+            // largest row threshold in a units, rounded up (pruning stays conservative)
+            float wm = row_ok ? __fadd_ru(thr, qq) : -INFINITY;
             for (int o = 16; o; o >>= 1) wm = fmaxf(wm, __shfl_xor_sync(FULL, wm, o));
             if (lane == 0) ((volatile float *)misc->part)[ew] = wm;
         }
-        // write this row's candidate list
+        // write this row's candidate list (slots >= KP hold -1)
         if (gi >= a.row0 && gi < a.row1 && row_ok) {
             int32_t *dst = a.cand + (gi - a.row0) * 32;
 #pragma unroll
-            for (int q = 0; q < 32; q++) dst[q] = li[q];
-            a.kth[gi - a.row0] = li[31] >= 0 ? lv[31] : INFINITY;
+            for (int q = 0; q < 32; q++) dst[q] = q < KP ? li[q < KP ? q : 0] : -1;
+            // a = |q~|^2 + b rounded down: a lower bound keeps the certificate rigorous
+            a.kth[gi - a.row0] = li[KP - 1] >= 0 ? __fadd_rd(lv[KP - 1], qq) : INFINITY;
             a.qhat[gi - a.row0] = qq;
         }
     }
@@ -459,33 +563,37 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_scan_kernel(TcArgs a) {
     }
 }
 
-template <int MODE, int R>
+template <int MODE, int KP>
 void launch_mode(const TcArgs &args, int64_t nqb, cudaStream_t s) {
-    const Plan P = make_plan(args.dk, R);
-    SLK_CUDA(cudaFuncSetAttribute(tc_scan_kernel<MODE, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    const Plan P = make_plan(args.dk);
+    SLK_CUDA(cudaFuncSetAttribute(tc_scan_kernel<MODE, KP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)P.total));
-    tc_scan_kernel<MODE, R><<<(unsigned)nqb, NTHREADS, P.total, s>>>(args);
+    tc_scan_kernel<MODE, KP><<<(unsigned)nqb, NTHREADS, P.total, s>>>(args);
     SLK_CHECK_LAUNCH();
 }
 
-template <int R>
-void launch_r(int mode, const TcArgs &args, int64_t nqb, cudaStream_t s) {
+template <int KP>
+void launch_kp(int mode, const TcArgs &args, int64_t nqb, cudaStream_t s) {
     switch (mode) {
-        case MODE_NONE: launch_mode<MODE_NONE, R>(args, nqb, s); break;
-        case MODE_MASK: launch_mode<MODE_MASK, R>(args, nqb, s); break;
-        case MODE_COLOR: launch_mode<MODE_COLOR, R>(args, nqb, s); break;
-        default: launch_mode<MODE_SELF, R>(args, nqb, s); break;
+        case MODE_NONE: launch_mode<MODE_NONE, KP>(args, nqb, s); break;
+        case MODE_MASK: launch_mode<MODE_MASK, KP>(args, nqb, s); break;
+        case MODE_COLOR: launch_mode<MODE_COLOR, KP>(args, nqb, s); break;
+        default: launch_mode<MODE_SELF, KP>(args, nqb, s); break;
     }
 }
 
-size_t smem_bytes(int d, int R) { return make_plan(((d + 15) / 16) * 16, R).total; }
+}  // namespace
 
-// Register lists hold K' = 32 candidates: the tensor path serves k <= 31.
-bool supported(int d, int R) { return R == 1 && d <= 256 && smem_bytes(d, R) <= 227 * 1024; }
+size_t smem_bytes(int d) { return make_plan(((d + 15) / 16) * 16).total; }
 
-void launch(int mode, int R, const TcArgs &args, int64_t nqb, cudaStream_t s) {
-    (void)R;
-    launch_r<1>(mode, args, nqb, s);
+// at least two B stages must fit next to the A tile
+bool supported(int d) { return make_plan(((d + 15) / 16) * 16).nb >= 2; }
+
+// K' = kp candidates per row (8, 16 or 32; kp > k for the certificate)
+void launch(int mode, int kp, const TcArgs &args, int64_t nqb, cudaStream_t s) {
+    if (kp <= 8) launch_kp<8>(mode, args, nqb, s);
+    else if (kp <= 16) launch_kp<16>(mode, args, nqb, s);
+    else launch_kp<32>(mode, args, nqb, s);
 }
 
 }  // namespace tc

@@ -8,8 +8,8 @@ namespace slk {
 namespace tc {
 
 struct TcArgs {
-    const float *qp;         // packed queries [nqb][dp][128]
-    const float *xp;         // packed index   [nxb][dp][128]
+    const float *qp;         // tc-packed queries [nqb][128 * dk] (knn.cu:tcpack_kernel)
+    const float *xp;         // tc-packed index   [nxb][128 * dk]
     int64_t nq, nx;
     int d, dp, dk;           // dims, packed dims (multiple of 16), MMA K extent
     int64_t qb0;             // first query block of this launch
@@ -18,9 +18,10 @@ struct TcArgs {
     float scale;             // power of two applied after centring
     float inv_scale2;        // 1 / scale^2 (exact)
     const uint8_t *mask;
-    const int32_t *qcolor, *xcolor;
-    int32_t *cand;           // [rows][32R]
-    float *kth;              // [rows] approximate K'-th value (scaled units)
+    const int32_t *qcolor;
+    const int32_t *xcolor;   // MODE_COLOR: padded to whole 128-point blocks
+    int32_t *cand;           // [rows][32] (slots >= K' hold -1)
+    float *kth;              // [rows] approximate K'-th value (scaled units, rounded down)
     float *qhat;             // [rows] |q^|^2 (scaled units)
     int64_t row0, row1;
     const int32_t *sb_order;
@@ -32,9 +33,10 @@ struct TcArgs {
     const int32_t *qid;      // query row -> id in the index, -1 = padding (or null)
 };
 
-size_t smem_bytes(int d, int R);
-bool supported(int d, int R);
-void launch(int mode, int R, const TcArgs &args, int64_t nqb, cudaStream_t s);
+size_t smem_bytes(int d);
+bool supported(int d);
+// kp: candidates kept per row (8, 16 or 32); the certificate needs kp > k
+void launch(int mode, int kp, const TcArgs &args, int64_t nqb, cudaStream_t s);
 
 }  // namespace tc
 }  // namespace slk
