@@ -298,6 +298,8 @@ def run_gpu(args, c, cfg_name):
             dist.barrier()
         torch.cuda.synchronize()
 
+    step_stages = []
+
     def timed(fn, steps):
         times = []
         for _ in range(steps):
@@ -313,11 +315,11 @@ def run_gpu(args, c, cfg_name):
                 dist.all_reduce(tt, op=dist.ReduceOp.MAX)
                 t = float(tt.item())
             times.append(t)
+            step_stages.append({k: round(v, 1) for k, v in getattr(out, "timings", {}).items()})
         return times, out
 
     for _ in range(args.warmup):
         value_step()
-        e2e_step()  # the host-buffer path too: pinned staging and pool growth happen here
     barrier()
     _lib.profile(reset=True)
     launches0 = _lib.kernel_launches()
@@ -327,6 +329,8 @@ def run_gpu(args, c, cfg_name):
     prof = _lib.profile(reset=True)
     value = float(np.mean(times))
 
+    for _ in range(args.warmup):
+        e2e_step()  # warm the host-buffer path too (pinned staging, pool growth)
     e2e_times, res_e2e = timed(e2e_step, max(1, args.steps))
     e2e = float(np.mean(e2e_times))
     n = c["n"]
@@ -362,6 +366,7 @@ def run_gpu(args, c, cfg_name):
         "e2e": {"value": e2e, "unit": "s", "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h), "steps_s": [round(t, 5) for t in e2e_times]},
         "value_steps_s": [round(t, 5) for t in times],
+        "stage_ms_by_step": step_stages,
         "gpu_launches": int(launches),
         "roofline": roofline,
         "cpu_baseline": cpu,

@@ -61,6 +61,12 @@ int guarded(F &&body) {
 // Keep freed scratch in the device's stream-ordered pool instead of returning
 // it to the driver at every synchronisation (default release threshold 0).
 void ensure_pool();
+// Reserve `bytes` of the device pool in one piece (see slink_api.cu).
+void reserve_pool(size_t bytes, cudaStream_t s);
+// SLK_TRACE=1 in the environment: sub-stage timings on stderr
+bool trace_on();
+// SLK_TRACE: host milliseconds since the previous mark on this thread
+void trace_mark(const char *what);
 
 // Stream-ordered scratch buffer (cudaMallocAsync pool); freed on destruction.
 template <class T>

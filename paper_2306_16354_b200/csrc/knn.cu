@@ -25,6 +25,7 @@
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
+#include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
 
@@ -955,6 +956,7 @@ int64_t search_ffma(const PointSet &Q, const PointSet &X, const int32_t *qid, in
         else launch_refine<4>(ra, rows, s);
         ev_refine.stop(s);
         unsigned long long done = read_scalar(tiles.get(), s);
+    trace_mark("scan+refine done");
         st.rows_refined += rows;
         st.tiles_computed += (int64_t)done;
         st.tiles_skipped += (qb1 - qb0) * X.nb - (int64_t)done;
@@ -1049,6 +1051,7 @@ int tc_pass(const PointSet &Q, const PointSet &X, const int32_t *qid, int k, int
     ev_order.start(s);
     VisitOrder V = visit_order(Q, X, qb0, qb1 - qb0, mode == MODE_COLOR ? qcolor : nullptr, xcolor, s);
     ev_order.stop(s);
+    trace_mark("visit_order enqueued");
     // colours of the index padded to whole blocks (one bulk copy per block)
     DevBuf<int32_t> xcolp;
     if (mode == MODE_COLOR) {
@@ -1070,12 +1073,17 @@ int tc_pass(const PointSet &Q, const PointSet &X, const int32_t *qid, int k, int
     ev_refine.start(s);
     launch_refine<1>(ra, rows, s);
     ev_refine.stop(s);
+    trace_mark("scan+refine enqueued");
     unsigned long long done = read_scalar(tiles.get(), s);
+    trace_mark("scan+refine done");
     st.rows_refined += rows;
     st.tiles_computed += (int64_t)done;
     st.tiles_skipped += (qb1 - qb0) * X.nb - (int64_t)done;
     record_profile(ev_order, ev_scan, ev_refine, rows, nx, d, done, (qb1 - qb0) * X.nb, true);
     const int nfail = read_scalar<int>(counters, s);
+    if (trace_on())
+        fprintf(stderr, "[slk] tc_pass mode %d rows %lld: order %.2f scan %.2f refine %.2f ms, tiles %llu, uncertified %d\n",
+                mode, (long long)rows, ev_order.ms(), ev_scan.ms(), ev_refine.ms(), done, nfail);
     st.rows_uncertified += nfail;
     profile().tc_uncertified += nfail;
     return nfail;
@@ -1226,7 +1234,9 @@ void search(const PointSet &Q, const PointSet &X, int k, int mode, const uint8_t
                 src.push_back(hglob[i]);
                 qid.push_back(hglob[i]);
             }
+            trace_mark("reblock plan");
             Gathered G = gather_queries(Q, src, qid, mode, qcolor, mask, nx, s);
+            trace_mark("gathered");
             DevBuf<int32_t> gidx(G.n * k, s);
             DevBuf<double> gdist(G.n * k, s);
             DevBuf<int> fail2;

@@ -4,12 +4,15 @@
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdarg.h>
+#include <stdio.h>
+#include <stdlib.h>
 #include <stdint.h>
 #include <string.h>
 
 #include <algorithm>
 #include <atomic>
 #include <chrono>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -48,6 +51,32 @@ void throw_internal(const char *fmt, ...) {
     throw Error{SLK_ERR_INTERNAL, m};
 }
 
+// Grows the device pool's reservation to `bytes` in one piece (allocate,
+// free, keep).  Without it the pool grows in many small mappings and a later
+// call can stall for 0.1-0.5 s in cudaMallocAsync while the driver maps new
+// physical memory (measured at C3 on the host-buffer path).  SLK_POOL_RESERVE_GB
+// overrides the size.
+void reserve_pool(size_t bytes, cudaStream_t s) {
+    static size_t reserved[64] = {};
+    static std::mutex mu;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return;
+    if (const char *e = getenv("SLK_POOL_RESERVE_GB")) bytes = (size_t)(atof(e) * (double)(1ull << 30));
+    std::lock_guard<std::mutex> lock(mu);
+    if (bytes <= reserved[dev]) return;
+    ensure_pool();
+    size_t free_b = 0, total_b = 0;
+    if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess && bytes > free_b / 2) bytes = free_b / 2;
+    void *p = nullptr;
+    if (bytes && cudaMallocAsync(&p, bytes, s) == cudaSuccess) {
+        cudaFreeAsync(p, s);
+        cudaStreamSynchronize(s);
+        reserved[dev] = bytes;
+    } else {
+        cudaGetLastError();  // best effort: a failed reservation is not an error
+    }
+}
+
 void ensure_pool() {
     static bool done[64] = {};
     int dev = 0;
@@ -58,6 +87,15 @@ void ensure_pool() {
         cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
     }
     done[dev] = true;
+}
+
+// SLK_TRACE=1: sub-stage timings on stderr (adds stream synchronisations)
+bool trace_on() {
+    static const bool on = [] {
+        const char *e = getenv("SLK_TRACE");
+        return e && *e && *e != '0';
+    }();
+    return on;
 }
 
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
@@ -92,11 +130,21 @@ __global__ void iota32_kernel(int64_t n, int32_t *v) {
         v[e] = (int32_t)e;
 }
 
+// The library's own stream for host-buffer entry points: one per device,
+// created once and kept, so the stream-ordered pool reuses the previous
+// call's scratch (a fresh stream per call made the pool map new memory:
+// up to 0.5 s stalls at 1M x 64).  Calls on one device serialise on it.
 struct StreamGuard {
     cudaStream_t s = nullptr;
-    StreamGuard() { SLK_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking)); }
-    ~StreamGuard() {
-        if (s) cudaStreamDestroy(s);
+    StreamGuard() {
+        static std::mutex mu;
+        static cudaStream_t streams[64] = {};
+        int dev = 0;
+        SLK_CUDA(cudaGetDevice(&dev));
+        if (dev < 0 || dev >= 64) throw_internal("device ordinal %d out of range", dev);
+        std::lock_guard<std::mutex> lock(mu);
+        if (!streams[dev]) SLK_CUDA(cudaStreamCreateWithFlags(&streams[dev], cudaStreamNonBlocking));
+        s = streams[dev];
     }
 };
 
@@ -104,6 +152,18 @@ double now_ms() {
     using namespace std::chrono;
     return duration<double, std::milli>(steady_clock::now().time_since_epoch()).count();
 }
+
+}  // namespace
+
+void trace_mark(const char *what) {
+    if (!trace_on()) return;
+    static thread_local double last = 0.0;
+    const double t = now_ms();
+    fprintf(stderr, "[slk]   %-28s +%.2f ms\n", what, last > 0.0 ? t - last : 0.0);
+    last = t;
+}
+
+namespace {
 
 std::string largest_sizes(const std::vector<int32_t> &colors) {
     std::vector<int64_t> counts(colors.size(), 0);
@@ -126,13 +186,28 @@ void single_linkage_device(const float *x32, const double *x64, int64_t n, int d
                            double *h_merges, int64_t *h_labels, int64_t *h_tree_src,
                            int64_t *h_tree_dst, double *h_tree_w, int64_t *n_iters,
                            double *timings, cudaStream_t s) {
+    // peak scratch of the pipeline, x2 headroom: operand copies (packed,
+    // tc-packed, f64), per-query-block visit bounds, k-NN lists, edge lists
+    {
+        const double nb = (double)((n + 127) / 128);
+        const double est = 4.0 * n * d * 4 + (x64 ? 8.0 * n * d : 0.0) + 8.0 * nb * nb +
+                           64.0 * n * k + 256.0 * n;
+        reserve_pool((size_t)(2.0 * est), s);
+    }
     double t0 = now_ms();
     // --- k-NN graph (linkage.py:287)
     auto P = make_pointset(x32, x64, n, d, s);
+    if (trace_on()) {
+        SLK_CUDA(cudaStreamSynchronize(s));
+        fprintf(stderr, "[slk] pointset %.1f ms\n", now_ms() - t0);
+    }
+    trace_mark("pointset");
     DevBuf<int32_t> idx(n * k, s);
     DevBuf<double> dist(n * k, s);
     knn_ps(*P, k, 0, n, idx, dist, s);
+    trace_mark("knn returned");
     SLK_CUDA(cudaStreamSynchronize(s));
+    trace_mark("knn synced");
     double t1 = now_ms();
     // --- symmetrise + spanning forest (linkage.py:289-290)
     DevBuf<int32_t> src(n * k, s);
@@ -401,10 +476,15 @@ int slk_single_linkage(const float *h_x32, const double *h_x64, int64_t n, int d
         cudaStream_t s = g.s;
         DevBuf<float> x32(n * (int64_t)d, s);
         DevBuf<double> x64;
+        const double th = now_ms();
         SLK_CUDA(cudaMemcpyAsync(x32.get(), h_x32, n * (int64_t)d * sizeof(float), cudaMemcpyHostToDevice, s));
         if (h_x64) {
             x64.alloc(n * (int64_t)d, s);
             SLK_CUDA(cudaMemcpyAsync(x64.get(), h_x64, n * (int64_t)d * sizeof(double), cudaMemcpyHostToDevice, s));
+        }
+        if (trace_on()) {
+            SLK_CUDA(cudaStreamSynchronize(s));
+            fprintf(stderr, "[slk] h2d %.1f ms\n", now_ms() - th);
         }
         single_linkage_device(x32, h_x64 ? x64.get() : nullptr, n, d, k, n_clusters, metric, seed,
                               max_connect_iters, h_merges, h_labels, h_tree_src, h_tree_dst,

@@ -24,12 +24,13 @@
 // ONE cp.async.bulk (TMA bulk copy, mbarrier complete_tx) and is converted
 // in place, each thread touching only its own point's bytes.
 //
-// CTA = 10 warps, warp-specialised, all hand-offs on mbarriers:
+// CTA = 14 warps, warp-specialised, all hand-offs on mbarriers:
 //   warp  9    producer: walks the pruned visit order (32 superblocks per
 //              step, ballots), issues the bulk copies of raw blocks (and their
 //              colours) into a ring of NB stages, NB - 1 blocks ahead.
-//   warps 0-3  convert:  centre / scale / split the stage in place into the
-//              canonical K-major no-swizzle layout + |x~|^2 per point.
+//   warps 0-3, 10-13  convert: centre / scale / split the stage in place into
+//              the canonical K-major no-swizzle layout + |x~|^2 per point (two
+//              threads per point, one per half of the dims).
 //   warp  8    MMA:      one elected thread issues tcgen05.mma (M=128, N=128,
 //              K=16) into one of NT TMEM accumulator stages, then commits to
 //              the stage's "B empty" and the accumulator's "full" barriers.
@@ -38,6 +39,7 @@
 //              only for chunks with a hit: exact pass mask, staging of the 32
 //              values in smem, shift-insertion into the row's K'-entry
 //              register list.  No distance tile ever reaches HBM.
+#include <cstdio>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -62,8 +64,14 @@ __device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
-__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+#ifdef SLK_WATCHDOG
+__device__ void watchdog_dump(int tag, int it, uint32_t parity, unsigned long long st);
+#endif
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity, int tag = 0, int it = 0) {
     uint32_t done;
+#ifdef SLK_WATCHDOG
+    long long spins = 0;
+#endif
     do {
         asm volatile(
             "{\n\t.reg .pred p;\n\t"
@@ -72,6 +80,13 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
             : "=r"(done)
             : "r"(smem_u32(bar)), "r"(parity)
             : "memory");
+#ifdef SLK_WATCHDOG
+        if (!done && ++spins == (1ll << 24)) {
+            unsigned long long st;
+            asm volatile("ld.shared.b64 %0, [%1];" : "=l"(st) : "r"(smem_u32(bar)));
+            watchdog_dump(tag, it, parity, st);
+        }
+#endif
     } while (!done);
 }
 __device__ __forceinline__ void fence_async_smem() {
@@ -130,6 +145,23 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
     for (int i = 0; i < 32; i++) v[i] = __uint_as_float(r[i]);
 }
 
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
+    uint32_t r[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+          "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 16; i++) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ void tmem_ld(uint32_t taddr, float (&v)[32]) { tmem_ld32(taddr, v); }
+__device__ __forceinline__ void tmem_ld(uint32_t taddr, float (&v)[16]) { tmem_ld16(taddr, v); }
+
 // Two-term fp16 split of a centred, scaled pair: v ~ hi + lo with relative
 // error <= 2^-22 (lo = fp16(v - hi), v - hi exact in fp32); accumulates the
 // squared norm of the represented value hi + lo (exact in fp32) into nrm.
@@ -145,16 +177,23 @@ __device__ __forceinline__ void split2(float v0, float v1, __half2 &hi, __half2 
 
 
 // ------------------------------------------------------------- smem plan
-constexpr int NTHREADS = 320;
+// Convert groups: NCG x 128 threads, NCG threads per point (each converts
+// dk / NCG dims and keeps its own partial |x~|^2).  Measured at C3/C5: one
+// group (4 warps, 157 registers, 32-column epilogue steps) beats two (8 warps,
+// capped at 128 registers, 16-column steps).
+constexpr int NCG = 1;
+constexpr int NTHREADS = 320 + 128 * (NCG - 1);  // convert 0-3 (+10-13), epilogue 4-7, MMA 8, producer 9
 constexpr int NT = 2;        // TMEM accumulator stages (128 fp32 columns each)
 constexpr int MAX_NB = 6;    // B operand stages
 constexpr int NMETA = MAX_NB + NT;  // per-tile metadata ring (see producer)
 constexpr uint32_t TMEM_COLS = NT * 128;
-constexpr int STG_STRIDE = 36;  // per-row chunk staging (36 floats: conflict-free STS.128)
+constexpr int CH = NCG == 1 ? 32 : 16;  // accumulator columns per epilogue step (tcgen05.ld .x32/.x16)
+constexpr uint32_t CH_ALL = CH == 32 ? 0xffffffffu : ((1u << (CH & 31)) - 1u);
+constexpr int STG_STRIDE = CH + 4;  // per-row chunk staging (CH + 4 floats: conflict-free STS.128)
 constexpr uint32_t SMEM_LIMIT = 227 * 1024;
 
 struct Plan {
-    uint32_t a, b, xx, xcol, qq, cq, stg, misc, bars, total;
+    uint32_t a, b, xx, xx1, xcol, qq, qq1, cq, stg, misc, bars, total;
     int nb;  // B stages that fit
 };
 
@@ -170,8 +209,10 @@ __host__ __device__ inline Plan make_plan(int dk) {
     const uint32_t stage = (uint32_t)BM * dk * 4;  // hi + lo fp16 tiles = raw fp32 block
     p.a = take(stage, 1024);
     p.xx = take(NMETA * BN * 4, 16);
+    p.xx1 = take(NMETA * BN * 4, 16);
     p.xcol = take(NMETA * BN * 4, 16);
     p.qq = take(BM * 4, 16);
+    p.qq1 = take(BM * 4, 16);
     p.cq = take(dk * 4, 16);
     p.stg = take(BM * STG_STRIDE * 4, 16);
     p.misc = take(128, 16);
@@ -188,7 +229,23 @@ struct Misc {
     float part[4];            // per epilogue warp: largest row threshold (a units)
     uint32_t tmem_base;
     int meta_blk[NMETA];      // block id of tile t at slot t % NMETA (-1 = end)
+#ifdef SLK_WATCHDOG
+    int dbg[4];               // last tile reached by producer / convert / epilogue / MMA
+#endif
 };
+
+#ifdef SLK_WATCHDOG
+__device__ void watchdog_dump(int tag, int it, uint32_t parity, unsigned long long st) {
+    extern __shared__ __align__(1024) unsigned char smem[];
+    const Plan P = make_plan(64);
+    const Misc *m = reinterpret_cast<const Misc *>(smem + P.misc);
+    const unsigned long long *bars = reinterpret_cast<const unsigned long long *>(smem + P.bars);
+    printf("watchdog: block %d thread %d tag %d it %d parity %u state %llx dbg %d %d %d %d "
+           "raw %llx %llx %llx %llx %llx\n",
+           blockIdx.x, threadIdx.x, tag, it, parity, st, m->dbg[0], m->dbg[1], m->dbg[2], m->dbg[3], bars[0],
+           bars[1], bars[2], bars[3], bars[4]);
+}
+#endif
 
 // ------------------------------------------------------------ PTX: TMA bulk
 __device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
@@ -203,16 +260,16 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
         : "memory");
 }
 
-// Converts one 128-point operand tile in place (raw tc-packed fp32 -> fp16
-// hi/lo canonical layout); thread r owns point r.  Returns |x~|^2 of the
-// represented point.
-__device__ __forceinline__ float convert_tile(unsigned char *tile, int r, int dk, float sc,
-                                              const float *s_cq) {
+// Converts core-matrix columns [g0, g1) (dims 8g0 .. 8g1-1) of point r of a
+// 128-point operand tile in place (raw tc-packed fp32 -> fp16 hi/lo canonical
+// layout).  Returns the partial |x~|^2 of the represented point over those dims.
+__device__ __forceinline__ float convert_tile(unsigned char *tile, int r, int g0, int g1, int dk,
+                                              float sc, const float *s_cq) {
     const uint32_t half_bytes = (uint32_t)BM * dk * 2;
     unsigned char *row = tile + (r >> 3) * (dk * 16) + (r & 7) * 16;
     float nrm = 0.0f;
 #pragma unroll 2
-    for (int g = 0; g < dk / 8; g++) {
+    for (int g = g0; g < g1; g++) {
         float4 *ph = reinterpret_cast<float4 *>(row + g * 128);
         float4 *pl = reinterpret_cast<float4 *>(row + half_bytes + g * 128);
         const float4 u = *ph, w = *pl;
@@ -284,9 +341,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_scan_kernel(TcArgs a) {
     const int nb = P.nb;
     unsigned char *sA = smem + P.a;
     unsigned char *sB = smem + P.b;
-    float *s_xx = reinterpret_cast<float *>(smem + P.xx);
+    float *s_xx = reinterpret_cast<float *>(smem + P.xx);    // |x~|^2 over dims [0, dk/2)
+    float *s_xx1 = reinterpret_cast<float *>(smem + P.xx1);  // ... over [dk/2, dk)
     int *s_xcol = reinterpret_cast<int *>(smem + P.xcol);
     float *s_qq = reinterpret_cast<float *>(smem + P.qq);
+    float *s_qq1 = reinterpret_cast<float *>(smem + P.qq1);
     float *s_cq = reinterpret_cast<float *>(smem + P.cq);
     float *s_stg = reinterpret_cast<float *>(smem + P.stg);
     Misc *misc = reinterpret_cast<Misc *>(smem + P.misc);
@@ -309,7 +368,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_scan_kernel(TcArgs a) {
     if (tid == 0) {
         for (int s = 0; s < MAX_NB; s++) {
             mbar_init(&rawfull[s], 1);
-            mbar_init(&bfull[s], 128);
+            mbar_init(&bfull[s], 128 * NCG);
             mbar_init(&bempty[s], 1);
         }
         for (int s = 0; s < NT; s++) {
@@ -349,10 +408,16 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_scan_kernel(TcArgs a) {
             const int s = it % nb;
             const uint32_t ph = (uint32_t)(it / nb) & 1u;
             volatile float *part = misc->part;
-            const float thr = fmaxf(fmaxf(part[0], part[1]), fmaxf(part[2], part[3])) * a.inv_scale2;
+            float thr = fmaxf(fmaxf(part[0], part[1]), fmaxf(part[2], part[3])) * a.inv_scale2;
+            // the visitor's control flow must be warp-uniform: lane 0 (which ran
+            // ahead into the barrier wait below) may have read newer thresholds
+            thr = __shfl_sync(FULL, thr, 0);
             const int64_t jb = vis.next(thr, lane);
+#ifdef SLK_WATCHDOG
+            if (lane == 0) misc->dbg[0] = it * 100000 + (int)(jb < 0 ? 99999 : jb % 100000);
+#endif
             if (lane == 0) {
-                mbar_wait(&bempty[s], ph ^ 1u);
+                mbar_wait(&bempty[s], ph ^ 1u, 1, it);
                 misc->meta_blk[it % NMETA] = (int)jb;
                 if (jb < 0) {
                     mbar_arrive(&rawfull[s]);
@@ -369,19 +434,27 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_scan_kernel(TcArgs a) {
             if (jb < 0) break;
         }
         if (lane == 0 && a.tiles_done) atomicAdd(a.tiles_done, (unsigned long long)computed);
-    } else if (warp < 4) {
-        // ===================== convert warps: A once, then every B stage in place
-        const int r = tid;  // 0..127: query row (A) / index point (B)
+    } else if (warp < 4 || (NCG == 2 && warp >= 10)) {
+        // ===================== convert warps: A once, then every B stage in place.
+        // 256 threads: point r = ct & 127, dims half h = ct >> 7 (two threads
+        // per point, each with its own partial |x~|^2; the epilogue adds them)
+        const int ct = warp < 4 ? tid : tid - 192;  // 0..128*NCG-1
+        const int r = ct & 127, h = ct >> 7;
+        const int g0 = h * (dk / (8 * NCG)), g1 = g0 + dk / (8 * NCG);
         const float sc = a.scale;
-        mbar_wait(afull, 0);
-        s_qq[r] = convert_tile(sA, r, dk, sc, s_cq);
+        float *xxh = h ? s_xx1 : s_xx;
+        mbar_wait(afull, 0, 2, 0);
+        (h ? s_qq1 : s_qq)[r] = convert_tile(sA, r, g0, g1, dk, sc, s_cq);
         for (int it = 0;; it++) {
             const int s = it % nb;
             const uint32_t ph = (uint32_t)(it / nb) & 1u;
-            mbar_wait(&rawfull[s], ph);
+            mbar_wait(&rawfull[s], ph, 3, it);
             const int jb = misc->meta_blk[it % NMETA];
+#ifdef SLK_WATCHDOG
+            if (ct == 200) misc->dbg[1] = it * 100000 + (jb < 0 ? 99999 : jb % 100000);
+#endif
             if (jb >= 0) {
-                s_xx[(it % NMETA) * BN + r] = convert_tile(sB + (size_t)s * stage_bytes, r, dk, sc, s_cq);
+                xxh[(it % NMETA) * BN + r] = convert_tile(sB + (size_t)s * stage_bytes, r, g0, g1, dk, sc, s_cq);
                 fence_async_smem();  // generic-proxy smem writes -> visible to the tensor core
             }
             mbar_arrive(&bfull[s]);
@@ -396,11 +469,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_scan_kernel(TcArgs a) {
                 const uint32_t ph = (uint32_t)(it / nb) & 1u;
                 const int ts = it % NT;
                 const uint32_t tph = (uint32_t)(it / NT) & 1u;
-                mbar_wait(&bfull[s], ph);
+                mbar_wait(&bfull[s], ph, 4, it);
+#ifdef SLK_WATCHDOG
+                misc->dbg[3] = it;
+#endif
                 // the accumulator stage must be drained even for the end marker:
                 // two completions of tfull[ts] ahead of the epilogue would alias
                 // its phase parity
-                mbar_wait(&tempty[ts], tph ^ 1u);
+                mbar_wait(&tempty[ts], tph ^ 1u, 5, it);
                 if (misc->meta_blk[it % NMETA] < 0) {
                     mbar_arrive(&tfull[ts]);
                     break;
@@ -421,6 +497,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_scan_kernel(TcArgs a) {
                 umma_commit(&bempty[s]);  // operands consumed: the producer may refill stage s
                 umma_commit(&tfull[ts]);  // accumulator ready
             }
+#ifdef SLK_WATCHDOG
+            ((volatile int *)misc->dbg)[3] = -2;
+#endif
         }
         __syncwarp();
     } else {
@@ -451,12 +530,15 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_scan_kernel(TcArgs a) {
         for (int it = 0;; it++) {
             const int ts = it % NT;
             const uint32_t tph = (uint32_t)(it / NT) & 1u;
-            mbar_wait(&tfull[ts], tph);
+            mbar_wait(&tfull[ts], tph, 6, it);
             tc_fence_after();
             // the convert warps wrote A (and |q~|^2) before their first bfull arrive
-            if (it == 0) qq = s_qq[row];
+            if (it == 0) qq = NCG == 2 ? s_qq[row] + s_qq1[row] : s_qq[row];
             const int slot = it % NMETA;
             const int jb = misc->meta_blk[slot];
+#ifdef SLK_WATCHDOG
+            if (row == 5) misc->dbg[2] = it * 100000 + (jb < 0 ? 99999 : jb % 100000);
+#endif
             if (jb < 0) break;
             const int64_t col0 = (int64_t)jb * BN;
             const uint32_t taddr = tmem + ((uint32_t)(ew * 32) << 16) + (uint32_t)ts * 128;
@@ -466,52 +548,58 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_scan_kernel(TcArgs a) {
             const int self_col =
                 (MODE == MODE_SELF && self_id >= col0 && self_id < col0 + BN) ? (int)(self_id - col0) : -1;
             const float *xxs = s_xx + slot * BN;
+            const float *xxs1 = s_xx1 + slot * BN;
             const int *xcs = s_xcol + slot * BN;
 #pragma unroll 1
-            for (int c0 = 0; c0 < BN; c0 += 32) {
-                float dot[32];
-                tmem_ld32(taddr + c0, dot);
+            for (int c0 = 0; c0 < BN; c0 += CH) {
+                float dot[CH];
+                __syncwarp();  // tcgen05.ld is .sync.aligned: reconverge after the insertion loop
+                tmem_ld(taddr + c0, dot);
                 // fast path: b = fma(-2, dot, |x~|^2) and the chunk minimum
-                float av[32];
+                float av[CH];
 #pragma unroll
-                for (int i = 0; i < 32; i += 4) {
-                    const float4 x4 = *reinterpret_cast<const float4 *>(xxs + c0 + i);
+                for (int i = 0; i < CH; i += 4) {
+                    float4 x4 = *reinterpret_cast<const float4 *>(xxs + c0 + i);
+                    if (NCG == 2) {
+                        const float4 x4b = *reinterpret_cast<const float4 *>(xxs1 + c0 + i);
+                        x4 = make_float4(x4.x + x4b.x, x4.y + x4b.y, x4.z + x4b.z, x4.w + x4b.w);
+                    }
                     av[i + 0] = __fmaf_rn(-2.0f, dot[i + 0], x4.x);
                     av[i + 1] = __fmaf_rn(-2.0f, dot[i + 1], x4.y);
                     av[i + 2] = __fmaf_rn(-2.0f, dot[i + 2], x4.z);
                     av[i + 3] = __fmaf_rn(-2.0f, dot[i + 3], x4.w);
                 }
-                float m16[16];
+                float mn[CH / 2];
 #pragma unroll
-                for (int i = 0; i < 16; i++) m16[i] = fminf(av[i], av[i + 16]);
+                for (int i = 0; i < CH / 2; i++) mn[i] = fminf(av[i], av[i + CH / 2]);
 #pragma unroll
-                for (int w = 8; w; w >>= 1)
+                for (int w = CH / 4; w; w >>= 1)
 #pragma unroll
-                    for (int i = 0; i < w; i++) m16[i] = fminf(m16[i], m16[i + w]);
-                const bool hit = m16[0] < thr;
+                    for (int i = 0; i < w; i++) mn[i] = fminf(mn[i], mn[i + w]);
+                const bool hit = mn[0] < thr;
                 if (!__any_sync(FULL, hit)) continue;  // warp-uniform: nothing to insert
                 uint32_t pass = 0;
                 if (hit) {
 #pragma unroll
-                    for (int i = 0; i < 32; i++) pass |= (av[i] < thr ? 1u : 0u) << i;
+                    for (int i = 0; i < CH; i++) pass |= (av[i] < thr ? 1u : 0u) << i;
                     uint32_t valid = c0 >= col_limit ? 0u
-                                     : (col_limit - c0 >= 32 ? 0xffffffffu : ((1u << (col_limit - c0)) - 1u));
-                    if (self_col >= c0 && self_col < c0 + 32) valid &= ~(1u << (self_col - c0));
+                                     : (col_limit - c0 >= CH ? CH_ALL : ((1u << (col_limit - c0)) - 1u));
+                    if (self_col >= c0 && self_col < c0 + CH) valid &= ~(1u << (self_col - c0));
                     pass &= valid;
                     if (MODE == MODE_COLOR && pass) {
 #pragma unroll
-                        for (int i = 0; i < 32; i++)
+                        for (int i = 0; i < CH; i++)
                             if (xcs[c0 + i] == qc) pass &= ~(1u << i);
                     }
                     if (MODE == MODE_MASK && pass) {
-                        for (int i = 0; i < 32; i++)
+                        for (int i = 0; i < CH; i++)
                             if (((pass >> i) & 1u) && a.mask[gi * a.nx + col0 + c0 + i] == 0) pass &= ~(1u << i);
                     }
                     if (pass) {
                         // stage the chunk: a passing value is one LDS away (no
                         // dynamic register indexing)
 #pragma unroll
-                        for (int i = 0; i < 32; i += 4)
+                        for (int i = 0; i < CH; i += 4)
                             *reinterpret_cast<float4 *>(stg + i) = make_float4(av[i], av[i + 1], av[i + 2], av[i + 3]);
                     }
                 }
@@ -537,6 +625,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_scan_kernel(TcArgs a) {
                     thr = lv[KP - 1];
                 }
             }
+            __syncwarp();
             tc_fence_before();
             mbar_arrive(&tempty[ts]);  // accumulator stage free (xx/xcol slots: see NMETA)
             // largest row threshold in a units, rounded up (pruning stays conservative)
@@ -554,6 +643,19 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_scan_kernel(TcArgs a) {
             a.qhat[gi - a.row0] = qq;
         }
     }
+#ifdef SLK_WATCHDOG
+    if (warp != 8) {
+        long long w = 0;
+        while (++w < (1ll << 24)) {
+            if (((volatile int *)misc->dbg)[3] < -1) break;
+        }
+        if (w >= (1ll << 24) && (tid == 0 || tid == 320 || tid == 128 || tid == 288))
+            printf("exit-wait: block %d tid %d dbg %d %d %d %d meta %d %d %d %d %d %d %d %d\n", blockIdx.x, tid,
+                   misc->dbg[0], misc->dbg[1], misc->dbg[2], misc->dbg[3], misc->meta_blk[0],
+                   misc->meta_blk[1], misc->meta_blk[2], misc->meta_blk[3], misc->meta_blk[4],
+                   misc->meta_blk[5], misc->meta_blk[6], misc->meta_blk[7]);
+    }
+#endif
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
