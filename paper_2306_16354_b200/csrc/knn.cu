@@ -143,14 +143,13 @@ struct ScanArgs {
     float *kth;        // [nq_rows_launch] approx K'-th value
     int64_t row0;      // global row of cand[0]
     int64_t row1;      // rows [row0, row1) are written
-    // visit order: per query block of the launch, the
-    // superblocks (32 index blocks) sorted by a lower bound on the squared
-    // distance between any of their points and any query point of the block,
-    // plus the per-block bounds; +inf = never admissible (same colour).
-    const int32_t *sb_order;  // [nqb_launch][nsb] ascending centroid distance
-    const float *sb_key;      // [nqb_launch][nsb] the sorted distances (+inf last)
-    const float *sb_lb;       // [nqb_launch][nsb] lower bound, by superblock id
-    const float *blk_lb;      // [nqb_launch][nxb]
+    // visit order (scan_common.cuh:BlockVisitor): per query
+    // block of the launch, the superblocks (32 index blocks) in ascending
+    // centroid distance and their member blocks' lower bounds in that order
+    const int32_t *sb_order;  // [nqb_launch][nsb]
+    const float *sb_lb;       // [nqb_launch][nsb] superblock bounds, visit order
+    const float *flat_lb;     // [nqb_launch][nsb][32], +inf = never admissible
+    const int32_t *nvalid;    // [nqb_launch] superblocks with a finite key
     int64_t nsb;
     unsigned long long *tiles_done;
     const int32_t *qid;  // query row -> id in the index (gathered queries), or null
@@ -181,9 +180,8 @@ __global__ void __launch_bounds__(NT, (R == 1 ? 2 : 1)) scan_kernel(ScanArgs a) 
     const int64_t row_base = qb * BM;
     const int nkc = a.dp / KC;
     const int64_t nxb = (a.nx + BN - 1) / BN;
-    BlockVisitor vis{a.sb_order + (int64_t)blockIdx.x * a.nsb, a.sb_key + (int64_t)blockIdx.x * a.nsb,
-                     a.sb_lb + (int64_t)blockIdx.x * a.nsb, a.blk_lb + (int64_t)blockIdx.x * nxb,
-                     a.nsb, nxb};
+    BlockVisitor vis(a.sb_order + (int64_t)blockIdx.x * a.nsb, a.sb_lb + (int64_t)blockIdx.x * a.nsb,
+                     a.flat_lb + (int64_t)blockIdx.x * a.nsb * 32, a.nvalid[blockIdx.x], lane);
 
     for (int e = tid; e < BM * 32 * R; e += NT) {
         (&S.list_v[0][0])[e] = INFINITY;
@@ -442,29 +440,49 @@ __device__ __forceinline__ bool same_colour(const int2 *qcol, const int2 *xcol, 
     return a.x == a.y && c.x == c.y && a.x == c.x;
 }
 
-// per (query block, index block): bound, +inf when every pair is same-coloured
-__global__ void block_lb_kernel(const float *__restrict__ qc, const float *__restrict__ qr,
-                                int64_t nqb_total, const float *__restrict__ xc,
-                                const float *__restrict__ xr, int64_t nxb, int d, int64_t qb0,
-                                int64_t nqb, const int2 *__restrict__ qcol,
-                                const int2 *__restrict__ xcol, float *__restrict__ lb) {
-    const int64_t total = nqb * nxb;
+// Flat visit order: for query block ql and the s-th superblock of its sorted
+// order, the superblock's bound and the bounds of its 32 member blocks (+inf
+// past the last block, for same-coloured pairs and for superblocks with an
+// infinite key); nvalid[ql] = the number of superblocks with a finite key
+// (they sort first).
+__global__ void flat_lb_kernel(const float *__restrict__ qc, const float *__restrict__ qr,
+                               int64_t nqb_total, const float *__restrict__ xc,
+                               const float *__restrict__ xr, int64_t nxb, int d, int64_t qb0,
+                               int64_t nqb, const int2 *__restrict__ qcol,
+                               const int2 *__restrict__ xcol, const int32_t *__restrict__ sb_order,
+                               const float *__restrict__ sb_key, int64_t nsb,
+                               const float *__restrict__ sc, const float *__restrict__ sr,
+                               float *__restrict__ flat, float *__restrict__ sblb,
+                               int32_t *__restrict__ nvalid) {
+    const int64_t per = nsb * 32, total = nqb * per;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
          e += (int64_t)gridDim.x * blockDim.x) {
-        int64_t ql = e / nxb, b = e - ql * nxb, q = qb0 + ql;
-        lb[e] = same_colour(qcol, xcol, q, b) ? INFINITY
-                                              : sphere_lb(qc, qr, nqb_total, q, xc, xr, nxb, b, d);
+        const int64_t ql = e / per, r = e - ql * per, sp = r >> 5, q = qb0 + ql;
+        const int m = (int)(r & 31);
+        const float key = sb_key[ql * nsb + sp];
+        const int64_t b = (int64_t)sb_order[ql * nsb + sp] * 32 + m;
+        float v = INFINITY;
+        if (key != INFINITY && b < nxb && !same_colour(qcol, xcol, q, b))
+            v = sphere_lb(qc, qr, nqb_total, q, xc, xr, nxb, b, d);
+        flat[e] = v;
+        if (m == 0) {
+            const bool fin = key != INFINITY;
+            const int64_t sb = sb_order[ql * nsb + sp];
+            sblb[ql * nsb + sp] = fin ? sphere_lb(qc, qr, nqb_total, q, sc, sr, nsb, sb, d) : INFINITY;
+            const bool next_inf = sp + 1 == nsb || sb_key[ql * nsb + sp + 1] == INFINITY;
+            if (fin && next_inf) nvalid[ql] = (int32_t)(sp + 1);
+            if (sp == 0 && !fin) nvalid[ql] = 0;
+        }
     }
 }
 
-// per (query block, superblock): lower bound (by id), sort key = centroid
-// distance (+inf when every pair is same-coloured), ids, segment offsets
+// per (query block, superblock): sort key = centroid distance (+inf when every
+// pair is same-coloured), ids, segment offsets
 __global__ void superblock_lb_kernel(const float *__restrict__ qc, const float *__restrict__ qr,
                                      int64_t nqb_total, const float *__restrict__ sc,
                                      const float *__restrict__ sr, int64_t nsb, int d, int64_t qb0,
                                      int64_t nqb, const int2 *__restrict__ qcol,
-                                     const int2 *__restrict__ scol, float *__restrict__ lb,
-                                     float *__restrict__ key, int32_t *__restrict__ ids,
+                                     const int2 *__restrict__ scol, float *__restrict__ key, int32_t *__restrict__ ids,
                                      int32_t *__restrict__ seg) {
     const int64_t total = nqb * nsb;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
@@ -476,7 +494,6 @@ __global__ void superblock_lb_kernel(const float *__restrict__ qc, const float *
             s += df * df;
         }
         const bool same = same_colour(qcol, scol, q, b);
-        lb[e] = same ? INFINITY : sphere_lb(qc, qr, nqb_total, q, sc, sr, nsb, b, d);
         key[e] = same ? INFINITY : (float)s;
         ids[e] = (int32_t)b;
         if (b == 0) seg[ql] = (int32_t)(ql * nsb);
@@ -544,7 +561,9 @@ struct RefineArgs {
     int64_t nq, nx;
     int64_t row0, row1;
     const int32_t *cand;
-    const float *kth;
+    const float *kth;         // [rows][kth_per_row]: the certificate uses their minimum
+    int kth_per_row;
+    float *kth_min;           // optional output: that minimum per row
     const double *max_xnorm;  // device scalar
     bool exact_f32;           // inputs are exactly their float32 values
     int32_t *out_idx;
@@ -594,21 +613,27 @@ __device__ double certified_floor(float a, int d, double nq, double max_xn, bool
 
 // Same bound for the tensor-core scan.  a: approximate value
 // in scaled units, a = |q~|^2 + |x~|^2 - 2<q~,x~> of the centred, scaled,
-// two-term-fp16 points, fp32 norms, tensor-core fp32 accumulation of the
-// hi.hi + hi.lo + lo.hi products:
-//   |a - D~| <= g (|q~| + |x~|)^2,  g = (3d + 8) 2^-23 1.1 + 2^-21
-//   (all fp32 roundings, and the dropped lo.lo term)
-//   |x~| <= |q~| + sqrt(D~)                              (triangle)
+// two-term-fp16 points, tensor-core fp32 accumulation of the hi.hi + hi.lo +
+// lo.hi products, the norms accumulated in fp32 from the unsplit values v:
+//   |a - D~| <= g (|q~| + |x~|)^2 + c0,
+//   g  = (3d + 8) 2^-23 1.1 + 2^-21        (fp32 roundings, dropped lo.lo)
+//        + 2^-20 + 2^-23 sqrt(d)          (|v|^2 in place of |hi + lo|^2:
+//   c0 = 2^-25 sqrt(d) + 2^-45 d           2^-21|v|^2 + 2^-24 sqrt(d)|v| + tiny
+//                                           per operand, t <= t^2 + 1/4)
+//   |x~| <= |q~| + sqrt(D~)                 (triangle)
 // gives the smallest sqrt(D~) compatible with a >= A; then
 //   sqrt(D) >= sqrt(D~) - eta (|q'| + |x'|) - 2 sqrt(d) 2^-25
 // (eta: fp32 centring + two-term fp16 representation, 2^-25: fp16 subnormal
 // spacing / 2 of the low term).
 __device__ double certified_floor_tc(float a, float qhat2, double scale, int d, double nq,
                                      double max_xn, bool exact_f32) {
-    const double A = (double)a;
-    if (!(A > 0.0) || !(A < INFINITY)) return -INFINITY;
-    const double r = sqrt((double)qhat2) * (1.0 + 1e-12);
-    const double g = (3.0 * d + 8.0) * 0x1p-23 * 1.1 + 0x1p-21;
+    const double sd_ = sqrt((double)d);
+    const double A = (double)a - (0x1p-25 * sd_ + 0x1p-45 * d);
+    if (!(A > 0.0) || !((double)a < INFINITY)) return -INFINITY;
+    // |q~| of the represented query from the fp32-accumulated |v|^2 (relative
+    // accumulation error <= (d + 4) 2^-24, representation 2^-22 |v| + 2^-25 sqrt(d))
+    const double r = sqrt((double)qhat2 * (1.0 + (d + 4) * 0x1p-24)) * (1.0 + 0x1p-21) + 0x1p-25 * sd_;
+    const double g = (3.0 * d + 8.0) * 0x1p-23 * 1.1 + 0x1p-21 + 0x1p-20 + 0x1p-23 * sd_;
     const double ca = 1.0 + g, cb = 4.0 * g * r, cc = 4.0 * g * r * r - A;
     const double disc = cb * cb - 4.0 * ca * cc;
     if (!(disc > 0.0)) return -INFINITY;
@@ -667,7 +692,9 @@ __global__ void refine_kernel(RefineArgs a) {
             ik = __shfl_sync(FULL, li[r], kl);
         }
     if (lane == 0) {
-        float kth = a.kth[wid];
+        float kth = a.kth[wid * a.kth_per_row];
+        for (int r = 1; r < a.kth_per_row; r++) kth = fminf(kth, a.kth[wid * a.kth_per_row + r]);
+        if (a.kth_min) a.kth_min[wid] = kth;
         bool ok;
         if (ik == 0x7fffffff) {
             ok = false;  // fewer than k admissible candidates in the list
@@ -799,13 +826,12 @@ void launch_exact(const ExactArgs &ea, cudaStream_t s) {
 // Per query block of [qb0, qb0 + nqb): superblocks in ascending centroid
 // distance, their lower bounds, and the per-block bounds.
 struct VisitOrder {
-    DevBuf<int32_t> sb_order;
-    DevBuf<float> sb_key, sb_lb, blk_lb;
+    DevBuf<int32_t> sb_order, nvalid;
+    DevBuf<float> sb_lb, flat_lb;
 };
-
 VisitOrder visit_order(const PointSet &Q, const PointSet &X, int64_t qb0, int64_t nqb,
                        const int32_t *qcolor, const int32_t *xcolor, cudaStream_t s) {
-    const int64_t nxb = X.nb, nsb = X.nsb, total = nqb * nxb, stotal = nqb * nsb;
+    const int64_t nxb = X.nb, nsb = X.nsb, stotal = nqb * nsb;
     if (stotal >= (1ll << 31)) throw_invalid("too many (query block, superblock) pairs: %lld", (long long)stotal);
     DevBuf<int2> qrange, xrange, srange;
     if (qcolor) {
@@ -820,28 +846,28 @@ VisitOrder visit_order(const PointSet &Q, const PointSet &X, int64_t qb0, int64_
         SLK_CHECK_LAUNCH();
     }
     VisitOrder V;
-    V.blk_lb.alloc(total, s);
-    block_lb_kernel<<<grid_for(total, 256), 256, 0, s>>>(Q.centroid, Q.radius, Q.nb, X.centroid,
-                                                         X.radius, nxb, Q.d, qb0, nqb, qrange.get(),
-                                                         xrange.get(), V.blk_lb);
-    SLK_CHECK_LAUNCH();
-    DevBuf<float> key(stotal, s);
+    DevBuf<float> key(stotal, s), skey(stotal, s);
     DevBuf<int32_t> ids(stotal, s), seg(nqb + 1, s);
-    V.sb_lb.alloc(stotal, s);
     superblock_lb_kernel<<<grid_for(stotal, 256), 256, 0, s>>>(
         Q.centroid, Q.radius, Q.nb, X.sb_centroid, X.sb_radius, nsb, Q.d, qb0, nqb, qrange.get(),
-        srange.get(), V.sb_lb, key, ids, seg);
+        srange.get(), key, ids, seg);
     SLK_CHECK_LAUNCH();
     V.sb_order.alloc(stotal, s);
-    V.sb_key.alloc(stotal, s);
     size_t tmp = 0;
-    SLK_CUDA(cub::DeviceSegmentedRadixSort::SortPairs(nullptr, tmp, key.get(), V.sb_key.get(), ids.get(),
+    SLK_CUDA(cub::DeviceSegmentedRadixSort::SortPairs(nullptr, tmp, key.get(), skey.get(), ids.get(),
                                                       V.sb_order.get(), (int)stotal, (int)nqb, seg.get(),
                                                       seg.get() + 1, 0, 32, s));
     DevBuf<unsigned char> t(tmp, s);
-    SLK_CUDA(cub::DeviceSegmentedRadixSort::SortPairs(t.get(), tmp, key.get(), V.sb_key.get(), ids.get(),
+    SLK_CUDA(cub::DeviceSegmentedRadixSort::SortPairs(t.get(), tmp, key.get(), skey.get(), ids.get(),
                                                       V.sb_order.get(), (int)stotal, (int)nqb, seg.get(),
                                                       seg.get() + 1, 0, 32, s));
+    V.flat_lb.alloc(stotal * 32, s);
+    V.sb_lb.alloc(stotal, s);
+    V.nvalid.alloc(nqb, s);
+    flat_lb_kernel<<<grid_for(stotal * 32, 256), 256, 0, s>>>(
+        Q.centroid, Q.radius, Q.nb, X.centroid, X.radius, nxb, Q.d, qb0, nqb, qrange.get(),
+        xrange.get(), V.sb_order, skey, nsb, X.sb_centroid, X.sb_radius, V.flat_lb, V.sb_lb, V.nvalid);
+    SLK_CHECK_LAUNCH();
     return V;
 }
 
@@ -941,14 +967,14 @@ int64_t search_ffma(const PointSet &Q, const PointSet &X, const int32_t *qid, in
                                    xcolor, s);
         ev_order.stop(s);
         ScanArgs sa{Q.packed, X.packed, nq, nx, X.dp, qb0, mask, qcolor, xcolor, cand, kth,
-                    q0, q1, V.sb_order, V.sb_key, V.sb_lb, V.blk_lb, X.nsb, tiles, qid};
+                    q0, q1, V.sb_order, V.sb_lb, V.flat_lb, V.nvalid, X.nsb, tiles, qid};
         ev_scan.start(s);
         if (Rsel == 1) dispatch_scan<1>(mode, sa, qb1 - qb0, s);
         else if (Rsel == 2) dispatch_scan<2>(mode, sa, qb1 - qb0, s);
         else dispatch_scan<4>(mode, sa, qb1 - qb0, s);
         ev_scan.stop(s);
         RefineArgs ra{Q.x32, Q.x64, Q.norms, X.x32, X.x64, X.norms, d, k, nq, nx, q0, q1,
-                      cand, kth, X.maxn, X.x64 == nullptr && Q.x64 == nullptr, out_idx, out_dist,
+                      cand, kth, 1, nullptr, X.maxn, X.x64 == nullptr && Q.x64 == nullptr, out_idx, out_dist,
                       fail_rows, counters, nullptr, 1.0, qid};
         ev_refine.start(s);
         if (Rsel == 1) launch_refine<1>(ra, rows, s);
@@ -997,9 +1023,9 @@ int64_t search_ffma(const PointSet &Q, const PointSet &X, const int32_t *qid, in
 // 0.5 %).  SLK_TC_KP overrides (it must exceed k).
 int tc_kp(int k) {
     int kp = 2 * k <= 8 ? 8 : (2 * k <= 16 ? 16 : 32);
-    if (const char *e = getenv("SLK_TC_KP")) {
+    if (const char *e = getenv(k == 1 ? "SLK_TC_KP1" : "SLK_TC_KP")) {
         int v = atoi(e);
-        if (v > k && v <= 32) kp = v <= 8 ? 8 : (v <= 16 ? 16 : 32);
+        if (v > k && v <= 32) kp = v <= 2 ? 2 : (v <= 4 ? 4 : (v <= 8 ? 8 : (v <= 16 ? 16 : 32)));
     }
     return kp;
 }
@@ -1039,8 +1065,15 @@ int tc_pass(const PointSet &Q, const PointSet &X, const int32_t *qid, int k, int
     const int d = X.d;
     const int64_t nq = Q.n, nx = X.n;
     const int64_t qb0 = q0 / BM, qb1 = (q1 + BM - 1) / BM;
-    DevBuf<int32_t> cand(rows * 32, s);
-    DevBuf<float> qhat(rows, s);
+    // small launches: deal each query block's visit order over nsplit CTAs
+    // (each keeps its own K' list; the refine takes the union) so that at
+    // least ~2 CTAs per SM run
+    int nsplit = 1;
+    while (nsplit < 8 && (qb1 - qb0) * nsplit < 2 * num_sms()) nsplit *= 2;
+    if (const char *e = getenv("SLK_TC_SPLIT")) nsplit = std::max(1, std::min(8, atoi(e)));
+    if (nsplit & (nsplit - 1)) nsplit = 1;
+    DevBuf<int32_t> cand(rows * 32 * nsplit, s);
+    DevBuf<float> qhat(rows, s), kth_split(rows * nsplit, s);
     DevBuf<unsigned long long> tiles(1, s);
     DevBuf<int> counters(1, s);
     kth.alloc(rows, s);
@@ -1062,16 +1095,21 @@ int tc_pass(const PointSet &Q, const PointSet &X, const int32_t *qid, int k, int
     const float *qtc = ensure_tcpack(Q, s), *xtc = ensure_tcpack(X, s);
     tc::TcArgs ta{qtc, xtc, nq, nx, d, X.dp, ((d + 15) / 16) * 16, qb0, Q.centroid,
                   Q.nb, scale, inv_scale2, mask, qcolor, mode == MODE_COLOR ? xcolp.get() : xcolor,
-                  cand, kth, qhat, q0, q1,
-                  V.sb_order, V.sb_key, V.sb_lb, V.blk_lb, X.nsb, tiles, qid};
+                  cand, kth_split, qhat, q0, q1,
+                  V.sb_order, V.sb_lb, V.flat_lb, V.nvalid, X.nsb, tiles, qid, nsplit};
     ev_scan.start(s);
     tc::launch(mode, tc_kp(k), ta, qb1 - qb0, s);
     ev_scan.stop(s);
     RefineArgs ra{Q.x32, Q.x64, Q.norms, X.x32, X.x64, X.norms, d, k, nq, nx, q0, q1,
-                  cand, kth, X.maxn, X.x64 == nullptr && Q.x64 == nullptr, out_idx, out_dist,
-                  fail, counters, qhat, (double)scale, qid};
+                  cand, kth_split, nsplit, kth, X.maxn, X.x64 == nullptr && Q.x64 == nullptr, out_idx,
+                  out_dist, fail, counters, qhat, (double)scale, qid};
     ev_refine.start(s);
-    launch_refine<1>(ra, rows, s);
+    switch (nsplit) {
+        case 1: launch_refine<1>(ra, rows, s); break;
+        case 2: launch_refine<2>(ra, rows, s); break;
+        case 4: launch_refine<4>(ra, rows, s); break;
+        default: launch_refine<8>(ra, rows, s); break;
+    }
     ev_refine.stop(s);
     trace_mark("scan+refine enqueued");
     unsigned long long done = read_scalar(tiles.get(), s);
@@ -1412,7 +1450,7 @@ void debug_tc_scan(const float *x32, int64_t n, int d, int k, int32_t *cand, flo
     const float *tcp = ensure_tcpack(*P, s);
     tc::TcArgs ta{tcp, tcp, n, n, d, P->dp, ((d + 15) / 16) * 16, 0, P->centroid,
                   P->nb, scale, inv2, nullptr, nullptr, nullptr, cand, kth, qhat, 0, n,
-                  V.sb_order, V.sb_key, V.sb_lb, V.blk_lb, P->nsb, tiles, nullptr};
+                  V.sb_order, V.sb_lb, V.flat_lb, V.nvalid, P->nsb, tiles, nullptr, 1};
     tc::launch(scan::MODE_SELF, tc_kp(k), ta, nqb, s);
     SLK_CUDA(cudaStreamSynchronize(s));
     *scale_out = scale;

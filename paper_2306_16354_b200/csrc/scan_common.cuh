@@ -174,44 +174,104 @@ __device__ __forceinline__ void warp_merge_batch(V (&lv)[R], int (&li)[R], V (&b
     warp_bitonic_merge<R>(lv, li, lane);
 }
 
-// Iterates the index blocks a query block must visit.  Superblocks come in
-// ascending centroid distance (the query's own cluster first, so row
-// thresholds tighten before distant blocks are considered); a superblock or
-// member block is skipped when its lower bound exceeds the current largest
-// row threshold (sb_lb / blk_lb are indexed by id).  Superblocks whose every
-// pair is same-coloured sort last (key +inf) and end the walk.  Every thread
-// runs it redundantly and gets the same answer (warp-uniform ballots).
+// Iterates the index blocks a query block must visit.  The
+// visit order: superblocks (32 index blocks) in ascending centroid distance
+// from the query block (its own cluster first, so row thresholds tighten
+// before distant blocks come up); within a superblock, its members in id
+// order.  Per query block the builder stores, in that order, each
+// superblock's id and lower bound (sb_order, sb_lb: [nsb]) and its 32 member
+// bounds (lb: [nsb][32]); +inf marks padding and same-coloured pairs, and
+// superblocks past `nvalid` are never admissible.  A superblock or member
+// whose bound exceeds the current largest row threshold is skipped
+// (thresholds only fall, so skipping stays exact).
+//
+// Latency hiding: superblock bounds are read 32 at a time (one coalesced load
+// per lane, ballot), the next 32 are prefetched, and the member bounds of the
+// next PF admissible superblocks are kept in flight in static register slots
+// (a load is only waited on when its slot is consumed).  Control flow is
+// warp-uniform given a warp-uniform threshold.  With nsplit > 1 the
+// positions are dealt round-robin over nsplit CTAs (small launches).
 struct BlockVisitor {
-    const int32_t *sb_order;  // superblock ids, ascending centroid distance
-    const float *sb_key;      // the sorted keys (+inf = never admissible)
-    const float *sb_lb;       // per superblock id
-    const float *blk_lb;      // per block id
-    int64_t nsb, nxb;
-    int64_t s = -1, sb = 0;
-    unsigned mask = 0;
+    static constexpr int PF = 4;
+    const int32_t *sb_order;
+    const float *sb_lb;
+    const float *lb;
+    int nvalid;
+    int split = 0, nsplit = 1;  // this CTA takes superblock positions p = split (mod nsplit)
+    int base = 0;             // next chunk of 32 superblock positions to take
+    unsigned sbmask = 0;      // admissible positions of the current chunk
+    int cbase = 0;            // first position of the current chunk
+    float c_lb = INFINITY;    // this lane's superblock bound in the current chunk
+    float n_lb = INFINITY;    // ... in the prefetched next chunk
+    int nq = 0, qh = 0;       // member-bound slots in flight, head slot
+    int q_sb[PF];
+    float q_lb[PF];
+    unsigned bmask = 0;
+    int cur_sb = 0;
     float my_lb = INFINITY;
 
-    __device__ int64_t next(float thr_max, int lane) {
-        while (true) {
-            if (mask == 0) {
-                if (++s >= nsb) return -1;
-                if (sb_key[s] == INFINITY) {
-                    s = nsb;
-                    return -1;
-                }
-                sb = sb_order[s];
-                const float l = sb_lb[sb];
-                if (l > thr_max) continue;  // members' bounds are >= their superblock's
-                int64_t b = sb * 32 + lane;
-                my_lb = b < nxb ? blk_lb[b] : INFINITY;
-                mask = __ballot_sync(0xffffffffu, my_lb != INFINITY && !(my_lb > thr_max));
-                continue;
+    __device__ BlockVisitor(const int32_t *order, const float *sblb, const float *lbs, int nv, int lane,
+                            int split_ = 0, int nsplit_ = 1)
+        : sb_order(order), sb_lb(sblb), lb(lbs), nvalid(nv), split(split_), nsplit(nsplit_) {
+        n_lb = lane < nvalid ? __ldg(sb_lb + lane) : INFINITY;
+    }
+    // next admissible superblock position, or -1
+    __device__ __forceinline__ int pop_position(float thr, int lane) {
+        while (!sbmask) {
+            if (base >= nvalid) return -1;
+            cbase = base;
+            c_lb = n_lb;
+            base += 32;
+            n_lb = base + lane < nvalid ? __ldg(sb_lb + base + lane) : INFINITY;
+            sbmask = __ballot_sync(0xffffffffu, c_lb != INFINITY && !(c_lb > thr) &&
+                                                    (nsplit == 1 || (cbase + lane) % nsplit == split));
+        }
+        const int i = __ffs(sbmask) - 1;
+        sbmask &= sbmask - 1;
+        return cbase + i;
+    }
+    template <int I>
+    __device__ __forceinline__ void put(int pos, int lane) {
+        q_sb[I] = __ldg(sb_order + pos);
+        q_lb[I] = __ldg(lb + (int64_t)pos * 32 + lane);
+    }
+    __device__ __forceinline__ void fill(float thr, int lane) {
+        while (nq < PF) {
+            const int pos = pop_position(thr, lane);
+            if (pos < 0) return;
+            switch ((qh + nq) & (PF - 1)) {
+                case 0: put<0>(pos, lane); break;
+                case 1: put<1>(pos, lane); break;
+                case 2: put<2>(pos, lane); break;
+                default: put<3>(pos, lane); break;
             }
-            int m = __ffs(mask) - 1;
-            mask &= mask - 1;
-            float l = __shfl_sync(0xffffffffu, my_lb, m);
-            if (l > thr_max) continue;
-            return sb * 32 + m;
+            nq++;
+        }
+    }
+    template <int I>
+    __device__ __forceinline__ void take() {
+        cur_sb = q_sb[I];
+        my_lb = q_lb[I];
+    }
+    __device__ int64_t next(float thr, int lane) {
+        while (true) {
+            if (bmask) {
+                const int m = __ffs(bmask) - 1;
+                bmask &= bmask - 1;
+                if (__shfl_sync(0xffffffffu, my_lb, m) > thr) continue;
+                return (int64_t)cur_sb * 32 + m;
+            }
+            fill(thr, lane);
+            if (nq == 0) return -1;
+            switch (qh) {
+                case 0: take<0>(); break;
+                case 1: take<1>(); break;
+                case 2: take<2>(); break;
+                default: take<3>(); break;
+            }
+            qh = (qh + 1) & (PF - 1);
+            nq--;
+            bmask = __ballot_sync(0xffffffffu, my_lb != INFINITY && !(my_lb > thr));
         }
     }
 };

@@ -73,12 +73,15 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity, int ta
     long long spins = 0;
 #endif
     do {
+        // suspend-time hint: the waiting warp sleeps in hardware until the phase
+        // completes (or 0.1 ms passes) instead of spinning on issue slots the
+        // working warps of its SM sub-partition need
         asm volatile(
             "{\n\t.reg .pred p;\n\t"
-            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
             "selp.u32 %0, 1, 0, p;\n\t}"
             : "=r"(done)
-            : "r"(smem_u32(bar)), "r"(parity)
+            : "r"(smem_u32(bar)), "r"(parity), "r"(100000u)
             : "memory");
 #ifdef SLK_WATCHDOG
         if (!done && ++spins == (1ll << 24)) {
@@ -162,19 +165,19 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
 __device__ __forceinline__ void tmem_ld(uint32_t taddr, float (&v)[32]) { tmem_ld32(taddr, v); }
 __device__ __forceinline__ void tmem_ld(uint32_t taddr, float (&v)[16]) { tmem_ld16(taddr, v); }
 
-// Two-term fp16 split of a centred, scaled pair: v ~ hi + lo with relative
-// error <= 2^-22 (lo = fp16(v - hi), v - hi exact in fp32); accumulates the
-// squared norm of the represented value hi + lo (exact in fp32) into nrm.
+// Two-term fp16 split of a centred, scaled pair: v ~ hi + lo with
+// |hi + lo - v| <= 2^-22 |v| + 2^-25 per component (lo = fp16(v - hi), v - hi
+// exact in fp32).  nrm accumulates |v|^2 of the unsplit fp32 values: the
+// certificate (knn.cu:certified_floor_tc) charges the difference to the
+// represented |hi + lo|^2 (<= 2^-21 |v|^2 + 2^-24 sqrt(d) |v|), which saves
+// unpacking lo and forming hi + lo.
 __device__ __forceinline__ void split2(float v0, float v1, __half2 &hi, __half2 &lo, float &nrm) {
     hi = __floats2half2_rn(v0, v1);
     const float2 fh = __half22float2(hi);
     lo = __floats2half2_rn(__fsub_rn(v0, fh.x), __fsub_rn(v1, fh.y));
-    const float2 fl = __half22float2(lo);
-    const float w0 = __fadd_rn(fh.x, fl.x), w1 = __fadd_rn(fh.y, fl.y);
-    nrm = __fmaf_rn(w0, w0, nrm);
-    nrm = __fmaf_rn(w1, w1, nrm);
+    nrm = __fmaf_rn(v0, v0, nrm);
+    nrm = __fmaf_rn(v1, v1, nrm);
 }
-
 
 // ------------------------------------------------------------- smem plan
 // Convert groups: NCG x 128 threads, NCG threads per point (each converts
@@ -183,7 +186,7 @@ __device__ __forceinline__ void split2(float v0, float v1, __half2 &hi, __half2 
 // capped at 128 registers, 16-column steps).
 constexpr int NCG = 1;
 constexpr int NTHREADS = 320 + 128 * (NCG - 1);  // convert 0-3 (+10-13), epilogue 4-7, MMA 8, producer 9
-constexpr int NT = 2;        // TMEM accumulator stages (128 fp32 columns each)
+constexpr int NT = 4;        // TMEM accumulator stages (128 fp32 columns each)
 constexpr int MAX_NB = 6;    // B operand stages
 constexpr int NMETA = MAX_NB + NT;  // per-tile metadata ring (see producer)
 constexpr uint32_t TMEM_COLS = NT * 128;
@@ -287,52 +290,6 @@ __device__ __forceinline__ float convert_tile(unsigned char *tile, int r, int g0
     return nrm;
 }
 
-// Pruned visit order of one query block, 32 superblocks per step: lanes load
-// the next 32 sorted superblock ids/keys and their bounds, a ballot keeps the
-// admissible ones, then each admissible superblock's 32 member bounds are
-// loaded at once.  Bounds are re-checked against the current threshold at
-// every step (thresholds only fall, so skipping stays exact).  Keys are
-// sorted with +inf (never admissible: every pair same-coloured) last.
-struct Visitor {
-    const int32_t *sb_order;
-    const float *sb_key, *sb_lb, *blk_lb;
-    int64_t nsb, nxb;
-    int64_t base = 0;
-    bool done = false;
-    unsigned sbmask = 0, bmask = 0;
-    int my_sb = 0, cur_sb = 0;
-    float my_sblb = INFINITY, my_blb = INFINITY;
-
-    __device__ int64_t next(float thr, int lane) {
-        while (true) {
-            if (bmask) {
-                const int m = __ffs(bmask) - 1;
-                bmask &= bmask - 1;
-                if (__shfl_sync(FULL, my_blb, m) > thr) continue;
-                return (int64_t)cur_sb * 32 + m;
-            }
-            if (sbmask) {
-                const int i = __ffs(sbmask) - 1;
-                sbmask &= sbmask - 1;
-                if (__shfl_sync(FULL, my_sblb, i) > thr) continue;
-                cur_sb = __shfl_sync(FULL, my_sb, i);
-                const int64_t b = (int64_t)cur_sb * 32 + lane;
-                my_blb = b < nxb ? __ldg(blk_lb + b) : INFINITY;
-                bmask = __ballot_sync(FULL, my_blb != INFINITY && !(my_blb > thr));
-                continue;
-            }
-            if (done) return -1;
-            const int64_t pos = base + lane;
-            const float key = pos < nsb ? __ldg(sb_key + pos) : INFINITY;
-            my_sb = pos < nsb ? __ldg(sb_order + pos) : 0;
-            my_sblb = key != INFINITY ? __ldg(sb_lb + my_sb) : INFINITY;
-            sbmask = __ballot_sync(FULL, key != INFINITY && !(my_sblb > thr));
-            base += 32;
-            if (base >= nsb || __ballot_sync(FULL, key == INFINITY)) done = true;
-        }
-    }
-};
-
 template <int MODE, int KP>
 __global__ void __launch_bounds__(NTHREADS, 1) tc_scan_kernel(TcArgs a) {
     extern __shared__ __align__(1024) unsigned char smem[];
@@ -357,7 +314,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_scan_kernel(TcArgs a) {
     uint64_t *afull = tempty + NT;                                      // A tile landed
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int64_t qb = a.qb0 + blockIdx.x;
+    const int64_t qbl = blockIdx.x / a.nsplit;  // query block within the launch
+    const int split = blockIdx.x - (int)qbl * a.nsplit;
+    const int64_t qb = a.qb0 + qbl;
     const int64_t row_base = qb * BM;
     const int64_t nxb = (a.nx + BN - 1) / BN;
     const uint32_t stage_bytes = (uint32_t)BM * dk * 4;
@@ -400,9 +359,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_scan_kernel(TcArgs a) {
             mbar_expect_tx(afull, stage_bytes);
             bulk_g2s(sA, a.qp + qb * (int64_t)dk * BM, stage_bytes, afull);
         }
-        Visitor vis{a.sb_order + (int64_t)blockIdx.x * a.nsb, a.sb_key + (int64_t)blockIdx.x * a.nsb,
-                    a.sb_lb + (int64_t)blockIdx.x * a.nsb, a.blk_lb + (int64_t)blockIdx.x * nxb,
-                    a.nsb, nxb};
+        BlockVisitor vis(a.sb_order + qbl * a.nsb, a.sb_lb + qbl * a.nsb, a.flat_lb + qbl * a.nsb * 32,
+                         a.nvalid[qbl], lane, split, a.nsplit);
         int64_t computed = 0;
         for (int it = 0;; it++) {
             const int s = it % nb;
@@ -635,11 +593,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_scan_kernel(TcArgs a) {
         }
         // write this row's candidate list (slots >= KP hold -1)
         if (gi >= a.row0 && gi < a.row1 && row_ok) {
-            int32_t *dst = a.cand + (gi - a.row0) * 32;
+            const int64_t slot = (gi - a.row0) * a.nsplit + split;
+            int32_t *dst = a.cand + slot * 32;
 #pragma unroll
             for (int q = 0; q < 32; q++) dst[q] = q < KP ? li[q < KP ? q : 0] : -1;
             // a = |q~|^2 + b rounded down: a lower bound keeps the certificate rigorous
-            a.kth[gi - a.row0] = li[KP - 1] >= 0 ? __fadd_rd(lv[KP - 1], qq) : INFINITY;
+            a.kth[slot] = li[KP - 1] >= 0 ? __fadd_rd(lv[KP - 1], qq) : INFINITY;
             a.qhat[gi - a.row0] = qq;
         }
     }
@@ -670,7 +629,7 @@ void launch_mode(const TcArgs &args, int64_t nqb, cudaStream_t s) {
     const Plan P = make_plan(args.dk);
     SLK_CUDA(cudaFuncSetAttribute(tc_scan_kernel<MODE, KP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)P.total));
-    tc_scan_kernel<MODE, KP><<<(unsigned)nqb, NTHREADS, P.total, s>>>(args);
+    tc_scan_kernel<MODE, KP><<<(unsigned)(nqb * args.nsplit), NTHREADS, P.total, s>>>(args);
     SLK_CHECK_LAUNCH();
 }
 
@@ -691,9 +650,11 @@ size_t smem_bytes(int d) { return make_plan(((d + 15) / 16) * 16).total; }
 // at least two B stages must fit next to the A tile
 bool supported(int d) { return make_plan(((d + 15) / 16) * 16).nb >= 2; }
 
-// K' = kp candidates per row (8, 16 or 32; kp > k for the certificate)
+// K' = kp candidates per row (2, 4, 8, 16 or 32; kp > k for the certificate)
 void launch(int mode, int kp, const TcArgs &args, int64_t nqb, cudaStream_t s) {
-    if (kp <= 8) launch_kp<8>(mode, args, nqb, s);
+    if (kp <= 2) launch_kp<2>(mode, args, nqb, s);
+    else if (kp <= 4) launch_kp<4>(mode, args, nqb, s);
+    else if (kp <= 8) launch_kp<8>(mode, args, nqb, s);
     else if (kp <= 16) launch_kp<16>(mode, args, nqb, s);
     else launch_kp<32>(mode, args, nqb, s);
 }

@@ -20,17 +20,18 @@ struct TcArgs {
     const uint8_t *mask;
     const int32_t *qcolor;
     const int32_t *xcolor;   // MODE_COLOR: padded to whole 128-point blocks
-    int32_t *cand;           // [rows][32] (slots >= K' hold -1)
-    float *kth;              // [rows] approximate K'-th value (scaled units, rounded down)
+    int32_t *cand;           // [rows][nsplit][32] (slots >= K' hold -1)
+    float *kth;              // [rows][nsplit] approximate K'-th value (scaled units, rounded down)
     float *qhat;             // [rows] |q^|^2 (scaled units)
     int64_t row0, row1;
-    const int32_t *sb_order;
-    const float *sb_key;
+    const int32_t *sb_order;  // visit order (scan_common.cuh:BlockVisitor)
     const float *sb_lb;
-    const float *blk_lb;
+    const float *flat_lb;
+    const int32_t *nvalid;
     int64_t nsb;
     unsigned long long *tiles_done;
     const int32_t *qid;      // query row -> id in the index, -1 = padding (or null)
+    int nsplit;              // CTAs per query block, each scanning 1/nsplit of the visit order
 };
 
 size_t smem_bytes(int d);
