@@ -440,6 +440,54 @@ __device__ __forceinline__ bool same_colour(const int2 *qcol, const int2 *xcol, 
     return a.x == a.y && c.x == c.y && a.x == c.x;
 }
 
+// Bounds for every (query block, index block) pair of the launch, tiled: a
+// 32 x 32 pair tile per CTA stages both centroid sets in shared memory in
+// 64-dim slices; each thread accumulates 4 pairs.  Same arithmetic as
+// sphere_lb (float64 squared differences summed in dimension order).
+__global__ void __launch_bounds__(256) pair_lb_kernel(const float *__restrict__ qc, const float *__restrict__ qr,
+                                                      int64_t nqb_total, const float *__restrict__ xc,
+                                                      const float *__restrict__ xr, int64_t nxb, int d,
+                                                      int64_t qb0, int64_t nqb, const int2 *__restrict__ qcol,
+                                                      const int2 *__restrict__ xcol, float *__restrict__ lb) {
+    __shared__ float sq[64][33], sx[64][33];
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // ty: 0..7
+    const int64_t b = (int64_t)blockIdx.x * 32 + tx;
+    const int64_t ql0 = (int64_t)blockIdx.y * 32;
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int t0 = 0; t0 < d; t0 += 64) {
+        const int tn = min(64, d - t0);
+        __syncthreads();
+        for (int e = threadIdx.x; e < tn * 32; e += 256) {
+            const int t = e >> 5, j = e & 31;
+            const int64_t qg = qb0 + ql0 + j, xg = (int64_t)blockIdx.x * 32 + j;
+            sq[t][j] = ql0 + j < nqb ? qc[(int64_t)(t0 + t) * nqb_total + qg] : 0.0f;
+            sx[t][j] = xg < nxb ? xc[(int64_t)(t0 + t) * nxb + xg] : 0.0f;
+        }
+        __syncthreads();
+        for (int t = 0; t < tn; t++) {
+            const double xv = (double)sx[t][tx];
+#pragma unroll
+            for (int i = 0; i < 4; i++) {
+                const double df = (double)sq[t][ty * 4 + i] - xv;
+                acc[i] += df * df;
+            }
+        }
+    }
+    if (b >= nxb) return;
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+        const int64_t ql = ql0 + ty * 4 + i;
+        if (ql >= nqb) continue;
+        const int64_t q = qb0 + ql;
+        float v = INFINITY;
+        if (!same_colour(qcol, xcol, q, b)) {
+            const double g = sqrt(acc[i]) * (1.0 - 1e-12) - (double)qr[q] - (double)xr[b];
+            v = g > 0.0 ? (float)(g * g * (1.0 - 1e-6)) : 0.0f;
+        }
+        lb[ql * nxb + b] = v;
+    }
+}
+
 // Flat visit order: for query block ql and the s-th superblock of its sorted
 // order, the superblock's bound and the bounds of its 32 member blocks (+inf
 // past the last block, for same-coloured pairs and for superblocks with an
@@ -451,9 +499,9 @@ __global__ void flat_lb_kernel(const float *__restrict__ qc, const float *__rest
                                int64_t nqb, const int2 *__restrict__ qcol,
                                const int2 *__restrict__ xcol, const int32_t *__restrict__ sb_order,
                                const float *__restrict__ sb_key, int64_t nsb,
-                               const float *__restrict__ sc, const float *__restrict__ sr,
-                               float *__restrict__ flat, float *__restrict__ sblb,
-                               int32_t *__restrict__ nvalid) {
+                               const float *__restrict__ sb_lb_id,
+                               const float *__restrict__ blk_lb, float *__restrict__ flat,
+                               float *__restrict__ sblb, int32_t *__restrict__ nvalid) {
     const int64_t per = nsb * 32, total = nqb * per;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
          e += (int64_t)gridDim.x * blockDim.x) {
@@ -461,14 +509,11 @@ __global__ void flat_lb_kernel(const float *__restrict__ qc, const float *__rest
         const int m = (int)(r & 31);
         const float key = sb_key[ql * nsb + sp];
         const int64_t b = (int64_t)sb_order[ql * nsb + sp] * 32 + m;
-        float v = INFINITY;
-        if (key != INFINITY && b < nxb && !same_colour(qcol, xcol, q, b))
-            v = sphere_lb(qc, qr, nqb_total, q, xc, xr, nxb, b, d);
-        flat[e] = v;
+        flat[e] = key != INFINITY && b < nxb ? blk_lb[ql * nxb + b] : INFINITY;
         if (m == 0) {
             const bool fin = key != INFINITY;
             const int64_t sb = sb_order[ql * nsb + sp];
-            sblb[ql * nsb + sp] = fin ? sphere_lb(qc, qr, nqb_total, q, sc, sr, nsb, sb, d) : INFINITY;
+            sblb[ql * nsb + sp] = fin ? sb_lb_id[ql * nsb + sb] : INFINITY;
             const bool next_inf = sp + 1 == nsb || sb_key[ql * nsb + sp + 1] == INFINITY;
             if (fin && next_inf) nvalid[ql] = (int32_t)(sp + 1);
             if (sp == 0 && !fin) nvalid[ql] = 0;
@@ -477,12 +522,13 @@ __global__ void flat_lb_kernel(const float *__restrict__ qc, const float *__rest
 }
 
 // per (query block, superblock): sort key = centroid distance (+inf when every
-// pair is same-coloured), ids, segment offsets
+// pair is same-coloured), lower bound (by id), ids, segment offsets
 __global__ void superblock_lb_kernel(const float *__restrict__ qc, const float *__restrict__ qr,
                                      int64_t nqb_total, const float *__restrict__ sc,
                                      const float *__restrict__ sr, int64_t nsb, int d, int64_t qb0,
                                      int64_t nqb, const int2 *__restrict__ qcol,
-                                     const int2 *__restrict__ scol, float *__restrict__ key, int32_t *__restrict__ ids,
+                                     const int2 *__restrict__ scol, float *__restrict__ key,
+                                     float *__restrict__ lb, int32_t *__restrict__ ids,
                                      int32_t *__restrict__ seg) {
     const int64_t total = nqb * nsb;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
@@ -495,6 +541,7 @@ __global__ void superblock_lb_kernel(const float *__restrict__ qc, const float *
         }
         const bool same = same_colour(qcol, scol, q, b);
         key[e] = same ? INFINITY : (float)s;
+        lb[e] = same ? INFINITY : sphere_lb(qc, qr, nqb_total, q, sc, sr, nsb, b, d);
         ids[e] = (int32_t)b;
         if (b == 0) seg[ql] = (int32_t)(ql * nsb);
         if (e == total - 1) seg[nqb] = (int32_t)total;
@@ -846,11 +893,11 @@ VisitOrder visit_order(const PointSet &Q, const PointSet &X, int64_t qb0, int64_
         SLK_CHECK_LAUNCH();
     }
     VisitOrder V;
-    DevBuf<float> key(stotal, s), skey(stotal, s);
+    DevBuf<float> key(stotal, s), skey(stotal, s), sblb_id(stotal, s);
     DevBuf<int32_t> ids(stotal, s), seg(nqb + 1, s);
     superblock_lb_kernel<<<grid_for(stotal, 256), 256, 0, s>>>(
         Q.centroid, Q.radius, Q.nb, X.sb_centroid, X.sb_radius, nsb, Q.d, qb0, nqb, qrange.get(),
-        srange.get(), key, ids, seg);
+        srange.get(), key, sblb_id, ids, seg);
     SLK_CHECK_LAUNCH();
     V.sb_order.alloc(stotal, s);
     size_t tmp = 0;
@@ -861,12 +908,17 @@ VisitOrder visit_order(const PointSet &Q, const PointSet &X, int64_t qb0, int64_
     SLK_CUDA(cub::DeviceSegmentedRadixSort::SortPairs(t.get(), tmp, key.get(), skey.get(), ids.get(),
                                                       V.sb_order.get(), (int)stotal, (int)nqb, seg.get(),
                                                       seg.get() + 1, 0, 32, s));
+    DevBuf<float> blk_lb(nqb * nxb, s);
+    pair_lb_kernel<<<dim3((unsigned)((nxb + 31) / 32), (unsigned)((nqb + 31) / 32)), 256, 0, s>>>(
+        Q.centroid, Q.radius, Q.nb, X.centroid, X.radius, nxb, Q.d, qb0, nqb, qrange.get(), xrange.get(),
+        blk_lb);
+    SLK_CHECK_LAUNCH();
     V.flat_lb.alloc(stotal * 32, s);
     V.sb_lb.alloc(stotal, s);
     V.nvalid.alloc(nqb, s);
     flat_lb_kernel<<<grid_for(stotal * 32, 256), 256, 0, s>>>(
         Q.centroid, Q.radius, Q.nb, X.centroid, X.radius, nxb, Q.d, qb0, nqb, qrange.get(),
-        xrange.get(), V.sb_order, skey, nsb, X.sb_centroid, X.sb_radius, V.flat_lb, V.sb_lb, V.nvalid);
+        xrange.get(), V.sb_order, skey, nsb, sblb_id, blk_lb, V.flat_lb, V.sb_lb, V.nvalid);
     SLK_CHECK_LAUNCH();
     return V;
 }
