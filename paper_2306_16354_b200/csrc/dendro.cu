@@ -93,67 +93,6 @@ void dendrogram_device_sort(const int32_t *src, const int32_t *dst, const double
     SLK_CUDA(cudaStreamSynchronize(s));
 }
 
-static inline int32_t uf_find(int32_t *parent, int32_t x) {
-    // path halving: same roots as the reference's full compression (_uf_find,
-    // linkage.py:91-100), and the merge table only depends on the roots
-    while (parent[x] != x) {
-        parent[x] = parent[parent[x]];
-        x = parent[x];
-    }
-    return x;
-}
-
-// linkage.py:103-129: fold edges in merge order; row i = (min(ca, cb),
-// max(ca, cb), w, size), parent id n + i.  When `labels` is given, the flat
-// cut for n_clusters (linkage.py:184-213) is taken from the union-find state
-// after the first cut = (n-1) - (n_clusters-1) merges: a point's nearest
-// labelled ancestor is the current cluster id of its component, and labels
-// rank those ids ascending.
-void dendrogram_fold(const int32_t *a, const int32_t *b, const double *w, int64_t n,
-                     double *merges, int64_t n_clusters, int64_t *labels, double *extract_ms) {
-    if (n >= (1ll << 30)) throw_invalid("n=%lld too large for the dendrogram fold", (long long)n);
-    std::vector<int32_t> parent(n), cid(n), size(n, 1);
-    std::vector<uint8_t> rank(n, 0);
-    for (int32_t v = 0; v < (int32_t)n; v++) {
-        parent[v] = v;
-        cid[v] = v;
-    }
-    const int64_t cut = labels ? (n - 1) - (n_clusters - 1) : -1;
-    auto snapshot = [&]() {
-        auto t0 = std::chrono::steady_clock::now();
-        std::vector<int32_t> node_label(2 * n, -1);
-        std::vector<int32_t> ids;
-        ids.reserve(n_clusters);
-        for (int32_t v = 0; v < (int32_t)n; v++)
-            if (parent[v] == v) ids.push_back(cid[v]);
-        if ((int64_t)ids.size() != n_clusters)
-            throw_invalid("internal: found %lld label roots for %lld clusters", (long long)ids.size(),
-                          (long long)n_clusters);
-        std::sort(ids.begin(), ids.end());
-        for (size_t r = 0; r < ids.size(); r++) node_label[ids[r]] = (int32_t)r;
-        for (int32_t p = 0; p < (int32_t)n; p++) labels[p] = node_label[cid[uf_find(parent.data(), p)]];
-        if (extract_ms)
-            *extract_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
-    };
-    if (cut == 0) snapshot();
-    for (int64_t i = 0; i < n - 1; i++) {
-        int32_t ra = uf_find(parent.data(), a[i]), rb = uf_find(parent.data(), b[i]);
-        if (ra == rb) throw_invalid("edges contain a cycle: not a spanning tree");
-        const int32_t ca = cid[ra], cb = cid[rb], merged = size[ra] + size[rb];
-        double *row = merges + 4 * i;
-        row[0] = (double)(ca < cb ? ca : cb);
-        row[1] = (double)(ca < cb ? cb : ca);
-        row[2] = w[i];
-        row[3] = (double)merged;
-        if (rank[ra] < rank[rb]) std::swap(ra, rb);
-        parent[rb] = ra;
-        if (rank[ra] == rank[rb]) rank[ra]++;
-        cid[ra] = (int32_t)(n + i);
-        size[ra] = merged;
-        if (i + 1 == cut) snapshot();
-    }
-}
-
 // linkage.py:184-213
 void extract_labels(const double *merges, int64_t n, int64_t n_clusters, int64_t *labels) {
     if (n_clusters < 1 || n_clusters > n)

@@ -257,9 +257,12 @@ void single_linkage_device(const float *x32, const double *x64, int64_t n, int d
     // --- dendrogram (linkage.py:295-300)
     std::vector<int32_t> ha(n - 1), hb(n - 1);
     std::vector<double> hw(n - 1);
+    trace_mark("dendrogram start");
     dendrogram_device_sort(ts, td, tw, n, metric == 0, ha.data(), hb.data(), hw.data(), s);
+    trace_mark("dendrogram sorted (host)");
     double extract_ms = 0.0;
     dendrogram_fold(ha.data(), hb.data(), hw.data(), n, h_merges, n_clusters, h_labels, &extract_ms);
+    trace_mark("dendrogram folded");
     double t5 = now_ms();
     double t4 = t5 - extract_ms;  // the cut is taken inside the fold
     if (h_tree_src || h_tree_dst || h_tree_w) {
