@@ -675,12 +675,16 @@ __device__ double certified_floor(float a, int d, double nq, double max_xn, bool
 __device__ double certified_floor_tc(float a, float qhat2, double scale, int d, double nq,
                                      double max_xn, bool exact_f32) {
     const double sd_ = sqrt((double)d);
-    const double A = (double)a - (0x1p-25 * sd_ + 0x1p-45 * d);
+    // c0: + 2^-10 for the fp16 low term of the augmented norm (subnormal
+    // spacing 2^-25, times 2^14 (A side) times 2 (b = -2 acc))
+    const double A = (double)a - (0x1p-25 * sd_ + 0x1p-45 * d + 0x1p-10);
     if (!(A > 0.0) || !((double)a < INFINITY)) return -INFINITY;
     // |q~| of the represented query from the fp32-accumulated |v|^2 (relative
     // accumulation error <= (d + 4) 2^-24, representation 2^-22 |v| + 2^-25 sqrt(d))
     const double r = sqrt((double)qhat2 * (1.0 + (d + 4) * 0x1p-24)) * (1.0 + 0x1p-21) + 0x1p-25 * sd_;
-    const double g = (3.0 * d + 8.0) * 0x1p-23 * 1.1 + 0x1p-21 + 0x1p-20 + 0x1p-23 * sd_;
+    // + 2^-21: two-term fp16 split of the augmented norm (2^-22 relative, x2);
+    // + 4 2^-23: its accumulation (one more MMA step, two products)
+    const double g = (3.0 * d + 12.0) * 0x1p-23 * 1.1 + 0x1p-21 + 0x1p-20 + 0x1p-21 + 0x1p-23 * sd_;
     const double ca = 1.0 + g, cb = 4.0 * g * r, cc = 4.0 * g * r * r - A;
     const double disc = cb * cb - 4.0 * ca * cc;
     if (!(disc > 0.0)) return -INFINITY;
@@ -1082,11 +1086,16 @@ int tc_kp(int k) {
     return kp;
 }
 
-// Power-of-two scale putting the centred operands in fp16's range: |x| s <= 2^13.
+// Power-of-two scale for the tensor operands: the centred, scaled values stay
+// within |x~_t| <= 2^14 (fp16 range with a bit to spare) and the augmented norm
+// term |x~|^2 2^-15 (tc_scan.cu) stays below 2^15 < fp16 max: with |x - c| <=
+// 2 max|x|, both hold when 2 max|x| s <= min(2^14, 2^15 / sqrt(dkm)).
 bool tensor_scale(const PointSet &Q, const PointSet &X, float *scale, float *inv_scale2) {
     float m = fmaxf(Q.maxabs, X.maxabs);
     if (!(m > 0.0f)) m = 1.0f;
-    int e = 13 - (int)ceilf(log2f(m));
+    const int dkm = ((X.d + 15) / 16) * 16;
+    const double lim = std::min(16384.0, 32768.0 / sqrt((double)dkm));
+    int e = (int)floor(log2(lim / (2.0 * (double)m)));
     if (e < -50 || e > 50) return false;
     *scale = ldexpf(1.0f, e);
     *inv_scale2 = ldexpf(1.0f, -2 * e);
@@ -1095,7 +1104,7 @@ bool tensor_scale(const PointSet &Q, const PointSet &X, float *scale, float *inv
 
 const float *ensure_tcpack(const PointSet &P, cudaStream_t s) {
     if (!P.tcpack) {
-        const int dk = ((P.d + 15) / 16) * 16;
+        const int dk = tc::k_extent(P.d);
         P.tcpack.alloc((size_t)P.nb * BN * dk, s);
         tcpack_kernel<<<grid_for(P.nb * BN * (int64_t)dk, 256), 256, 0, s>>>(P.x32, P.n, P.d, dk, P.nb,
                                                                             P.tcpack);
@@ -1145,7 +1154,7 @@ int tc_pass(const PointSet &Q, const PointSet &X, const int32_t *qid, int k, int
         SLK_CUDA(cudaMemcpyAsync(xcolp, xcolor, (size_t)nx * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
     }
     const float *qtc = ensure_tcpack(Q, s), *xtc = ensure_tcpack(X, s);
-    tc::TcArgs ta{qtc, xtc, nq, nx, d, X.dp, ((d + 15) / 16) * 16, qb0, Q.centroid,
+    tc::TcArgs ta{qtc, xtc, nq, nx, d, X.dp, tc::k_extent(d), qb0, Q.centroid,
                   Q.nb, scale, inv_scale2, mask, qcolor, mode == MODE_COLOR ? xcolp.get() : xcolor,
                   cand, kth_split, qhat, q0, q1,
                   V.sb_order, V.sb_lb, V.flat_lb, V.nvalid, X.nsb, tiles, qid, nsplit};
@@ -1500,7 +1509,7 @@ void debug_tc_scan(const float *x32, int64_t n, int d, int k, int32_t *cand, flo
     DevBuf<unsigned long long> tiles(1, s);
     SLK_CUDA(cudaMemsetAsync(tiles, 0, sizeof(unsigned long long), s));
     const float *tcp = ensure_tcpack(*P, s);
-    tc::TcArgs ta{tcp, tcp, n, n, d, P->dp, ((d + 15) / 16) * 16, 0, P->centroid,
+    tc::TcArgs ta{tcp, tcp, n, n, d, P->dp, tc::k_extent(d), 0, P->centroid,
                   P->nb, scale, inv2, nullptr, nullptr, nullptr, cand, kth, qhat, 0, n,
                   V.sb_order, V.sb_lb, V.flat_lb, V.nvalid, P->nsb, tiles, nullptr, 1};
     tc::launch(scan::MODE_SELF, tc_kp(k), ta, nqb, s);

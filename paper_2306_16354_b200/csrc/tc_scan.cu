@@ -180,27 +180,32 @@ __device__ __forceinline__ void split2(float v0, float v1, __half2 &hi, __half2 
 }
 
 // ------------------------------------------------------------- smem plan
-// Convert groups: NCG x 128 threads, NCG threads per point (each converts
-// dk / NCG dims and keeps its own partial |x~|^2).  Measured at C3/C5: one
-// group (4 warps, 157 registers, 32-column epilogue steps) beats two (8 warps,
-// capped at 128 registers, 16-column steps).
-constexpr int NCG = 1;
-constexpr int NTHREADS = 320 + 128 * (NCG - 1);  // convert 0-3 (+10-13), epilogue 4-7, MMA 8, producer 9
+// (Measured at C3/C5: 4 convert warps with 157 registers and 32-column
+// epilogue steps beat 8 convert warps capped at 128 registers.)
+constexpr int NTHREADS = 320;  // convert 0-3, epilogue 4-7, MMA 8, producer 9
 constexpr int NT = 4;        // TMEM accumulator stages (128 fp32 columns each)
 constexpr int MAX_NB = 6;    // B operand stages
 constexpr int NMETA = MAX_NB + NT;  // per-tile metadata ring (see producer)
 constexpr uint32_t TMEM_COLS = NT * 128;
-constexpr int CH = NCG == 1 ? 32 : 16;  // accumulator columns per epilogue step (tcgen05.ld .x32/.x16)
-constexpr uint32_t CH_ALL = CH == 32 ? 0xffffffffu : ((1u << (CH & 31)) - 1u);
+constexpr int CH = 32;  // accumulator columns per epilogue step (tcgen05.ld .x32)
+constexpr uint32_t CH_ALL = 0xffffffffu;
+// Augmented K: the last 16-column step of every operand tile carries the
+// norm term.  A: hi[dkm] = hi[dkm+1] = 2^14; B: hi[dkm] + hi[dkm+1] = two-term
+// fp16 split of -|x~|^2 2^-15.  One extra hi.hi MMA adds -|x~|^2 / 2 to the
+// accumulator, so the epilogue reads acc = <q~,x~> - |x~|^2 / 2 = -b / 2
+// directly (knn.cu:tensor_scale keeps |x~|^2 2^-15 below the fp16 range).
+constexpr float NORM_A = 16384.0f;       // 2^14
+constexpr float NORM_B_SCALE = -0x1p-15f;
 constexpr int STG_STRIDE = CH + 4;  // per-row chunk staging (CH + 4 floats: conflict-free STS.128)
 constexpr uint32_t SMEM_LIMIT = 227 * 1024;
 
 struct Plan {
-    uint32_t a, b, xx, xx1, xcol, qq, qq1, cq, stg, misc, bars, total;
+    uint32_t a, b, xx, xcol, qq, cq, stg, misc, bars, total;
     int nb;  // B stages that fit
 };
 
-__host__ __device__ inline Plan make_plan(int dk) {
+// aug: the norm rides in the augmented K step (no |x~|^2 array)
+__host__ __device__ inline Plan make_plan(int dk, bool aug) {
     Plan p{};
     uint32_t off = 0;
     auto take = [&](uint32_t bytes, uint32_t align) {
@@ -211,11 +216,9 @@ __host__ __device__ inline Plan make_plan(int dk) {
     };
     const uint32_t stage = (uint32_t)BM * dk * 4;  // hi + lo fp16 tiles = raw fp32 block
     p.a = take(stage, 1024);
-    p.xx = take(NMETA * BN * 4, 16);
-    p.xx1 = take(NMETA * BN * 4, 16);
+    p.xx = aug ? 0u : take(NMETA * BN * 4, 16);
     p.xcol = take(NMETA * BN * 4, 16);
     p.qq = take(BM * 4, 16);
-    p.qq1 = take(BM * 4, 16);
     p.cq = take(dk * 4, 16);
     p.stg = take(BM * STG_STRIDE * 4, 16);
     p.misc = take(128, 16);
@@ -240,7 +243,7 @@ struct Misc {
 #ifdef SLK_WATCHDOG
 __device__ void watchdog_dump(int tag, int it, uint32_t parity, unsigned long long st) {
     extern __shared__ __align__(1024) unsigned char smem[];
-    const Plan P = make_plan(64);
+    const Plan P = make_plan(64, true);
     const Misc *m = reinterpret_cast<const Misc *>(smem + P.misc);
     const unsigned long long *bars = reinterpret_cast<const unsigned long long *>(smem + P.bars);
     printf("watchdog: block %d thread %d tag %d it %d parity %u state %llx dbg %d %d %d %d "
@@ -263,16 +266,16 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
         : "memory");
 }
 
-// Converts core-matrix columns [g0, g1) (dims 8g0 .. 8g1-1) of point r of a
+// Converts the dkm main dims (core-matrix columns [0, dkm/8)) of point r of a
 // 128-point operand tile in place (raw tc-packed fp32 -> fp16 hi/lo canonical
-// layout).  Returns the partial |x~|^2 of the represented point over those dims.
-__device__ __forceinline__ float convert_tile(unsigned char *tile, int r, int g0, int g1, int dk,
-                                              float sc, const float *s_cq) {
+// layout, K extent dk = dkm + 16) and returns |v|^2 of the unsplit values.
+__device__ __forceinline__ float convert_tile(unsigned char *tile, int r, int dkm, int dk, float sc,
+                                              const float *s_cq) {
     const uint32_t half_bytes = (uint32_t)BM * dk * 2;
     unsigned char *row = tile + (r >> 3) * (dk * 16) + (r & 7) * 16;
     float nrm = 0.0f;
 #pragma unroll 2
-    for (int g = g0; g < g1; g++) {
+    for (int g = 0; g < dkm / 8; g++) {
         float4 *ph = reinterpret_cast<float4 *>(row + g * 128);
         float4 *pl = reinterpret_cast<float4 *>(row + half_bytes + g * 128);
         const float4 u = *ph, w = *pl;
@@ -290,19 +293,32 @@ __device__ __forceinline__ float convert_tile(unsigned char *tile, int r, int g0
     return nrm;
 }
 
-template <int MODE, int KP>
+// Writes the hi entries (dkm, dkm+1) of point r's augmented K step; the rest
+// of the step is zero already (padding of the tc-packed layout).
+__device__ __forceinline__ void put_norm_terms(unsigned char *tile, int r, int dkm, int dk, float t0, float t1) {
+    unsigned char *p = tile + (r >> 3) * (dk * 16) + (r & 7) * 16 + (dkm / 8) * 128;
+    *reinterpret_cast<__half2 *>(p) = __floats2half2_rn(t0, t1);
+}
+
+// -|x~|^2 2^-15 as hi + lo fp16 (|hi + lo - v| <= 2^-22 |v| + 2^-25)
+__device__ __forceinline__ void norm_split(float xx, float &t0, float &t1) {
+    const float v = xx * NORM_B_SCALE;  // exact: power of two
+    const float hi = __half2float(__float2half_rn(v));
+    t0 = hi;
+    t1 = __fsub_rn(v, hi);
+}
+
+template <int MODE, int KP, bool AUG>
 __global__ void __launch_bounds__(NTHREADS, 1) tc_scan_kernel(TcArgs a) {
     extern __shared__ __align__(1024) unsigned char smem[];
     const int dk = a.dk;
-    const Plan P = make_plan(dk);
+    const Plan P = make_plan(dk, AUG);
+    float *s_xx = reinterpret_cast<float *>(smem + P.xx);  // !AUG: |x~|^2 per meta slot
     const int nb = P.nb;
     unsigned char *sA = smem + P.a;
     unsigned char *sB = smem + P.b;
-    float *s_xx = reinterpret_cast<float *>(smem + P.xx);    // |x~|^2 over dims [0, dk/2)
-    float *s_xx1 = reinterpret_cast<float *>(smem + P.xx1);  // ... over [dk/2, dk)
     int *s_xcol = reinterpret_cast<int *>(smem + P.xcol);
     float *s_qq = reinterpret_cast<float *>(smem + P.qq);
-    float *s_qq1 = reinterpret_cast<float *>(smem + P.qq1);
     float *s_cq = reinterpret_cast<float *>(smem + P.cq);
     float *s_stg = reinterpret_cast<float *>(smem + P.stg);
     Misc *misc = reinterpret_cast<Misc *>(smem + P.misc);
@@ -322,12 +338,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_scan_kernel(TcArgs a) {
     const uint32_t stage_bytes = (uint32_t)BM * dk * 4;
     const uint32_t half_bytes = (uint32_t)BM * dk * 2;
     const uint32_t sbo = (uint32_t)dk * 16;  // (dk/8) core matrices of 128 B per 8-row group
+    const int dkm = AUG ? dk - 16 : dk;     // main dims (d rounded up to 16); then the norm step
 
     // ---- setup: barriers, TMEM, centring constants
     if (tid == 0) {
         for (int s = 0; s < MAX_NB; s++) {
             mbar_init(&rawfull[s], 1);
-            mbar_init(&bfull[s], 128 * NCG);
+            mbar_init(&bfull[s], 128);
             mbar_init(&bempty[s], 1);
         }
         for (int s = 0; s < NT; s++) {
@@ -392,27 +409,31 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_scan_kernel(TcArgs a) {
             if (jb < 0) break;
         }
         if (lane == 0 && a.tiles_done) atomicAdd(a.tiles_done, (unsigned long long)computed);
-    } else if (warp < 4 || (NCG == 2 && warp >= 10)) {
-        // ===================== convert warps: A once, then every B stage in place.
-        // 256 threads: point r = ct & 127, dims half h = ct >> 7 (two threads
-        // per point, each with its own partial |x~|^2; the epilogue adds them)
-        const int ct = warp < 4 ? tid : tid - 192;  // 0..128*NCG-1
-        const int r = ct & 127, h = ct >> 7;
-        const int g0 = h * (dk / (8 * NCG)), g1 = g0 + dk / (8 * NCG);
+    } else if (warp < 4) {
+        // ===================== convert warps: A once, then every B stage in place
+        const int r = tid;  // 0..127: query row (A) / index point (B)
         const float sc = a.scale;
-        float *xxh = h ? s_xx1 : s_xx;
         mbar_wait(afull, 0, 2, 0);
-        (h ? s_qq1 : s_qq)[r] = convert_tile(sA, r, g0, g1, dk, sc, s_cq);
+        s_qq[r] = convert_tile(sA, r, dkm, dk, sc, s_cq);
+        if (AUG) put_norm_terms(sA, r, dkm, dk, NORM_A, NORM_A);
         for (int it = 0;; it++) {
             const int s = it % nb;
             const uint32_t ph = (uint32_t)(it / nb) & 1u;
             mbar_wait(&rawfull[s], ph, 3, it);
             const int jb = misc->meta_blk[it % NMETA];
 #ifdef SLK_WATCHDOG
-            if (ct == 200) misc->dbg[1] = it * 100000 + (jb < 0 ? 99999 : jb % 100000);
+            if (r == 100) misc->dbg[1] = it * 100000 + (jb < 0 ? 99999 : jb % 100000);
 #endif
             if (jb >= 0) {
-                xxh[(it % NMETA) * BN + r] = convert_tile(sB + (size_t)s * stage_bytes, r, g0, g1, dk, sc, s_cq);
+                unsigned char *tile = sB + (size_t)s * stage_bytes;
+                const float xx = convert_tile(tile, r, dkm, dk, sc, s_cq);
+                if (AUG) {
+                    float t0, t1;
+                    norm_split(xx, t0, t1);
+                    put_norm_terms(tile, r, dkm, dk, t0, t1);
+                } else {
+                    s_xx[(it % NMETA) * BN + r] = xx;
+                }
                 fence_async_smem();  // generic-proxy smem writes -> visible to the tensor core
             }
             mbar_arrive(&bfull[s]);
@@ -443,7 +464,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_scan_kernel(TcArgs a) {
                 const uint32_t d_tmem = tmem + (uint32_t)ts * 128;
                 // <q~, x~> = hi.hi + hi.lo + lo.hi (the lo.lo term, <= 2^-22 |q~||x~|, is dropped)
                 const uint32_t bs = b_base + s * stage_bytes;
-                for (int k = 0; k < dk / 16; k++) {
+                for (int k = 0; k < dkm / 16; k++) {
                     const uint64_t ah = umma_desc(a_base + k * 256, 128, sbo);
                     const uint64_t al = umma_desc(a_base + half_bytes + k * 256, 128, sbo);
                     const uint64_t bh = umma_desc(bs + k * 256, 128, sbo);
@@ -452,6 +473,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_scan_kernel(TcArgs a) {
                     umma_f16(d_tmem, ah, bl, 1u);
                     umma_f16(d_tmem, al, bh, 1u);
                 }
+                // augmented step: + 2^14 (-|x~|^2 2^-15) = -|x~|^2 / 2
+                if (AUG)
+                    umma_f16(d_tmem, umma_desc(a_base + (dkm / 16) * 256, 128, sbo),
+                             umma_desc(bs + (dkm / 16) * 256, 128, sbo), 1u);
                 umma_commit(&bempty[s]);  // operands consumed: the producer may refill stage s
                 umma_commit(&tfull[ts]);  // accumulator ready
             }
@@ -491,7 +516,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_scan_kernel(TcArgs a) {
             mbar_wait(&tfull[ts], tph, 6, it);
             tc_fence_after();
             // the convert warps wrote A (and |q~|^2) before their first bfull arrive
-            if (it == 0) qq = NCG == 2 ? s_qq[row] + s_qq1[row] : s_qq[row];
+            if (it == 0) qq = s_qq[row];
             const int slot = it % NMETA;
             const int jb = misc->meta_blk[slot];
 #ifdef SLK_WATCHDOG
@@ -505,39 +530,43 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_scan_kernel(TcArgs a) {
             const int col_limit = row_ok ? (rem < BN ? (int)rem : BN) : 0;
             const int self_col =
                 (MODE == MODE_SELF && self_id >= col0 && self_id < col0 + BN) ? (int)(self_id - col0) : -1;
-            const float *xxs = s_xx + slot * BN;
-            const float *xxs1 = s_xx1 + slot * BN;
             const int *xcs = s_xcol + slot * BN;
 #pragma unroll 1
             for (int c0 = 0; c0 < BN; c0 += CH) {
                 float dot[CH];
                 __syncwarp();  // tcgen05.ld is .sync.aligned: reconverge after the insertion loop
                 tmem_ld(taddr + c0, dot);
-                // fast path: b = fma(-2, dot, |x~|^2) and the chunk minimum
+                // fast path.  AUG: acc = -b / 2, hit iff max(acc) > -thr / 2 (exact
+                // scalings).  Else b = fma(-2, acc, |x~|^2) (|x~|^2 from smem), hit
+                // iff min(b) < thr.
                 float av[CH];
+                if (!AUG) {
+                    const float *xxs = s_xx + slot * BN;
 #pragma unroll
-                for (int i = 0; i < CH; i += 4) {
-                    float4 x4 = *reinterpret_cast<const float4 *>(xxs + c0 + i);
-                    if (NCG == 2) {
-                        const float4 x4b = *reinterpret_cast<const float4 *>(xxs1 + c0 + i);
-                        x4 = make_float4(x4.x + x4b.x, x4.y + x4b.y, x4.z + x4b.z, x4.w + x4b.w);
+                    for (int i = 0; i < CH; i += 4) {
+                        const float4 x4 = *reinterpret_cast<const float4 *>(xxs + c0 + i);
+                        av[i + 0] = __fmaf_rn(-2.0f, dot[i + 0], x4.x);
+                        av[i + 1] = __fmaf_rn(-2.0f, dot[i + 1], x4.y);
+                        av[i + 2] = __fmaf_rn(-2.0f, dot[i + 2], x4.z);
+                        av[i + 3] = __fmaf_rn(-2.0f, dot[i + 3], x4.w);
                     }
-                    av[i + 0] = __fmaf_rn(-2.0f, dot[i + 0], x4.x);
-                    av[i + 1] = __fmaf_rn(-2.0f, dot[i + 1], x4.y);
-                    av[i + 2] = __fmaf_rn(-2.0f, dot[i + 2], x4.z);
-                    av[i + 3] = __fmaf_rn(-2.0f, dot[i + 3], x4.w);
                 }
-                float mn[CH / 2];
+                float mx[CH / 2];
 #pragma unroll
-                for (int i = 0; i < CH / 2; i++) mn[i] = fminf(av[i], av[i + CH / 2]);
+                for (int i = 0; i < CH / 2; i++)
+                    mx[i] = AUG ? fmaxf(dot[i], dot[i + CH / 2]) : fminf(av[i], av[i + CH / 2]);
 #pragma unroll
                 for (int w = CH / 4; w; w >>= 1)
 #pragma unroll
-                    for (int i = 0; i < w; i++) mn[i] = fminf(mn[i], mn[i + w]);
-                const bool hit = mn[0] < thr;
+                    for (int i = 0; i < w; i++) mx[i] = AUG ? fmaxf(mx[i], mx[i + w]) : fminf(mx[i], mx[i + w]);
+                const bool hit = AUG ? mx[0] > -0.5f * thr : mx[0] < thr;
                 if (!__any_sync(FULL, hit)) continue;  // warp-uniform: nothing to insert
                 uint32_t pass = 0;
                 if (hit) {
+                    if (AUG) {
+#pragma unroll
+                        for (int i = 0; i < CH; i++) av[i] = -2.0f * dot[i];  // b, exact
+                    }
 #pragma unroll
                     for (int i = 0; i < CH; i++) pass |= (av[i] < thr ? 1u : 0u) << i;
                     uint32_t valid = c0 >= col_limit ? 0u
@@ -624,39 +653,52 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_scan_kernel(TcArgs a) {
     }
 }
 
-template <int MODE, int KP>
+template <int MODE, int KP, bool AUG>
 void launch_mode(const TcArgs &args, int64_t nqb, cudaStream_t s) {
-    const Plan P = make_plan(args.dk);
-    SLK_CUDA(cudaFuncSetAttribute(tc_scan_kernel<MODE, KP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    const Plan P = make_plan(args.dk, AUG);
+    SLK_CUDA(cudaFuncSetAttribute(tc_scan_kernel<MODE, KP, AUG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)P.total));
-    tc_scan_kernel<MODE, KP><<<(unsigned)(nqb * args.nsplit), NTHREADS, P.total, s>>>(args);
+    tc_scan_kernel<MODE, KP, AUG><<<(unsigned)(nqb * args.nsplit), NTHREADS, P.total, s>>>(args);
     SLK_CHECK_LAUNCH();
 }
 
-template <int KP>
+template <int KP, bool AUG>
 void launch_kp(int mode, const TcArgs &args, int64_t nqb, cudaStream_t s) {
     switch (mode) {
-        case MODE_NONE: launch_mode<MODE_NONE, KP>(args, nqb, s); break;
-        case MODE_MASK: launch_mode<MODE_MASK, KP>(args, nqb, s); break;
-        case MODE_COLOR: launch_mode<MODE_COLOR, KP>(args, nqb, s); break;
-        default: launch_mode<MODE_SELF, KP>(args, nqb, s); break;
+        case MODE_NONE: launch_mode<MODE_NONE, KP, AUG>(args, nqb, s); break;
+        case MODE_MASK: launch_mode<MODE_MASK, KP, AUG>(args, nqb, s); break;
+        case MODE_COLOR: launch_mode<MODE_COLOR, KP, AUG>(args, nqb, s); break;
+        default: launch_mode<MODE_SELF, KP, AUG>(args, nqb, s); break;
     }
+}
+
+template <bool AUG>
+void launch_aug(int mode, int kp, const TcArgs &args, int64_t nqb, cudaStream_t s) {
+    if (kp <= 2) launch_kp<2, AUG>(mode, args, nqb, s);
+    else if (kp <= 4) launch_kp<4, AUG>(mode, args, nqb, s);
+    else if (kp <= 8) launch_kp<8, AUG>(mode, args, nqb, s);
+    else if (kp <= 16) launch_kp<16, AUG>(mode, args, nqb, s);
+    else launch_kp<32, AUG>(mode, args, nqb, s);
 }
 
 }  // namespace
 
-size_t smem_bytes(int d) { return make_plan(((d + 15) / 16) * 16).total; }
+// The augmented norm step when at least 3 B stages still fit (measured: the
+// max-only epilogue pays for the extra MMA and the 16 extra K columns);
+// otherwise |x~|^2 goes through shared memory (large d).
+bool use_aug(int d) { return make_plan(((d + 15) / 16) * 16 + 16, true).nb >= 3; }
+
+int k_extent(int d) { return ((d + 15) / 16) * 16 + (use_aug(d) ? 16 : 0); }
+
+size_t smem_bytes(int d) { return make_plan(k_extent(d), use_aug(d)).total; }
 
 // at least two B stages must fit next to the A tile
-bool supported(int d) { return make_plan(((d + 15) / 16) * 16).nb >= 2; }
+bool supported(int d) { return make_plan(k_extent(d), use_aug(d)).nb >= 2; }
 
 // K' = kp candidates per row (2, 4, 8, 16 or 32; kp > k for the certificate)
 void launch(int mode, int kp, const TcArgs &args, int64_t nqb, cudaStream_t s) {
-    if (kp <= 2) launch_kp<2>(mode, args, nqb, s);
-    else if (kp <= 4) launch_kp<4>(mode, args, nqb, s);
-    else if (kp <= 8) launch_kp<8>(mode, args, nqb, s);
-    else if (kp <= 16) launch_kp<16>(mode, args, nqb, s);
-    else launch_kp<32>(mode, args, nqb, s);
+    if (use_aug(args.d)) launch_aug<true>(mode, kp, args, nqb, s);
+    else launch_aug<false>(mode, kp, args, nqb, s);
 }
 
 }  // namespace tc

@@ -11,7 +11,7 @@ struct TcArgs {
     const float *qp;         // tc-packed queries [nqb][128 * dk] (knn.cu:tcpack_kernel)
     const float *xp;         // tc-packed index   [nxb][128 * dk]
     int64_t nq, nx;
-    int d, dp, dk;           // dims, packed dims (multiple of 16), MMA K extent
+    int d, dp, dk;           // dims, packed dims (multiple of 16), MMA K extent (k_extent)
     int64_t qb0;             // first query block of this launch
     const float *qcentroid;  // query block centroids, dims-major [dp][nqb_total]
     int64_t nqb_total;
@@ -34,6 +34,10 @@ struct TcArgs {
     int nsplit;              // CTAs per query block, each scanning 1/nsplit of the visit order
 };
 
+// MMA K extent for d dims: d rounded up to 16, plus the augmented norm step
+// when use_aug(d) (tc_scan.cu)
+bool use_aug(int d);
+int k_extent(int d);
 size_t smem_bytes(int d);
 bool supported(int d);
 // kp: candidates kept per row (8, 16 or 32); the certificate needs kp > k
