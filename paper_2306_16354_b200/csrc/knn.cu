@@ -419,6 +419,44 @@ __global__ void block_color_range_kernel(const int32_t *__restrict__ color, int6
     if (lane == 0) range[b] = make_int2(lo, hi);
 }
 
+// Query groups of QB consecutive blocks [qb0 + g QB, qb0 + (g+1) QB): a sphere
+// containing the members' spheres (centre = point-weighted mean of their
+// centres, radius = max(|c_g - c_b| + r_b), rounded up) and the union of
+// their colour ranges.
+__global__ void group_sphere_kernel(const float *__restrict__ bc, const float *__restrict__ br,
+                                    const int2 *__restrict__ brange, int64_t n, int64_t nb, int d,
+                                    int64_t qb0, int64_t ng, int qbn, float *__restrict__ gc,
+                                    float *__restrict__ gr, int2 *__restrict__ grange) {
+    for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < ng;
+         g += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t b0 = qb0 + g * qbn, b1 = min(b0 + qbn, nb);
+        double wsum = 0.0;
+        for (int64_t b = b0; b < b1; b++) wsum += (double)min((int64_t)BN, n - b * BN);
+        for (int t = 0; t < d; t++) {
+            double acc = 0.0;
+            for (int64_t b = b0; b < b1; b++)
+                acc += (double)min((int64_t)BN, n - b * BN) * (double)bc[(int64_t)t * nb + b];
+            gc[(int64_t)t * ng + g] = (float)(acc / wsum);
+        }
+        double r = 0.0;
+        int lo = 0x7fffffff, hi = -1;
+        for (int64_t b = b0; b < b1; b++) {
+            double s2 = 0.0;
+            for (int t = 0; t < d; t++) {
+                const double df = (double)gc[(int64_t)t * ng + g] - (double)bc[(int64_t)t * nb + b];
+                s2 += df * df;
+            }
+            r = fmax(r, sqrt(s2) + (double)br[b]);
+            if (brange) {
+                lo = min(lo, brange[b].x);
+                hi = max(hi, brange[b].y);
+            }
+        }
+        gr[g] = (float)(r * (1.0 + 1e-6)) + 1e-30f;
+        if (grange) grange[g] = make_int2(lo, hi);
+    }
+}
+
 // Lower bound on the squared distance between any point of query block q and
 // any point of a sphere (c, r): (|c_q - c| - r_q - r)^2 by the triangle
 // inequality, rounded down.
@@ -876,21 +914,47 @@ void launch_exact(const ExactArgs &ea, cudaStream_t s) {
 
 // Per query block of [qb0, qb0 + nqb): superblocks in ascending centroid
 // distance, their lower bounds, and the per-block bounds.
+// Query groups of 1 or 2 consecutive query blocks (one CTA each in the tensor
+// scan): bounding spheres (dims-major centres) and colour ranges.
+struct QueryGroups {
+    DevBuf<float> cent, rad;
+    DevBuf<int2> range;
+    int64_t ng = 0;
+};
+
 struct VisitOrder {
     DevBuf<int32_t> sb_order, nvalid;
     DevBuf<float> sb_lb, flat_lb;
 };
-VisitOrder visit_order(const PointSet &Q, const PointSet &X, int64_t qb0, int64_t nqb,
-                       const int32_t *qcolor, const int32_t *xcolor, cudaStream_t s) {
+QueryGroups make_groups(const PointSet &Q, int64_t qb0, int64_t nqb, int qbn, const int32_t *qcolor,
+                        cudaStream_t s) {
+    QueryGroups G;
+    G.ng = (nqb + qbn - 1) / qbn;
+    G.cent.alloc((size_t)Q.dp * G.ng, s);
+    G.rad.alloc(G.ng, s);
+    DevBuf<int2> brange;
+    if (qcolor) {
+        brange.alloc(Q.nb, s);
+        block_color_range_kernel<<<(unsigned)((Q.nb * 32 + 255) / 256), 256, 0, s>>>(qcolor, Q.n, Q.nb, brange);
+        SLK_CHECK_LAUNCH();
+        G.range.alloc(G.ng, s);
+    }
+    group_sphere_kernel<<<grid_for(G.ng, 128), 128, 0, s>>>(Q.centroid, Q.radius, brange.get(), Q.n, Q.nb,
+                                                            Q.d, qb0, G.ng, qbn, G.cent, G.rad, G.range.get());
+    SLK_CHECK_LAUNCH();
+    return G;
+}
+
+// Visit order of every query group against X (colour mode iff xcolor).
+VisitOrder visit_order(const QueryGroups &G, const PointSet &X, int d, const int32_t *xcolor, cudaStream_t s) {
+    const int64_t nqb = G.ng, qb0 = 0;
     const int64_t nxb = X.nb, nsb = X.nsb, stotal = nqb * nsb;
     if (stotal >= (1ll << 31)) throw_invalid("too many (query block, superblock) pairs: %lld", (long long)stotal);
-    DevBuf<int2> qrange, xrange, srange;
-    if (qcolor) {
-        qrange.alloc(Q.nb, s);
+    const int2 *qrange = xcolor ? G.range.get() : nullptr;
+    DevBuf<int2> xrange, srange;
+    if (xcolor) {
         xrange.alloc(X.nb, s);
         srange.alloc(nsb, s);
-        block_color_range_kernel<<<(unsigned)((Q.nb * 32 + 255) / 256), 256, 0, s>>>(qcolor, Q.n, Q.nb, qrange);
-        SLK_CHECK_LAUNCH();
         block_color_range_kernel<<<(unsigned)((X.nb * 32 + 255) / 256), 256, 0, s>>>(xcolor, X.n, X.nb, xrange);
         SLK_CHECK_LAUNCH();
         superblock_color_kernel<<<(unsigned)((nsb * 32 + 255) / 256), 256, 0, s>>>(xrange, X.nb, nsb, srange);
@@ -900,7 +964,7 @@ VisitOrder visit_order(const PointSet &Q, const PointSet &X, int64_t qb0, int64_
     DevBuf<float> key(stotal, s), skey(stotal, s), sblb_id(stotal, s);
     DevBuf<int32_t> ids(stotal, s), seg(nqb + 1, s);
     superblock_lb_kernel<<<grid_for(stotal, 256), 256, 0, s>>>(
-        Q.centroid, Q.radius, Q.nb, X.sb_centroid, X.sb_radius, nsb, Q.d, qb0, nqb, qrange.get(),
+        G.cent, G.rad, G.ng, X.sb_centroid, X.sb_radius, nsb, d, qb0, nqb, qrange,
         srange.get(), key, sblb_id, ids, seg);
     SLK_CHECK_LAUNCH();
     V.sb_order.alloc(stotal, s);
@@ -914,17 +978,22 @@ VisitOrder visit_order(const PointSet &Q, const PointSet &X, int64_t qb0, int64_
                                                       seg.get() + 1, 0, 32, s));
     DevBuf<float> blk_lb(nqb * nxb, s);
     pair_lb_kernel<<<dim3((unsigned)((nxb + 31) / 32), (unsigned)((nqb + 31) / 32)), 256, 0, s>>>(
-        Q.centroid, Q.radius, Q.nb, X.centroid, X.radius, nxb, Q.d, qb0, nqb, qrange.get(), xrange.get(),
-        blk_lb);
+        G.cent, G.rad, G.ng, X.centroid, X.radius, nxb, d, qb0, nqb, qrange, xrange.get(), blk_lb);
     SLK_CHECK_LAUNCH();
     V.flat_lb.alloc(stotal * 32, s);
     V.sb_lb.alloc(stotal, s);
     V.nvalid.alloc(nqb, s);
     flat_lb_kernel<<<grid_for(stotal * 32, 256), 256, 0, s>>>(
-        Q.centroid, Q.radius, Q.nb, X.centroid, X.radius, nxb, Q.d, qb0, nqb, qrange.get(),
+        G.cent, G.rad, G.ng, X.centroid, X.radius, nxb, d, qb0, nqb, qrange,
         xrange.get(), V.sb_order, skey, nsb, sblb_id, blk_lb, V.flat_lb, V.sb_lb, V.nvalid);
     SLK_CHECK_LAUNCH();
     return V;
+}
+
+VisitOrder visit_order(const PointSet &Q, const PointSet &X, int64_t qb0, int64_t nqb,
+                       const int32_t *qcolor, const int32_t *xcolor, cudaStream_t s) {
+    QueryGroups G = make_groups(Q, qb0, nqb, 1, qcolor, s);
+    return visit_order(G, X, Q.d, qcolor ? xcolor : nullptr, s);
 }
 
 __global__ void gather_rows_kernel(const float *x32, const double *x64, const int32_t *rows,
@@ -1037,7 +1106,8 @@ int64_t search_ffma(const PointSet &Q, const PointSet &X, const int32_t *qid, in
         else if (Rsel == 2) launch_refine<2>(ra, rows, s);
         else launch_refine<4>(ra, rows, s);
         ev_refine.stop(s);
-        unsigned long long done = read_scalar(tiles.get(), s);
+        // 128 x 128 tiles computed (a B tile serves every query block of its CTA)
+    unsigned long long done = read_scalar(tiles.get(), s);
     trace_mark("scan+refine done");
         st.rows_refined += rows;
         st.tiles_computed += (int64_t)done;
@@ -1126,11 +1196,17 @@ int tc_pass(const PointSet &Q, const PointSet &X, const int32_t *qid, int k, int
     const int d = X.d;
     const int64_t nq = Q.n, nx = X.n;
     const int64_t qb0 = q0 / BM, qb1 = (q1 + BM - 1) / BM;
-    // small launches: deal each query block's visit order over nsplit CTAs
+    const int kp = tc_kp(k);
+    // query blocks per CTA: pairs share every converted index tile, when the
+    // launch still fills the GPU with them
+    int qbn = tc::group_blocks(d, kp);
+    if (qbn == 2 && (qb1 - qb0) < 4 * num_sms()) qbn = 1;
+    const int64_t ngroups = (qb1 - qb0 + qbn - 1) / qbn;
+    // small launches: deal each query group's visit order over nsplit CTAs
     // (each keeps its own K' list; the refine takes the union) so that at
     // least ~2 CTAs per SM run
     int nsplit = 1;
-    while (nsplit < 8 && (qb1 - qb0) * nsplit < 2 * num_sms()) nsplit *= 2;
+    while (nsplit < 8 && ngroups * nsplit < 2 * num_sms()) nsplit *= 2;
     if (const char *e = getenv("SLK_TC_SPLIT")) nsplit = std::max(1, std::min(8, atoi(e)));
     if (nsplit & (nsplit - 1)) nsplit = 1;
     DevBuf<int32_t> cand(rows * 32 * nsplit, s);
@@ -1143,7 +1219,8 @@ int tc_pass(const PointSet &Q, const PointSet &X, const int32_t *qid, int k, int
     SLK_CUDA(cudaMemsetAsync(counters, 0, sizeof(int), s));
     EventPair ev_order, ev_scan, ev_refine;
     ev_order.start(s);
-    VisitOrder V = visit_order(Q, X, qb0, qb1 - qb0, mode == MODE_COLOR ? qcolor : nullptr, xcolor, s);
+    QueryGroups G = make_groups(Q, qb0, qb1 - qb0, qbn, mode == MODE_COLOR ? qcolor : nullptr, s);
+    VisitOrder V = visit_order(G, X, d, mode == MODE_COLOR ? xcolor : nullptr, s);
     ev_order.stop(s);
     trace_mark("visit_order enqueued");
     // colours of the index padded to whole blocks (one bulk copy per block)
@@ -1154,12 +1231,12 @@ int tc_pass(const PointSet &Q, const PointSet &X, const int32_t *qid, int k, int
         SLK_CUDA(cudaMemcpyAsync(xcolp, xcolor, (size_t)nx * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
     }
     const float *qtc = ensure_tcpack(Q, s), *xtc = ensure_tcpack(X, s);
-    tc::TcArgs ta{qtc, xtc, nq, nx, d, X.dp, tc::k_extent(d), qb0, Q.centroid,
+    tc::TcArgs ta{qtc, xtc, nq, nx, d, X.dp, tc::k_extent(d), qb0, G.cent, G.ng,
                   Q.nb, scale, inv_scale2, mask, qcolor, mode == MODE_COLOR ? xcolp.get() : xcolor,
                   cand, kth_split, qhat, q0, q1,
                   V.sb_order, V.sb_lb, V.flat_lb, V.nvalid, X.nsb, tiles, qid, nsplit};
     ev_scan.start(s);
-    tc::launch(mode, tc_kp(k), ta, qb1 - qb0, s);
+    tc::launch(mode, kp, qbn, ta, ngroups, s);
     ev_scan.stop(s);
     RefineArgs ra{Q.x32, Q.x64, Q.norms, X.x32, X.x64, X.norms, d, k, nq, nx, q0, q1,
                   cand, kth_split, nsplit, kth, X.maxn, X.x64 == nullptr && Q.x64 == nullptr, out_idx,
@@ -1173,7 +1250,8 @@ int tc_pass(const PointSet &Q, const PointSet &X, const int32_t *qid, int k, int
     }
     ev_refine.stop(s);
     trace_mark("scan+refine enqueued");
-    unsigned long long done = read_scalar(tiles.get(), s);
+    // 128 x 128 tiles computed (a B tile serves every query block of its CTA)
+    unsigned long long done = read_scalar(tiles.get(), s) * (unsigned long long)qbn;
     trace_mark("scan+refine done");
     st.rows_refined += rows;
     st.tiles_computed += (int64_t)done;
@@ -1181,8 +1259,8 @@ int tc_pass(const PointSet &Q, const PointSet &X, const int32_t *qid, int k, int
     record_profile(ev_order, ev_scan, ev_refine, rows, nx, d, done, (qb1 - qb0) * X.nb, true);
     const int nfail = read_scalar<int>(counters, s);
     if (trace_on())
-        fprintf(stderr, "[slk] tc_pass mode %d rows %lld: order %.2f scan %.2f refine %.2f ms, tiles %llu, uncertified %d\n",
-                mode, (long long)rows, ev_order.ms(), ev_scan.ms(), ev_refine.ms(), done, nfail);
+        fprintf(stderr, "[slk] tc_pass mode %d rows %lld (x%d blocks/CTA, split %d): order %.2f scan %.2f refine %.2f ms, tiles %llu, uncertified %d\n",
+                mode, (long long)rows, qbn, nsplit, ev_order.ms(), ev_scan.ms(), ev_refine.ms(), done, nfail);
     st.rows_uncertified += nfail;
     profile().tc_uncertified += nfail;
     return nfail;
@@ -1509,10 +1587,11 @@ void debug_tc_scan(const float *x32, int64_t n, int d, int k, int32_t *cand, flo
     DevBuf<unsigned long long> tiles(1, s);
     SLK_CUDA(cudaMemsetAsync(tiles, 0, sizeof(unsigned long long), s));
     const float *tcp = ensure_tcpack(*P, s);
-    tc::TcArgs ta{tcp, tcp, n, n, d, P->dp, tc::k_extent(d), 0, P->centroid,
+    QueryGroups G = make_groups(*P, 0, nqb, 1, nullptr, s);
+    tc::TcArgs ta{tcp, tcp, n, n, d, P->dp, tc::k_extent(d), 0, G.cent, G.ng,
                   P->nb, scale, inv2, nullptr, nullptr, nullptr, cand, kth, qhat, 0, n,
                   V.sb_order, V.sb_lb, V.flat_lb, V.nvalid, P->nsb, tiles, nullptr, 1};
-    tc::launch(scan::MODE_SELF, tc_kp(k), ta, nqb, s);
+    tc::launch(scan::MODE_SELF, tc_kp(k), 1, ta, nqb, s);
     SLK_CUDA(cudaStreamSynchronize(s));
     *scale_out = scale;
 }

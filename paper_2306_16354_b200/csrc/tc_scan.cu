@@ -43,6 +43,7 @@
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 #include "scan_common.cuh"
@@ -182,11 +183,20 @@ __device__ __forceinline__ void split2(float v0, float v1, __half2 &hi, __half2 
 // ------------------------------------------------------------- smem plan
 // (Measured at C3/C5: 4 convert warps with 157 registers and 32-column
 // epilogue steps beat 8 convert warps capped at 128 registers.)
-constexpr int NTHREADS = 320;  // convert 0-3, epilogue 4-7, MMA 8, producer 9
-constexpr int NT = 4;        // TMEM accumulator stages (128 fp32 columns each)
+// QB query blocks per CTA share every converted index tile (QB = 2 halves the
+// conversion work per query row; its 8 epilogue warps cap registers at 128,
+// so it serves K' <= 16).  Warps: convert 0-3, epilogue 4 .. 4+4QB-1, then
+// MMA, then producer.
+template <int QB> struct Cfg {
+    static constexpr int NTHREADS = 192 + 128 * QB;
+    static constexpr int WARP_MMA = 4 + 4 * QB;
+    static constexpr int WARP_PROD = 5 + 4 * QB;
+    static constexpr int NT = 4 / QB;  // TMEM accumulator stages of 128 QB columns: 512 columns
+};
+constexpr int NTMAX = 4;
 constexpr int MAX_NB = 6;    // B operand stages
-constexpr int NMETA = MAX_NB + NT;  // per-tile metadata ring (see producer)
-constexpr uint32_t TMEM_COLS = NT * 128;
+constexpr int NMETA = MAX_NB + NTMAX;  // per-tile metadata ring (see producer)
+constexpr uint32_t TMEM_COLS = 512;
 constexpr int CH = 32;  // accumulator columns per epilogue step (tcgen05.ld .x32)
 constexpr uint32_t CH_ALL = 0xffffffffu;
 // Augmented K: the last 16-column step of every operand tile carries the
@@ -205,7 +215,7 @@ struct Plan {
 };
 
 // aug: the norm rides in the augmented K step (no |x~|^2 array)
-__host__ __device__ inline Plan make_plan(int dk, bool aug) {
+__host__ __device__ inline Plan make_plan(int dk, bool aug, int qb) {
     Plan p{};
     uint32_t off = 0;
     auto take = [&](uint32_t bytes, uint32_t align) {
@@ -215,14 +225,14 @@ __host__ __device__ inline Plan make_plan(int dk, bool aug) {
         return at;
     };
     const uint32_t stage = (uint32_t)BM * dk * 4;  // hi + lo fp16 tiles = raw fp32 block
-    p.a = take(stage, 1024);
+    p.a = take(stage * qb, 1024);
     p.xx = aug ? 0u : take(NMETA * BN * 4, 16);
     p.xcol = take(NMETA * BN * 4, 16);
-    p.qq = take(BM * 4, 16);
+    p.qq = take(qb * BM * 4, 16);
     p.cq = take(dk * 4, 16);
-    p.stg = take(BM * STG_STRIDE * 4, 16);
+    p.stg = take(qb * BM * STG_STRIDE * 4, 16);
     p.misc = take(128, 16);
-    p.bars = take(8 * (4 * MAX_NB + 2 * NT + 1), 8);
+    p.bars = take(8 * (4 * MAX_NB + 2 * NTMAX + 1), 8);
     off = (off + 1023) / 1024 * 1024;
     int nb = off >= SMEM_LIMIT ? 0 : (int)((SMEM_LIMIT - off) / stage);
     p.nb = nb > MAX_NB ? MAX_NB : nb;
@@ -232,7 +242,7 @@ __host__ __device__ inline Plan make_plan(int dk, bool aug) {
 }
 
 struct Misc {
-    float part[4];            // per epilogue warp: largest row threshold (a units)
+    float part[8];            // per epilogue warp: largest row threshold (a units)
     uint32_t tmem_base;
     int meta_blk[NMETA];      // block id of tile t at slot t % NMETA (-1 = end)
 #ifdef SLK_WATCHDOG
@@ -308,11 +318,12 @@ __device__ __forceinline__ void norm_split(float xx, float &t0, float &t1) {
     t1 = __fsub_rn(v, hi);
 }
 
-template <int MODE, int KP, bool AUG>
-__global__ void __launch_bounds__(NTHREADS, 1) tc_scan_kernel(TcArgs a) {
+template <int MODE, int KP, bool AUG, int QB>
+__global__ void __launch_bounds__(Cfg<QB>::NTHREADS, 1) tc_scan_kernel(TcArgs a) {
     extern __shared__ __align__(1024) unsigned char smem[];
+    constexpr int NTHREADS = Cfg<QB>::NTHREADS, NT = Cfg<QB>::NT;
     const int dk = a.dk;
-    const Plan P = make_plan(dk, AUG);
+    const Plan P = make_plan(dk, AUG, QB);
     float *s_xx = reinterpret_cast<float *>(smem + P.xx);  // !AUG: |x~|^2 per meta slot
     const int nb = P.nb;
     unsigned char *sA = smem + P.a;
@@ -330,10 +341,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_scan_kernel(TcArgs a) {
     uint64_t *afull = tempty + NT;                                      // A tile landed
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int64_t qbl = blockIdx.x / a.nsplit;  // query block within the launch
+    const int64_t qbl = blockIdx.x / a.nsplit;  // query group (QB blocks) within the launch
     const int split = blockIdx.x - (int)qbl * a.nsplit;
-    const int64_t qb = a.qb0 + qbl;
-    const int64_t row_base = qb * BM;
+    const int64_t qb = a.qb0 + qbl * QB;        // first query block of the group
+    const int nqa = (int)min((int64_t)QB, a.nqb_total - qb);  // query blocks present
     const int64_t nxb = (a.nx + BN - 1) / BN;
     const uint32_t stage_bytes = (uint32_t)BM * dk * 4;
     const uint32_t half_bytes = (uint32_t)BM * dk * 2;
@@ -349,13 +360,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_scan_kernel(TcArgs a) {
         }
         for (int s = 0; s < NT; s++) {
             mbar_init(&tfull[s], 1);
-            mbar_init(&tempty[s], 128);
+            mbar_init(&tempty[s], 128 * QB);
         }
         mbar_init(afull, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        for (int i = 0; i < 4; i++) misc->part[i] = INFINITY;
+        for (int i = 0; i < 8; i++) misc->part[i] = INFINITY;
     }
-    if (warp == 8) {
+    if (warp == Cfg<QB>::WARP_MMA) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                          smem_u32(&misc->tmem_base)),
                      "r"(TMEM_COLS)
@@ -364,17 +375,18 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_scan_kernel(TcArgs a) {
     }
     // s_cq[t] = -c_t * s (exact: s is a power of two), so x~ = fma(x, s, s_cq[t])
     for (int t = tid; t < dk; t += NTHREADS)
-        s_cq[t] = t < a.d ? -a.qcentroid[(int64_t)t * a.nqb_total + qb] * a.scale : 0.0f;
+        s_cq[t] = t < a.d ? -a.gcentroid[(int64_t)t * a.ngroups + qbl] * a.scale : 0.0f;
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = misc->tmem_base;
 
-    if (warp == 9) {
+    if (warp == Cfg<QB>::WARP_PROD) {
         // ===================== producer: visit order + bulk copies
         if (lane == 0) {
-            mbar_expect_tx(afull, stage_bytes);
-            bulk_g2s(sA, a.qp + qb * (int64_t)dk * BM, stage_bytes, afull);
+            mbar_expect_tx(afull, stage_bytes * nqa);
+            for (int q = 0; q < nqa; q++)
+                bulk_g2s(sA + q * stage_bytes, a.qp + (qb + q) * (int64_t)dk * BM, stage_bytes, afull);
         }
         BlockVisitor vis(a.sb_order + qbl * a.nsb, a.sb_lb + qbl * a.nsb, a.flat_lb + qbl * a.nsb * 32,
                          a.nvalid[qbl], lane, split, a.nsplit);
@@ -383,7 +395,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_scan_kernel(TcArgs a) {
             const int s = it % nb;
             const uint32_t ph = (uint32_t)(it / nb) & 1u;
             volatile float *part = misc->part;
-            float thr = fmaxf(fmaxf(part[0], part[1]), fmaxf(part[2], part[3])) * a.inv_scale2;
+            float thr = fmaxf(fmaxf(part[0], part[1]), fmaxf(part[2], part[3]));
+            if (QB == 2) thr = fmaxf(thr, fmaxf(fmaxf(part[4], part[5]), fmaxf(part[6], part[7])));
+            thr *= a.inv_scale2;
             // the visitor's control flow must be warp-uniform: lane 0 (which ran
             // ahead into the barrier wait below) may have read newer thresholds
             thr = __shfl_sync(FULL, thr, 0);
@@ -414,8 +428,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_scan_kernel(TcArgs a) {
         const int r = tid;  // 0..127: query row (A) / index point (B)
         const float sc = a.scale;
         mbar_wait(afull, 0, 2, 0);
-        s_qq[r] = convert_tile(sA, r, dkm, dk, sc, s_cq);
-        if (AUG) put_norm_terms(sA, r, dkm, dk, NORM_A, NORM_A);
+#pragma unroll
+        for (int q = 0; q < QB; q++) {
+            // a missing second block (odd count) converts stale smem: its rows are never output
+            s_qq[q * BM + r] = convert_tile(sA + q * stage_bytes, r, dkm, dk, sc, s_cq);
+            if (AUG) put_norm_terms(sA + q * stage_bytes, r, dkm, dk, NORM_A, NORM_A);
+        }
         for (int it = 0;; it++) {
             const int s = it % nb;
             const uint32_t ph = (uint32_t)(it / nb) & 1u;
@@ -439,7 +457,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_scan_kernel(TcArgs a) {
             mbar_arrive(&bfull[s]);
             if (jb < 0) break;
         }
-    } else if (warp == 8) {
+    } else if (warp == Cfg<QB>::WARP_MMA) {
         // ===================== MMA issuer (one elected thread)
         if (lane == 0) {
             const uint32_t a_base = smem_u32(sA), b_base = smem_u32(sB);
@@ -461,22 +479,26 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_scan_kernel(TcArgs a) {
                     break;
                 }
                 tc_fence_after();
-                const uint32_t d_tmem = tmem + (uint32_t)ts * 128;
-                // <q~, x~> = hi.hi + hi.lo + lo.hi (the lo.lo term, <= 2^-22 |q~||x~|, is dropped)
                 const uint32_t bs = b_base + s * stage_bytes;
-                for (int k = 0; k < dkm / 16; k++) {
-                    const uint64_t ah = umma_desc(a_base + k * 256, 128, sbo);
-                    const uint64_t al = umma_desc(a_base + half_bytes + k * 256, 128, sbo);
-                    const uint64_t bh = umma_desc(bs + k * 256, 128, sbo);
-                    const uint64_t bl = umma_desc(bs + half_bytes + k * 256, 128, sbo);
-                    umma_f16(d_tmem, ah, bh, k > 0 ? 1u : 0u);
-                    umma_f16(d_tmem, ah, bl, 1u);
-                    umma_f16(d_tmem, al, bh, 1u);
+#pragma unroll
+                for (int q = 0; q < QB; q++) {
+                    const uint32_t d_tmem = tmem + (uint32_t)(ts * QB + q) * 128;
+                    const uint32_t aq = a_base + q * stage_bytes;
+                    // <q~, x~> = hi.hi + hi.lo + lo.hi (the lo.lo term, <= 2^-22 |q~||x~|, is dropped)
+                    for (int k = 0; k < dkm / 16; k++) {
+                        const uint64_t ah = umma_desc(aq + k * 256, 128, sbo);
+                        const uint64_t al = umma_desc(aq + half_bytes + k * 256, 128, sbo);
+                        const uint64_t bh = umma_desc(bs + k * 256, 128, sbo);
+                        const uint64_t bl = umma_desc(bs + half_bytes + k * 256, 128, sbo);
+                        umma_f16(d_tmem, ah, bh, k > 0 ? 1u : 0u);
+                        umma_f16(d_tmem, ah, bl, 1u);
+                        umma_f16(d_tmem, al, bh, 1u);
+                    }
+                    // augmented step: + 2^14 (-|x~|^2 2^-15) = -|x~|^2 / 2
+                    if (AUG)
+                        umma_f16(d_tmem, umma_desc(aq + (dkm / 16) * 256, 128, sbo),
+                                 umma_desc(bs + (dkm / 16) * 256, 128, sbo), 1u);
                 }
-                // augmented step: + 2^14 (-|x~|^2 2^-15) = -|x~|^2 / 2
-                if (AUG)
-                    umma_f16(d_tmem, umma_desc(a_base + (dkm / 16) * 256, 128, sbo),
-                             umma_desc(bs + (dkm / 16) * 256, 128, sbo), 1u);
                 umma_commit(&bempty[s]);  // operands consumed: the producer may refill stage s
                 umma_commit(&tfull[ts]);  // accumulator ready
             }
@@ -485,17 +507,18 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_scan_kernel(TcArgs a) {
 #endif
         }
         __syncwarp();
-    } else {
-        // ===================== epilogue warps (4-7): one query row per thread
-        const int ew = warp - 4;  // TMEM lane quarter
+    } else if (warp >= 4) {
+        // ===================== epilogue warps: one query row per thread
+        const int ew = (warp - 4) & 3;   // TMEM lane quarter
+        const int grp = (warp - 4) >> 2;  // query block of the group
         const int row = ew * 32 + lane;
-        const int64_t gi = row_base + row;
+        const int64_t gi = (qb + grp) * BM + row;
         // qid (gathered queries): id of the row in the index, -1 for padding
         const int64_t self_id = (gi < a.nq && a.qid) ? (int64_t)a.qid[gi] : gi;
         const bool row_ok = gi < a.nq && self_id >= 0;
         float qq = 0.0f;  // |q~|^2, written by the convert warps: read after the first tfull
         const int qc = (MODE == MODE_COLOR && row_ok) ? a.qcolor[gi] : -1;
-        float *stg = s_stg + row * STG_STRIDE;
+        float *stg = s_stg + (grp * BM + row) * STG_STRIDE;
         // This thread's row keeps its KP best (b, id) pairs in registers,
         // ascending, where b = |x~|^2 - 2<q~,x~> (a = |q~|^2 + b).  thr = the
         // KP-th b; padding rows use -inf so they never take a candidate.  Ties
@@ -516,7 +539,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_scan_kernel(TcArgs a) {
             mbar_wait(&tfull[ts], tph, 6, it);
             tc_fence_after();
             // the convert warps wrote A (and |q~|^2) before their first bfull arrive
-            if (it == 0) qq = s_qq[row];
+            if (it == 0) qq = s_qq[grp * BM + row];
             const int slot = it % NMETA;
             const int jb = misc->meta_blk[slot];
 #ifdef SLK_WATCHDOG
@@ -524,7 +547,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_scan_kernel(TcArgs a) {
 #endif
             if (jb < 0) break;
             const int64_t col0 = (int64_t)jb * BN;
-            const uint32_t taddr = tmem + ((uint32_t)(ew * 32) << 16) + (uint32_t)ts * 128;
+            const uint32_t taddr = tmem + ((uint32_t)(ew * 32) << 16) + (uint32_t)(ts * QB + grp) * 128;
             // columns this row may take from this block: inside the index, not itself
             const int64_t rem = a.nx - col0;
             const int col_limit = row_ok ? (rem < BN ? (int)rem : BN) : 0;
@@ -618,7 +641,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_scan_kernel(TcArgs a) {
             // largest row threshold in a units, rounded up (pruning stays conservative)
             float wm = row_ok ? __fadd_ru(thr, qq) : -INFINITY;
             for (int o = 16; o; o >>= 1) wm = fmaxf(wm, __shfl_xor_sync(FULL, wm, o));
-            if (lane == 0) ((volatile float *)misc->part)[ew] = wm;
+            if (lane == 0) ((volatile float *)misc->part)[grp * 4 + ew] = wm;
         }
         // write this row's candidate list (slots >= KP hold -1)
         if (gi >= a.row0 && gi < a.row1 && row_ok) {
@@ -647,38 +670,45 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_scan_kernel(TcArgs a) {
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
-    if (warp == 8) {
+    if (warp == Cfg<QB>::WARP_MMA) {
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS)
                      : "memory");
     }
 }
 
-template <int MODE, int KP, bool AUG>
-void launch_mode(const TcArgs &args, int64_t nqb, cudaStream_t s) {
-    const Plan P = make_plan(args.dk, AUG);
-    SLK_CUDA(cudaFuncSetAttribute(tc_scan_kernel<MODE, KP, AUG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)P.total));
-    tc_scan_kernel<MODE, KP, AUG><<<(unsigned)(nqb * args.nsplit), NTHREADS, P.total, s>>>(args);
+template <int MODE, int KP, bool AUG, int QB>
+void launch_mode(const TcArgs &args, int64_t ngroups, cudaStream_t s) {
+    const Plan P = make_plan(args.dk, AUG, QB);
+    SLK_CUDA(cudaFuncSetAttribute(tc_scan_kernel<MODE, KP, AUG, QB>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P.total));
+    tc_scan_kernel<MODE, KP, AUG, QB><<<(unsigned)(ngroups * args.nsplit), Cfg<QB>::NTHREADS, P.total, s>>>(args);
     SLK_CHECK_LAUNCH();
 }
 
-template <int KP, bool AUG>
-void launch_kp(int mode, const TcArgs &args, int64_t nqb, cudaStream_t s) {
+template <int KP, bool AUG, int QB>
+void launch_kp(int mode, const TcArgs &args, int64_t ngroups, cudaStream_t s) {
     switch (mode) {
-        case MODE_NONE: launch_mode<MODE_NONE, KP, AUG>(args, nqb, s); break;
-        case MODE_MASK: launch_mode<MODE_MASK, KP, AUG>(args, nqb, s); break;
-        case MODE_COLOR: launch_mode<MODE_COLOR, KP, AUG>(args, nqb, s); break;
-        default: launch_mode<MODE_SELF, KP, AUG>(args, nqb, s); break;
+        case MODE_NONE: launch_mode<MODE_NONE, KP, AUG, QB>(args, ngroups, s); break;
+        case MODE_MASK: launch_mode<MODE_MASK, KP, AUG, QB>(args, ngroups, s); break;
+        case MODE_COLOR: launch_mode<MODE_COLOR, KP, AUG, QB>(args, ngroups, s); break;
+        default: launch_mode<MODE_SELF, KP, AUG, QB>(args, ngroups, s); break;
     }
 }
 
 template <bool AUG>
-void launch_aug(int mode, int kp, const TcArgs &args, int64_t nqb, cudaStream_t s) {
-    if (kp <= 2) launch_kp<2, AUG>(mode, args, nqb, s);
-    else if (kp <= 4) launch_kp<4, AUG>(mode, args, nqb, s);
-    else if (kp <= 8) launch_kp<8, AUG>(mode, args, nqb, s);
-    else if (kp <= 16) launch_kp<16, AUG>(mode, args, nqb, s);
-    else launch_kp<32, AUG>(mode, args, nqb, s);
+void launch_aug(int mode, int kp, int qb, const TcArgs &args, int64_t ngroups, cudaStream_t s) {
+    if (qb == 2) {
+        if (kp <= 2) launch_kp<2, AUG, 2>(mode, args, ngroups, s);
+        else if (kp <= 4) launch_kp<4, AUG, 2>(mode, args, ngroups, s);
+        else if (kp <= 8) launch_kp<8, AUG, 2>(mode, args, ngroups, s);
+        else launch_kp<16, AUG, 2>(mode, args, ngroups, s);
+        return;
+    }
+    if (kp <= 2) launch_kp<2, AUG, 1>(mode, args, ngroups, s);
+    else if (kp <= 4) launch_kp<4, AUG, 1>(mode, args, ngroups, s);
+    else if (kp <= 8) launch_kp<8, AUG, 1>(mode, args, ngroups, s);
+    else if (kp <= 16) launch_kp<16, AUG, 1>(mode, args, ngroups, s);
+    else launch_kp<32, AUG, 1>(mode, args, ngroups, s);
 }
 
 }  // namespace
@@ -686,19 +716,32 @@ void launch_aug(int mode, int kp, const TcArgs &args, int64_t nqb, cudaStream_t 
 // The augmented norm step when at least 3 B stages still fit (measured: the
 // max-only epilogue pays for the extra MMA and the 16 extra K columns);
 // otherwise |x~|^2 goes through shared memory (large d).
-bool use_aug(int d) { return make_plan(((d + 15) / 16) * 16 + 16, true).nb >= 3; }
+bool use_aug(int d) { return make_plan(((d + 15) / 16) * 16 + 16, true, 1).nb >= 3; }
 
 int k_extent(int d) { return ((d + 15) / 16) * 16 + (use_aug(d) ? 16 : 0); }
 
-size_t smem_bytes(int d) { return make_plan(k_extent(d), use_aug(d)).total; }
+size_t smem_bytes(int d) { return make_plan(k_extent(d), use_aug(d), 1).total; }
 
 // at least two B stages must fit next to the A tile
-bool supported(int d) { return make_plan(k_extent(d), use_aug(d)).nb >= 2; }
+bool supported(int d) { return make_plan(k_extent(d), use_aug(d), 1).nb >= 2; }
 
-// K' = kp candidates per row (2, 4, 8, 16 or 32; kp > k for the certificate)
-void launch(int mode, int kp, const TcArgs &args, int64_t nqb, cudaStream_t s) {
-    if (use_aug(args.d)) launch_aug<true>(mode, kp, args, nqb, s);
-    else launch_aug<false>(mode, kp, args, nqb, s);
+// query blocks per CTA for K' = kp candidates: pairs need K' <= 16 (the 8
+// epilogue warps cap registers) and 2 B stages next to two A tiles
+// Measured: pairs cut the cross-colour passes by 13 % at C3 (blocks of one
+// cluster pair well) but the union of two blocks' visit lists costs 1.4-2.5x
+// the tiles when clusters span only a few blocks (C5), so they are opt-in
+// (SLK_TC_QB=2) until groups are formed adaptively.
+int group_blocks(int d, int kp) {
+    const char *e = getenv("SLK_TC_QB");
+    if (!e || atoi(e) != 2 || kp > 16) return 1;
+    return make_plan(k_extent(d), use_aug(d), 2).nb >= 2 ? 2 : 1;
+}
+
+// K' = kp candidates per row (2, 4, 8, 16 or 32; kp > k for the certificate);
+// qb query blocks per CTA (group_blocks), ngroups groups in the launch
+void launch(int mode, int kp, int qb, const TcArgs &args, int64_t ngroups, cudaStream_t s) {
+    if (use_aug(args.d)) launch_aug<true>(mode, kp, qb, args, ngroups, s);
+    else launch_aug<false>(mode, kp, qb, args, ngroups, s);
 }
 
 }  // namespace tc

@@ -13,8 +13,9 @@ struct TcArgs {
     int64_t nq, nx;
     int d, dp, dk;           // dims, packed dims (multiple of 16), MMA K extent (k_extent)
     int64_t qb0;             // first query block of this launch
-    const float *qcentroid;  // query block centroids, dims-major [dp][nqb_total]
-    int64_t nqb_total;
+    const float *gcentroid;  // centring point of each query group of the launch, dims-major [dp][ngroups]
+    int64_t ngroups;
+    int64_t nqb_total;       // query blocks of the query set
     float scale;             // power of two applied after centring
     float inv_scale2;        // 1 / scale^2 (exact)
     const uint8_t *mask;
@@ -40,8 +41,11 @@ bool use_aug(int d);
 int k_extent(int d);
 size_t smem_bytes(int d);
 bool supported(int d);
-// kp: candidates kept per row (8, 16 or 32); the certificate needs kp > k
-void launch(int mode, int kp, const TcArgs &args, int64_t nqb, cudaStream_t s);
+// Query blocks per CTA (1 or 2) for d dims and K' = kp.
+int group_blocks(int d, int kp);
+// kp: candidates kept per row (2..32; the certificate needs kp > k); qb query
+// blocks per CTA sharing one centring point (group_blocks)
+void launch(int mode, int kp, int qb, const TcArgs &args, int64_t ngroups, cudaStream_t s);
 
 }  // namespace tc
 }  // namespace slk
