@@ -671,6 +671,18 @@ __device__ __forceinline__ double exact_dist(const float *q32, const double *q64
         const double *qr = q64 + i * d;
         const double *xr = x64 + j * d;
         for (int t = 0; t < d; t++) dot = __dadd_rn(dot, __dmul_rn(qr[t], xr[t]));
+    } else if ((d & 3) == 0) {
+        // 16-byte loads (rows are 16-byte aligned when d % 4 == 0); same
+        // sequential order of the float64 products and sums
+        const float4 *qr = reinterpret_cast<const float4 *>(q32 + i * d);
+        const float4 *xr = reinterpret_cast<const float4 *>(x32 + j * d);
+        for (int t = 0; t < d / 4; t++) {
+            const float4 a = __ldg(qr + t), b = __ldg(xr + t);
+            dot = __dadd_rn(dot, __dmul_rn((double)a.x, (double)b.x));
+            dot = __dadd_rn(dot, __dmul_rn((double)a.y, (double)b.y));
+            dot = __dadd_rn(dot, __dmul_rn((double)a.z, (double)b.z));
+            dot = __dadd_rn(dot, __dmul_rn((double)a.w, (double)b.w));
+        }
     } else {
         const float *qr = q32 + i * d;
         const float *xr = x32 + j * d;
