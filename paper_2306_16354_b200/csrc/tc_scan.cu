@@ -283,8 +283,10 @@ __device__ __forceinline__ float convert_tile(unsigned char *tile, int r, int dk
                                               const float *s_cq) {
     const uint32_t half_bytes = (uint32_t)BM * dk * 2;
     unsigned char *row = tile + (r >> 3) * (dk * 16) + (r & 7) * 16;
-    float nrm = 0.0f;
-#pragma unroll 2
+    // four independent partial norms: the accumulation chain would otherwise
+    // serialise the conversion (the error bound does not depend on order)
+    float nrm4[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll 4
     for (int g = 0; g < dkm / 8; g++) {
         float4 *ph = reinterpret_cast<float4 *>(row + g * 128);
         float4 *pl = reinterpret_cast<float4 *>(row + half_bytes + g * 128);
@@ -296,11 +298,11 @@ __device__ __forceinline__ float convert_tile(unsigned char *tile, int r, int dk
                             __fmaf_rn(w.z, sc, c1.z), __fmaf_rn(w.w, sc, c1.w)};
         __half2 h[4], l[4];
 #pragma unroll
-        for (int q = 0; q < 4; q++) split2(v[2 * q], v[2 * q + 1], h[q], l[q], nrm);
+        for (int q = 0; q < 4; q++) split2(v[2 * q], v[2 * q + 1], h[q], l[q], nrm4[q]);
         *reinterpret_cast<uint4 *>(ph) = *reinterpret_cast<uint4 *>(h);
         *reinterpret_cast<uint4 *>(pl) = *reinterpret_cast<uint4 *>(l);
     }
-    return nrm;
+    return __fadd_rn(__fadd_rn(nrm4[0], nrm4[1]), __fadd_rn(nrm4[2], nrm4[3]));
 }
 
 // Writes the hi entries (dkm, dkm+1) of point r's augmented K step; the rest
