@@ -84,16 +84,35 @@ class DeviceEngine:
         self.torch.cuda.synchronize()
 
 
+def _host_staged(dist, group, t) -> bool:
+    """gloo moves host tensors only: device tensors are staged through the host
+    (lets the orchestration run with several ranks on one GPU, e.g. in tests)."""
+    return t.is_cuda and dist.get_backend(group) == "gloo"
+
+
 def _gather_rows(torch, dist, group, t, rows_per_rank, world):
     """All-gather variable-length row shards (padded to the largest) → concatenated."""
     cap = max(rows_per_rank)
+    dev = t.device
+    if _host_staged(dist, group, t):
+        t = t.cpu()
     shape = (cap,) + tuple(t.shape[1:])
     pad = torch.zeros(shape, dtype=t.dtype, device=t.device)
     pad[: t.shape[0]] = t
     out = torch.empty((world * cap,) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
     dist.all_gather_into_tensor(out, pad, group=group)
     parts = [out[r * cap: r * cap + rows_per_rank[r]] for r in range(world)]
-    return torch.cat(parts)
+    return torch.cat(parts).to(dev)
+
+
+def _broadcast(dist, group, t):
+    """In-place broadcast from rank 0 (host-staged under gloo)."""
+    if _host_staged(dist, group, t):
+        h = t.cpu()
+        dist.broadcast(h, 0, group=group)
+        t.copy_(h)
+    else:
+        dist.broadcast(t, 0, group=group)
 
 
 def single_linkage_distributed(x, cfg: LinkageConfig, *, engine=None, group=None):
@@ -137,7 +156,7 @@ def single_linkage_distributed(x, cfg: LinkageConfig, *, engine=None, group=None
         ncomp_t.fill_(state[5])
         colors.copy_(state[3][:n])
     del idx_all, dst_all
-    dist.broadcast(ncomp_t, 0, group=group)
+    _broadcast(dist, group, ncomp_t)
     marks.append(time.perf_counter())
 
     # --- connect loop: colours broadcast, sharded cross-colour 1-NN, gather bridges
@@ -150,7 +169,7 @@ def single_linkage_distributed(x, cfg: LinkageConfig, *, engine=None, group=None
             raise ConvergenceError(
                 f"reconnection did not converge within {budget} iterations: "
                 f"{int(ncomp_t.item())} components remain")
-        dist.broadcast(colors, 0, group=group)
+        _broadcast(dist, group, colors)
         bidx, bw = engine.nn1_shard(pts, colors, ranges[rank])
         bidx_all = _gather_rows(torch, dist, group, bidx, rows_per_rank, world)
         bw_all = _gather_rows(torch, dist, group, bw, rows_per_rank, world)
@@ -162,7 +181,7 @@ def single_linkage_distributed(x, cfg: LinkageConfig, *, engine=None, group=None
             state = engine.msf(n, u_src, u_dst, u_w, ne + n, cfg.seed)
             ncomp_t.fill_(state[5])
             colors.copy_(state[3][:n])
-        dist.broadcast(ncomp_t, 0, group=group)
+        _broadcast(dist, group, ncomp_t)
         iters += 1
     engine.sync()
     marks.append(time.perf_counter())

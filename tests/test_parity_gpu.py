@@ -5,6 +5,8 @@ north-star tolerance is named: MST total weight / dendrogram heights within
 1e-5 relative, labels ARI == 1.0.  All tests need a B200.
 """
 
+from pathlib import Path
+
 import numpy as np
 import pytest
 
@@ -232,3 +234,18 @@ def test_single_linkage_blobs_match_oracle(slk, oracle):
     assert np.array_equal(res.dendrogram.merges, ref["merges"])
     assert np.array_equal(res.labels.labels, ref["labels"])
     assert res.connect_iters == ref["connect_iters"]
+
+
+def test_distributed_two_ranks_one_gpu(slk):
+    """The multi-GPU path (parallel.py) end to end on the device engine: two
+    torchrun ranks share cuda:0 over gloo (host-staged collectives) and rank 0
+    must reproduce the single-process result bit for bit."""
+    import subprocess
+    import sys
+
+    worker = Path(__file__).resolve().parent / "dist_gpu_worker.py"
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port", "29561", str(worker)]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-4000:]
+    assert "DIST_OK" in out.stdout, out.stdout[-2000:]
