@@ -199,18 +199,20 @@ constexpr int NMETA = MAX_NB + NTMAX;  // per-tile metadata ring (see producer)
 constexpr uint32_t TMEM_COLS = 512;
 constexpr int CH = 32;  // accumulator columns per epilogue step (tcgen05.ld .x32)
 constexpr uint32_t CH_ALL = 0xffffffffu;
-// Augmented K: the last 16-column step of every operand tile carries the
-// norm term.  A: hi[dkm] = hi[dkm+1] = 2^14; B: hi[dkm] + hi[dkm+1] = two-term
-// fp16 split of -|x~|^2 2^-15.  One extra hi.hi MMA adds -|x~|^2 / 2 to the
+// Augmented K: one extra 16-column K step carries the norm term, in small
+// separate tiles (128 rows x 16 fp16, hi only) so the bulk copies move only
+// the real dims.  A: columns 0, 1 = 2^14; B: columns 0, 1 = two-term fp16
+// split of -|x~|^2 2^-15.  One extra hi.hi MMA adds -|x~|^2 / 2 to the
 // accumulator, so the epilogue reads acc = <q~,x~> - |x~|^2 / 2 = -b / 2
 // directly (knn.cu:tensor_scale keeps |x~|^2 2^-15 below the fp16 range).
+constexpr uint32_t AUG_TILE = BM * 16 * 2;  // bytes; canonical layout, SBO = 256
 constexpr float NORM_A = 16384.0f;       // 2^14
 constexpr float NORM_B_SCALE = -0x1p-15f;
 constexpr int STG_STRIDE = CH + 4;  // per-row chunk staging (CH + 4 floats: conflict-free STS.128)
 constexpr uint32_t SMEM_LIMIT = 227 * 1024;
 
 struct Plan {
-    uint32_t a, b, xx, xcol, qq, cq, stg, misc, bars, total;
+    uint32_t a, b, aaug, baug, xx, xcol, qq, cq, stg, misc, bars, total;
     int nb;  // B stages that fit
 };
 
@@ -226,6 +228,7 @@ __host__ __device__ inline Plan make_plan(int dk, bool aug, int qb) {
     };
     const uint32_t stage = (uint32_t)BM * dk * 4;  // hi + lo fp16 tiles = raw fp32 block
     p.a = take(stage * qb, 1024);
+    p.aaug = aug ? take(AUG_TILE, 1024) : 0u;
     p.xx = aug ? 0u : take(NMETA * BN * 4, 16);
     p.xcol = take(NMETA * BN * 4, 16);
     p.qq = take(qb * BM * 4, 16);
@@ -234,9 +237,11 @@ __host__ __device__ inline Plan make_plan(int dk, bool aug, int qb) {
     p.misc = take(128, 16);
     p.bars = take(8 * (4 * MAX_NB + 2 * NTMAX + 1), 8);
     off = (off + 1023) / 1024 * 1024;
-    int nb = off >= SMEM_LIMIT ? 0 : (int)((SMEM_LIMIT - off) / stage);
+    const uint32_t per = stage + (aug ? AUG_TILE : 0u);
+    int nb = off >= SMEM_LIMIT ? 0 : (int)((SMEM_LIMIT - off) / per);
     p.nb = nb > MAX_NB ? MAX_NB : nb;
     p.b = take(stage * (p.nb > 0 ? p.nb : 0), 1024);
+    p.baug = aug ? take(AUG_TILE * (p.nb > 0 ? p.nb : 0), 1024) : 0u;
     p.total = off;
     return p;
 }
@@ -276,9 +281,9 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
         : "memory");
 }
 
-// Converts the dkm main dims (core-matrix columns [0, dkm/8)) of point r of a
+// Converts the dkm dims (core-matrix columns [0, dkm/8)) of point r of a
 // 128-point operand tile in place (raw tc-packed fp32 -> fp16 hi/lo canonical
-// layout, K extent dk = dkm + 16) and returns |v|^2 of the unsplit values.
+// layout, K extent dk = dkm) and returns |v|^2 of the unsplit values.
 __device__ __forceinline__ float convert_tile(unsigned char *tile, int r, int dkm, int dk, float sc,
                                               const float *s_cq) {
     const uint32_t half_bytes = (uint32_t)BM * dk * 2;
@@ -305,11 +310,10 @@ __device__ __forceinline__ float convert_tile(unsigned char *tile, int r, int dk
     return __fadd_rn(__fadd_rn(nrm4[0], nrm4[1]), __fadd_rn(nrm4[2], nrm4[3]));
 }
 
-// Writes the hi entries (dkm, dkm+1) of point r's augmented K step; the rest
-// of the step is zero already (padding of the tc-packed layout).
-__device__ __forceinline__ void put_norm_terms(unsigned char *tile, int r, int dkm, int dk, float t0, float t1) {
-    unsigned char *p = tile + (r >> 3) * (dk * 16) + (r & 7) * 16 + (dkm / 8) * 128;
-    *reinterpret_cast<__half2 *>(p) = __floats2half2_rn(t0, t1);
+// Writes columns 0, 1 of point r's row of an augmented-step tile (the other
+// 14 columns are zeroed once per CTA).
+__device__ __forceinline__ void put_norm_terms(unsigned char *aug, int r, float t0, float t1) {
+    *reinterpret_cast<__half2 *>(aug + (r >> 3) * 256 + (r & 7) * 16) = __floats2half2_rn(t0, t1);
 }
 
 // -|x~|^2 2^-15 as hi + lo fp16 (|hi + lo - v| <= 2^-22 |v| + 2^-25)
@@ -351,7 +355,9 @@ __global__ void __launch_bounds__(Cfg<QB>::NTHREADS, 1) tc_scan_kernel(TcArgs a)
     const uint32_t stage_bytes = (uint32_t)BM * dk * 4;
     const uint32_t half_bytes = (uint32_t)BM * dk * 2;
     const uint32_t sbo = (uint32_t)dk * 16;  // (dk/8) core matrices of 128 B per 8-row group
-    const int dkm = AUG ? dk - 16 : dk;     // main dims (d rounded up to 16); then the norm step
+    const int dkm = dk;                      // dims (d rounded up to 16); the norm step is separate
+    unsigned char *sAaug = smem + P.aaug;    // AUG: norm-step tiles of A and of each B stage
+    unsigned char *sBaug = smem + P.baug;
 
     // ---- setup: barriers, TMEM, centring constants
     if (tid == 0) {
@@ -378,6 +384,14 @@ __global__ void __launch_bounds__(Cfg<QB>::NTHREADS, 1) tc_scan_kernel(TcArgs a)
     // s_cq[t] = -c_t * s (exact: s is a power of two), so x~ = fma(x, s, s_cq[t])
     for (int t = tid; t < dk; t += NTHREADS)
         s_cq[t] = t < a.d ? -a.gcentroid[(int64_t)t * a.ngroups + qbl] * a.scale : 0.0f;
+    if (AUG) {
+        // norm-step tiles: columns 2..15 stay zero (columns 0, 1 written per tile)
+        for (uint32_t e = tid; e < AUG_TILE / 16; e += NTHREADS)
+            reinterpret_cast<uint4 *>(sAaug)[e] = make_uint4(0u, 0u, 0u, 0u);
+        for (uint32_t e = tid; e < AUG_TILE * nb / 16; e += NTHREADS)
+            reinterpret_cast<uint4 *>(sBaug)[e] = make_uint4(0u, 0u, 0u, 0u);
+        fence_async_smem();
+    }
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -434,7 +448,7 @@ __global__ void __launch_bounds__(Cfg<QB>::NTHREADS, 1) tc_scan_kernel(TcArgs a)
         for (int q = 0; q < QB; q++) {
             // a missing second block (odd count) converts stale smem: its rows are never output
             s_qq[q * BM + r] = convert_tile(sA + q * stage_bytes, r, dkm, dk, sc, s_cq);
-            if (AUG) put_norm_terms(sA + q * stage_bytes, r, dkm, dk, NORM_A, NORM_A);
+            if (AUG && q == 0) put_norm_terms(sAaug, r, NORM_A, NORM_A);  // shared by the group
         }
         for (int it = 0;; it++) {
             const int s = it % nb;
@@ -450,7 +464,7 @@ __global__ void __launch_bounds__(Cfg<QB>::NTHREADS, 1) tc_scan_kernel(TcArgs a)
                 if (AUG) {
                     float t0, t1;
                     norm_split(xx, t0, t1);
-                    put_norm_terms(tile, r, dkm, dk, t0, t1);
+                    put_norm_terms(sBaug + (size_t)s * AUG_TILE, r, t0, t1);
                 } else {
                     s_xx[(it % NMETA) * BN + r] = xx;
                 }
@@ -498,8 +512,8 @@ __global__ void __launch_bounds__(Cfg<QB>::NTHREADS, 1) tc_scan_kernel(TcArgs a)
                     }
                     // augmented step: + 2^14 (-|x~|^2 2^-15) = -|x~|^2 / 2
                     if (AUG)
-                        umma_f16(d_tmem, umma_desc(aq + (dkm / 16) * 256, 128, sbo),
-                                 umma_desc(bs + (dkm / 16) * 256, 128, sbo), 1u);
+                        umma_f16(d_tmem, umma_desc(smem_u32(sAaug), 128, 256),
+                                 umma_desc(smem_u32(sBaug) + s * AUG_TILE, 128, 256), 1u);
                 }
                 umma_commit(&bempty[s]);  // operands consumed: the producer may refill stage s
                 umma_commit(&tfull[ts]);  // accumulator ready
@@ -718,9 +732,9 @@ void launch_aug(int mode, int kp, int qb, const TcArgs &args, int64_t ngroups, c
 // The augmented norm step when at least 3 B stages still fit (measured: the
 // max-only epilogue pays for the extra MMA and the 16 extra K columns);
 // otherwise |x~|^2 goes through shared memory (large d).
-bool use_aug(int d) { return make_plan(((d + 15) / 16) * 16 + 16, true, 1).nb >= 3; }
+bool use_aug(int d) { return make_plan(((d + 15) / 16) * 16, true, 1).nb >= 3; }
 
-int k_extent(int d) { return ((d + 15) / 16) * 16 + (use_aug(d) ? 16 : 0); }
+int k_extent(int d) { return ((d + 15) / 16) * 16; }
 
 size_t smem_bytes(int d) { return make_plan(k_extent(d), use_aug(d), 1).total; }
 
