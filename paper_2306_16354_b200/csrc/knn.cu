@@ -1154,16 +1154,23 @@ int64_t search_ffma(const PointSet &Q, const PointSet &X, const int32_t *qid, in
     return missing == 0x7fffffff ? -1 : missing;
 }
 
-// Candidates the tensor scan keeps per row: the smallest of 8 / 16 / 32 that
-// is at least 2k (the certificate compares the K'-th approximate value with
-// the k-th exact one, so K' = k + 1 leaves no slack for near-ties; measured
-// at C3: K' = 16 for k = 15 leaves 12 % of the rows uncertified, K' = 32
-// 0.5 %).  SLK_TC_KP overrides (it must exceed k).
-int tc_kp(int k) {
-    int kp = 2 * k <= 8 ? 8 : (2 * k <= 16 ? 16 : 32);
-    if (const char *e = getenv(k == 1 ? "SLK_TC_KP1" : "SLK_TC_KP")) {
-        int v = atoi(e);
-        if (v > k && v <= 32) kp = v <= 2 ? 2 : (v <= 4 ? 4 : (v <= 8 ? 8 : (v <= 16 ? 16 : 32)));
+// Candidates the tensor scan keeps per row.  The certificate compares the
+// K'-th approximate value with the k-th exact one, so K' = k + 1 leaves no
+// slack for near-ties, while every extra slot makes each insertion dearer.
+// First pass: the smallest of 8 / 16 / 32 above k (measured at C3, k = 15:
+// K' = 16 leaves 7 % of the rows uncertified but halves the insertion cost);
+// the re-blocked rerun of those rows: the smallest at least 2k (K' = 32).
+// SLK_TC_KP / SLK_TC_KP1 (k = 1) override the first pass (must exceed k).
+int tc_kp(int k, bool rerun) {
+    auto round_up = [](int v) { return v <= 2 ? 2 : (v <= 4 ? 4 : (v <= 8 ? 8 : (v <= 16 ? 16 : 32))); };
+    // at least 8 (smaller lists save little and certify less: C5, k = 2)
+    const int first = std::max(8, round_up(k + 1));
+    int kp = rerun ? std::max(first, round_up(2 * k)) : first;
+    if (!rerun) {
+        if (const char *e = getenv(k == 1 ? "SLK_TC_KP1" : "SLK_TC_KP")) {
+            int v = atoi(e);
+            if (v > k && v <= 32) kp = round_up(v);
+        }
     }
     return kp;
 }
@@ -1199,7 +1206,7 @@ const float *ensure_tcpack(const PointSet &P, cudaStream_t s) {
 // Writes certified and uncertified rows alike into out_*; returns the
 // uncertified rows (relative to q0) in `fail` and their count, and the
 // approximate K'-th values (scaled units) in `kth`.
-int tc_pass(const PointSet &Q, const PointSet &X, const int32_t *qid, int k, int mode,
+int tc_pass(const PointSet &Q, const PointSet &X, const int32_t *qid, int k, int kp, int mode,
             const uint8_t *mask, const int32_t *qcolor, const int32_t *xcolor, int64_t q0,
             int64_t q1, float scale, float inv_scale2, int32_t *out_idx, double *out_dist,
             DevBuf<int> &fail, DevBuf<float> &kth, cudaStream_t s) {
@@ -1208,7 +1215,6 @@ int tc_pass(const PointSet &Q, const PointSet &X, const int32_t *qid, int k, int
     const int d = X.d;
     const int64_t nq = Q.n, nx = X.n;
     const int64_t qb0 = q0 / BM, qb1 = (q1 + BM - 1) / BM;
-    const int kp = tc_kp(k);
     // query blocks per CTA: pairs share every converted index tile, when the
     // launch still fills the GPU with them
     int qbn = tc::group_blocks(d, kp);
@@ -1386,7 +1392,7 @@ void search(const PointSet &Q, const PointSet &X, int k, int mode, const uint8_t
     } else {
         DevBuf<int> fail;
         DevBuf<float> kth;
-        const int nfail = tc_pass(Q, X, nullptr, k, mode, mask, qcolor, xcolor, q0, q1, scale,
+        const int nfail = tc_pass(Q, X, nullptr, k, tc_kp(k, false), mode, mask, qcolor, xcolor, q0, q1, scale,
                                   inv_scale2, out_idx, out_dist, fail, kth, s);
         (void)Rsel;
         if (nfail > 0) {
@@ -1430,7 +1436,7 @@ void search(const PointSet &Q, const PointSet &X, int k, int mode, const uint8_t
             DevBuf<double> gdist(G.n * k, s);
             DevBuf<int> fail2;
             DevBuf<float> kth2;
-            const int nfail2 = tc_pass(*G.P, X, G.qid, k, mode, G.mask.get(), G.qcolor.get(),
+            const int nfail2 = tc_pass(*G.P, X, G.qid, k, tc_kp(k, true), mode, G.mask.get(), G.qcolor.get(),
                                        xcolor, 0, G.n, scale, inv_scale2, gidx, gdist, fail2, kth2, s);
             // global query ids in the gathered set are Q row ids: scatter to q0-relative rows
             scatter_gathered_kernel<<<grid_for(G.n * k, 256), 256, 0, s>>>(gidx, gdist, G.qid, G.n,
@@ -1603,7 +1609,7 @@ void debug_tc_scan(const float *x32, int64_t n, int d, int k, int32_t *cand, flo
     tc::TcArgs ta{tcp, tcp, n, n, d, P->dp, tc::k_extent(d), 0, G.cent, G.ng,
                   P->nb, scale, inv2, nullptr, nullptr, nullptr, cand, kth, qhat, 0, n,
                   V.sb_order, V.sb_lb, V.flat_lb, V.nvalid, P->nsb, tiles, nullptr, 1};
-    tc::launch(scan::MODE_SELF, tc_kp(k), 1, ta, nqb, s);
+    tc::launch(scan::MODE_SELF, tc_kp(k, false), 1, ta, nqb, s);
     SLK_CUDA(cudaStreamSynchronize(s));
     *scale_out = scale;
 }
