@@ -957,6 +957,33 @@ QueryGroups make_groups(const PointSet &Q, int64_t qb0, int64_t nqb, int qbn, co
     return G;
 }
 
+__global__ void tight_pairs_kernel(const float *__restrict__ br, int64_t qb0, int64_t nb,
+                                   const float *__restrict__ gr, int64_t ng, unsigned long long *count) {
+    unsigned long long c = 0;
+    for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < ng;
+         g += (int64_t)gridDim.x * blockDim.x) {
+        float m = br[qb0 + 2 * g];
+        if (2 * g + 1 < nb) m = fmaxf(m, br[qb0 + 2 * g + 1]);
+        c += gr[g] <= 1.15f * m ? 1ull : 0ull;
+    }
+    for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(FULL, c, o);
+    if ((threadIdx.x & 31) == 0) atomicAdd(count, c);
+}
+
+// Pairs of consecutive query blocks share one CTA when at least 90 % of the
+// pair spheres are within 15 % of their larger member's radius (blocks of one
+// cluster); looser pairs would visit the union of two neighbourhoods.  (The
+// mean is no guide: the few pairs that straddle two clusters are huge.)
+bool pairs_are_tight(const PointSet &Q, int64_t qb0, int64_t nqb, const QueryGroups &G2, cudaStream_t s) {
+    DevBuf<unsigned long long> cnt(1, s);
+    SLK_CUDA(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long), s));
+    tight_pairs_kernel<<<grid_for(G2.ng, 256, 256), 256, 0, s>>>(Q.radius, qb0, nqb, G2.rad, G2.ng, cnt);
+    SLK_CHECK_LAUNCH();
+    const double frac = (double)read_scalar(cnt.get(), s) / (double)G2.ng;
+    if (trace_on()) fprintf(stderr, "[slk] tight query-block pairs %.3f\n", frac);
+    return frac >= 0.9;
+}
+
 // Visit order of every query group against X (colour mode iff xcolor).
 VisitOrder visit_order(const QueryGroups &G, const PointSet &X, int d, const int32_t *xcolor, cudaStream_t s) {
     const int64_t nqb = G.ng, qb0 = 0;
@@ -1218,8 +1245,18 @@ int tc_pass(const PointSet &Q, const PointSet &X, const int32_t *qid, int k, int
     // query blocks per CTA: pairs share every converted index tile, when the
     // launch still fills the GPU with them
     int qbn = tc::group_blocks(d, kp);
+    // pairs pay in the 1-NN passes (conversion-bound); the k-NN pass is
+    // insertion-bound and only sees the extra tiles (C3: +18 %)
+    if (mode == MODE_SELF && !getenv("SLK_TC_QB")) qbn = 1;
     if (qbn == 2 && (qb1 - qb0) < 4 * num_sms()) qbn = 1;
-    const int64_t ngroups = (qb1 - qb0 + qbn - 1) / qbn;
+    QueryGroups G;
+    if (qbn == 2) {
+        G = make_groups(Q, qb0, qb1 - qb0, 2, mode == MODE_COLOR ? qcolor : nullptr, s);
+        const char *e = getenv("SLK_TC_QB");
+        if (!(e && atoi(e) == 2) && !pairs_are_tight(Q, qb0, qb1 - qb0, G, s)) qbn = 1;
+    }
+    if (qbn == 1) G = make_groups(Q, qb0, qb1 - qb0, 1, mode == MODE_COLOR ? qcolor : nullptr, s);
+    const int64_t ngroups = G.ng;
     // small launches: deal each query group's visit order over nsplit CTAs
     // (each keeps its own K' list; the refine takes the union) so that at
     // least ~2 CTAs per SM run
@@ -1237,7 +1274,6 @@ int tc_pass(const PointSet &Q, const PointSet &X, const int32_t *qid, int k, int
     SLK_CUDA(cudaMemsetAsync(counters, 0, sizeof(int), s));
     EventPair ev_order, ev_scan, ev_refine;
     ev_order.start(s);
-    QueryGroups G = make_groups(Q, qb0, qb1 - qb0, qbn, mode == MODE_COLOR ? qcolor : nullptr, s);
     VisitOrder V = visit_order(G, X, d, mode == MODE_COLOR ? xcolor : nullptr, s);
     ev_order.stop(s);
     trace_mark("visit_order enqueued");

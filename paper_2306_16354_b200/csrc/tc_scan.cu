@@ -745,11 +745,12 @@ bool supported(int d) { return make_plan(k_extent(d), use_aug(d), 1).nb >= 2; }
 // epilogue warps cap registers) and 2 B stages next to two A tiles
 // Measured: pairs cut the cross-colour passes by 13 % at C3 (blocks of one
 // cluster pair well) but the union of two blocks' visit lists costs 1.4-2.5x
-// the tiles when clusters span only a few blocks (C5), so they are opt-in
-// (SLK_TC_QB=2) until groups are formed adaptively.
+// the tiles when clusters span only a few blocks (C5): knn.cu:tc_pass uses
+// them only when the pair spheres are nearly as tight as the blocks'
+// (SLK_TC_QB=1 / 2 force singles / pairs).
 int group_blocks(int d, int kp) {
     const char *e = getenv("SLK_TC_QB");
-    if (!e || atoi(e) != 2 || kp > 16) return 1;
+    if ((e && atoi(e) == 1) || kp > 16) return 1;
     return make_plan(k_extent(d), use_aug(d), 2).nb >= 2 ? 2 : 1;
 }
 
