@@ -104,13 +104,16 @@ __global__ void norms_kernel(const float *__restrict__ x32, const double *__rest
     }
 }
 
+// max |x| as the bit pattern of a non-negative float: integer order is float
+// order for finite values, and inf (0x7f800000) / NaN (above) win, so the
+// result also says whether the matrix is finite (ref core.py:40-63)
 __global__ void maxabs_kernel(const float *__restrict__ x, int64_t m, unsigned int *out) {
-    float v = 0.0f;
+    unsigned int v = 0u;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
          i += (int64_t)gridDim.x * blockDim.x)
-        v = fmaxf(v, fabsf(x[i]));
-    for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(FULL, v, o));
-    if ((threadIdx.x & 31) == 0) atomicMax(out, __float_as_uint(v));  // v >= 0: bit order
+        v = max(v, __float_as_uint(x[i]) & 0x7fffffffu);
+    for (int o = 16; o; o >>= 1) v = max(v, __shfl_xor_sync(FULL, v, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(out, v);
 }
 
 inline float __uint_as_float_host(unsigned int b) {
@@ -1539,6 +1542,7 @@ std::shared_ptr<PointSet> make_pointset(const float *x32, const double *x64, int
         maxabs_kernel<<<grid_for(n * (int64_t)d, 256, 2048), 256, 0, s>>>(x32, n * (int64_t)d, mx);
         SLK_CHECK_LAUNCH();
         unsigned int bits = read_scalar(mx.get(), s);
+        if (bits >= 0x7f800000u) throw_invalid("point matrix contains non-finite values");
         P->maxabs = __uint_as_float_host(bits);
     }
     P->centroid.alloc((size_t)P->dp * P->nb, s);

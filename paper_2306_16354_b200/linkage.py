@@ -22,6 +22,7 @@ from .core import (
     ConvergenceError,
     Dendrogram,
     EdgeList,
+    PointMatrix,
     ValidationError,
     _trusted,
     as_point_matrix,
@@ -238,7 +239,10 @@ def _run(pm, cfg: LinkageConfig, device_points=None) -> SingleLinkageResult:
 
 def single_linkage_result(x, cfg: LinkageConfig) -> SingleLinkageResult:
     """single_linkage plus the spanning tree, connect iterations and stage timings."""
-    pm = as_point_matrix(x)
+    if isinstance(x, np.ndarray) and x.dtype == np.float32 and x.ndim == 2:
+        pm = PointMatrix._float32_device_checked(x)  # finiteness checked on the GPU
+    else:
+        pm = as_point_matrix(x)
     _validate_run(pm, cfg)
     return _run(pm, cfg)
 

@@ -200,6 +200,12 @@ def test_errors(slk, rng):
         slk.solve_mst(slk.edge_list_to_csr(slk.EdgeList.from_pairs(0, [])))
     with pytest.raises(slk.ValidationError, match="cycle"):
         slk.build_dendrogram(slk.EdgeList.from_pairs(4, [(0, 1, 1.0), (1, 2, 2.0), (2, 0, 3.0)]), 4)
+    # float32 input: finiteness is checked on the device (knn.cu:make_pointset)
+    for bad in (np.nan, np.inf, -np.inf):
+        xf = rng.standard_normal((300, 8)).astype(np.float32)
+        xf[123, 5] = bad
+        with pytest.raises(slk.ValidationError, match="non-finite"):
+            slk.single_linkage(xf, slk.LinkageConfig(n_clusters=2, k=3))
 
 
 @pytest.mark.parametrize("n,d,k,c", [(20000, 64, 15, 20), (6000, 128, 32, 6), (5000, 32, 64, 5),
