@@ -1263,10 +1263,16 @@ int tc_pass(const PointSet &Q, const PointSet &X, const int32_t *qid, int k, int
     // small launches: deal each query group's visit order over nsplit CTAs
     // (each keeps its own K' list; the refine takes the union) so that at
     // least ~2 CTAs per SM run
+    // Large k: the register lists hold at most 32, so the index is dealt over
+    // nsplit CTAs per query block with 32 * nsplit >= 2k; each keeps its own
+    // top-32, their union holds the row's top-k and the certificate uses the
+    // smallest of their 32nd values (k = 32: 2 splits, k = 64: 4).
     int nsplit = 1;
+    if (k >= 32)
+        while (nsplit < 8 && kp * nsplit < 2 * k) nsplit *= 2;
     while (nsplit < 8 && ngroups * nsplit < 2 * num_sms()) nsplit *= 2;
-    if (const char *e = getenv("SLK_TC_SPLIT")) nsplit = std::max(1, std::min(8, atoi(e)));
-    if (nsplit & (nsplit - 1)) nsplit = 1;
+    if (const char *e = getenv("SLK_TC_SPLIT")) nsplit = std::max(nsplit, std::min(8, atoi(e)));
+    if (nsplit & (nsplit - 1)) nsplit = 8;
     DevBuf<int32_t> cand(rows * 32 * nsplit, s);
     DevBuf<float> qhat(rows, s), kth_split(rows * nsplit, s);
     DevBuf<unsigned long long> tiles(1, s);
@@ -1422,7 +1428,7 @@ void search(const PointSet &Q, const PointSet &X, int k, int mode, const uint8_t
     const int Rsel = k < 32 ? 1 : (k < 64 ? 2 : 4);
     const Engine eng = engine_choice();
     float scale = 1.0f, inv_scale2 = 1.0f;
-    const bool use_tc = eng != Engine::Ffma && k <= 31 && tc::supported(d) &&
+    const bool use_tc = eng != Engine::Ffma && k <= 127 && tc::supported(d) &&
                         tensor_scale(Q, X, &scale, &inv_scale2);
     int64_t missing = -1;
     if (!use_tc) {
