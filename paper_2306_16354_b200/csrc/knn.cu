@@ -1250,13 +1250,13 @@ int tc_pass(const PointSet &Q, const PointSet &X, const int32_t *qid, int k, int
     int qbn = tc::group_blocks(d, kp);
     // pairs pay in the 1-NN passes (conversion-bound); the k-NN pass is
     // insertion-bound and only sees the extra tiles (C3: +18 %)
-    if (mode == MODE_SELF && !getenv("SLK_TC_QB")) qbn = 1;
-    if (qbn == 2 && (qb1 - qb0) < 4 * num_sms()) qbn = 1;
+    const char *force_qb = getenv("SLK_TC_QB");  // 1 / 2: force singles / pairs (tests)
+    if (mode == MODE_SELF && !force_qb) qbn = 1;
+    if (qbn == 2 && !force_qb && (qb1 - qb0) < 4 * num_sms()) qbn = 1;
     QueryGroups G;
     if (qbn == 2) {
         G = make_groups(Q, qb0, qb1 - qb0, 2, mode == MODE_COLOR ? qcolor : nullptr, s);
-        const char *e = getenv("SLK_TC_QB");
-        if (!(e && atoi(e) == 2) && !pairs_are_tight(Q, qb0, qb1 - qb0, G, s)) qbn = 1;
+        if (!(force_qb && atoi(force_qb) == 2) && !pairs_are_tight(Q, qb0, qb1 - qb0, G, s)) qbn = 1;
     }
     if (qbn == 1) G = make_groups(Q, qb0, qb1 - qb0, 1, mode == MODE_COLOR ? qcolor : nullptr, s);
     const int64_t ngroups = G.ng;

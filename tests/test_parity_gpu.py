@@ -255,3 +255,31 @@ def test_distributed_two_ranks_one_gpu(slk):
     out = subprocess.run(cmd, capture_output=True, text=True, timeout=300)
     assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-4000:]
     assert "DIST_OK" in out.stdout, out.stdout[-2000:]
+
+
+@pytest.mark.parametrize("qb,k", [("2", 5), ("1", 5), ("2", 1)])
+def test_single_linkage_grouping_modes_match_oracle(slk, oracle, monkeypatch, qb, k):
+    """Query-block pairs (two blocks per CTA sharing each converted index
+    tile; at scale chosen by knn.cu:pairs_are_tight) and forced single blocks
+    must both reproduce the oracle exactly, including ragged last groups."""
+    from paper_2306_16354_b200.synthetic import make_blobs
+
+    monkeypatch.setenv("SLK_TC_QB", qb)
+    x = make_blobs(np.random.default_rng(5), 9000 + 77, 20, 12).astype(np.float32)
+    cfg = slk.LinkageConfig(n_clusters=12, k=k, seed=1)
+    res = slk.single_linkage_result(x, cfg)
+    ref = oracle.single_linkage(x, 12, k=k, seed=1)
+    assert np.array_equal(res.tree.src, ref["tree_src"]) and np.array_equal(res.tree.weight, ref["tree_w"])
+    assert np.array_equal(res.dendrogram.merges, ref["merges"])
+    assert np.array_equal(res.labels.labels, ref["labels"])
+
+
+@pytest.mark.parametrize("k", [32, 48, 64])
+def test_knn_large_k_tensor_path_matches_oracle(slk, oracle, k):
+    """k >= 32 on the tensor path: the index is dealt over several CTAs per
+    query block whose top-32 lists the refine unites (knn.cu:tc_pass)."""
+    rng = np.random.default_rng(k)
+    x = rng.standard_normal((6000, 40)).astype(np.float32)
+    g = slk.fused_knn(x, k)
+    oi, od = oracle.fused_knn(x.astype(np.float64), k, rows=(0, 1500))
+    assert np.array_equal(g.indices[:1500], oi) and np.array_equal(g.distances[:1500], od)
