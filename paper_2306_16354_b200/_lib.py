@@ -10,6 +10,7 @@ from __future__ import annotations
 
 import ctypes
 import threading
+import warnings
 
 import numpy as np
 
@@ -119,7 +120,10 @@ def to_device(arr: np.ndarray, dtype):
     """Host array → contiguous device tensor of the given numpy dtype."""
     torch = torch_cuda()
     a = np.ascontiguousarray(arr, dtype=dtype)
-    return torch.from_numpy(a).to(device(), non_blocking=False)
+    with warnings.catch_warnings():
+        # read-only host arrays are fine: the tensor is only read, by the copy below
+        warnings.filterwarnings("ignore", message="The given NumPy array is not writable")
+        return torch.from_numpy(a).to(device(), non_blocking=False)
 
 
 def empty(shape, dtype):

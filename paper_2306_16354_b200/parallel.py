@@ -18,6 +18,7 @@ sharding and collective logic without a GPU.
 from __future__ import annotations
 
 import math
+import os
 
 import numpy as np
 
@@ -25,6 +26,22 @@ from .core import ConvergenceError, Dendrogram, EdgeList, ValidationError, as_po
 from .linkage import STAGES, LabelArray, LinkageConfig, SingleLinkageResult
 
 ROW_ALIGN = 128  # query-block granularity of the scan kernel
+THREADS_ENV_VAR = "PARLINK_THREADS"
+
+
+def resolve_threads(threads: int | None = None) -> int:
+    """Host worker count: the argument, else $PARLINK_THREADS, else the CPU count.
+
+    Same rule and error as /root/reference/pkg/src/parlink/parallel.py:16-26.
+    The CUDA path does not use host threads for compute; the count is
+    validated and recorded (run manifests, bench CSV) for compatibility.
+    """
+    if threads is None:
+        env = os.environ.get(THREADS_ENV_VAR)
+        threads = int(env) if env is not None else (os.cpu_count() or 1)
+    if threads < 1:
+        raise ValueError(f"thread count must be >= 1, got {threads}")
+    return threads
 
 
 def shard_rows(n: int, world: int, rank: int, align: int = ROW_ALIGN) -> tuple[int, int]:
