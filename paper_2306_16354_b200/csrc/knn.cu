@@ -67,10 +67,12 @@ __global__ void pack_blocks_kernel(const float *__restrict__ x, int64_t n, int d
 // dk*16 bytes, core matrix g every 128 bytes, row r&7 every 16 bytes).  One
 // bulk copy brings a block into shared memory and each thread converts its
 // own point in place (tc_scan.cu:convert_tile).
-__global__ void tcpack_kernel(const float *__restrict__ x, int64_t n, int d, int dk, int64_t nblocks,
+// Large d (tc::chunked): each block is dk / kc such runs of kc dims back to
+// back, one per pipeline stage of the chunked kernel (kc = dk otherwise).
+__global__ void tcpack_kernel(const float *__restrict__ x, int64_t n, int d, int dk, int kc, int64_t nblocks,
                               float *__restrict__ out) {
     const int64_t total = nblocks * BN * (int64_t)dk;
-    const int64_t half = (int64_t)BN * dk / 2;  // floats per fp16 tile half
+    const int64_t half = (int64_t)BN * kc / 2;  // floats per fp16 tile half of one chunk
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
          e += (int64_t)gridDim.x * blockDim.x) {
         const int64_t p = e / dk;
@@ -78,9 +80,10 @@ __global__ void tcpack_kernel(const float *__restrict__ x, int64_t n, int d, int
         const float v = (p < n && t < d) ? x[p * d + t] : 0.0f;
         const int64_t b = p / BN;
         const int r = (int)(p - b * BN);
-        const int g = t >> 3, w = t & 7;
-        const int64_t off = (int64_t)(r >> 3) * (dk * 4) + g * 32 + (r & 7) * 4 + (w & 3);
-        out[b * BN * dk + (w >> 2) * half + off] = v;
+        const int c = t / kc, tt = t - c * kc;
+        const int g = tt >> 3, w = tt & 7;
+        const int64_t off = (int64_t)(r >> 3) * (kc * 4) + g * 32 + (r & 7) * 4 + (w & 3);
+        out[b * BN * dk + (int64_t)c * BN * kc + (w >> 2) * half + off] = v;
     }
 }
 
@@ -1225,8 +1228,8 @@ const float *ensure_tcpack(const PointSet &P, cudaStream_t s) {
     if (!P.tcpack) {
         const int dk = tc::k_extent(P.d);
         P.tcpack.alloc((size_t)P.nb * BN * dk, s);
-        tcpack_kernel<<<grid_for(P.nb * BN * (int64_t)dk, 256), 256, 0, s>>>(P.x32, P.n, P.d, dk, P.nb,
-                                                                            P.tcpack);
+        tcpack_kernel<<<grid_for(P.nb * BN * (int64_t)dk, 256), 256, 0, s>>>(
+            P.x32, P.n, P.d, dk, tc::chunk_dims(P.d), P.nb, P.tcpack);
         SLK_CHECK_LAUNCH();
     }
     return P.tcpack;

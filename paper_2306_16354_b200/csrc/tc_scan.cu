@@ -126,6 +126,29 @@ __device__ __forceinline__ void umma_f16(uint32_t tmem_d, uint64_t a, uint64_t b
         "l"(a), "l"(b), "r"(IDESC), "r"(accumulate)
         : "memory");
 }
+// A operand from tensor memory (lane = query row, 32-bit column c = fp16
+// elements 2c, 2c+1 of the K step): the chunked large-d kernel keeps the hi
+// term of its query tile there
+__device__ __forceinline__ void umma_f16_ta(uint32_t tmem_d, uint32_t tmem_a, uint64_t b, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "r"(tmem_a), "l"(b), "r"(IDESC), "r"(accumulate)
+        : "memory");
+}
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+        "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+        "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+        "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]),
+        "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]),
+        "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]),
+        "r"(r[29]), "r"(r[30]), "r"(r[31])
+        : "memory");
+}
 __device__ __forceinline__ void umma_commit(uint64_t *bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                      smem_u32(bar))
@@ -216,8 +239,18 @@ struct Plan {
     int nb;  // B stages that fit
 };
 
-// aug: the norm rides in the augmented K step (no |x~|^2 array)
-__host__ __device__ inline Plan make_plan(int dk, bool aug, int qb) {
+// Large d (chunked kernel, CK): the query tile's hi term lives in TMEM
+// columns [A_COL, A_COL + dk/2), its lo term in shared memory, and the index
+// blocks stream in KC-dim chunks (tcpack stores each block as dk/KC
+// consecutive KC-dim sub-blocks), so d up to CK_MAX_DK fits.  Two
+// accumulator stages (columns 0-255).
+constexpr int KC = 32;
+constexpr int CK_MAX_DK = 512;
+constexpr uint32_t A_COL = 256;
+
+// aug: the norm rides in the augmented K step (no |x~|^2 array); kc > 0: the
+// chunked large-d layout (A = lo term only, B stages of kc dims)
+__host__ __device__ inline Plan make_plan(int dk, bool aug, int qb, int kc = 0) {
     Plan p{};
     uint32_t off = 0;
     auto take = [&](uint32_t bytes, uint32_t align) {
@@ -226,8 +259,8 @@ __host__ __device__ inline Plan make_plan(int dk, bool aug, int qb) {
         off += bytes;
         return at;
     };
-    const uint32_t stage = (uint32_t)BM * dk * 4;  // hi + lo fp16 tiles = raw fp32 block
-    p.a = take(stage * qb, 1024);
+    const uint32_t stage = (uint32_t)BM * (kc > 0 ? kc : dk) * 4;  // hi + lo fp16 tiles = raw fp32 block
+    p.a = take(kc > 0 ? (uint32_t)BM * dk * 2 : stage * qb, 1024);
     p.aaug = aug ? take(AUG_TILE, 1024) : 0u;
     p.xx = aug ? 0u : take(NMETA * BN * 4, 16);
     p.xcol = take(NMETA * BN * 4, 16);
@@ -324,12 +357,53 @@ __device__ __forceinline__ void norm_split(float xx, float &t0, float &t1) {
     t1 = __fsub_rn(v, hi);
 }
 
-template <int MODE, int KP, bool AUG, int QB>
+// Converts query row r of block qb for the chunked kernel straight from the
+// tc-packed global copy: the hi term goes to TMEM lane r (columns A_COL +
+// dims / 2), the lo term to the shared-memory A tile (canonical K-major,
+// SBO = dk * 16).  Returns |q~|^2 of the unsplit values.
+__device__ __forceinline__ float convert_query_ck(const float *qblk, unsigned char *sA, int r, int dk, float sc,
+                                                  const float *s_cq, uint32_t tmem_lane) {
+    float nrm4[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+    for (int b64 = 0; b64 < dk / 64; b64++) {
+        uint32_t hreg[32];
+#pragma unroll
+        for (int gg = 0; gg < 8; gg++) {
+            const int t0 = b64 * 64 + gg * 8;  // first dim of the 8-dim group
+            const int c = t0 / KC, g = (t0 % KC) >> 3;
+            const float *hp = qblk + (int64_t)c * BM * KC + (r >> 3) * (KC * 4) + g * 32 + (r & 7) * 4;
+            const float4 u = *reinterpret_cast<const float4 *>(hp);
+            const float4 w = *reinterpret_cast<const float4 *>(hp + BM * KC / 2);
+            const float4 c0 = *reinterpret_cast<const float4 *>(s_cq + t0);
+            const float4 c1 = *reinterpret_cast<const float4 *>(s_cq + t0 + 4);
+            const float v[8] = {__fmaf_rn(u.x, sc, c0.x), __fmaf_rn(u.y, sc, c0.y), __fmaf_rn(u.z, sc, c0.z),
+                                __fmaf_rn(u.w, sc, c0.w), __fmaf_rn(w.x, sc, c1.x), __fmaf_rn(w.y, sc, c1.y),
+                                __fmaf_rn(w.z, sc, c1.z), __fmaf_rn(w.w, sc, c1.w)};
+            __half2 h[4], l[4];
+#pragma unroll
+            for (int q = 0; q < 4; q++) {
+                split2(v[2 * q], v[2 * q + 1], h[q], l[q], nrm4[q]);
+                hreg[gg * 4 + q] = *reinterpret_cast<uint32_t *>(&h[q]);
+            }
+            *reinterpret_cast<uint4 *>(sA + (r >> 3) * (dk * 16) + (t0 >> 3) * 128 + (r & 7) * 16) =
+                *reinterpret_cast<uint4 *>(l);
+        }
+        tmem_st32(tmem_lane + A_COL + (uint32_t)b64 * 32, hreg);
+    }
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    return __fadd_rn(__fadd_rn(nrm4[0], nrm4[1]), __fadd_rn(nrm4[2], nrm4[3]));
+}
+
+// CK: chunked large-d variant (QB = 1, no augmented step): every index block
+// arrives as dk / KC stages of KC dims that accumulate into one TMEM stage.
+template <int MODE, int KP, bool AUG, int QB, bool CK>
 __global__ void __launch_bounds__(Cfg<QB>::NTHREADS, 1) tc_scan_kernel(TcArgs a) {
     extern __shared__ __align__(1024) unsigned char smem[];
-    constexpr int NTHREADS = Cfg<QB>::NTHREADS, NT = Cfg<QB>::NT;
+    static_assert(!CK || (QB == 1 && !AUG), "chunked kernel: single query block, norms via smem");
+    constexpr int NTHREADS = Cfg<QB>::NTHREADS, NT = CK ? 2 : Cfg<QB>::NT;
     const int dk = a.dk;
-    const Plan P = make_plan(dk, AUG, QB);
+    const int kc = CK ? KC : dk;  // dims per B stage
+    const int nck = dk / kc;      // stages per index block
+    const Plan P = make_plan(dk, AUG, QB, CK ? KC : 0);
     float *s_xx = reinterpret_cast<float *>(smem + P.xx);  // !AUG: |x~|^2 per meta slot
     const int nb = P.nb;
     unsigned char *sA = smem + P.a;
@@ -352,9 +426,9 @@ __global__ void __launch_bounds__(Cfg<QB>::NTHREADS, 1) tc_scan_kernel(TcArgs a)
     const int64_t qb = a.qb0 + qbl * QB;        // first query block of the group
     const int nqa = (int)min((int64_t)QB, a.nqb_total - qb);  // query blocks present
     const int64_t nxb = (a.nx + BN - 1) / BN;
-    const uint32_t stage_bytes = (uint32_t)BM * dk * 4;
-    const uint32_t half_bytes = (uint32_t)BM * dk * 2;
-    const uint32_t sbo = (uint32_t)dk * 16;  // (dk/8) core matrices of 128 B per 8-row group
+    const uint32_t stage_bytes = (uint32_t)BM * kc * 4;
+    const uint32_t half_bytes = (uint32_t)BM * kc * 2;
+    const uint32_t sbo = (uint32_t)kc * 16;  // (kc/8) core matrices of 128 B per 8-row group
     const int dkm = dk;                      // dims (d rounded up to 16); the norm step is separate
     unsigned char *sAaug = smem + P.aaug;    // AUG: norm-step tiles of A and of each B stage
     unsigned char *sBaug = smem + P.baug;
@@ -399,7 +473,7 @@ __global__ void __launch_bounds__(Cfg<QB>::NTHREADS, 1) tc_scan_kernel(TcArgs a)
 
     if (warp == Cfg<QB>::WARP_PROD) {
         // ===================== producer: visit order + bulk copies
-        if (lane == 0) {
+        if (lane == 0 && !CK) {
             mbar_expect_tx(afull, stage_bytes * nqa);
             for (int q = 0; q < nqa; q++)
                 bulk_g2s(sA + q * stage_bytes, a.qp + (qb + q) * (int64_t)dk * BM, stage_bytes, afull);
@@ -407,9 +481,8 @@ __global__ void __launch_bounds__(Cfg<QB>::NTHREADS, 1) tc_scan_kernel(TcArgs a)
         BlockVisitor vis(a.sb_order + qbl * a.nsb, a.sb_lb + qbl * a.nsb, a.flat_lb + qbl * a.nsb * 32,
                          a.nvalid[qbl], lane, split, a.nsplit);
         int64_t computed = 0;
+        int st = 0;  // B stage counter (nck stages per index block)
         for (int it = 0;; it++) {
-            const int s = it % nb;
-            const uint32_t ph = (uint32_t)(it / nb) & 1u;
             volatile float *part = misc->part;
             float thr = fmaxf(fmaxf(part[0], part[1]), fmaxf(part[2], part[3]));
             if (QB == 2) thr = fmaxf(thr, fmaxf(fmaxf(part[4], part[5]), fmaxf(part[6], part[7])));
@@ -422,19 +495,24 @@ __global__ void __launch_bounds__(Cfg<QB>::NTHREADS, 1) tc_scan_kernel(TcArgs a)
             if (lane == 0) misc->dbg[0] = it * 100000 + (int)(jb < 0 ? 99999 : jb % 100000);
 #endif
             if (lane == 0) {
-                mbar_wait(&bempty[s], ph ^ 1u, 1, it);
-                misc->meta_blk[it % NMETA] = (int)jb;
-                if (jb < 0) {
-                    mbar_arrive(&rawfull[s]);
-                } else {
-                    const bool col = MODE == MODE_COLOR;
-                    mbar_expect_tx(&rawfull[s], stage_bytes + (col ? BN * 4 : 0));
-                    bulk_g2s(sB + (size_t)s * stage_bytes, a.xp + jb * (int64_t)dk * BN, stage_bytes,
-                             &rawfull[s]);
-                    if (col)
-                        bulk_g2s(s_xcol + (it % NMETA) * BN, a.xcolor + jb * BN, BN * 4, &rawfull[s]);
-                    computed++;
+                // the end marker is one stage; a block is nck stages
+                for (int c = 0; c < (jb < 0 ? 1 : nck); c++, st++) {
+                    const int s = st % nb;
+                    const uint32_t ph = (uint32_t)(st / nb) & 1u;
+                    mbar_wait(&bempty[s], ph ^ 1u, 1, it);
+                    if (c == 0) misc->meta_blk[it % NMETA] = (int)jb;
+                    if (jb < 0) {
+                        mbar_arrive(&rawfull[s]);
+                    } else {
+                        const bool col = MODE == MODE_COLOR && c == 0;
+                        mbar_expect_tx(&rawfull[s], stage_bytes + (col ? BN * 4 : 0));
+                        bulk_g2s(sB + (size_t)s * stage_bytes, a.xp + (jb * nck + c) * (int64_t)kc * BN,
+                                 stage_bytes, &rawfull[s]);
+                        if (col)
+                            bulk_g2s(s_xcol + (it % NMETA) * BN, a.xcolor + jb * BN, BN * 4, &rawfull[s]);
+                    }
                 }
+                if (jb >= 0) computed++;
             }
             if (jb < 0) break;
         }
@@ -443,59 +521,95 @@ __global__ void __launch_bounds__(Cfg<QB>::NTHREADS, 1) tc_scan_kernel(TcArgs a)
         // ===================== convert warps: A once, then every B stage in place
         const int r = tid;  // 0..127: query row (A) / index point (B)
         const float sc = a.scale;
-        mbar_wait(afull, 0, 2, 0);
+        if (CK) {
+            s_qq[r] = convert_query_ck(a.qp + qb * (int64_t)dk * BM, sA, r, dk, sc, s_cq,
+                                       tmem + ((uint32_t)(warp * 32) << 16));
+            tc_fence_before();  // published to the MMA warp by the first bfull arrive
+        } else {
+            mbar_wait(afull, 0, 2, 0);
 #pragma unroll
-        for (int q = 0; q < QB; q++) {
-            // a missing second block (odd count) converts stale smem: its rows are never output
-            s_qq[q * BM + r] = convert_tile(sA + q * stage_bytes, r, dkm, dk, sc, s_cq);
-            if (AUG && q == 0) put_norm_terms(sAaug, r, NORM_A, NORM_A);  // shared by the group
+            for (int q = 0; q < QB; q++) {
+                // a missing second block (odd count) converts stale smem: its rows are never output
+                s_qq[q * BM + r] = convert_tile(sA + q * stage_bytes, r, dkm, dk, sc, s_cq);
+                if (AUG && q == 0) put_norm_terms(sAaug, r, NORM_A, NORM_A);  // shared by the group
+            }
         }
+        int st = 0;
         for (int it = 0;; it++) {
-            const int s = it % nb;
-            const uint32_t ph = (uint32_t)(it / nb) & 1u;
-            mbar_wait(&rawfull[s], ph, 3, it);
-            const int jb = misc->meta_blk[it % NMETA];
+            float xx = 0.0f;
+            bool end = false;
+            for (int c = 0; c < nck; c++, st++) {
+                const int s = st % nb;
+                const uint32_t ph = (uint32_t)(st / nb) & 1u;
+                mbar_wait(&rawfull[s], ph, 3, it);
+                const int jb = misc->meta_blk[it % NMETA];
 #ifdef SLK_WATCHDOG
-            if (r == 100) misc->dbg[1] = it * 100000 + (jb < 0 ? 99999 : jb % 100000);
+                if (r == 100) misc->dbg[1] = it * 100000 + (jb < 0 ? 99999 : jb % 100000);
 #endif
-            if (jb >= 0) {
+                if (jb < 0) {
+                    mbar_arrive(&bfull[s]);
+                    end = true;
+                    break;
+                }
                 unsigned char *tile = sB + (size_t)s * stage_bytes;
-                const float xx = convert_tile(tile, r, dkm, dk, sc, s_cq);
-                if (AUG) {
-                    float t0, t1;
-                    norm_split(xx, t0, t1);
-                    put_norm_terms(sBaug + (size_t)s * AUG_TILE, r, t0, t1);
-                } else {
-                    s_xx[(it % NMETA) * BN + r] = xx;
+                xx = __fadd_rn(xx, convert_tile(tile, r, kc, kc, sc, s_cq + c * kc));
+                if (c == nck - 1) {
+                    if (AUG) {
+                        float t0, t1;
+                        norm_split(xx, t0, t1);
+                        put_norm_terms(sBaug + (size_t)s * AUG_TILE, r, t0, t1);
+                    } else {
+                        s_xx[(it % NMETA) * BN + r] = xx;
+                    }
                 }
                 fence_async_smem();  // generic-proxy smem writes -> visible to the tensor core
+                mbar_arrive(&bfull[s]);
             }
-            mbar_arrive(&bfull[s]);
-            if (jb < 0) break;
+            if (end) break;
         }
     } else if (warp == Cfg<QB>::WARP_MMA) {
         // ===================== MMA issuer (one elected thread)
         if (lane == 0) {
             const uint32_t a_base = smem_u32(sA), b_base = smem_u32(sB);
+            int st = 0;
             for (int it = 0;; it++) {
-                const int s = it % nb;
-                const uint32_t ph = (uint32_t)(it / nb) & 1u;
                 const int ts = it % NT;
                 const uint32_t tph = (uint32_t)(it / NT) & 1u;
+                bool end = false;
+                for (int c = 0; c < nck; c++, st++) {
+                const int s = st % nb;
+                const uint32_t ph = (uint32_t)(st / nb) & 1u;
                 mbar_wait(&bfull[s], ph, 4, it);
 #ifdef SLK_WATCHDOG
                 misc->dbg[3] = it;
 #endif
-                // the accumulator stage must be drained even for the end marker:
-                // two completions of tfull[ts] ahead of the epilogue would alias
-                // its phase parity
-                mbar_wait(&tempty[ts], tph ^ 1u, 5, it);
-                if (misc->meta_blk[it % NMETA] < 0) {
-                    mbar_arrive(&tfull[ts]);
-                    break;
+                if (c == 0) {
+                    // the accumulator stage must be drained even for the end marker:
+                    // two completions of tfull[ts] ahead of the epilogue would alias
+                    // its phase parity
+                    mbar_wait(&tempty[ts], tph ^ 1u, 5, it);
+                    if (misc->meta_blk[it % NMETA] < 0) {
+                        mbar_arrive(&tfull[ts]);
+                        end = true;
+                        break;
+                    }
                 }
                 tc_fence_after();
                 const uint32_t bs = b_base + s * stage_bytes;
+                if (CK) {
+                    // <q~, x~> over this chunk's K steps: hi from TMEM, lo from smem
+                    const uint32_t d_tmem = tmem + (uint32_t)ts * 128;
+                    for (int k = 0; k < kc / 16; k++) {
+                        const int kg = c * (kc / 16) + k;
+                        const uint32_t ta = tmem + A_COL + (uint32_t)kg * 8;
+                        const uint64_t al = umma_desc(a_base + kg * 256, 128, (uint32_t)dk * 16);
+                        const uint64_t bh = umma_desc(bs + k * 256, 128, sbo);
+                        const uint64_t bl = umma_desc(bs + half_bytes + k * 256, 128, sbo);
+                        umma_f16_ta(d_tmem, ta, bh, kg > 0 ? 1u : 0u);
+                        umma_f16_ta(d_tmem, ta, bl, 1u);
+                        umma_f16(d_tmem, al, bh, 1u);
+                    }
+                } else {
 #pragma unroll
                 for (int q = 0; q < QB; q++) {
                     const uint32_t d_tmem = tmem + (uint32_t)(ts * QB + q) * 128;
@@ -515,7 +629,10 @@ __global__ void __launch_bounds__(Cfg<QB>::NTHREADS, 1) tc_scan_kernel(TcArgs a)
                         umma_f16(d_tmem, umma_desc(smem_u32(sAaug), 128, 256),
                                  umma_desc(smem_u32(sBaug) + s * AUG_TILE, 128, 256), 1u);
                 }
+                }
                 umma_commit(&bempty[s]);  // operands consumed: the producer may refill stage s
+                }
+                if (end) break;
                 umma_commit(&tfull[ts]);  // accumulator ready
             }
 #ifdef SLK_WATCHDOG
@@ -692,23 +809,32 @@ __global__ void __launch_bounds__(Cfg<QB>::NTHREADS, 1) tc_scan_kernel(TcArgs a)
     }
 }
 
-template <int MODE, int KP, bool AUG, int QB>
+template <int MODE, int KP, bool AUG, int QB, bool CK>
 void launch_mode(const TcArgs &args, int64_t ngroups, cudaStream_t s) {
-    const Plan P = make_plan(args.dk, AUG, QB);
-    SLK_CUDA(cudaFuncSetAttribute(tc_scan_kernel<MODE, KP, AUG, QB>,
+    const Plan P = make_plan(args.dk, AUG, QB, CK ? KC : 0);
+    SLK_CUDA(cudaFuncSetAttribute(tc_scan_kernel<MODE, KP, AUG, QB, CK>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P.total));
-    tc_scan_kernel<MODE, KP, AUG, QB><<<(unsigned)(ngroups * args.nsplit), Cfg<QB>::NTHREADS, P.total, s>>>(args);
+    tc_scan_kernel<MODE, KP, AUG, QB, CK>
+        <<<(unsigned)(ngroups * args.nsplit), Cfg<QB>::NTHREADS, P.total, s>>>(args);
     SLK_CHECK_LAUNCH();
 }
 
-template <int KP, bool AUG, int QB>
+template <int KP, bool AUG, int QB, bool CK = false>
 void launch_kp(int mode, const TcArgs &args, int64_t ngroups, cudaStream_t s) {
     switch (mode) {
-        case MODE_NONE: launch_mode<MODE_NONE, KP, AUG, QB>(args, ngroups, s); break;
-        case MODE_MASK: launch_mode<MODE_MASK, KP, AUG, QB>(args, ngroups, s); break;
-        case MODE_COLOR: launch_mode<MODE_COLOR, KP, AUG, QB>(args, ngroups, s); break;
-        default: launch_mode<MODE_SELF, KP, AUG, QB>(args, ngroups, s); break;
+        case MODE_NONE: launch_mode<MODE_NONE, KP, AUG, QB, CK>(args, ngroups, s); break;
+        case MODE_MASK: launch_mode<MODE_MASK, KP, AUG, QB, CK>(args, ngroups, s); break;
+        case MODE_COLOR: launch_mode<MODE_COLOR, KP, AUG, QB, CK>(args, ngroups, s); break;
+        default: launch_mode<MODE_SELF, KP, AUG, QB, CK>(args, ngroups, s); break;
     }
+}
+
+void launch_ck(int mode, int kp, const TcArgs &args, int64_t ngroups, cudaStream_t s) {
+    if (kp <= 2) launch_kp<2, false, 1, true>(mode, args, ngroups, s);
+    else if (kp <= 4) launch_kp<4, false, 1, true>(mode, args, ngroups, s);
+    else if (kp <= 8) launch_kp<8, false, 1, true>(mode, args, ngroups, s);
+    else if (kp <= 16) launch_kp<16, false, 1, true>(mode, args, ngroups, s);
+    else launch_kp<32, false, 1, true>(mode, args, ngroups, s);
 }
 
 template <bool AUG>
@@ -729,17 +855,33 @@ void launch_aug(int mode, int kp, int qb, const TcArgs &args, int64_t ngroups, c
 
 }  // namespace
 
+static int round16(int d) { return ((d + 15) / 16) * 16; }
+static bool aug_fits(int d) { return make_plan(round16(d), true, 1).nb >= 3; }
+
+// Chunked (large-d) kernel when the whole-block kernel cannot hold its A
+// tile plus two B stages (d > 128)
+bool chunked(int d) { return make_plan(round16(d), aug_fits(d), 1).nb < 2; }
+
 // The augmented norm step when at least 3 B stages still fit (measured: the
 // max-only epilogue pays for the extra MMA and the 16 extra K columns);
 // otherwise |x~|^2 goes through shared memory (large d).
-bool use_aug(int d) { return make_plan(((d + 15) / 16) * 16, true, 1).nb >= 3; }
+bool use_aug(int d) { return !chunked(d) && aug_fits(d); }
 
-int k_extent(int d) { return ((d + 15) / 16) * 16; }
+// chunked: whole 64-dim TMEM stores of the query's hi term
+int k_extent(int d) { return chunked(d) ? ((d + 63) / 64) * 64 : round16(d); }
 
-size_t smem_bytes(int d) { return make_plan(k_extent(d), use_aug(d), 1).total; }
+int chunk_dims(int d) { return chunked(d) ? KC : k_extent(d); }
 
-// at least two B stages must fit next to the A tile
-bool supported(int d) { return make_plan(k_extent(d), use_aug(d), 1).nb >= 2; }
+size_t smem_bytes(int d) {
+    return chunked(d) ? make_plan(k_extent(d), false, 1, KC).total : make_plan(k_extent(d), use_aug(d), 1).total;
+}
+
+// at least two B stages must fit next to the A tile; chunked: the query's hi
+// term must fit in TMEM next to two accumulator stages
+bool supported(int d) {
+    if (!chunked(d)) return true;
+    return k_extent(d) <= CK_MAX_DK && make_plan(k_extent(d), false, 1, KC).nb >= 2;
+}
 
 // query blocks per CTA for K' = kp candidates: pairs need K' <= 16 (the 8
 // epilogue warps cap registers) and 2 B stages next to two A tiles
@@ -750,14 +892,15 @@ bool supported(int d) { return make_plan(k_extent(d), use_aug(d), 1).nb >= 2; }
 // (SLK_TC_QB=1 / 2 force singles / pairs).
 int group_blocks(int d, int kp) {
     const char *e = getenv("SLK_TC_QB");
-    if ((e && atoi(e) == 1) || kp > 16) return 1;
+    if ((e && atoi(e) == 1) || kp > 16 || chunked(d)) return 1;
     return make_plan(k_extent(d), use_aug(d), 2).nb >= 2 ? 2 : 1;
 }
 
 // K' = kp candidates per row (2, 4, 8, 16 or 32; kp > k for the certificate);
 // qb query blocks per CTA (group_blocks), ngroups groups in the launch
 void launch(int mode, int kp, int qb, const TcArgs &args, int64_t ngroups, cudaStream_t s) {
-    if (use_aug(args.d)) launch_aug<true>(mode, kp, qb, args, ngroups, s);
+    if (chunked(args.d)) launch_ck(mode, kp, args, ngroups, s);
+    else if (use_aug(args.d)) launch_aug<true>(mode, kp, qb, args, ngroups, s);
     else launch_aug<false>(mode, kp, qb, args, ngroups, s);
 }
 

@@ -38,7 +38,12 @@ struct TcArgs {
 // MMA K extent for d dims: d rounded up to 16, plus the augmented norm step
 // when use_aug(d) (tc_scan.cu)
 bool use_aug(int d);
+// d > 128: chunked kernel (query hi term in TMEM, index blocks streamed in
+// chunk_dims(d)-dim stages); k_extent(d) is then d rounded up to 64
+bool chunked(int d);
 int k_extent(int d);
+// dims per contiguous sub-block of the tc-packed layout (= k_extent unless chunked)
+int chunk_dims(int d);
 size_t smem_bytes(int d);
 bool supported(int d);
 // Query blocks per CTA (1 or 2) for d dims and K' = kp.

@@ -5,7 +5,8 @@ k in {8,32,64}; N(0,1) points, no cluster structure, so pruning skips little).
 
 One JSON line per (d, k): seconds per k-NN graph (CUDA events, points resident
 in HBM, warm-up first), the scan engine the library chose (tcgen05 tensor
-cores for k < 32 and d <= 256, else the exact-fp32 FFMA scan), the
+cores for k <= 127 and d <= 512 — the chunked kernel above d = 128 — else the
+exact-fp32 FFMA scan), the
 computed-tile work and its rate against the matching peak.
 """
 import argparse

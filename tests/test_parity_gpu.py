@@ -283,3 +283,31 @@ def test_knn_large_k_tensor_path_matches_oracle(slk, oracle, k):
     g = slk.fused_knn(x, k)
     oi, od = oracle.fused_knn(x.astype(np.float64), k, rows=(0, 1500))
     assert np.array_equal(g.indices[:1500], oi) and np.array_equal(g.distances[:1500], od)
+
+
+@pytest.mark.parametrize("d,k", [(136, 8), (256, 15), (512, 8), (512, 40), (300, 1)])
+def test_knn_large_d_chunked_tensor_path_matches_oracle(slk, oracle, d, k):
+    """d > 128 runs the chunked tcgen05 kernel (query hi term in TMEM, index
+    blocks streamed in 32-dim stages, tc_scan.cu CK); it must be the engine
+    that ran (tensor-core time recorded) and match the oracle exactly."""
+    from paper_2306_16354_b200 import _lib
+
+    x = np.random.default_rng(d + k).standard_normal((5000, d), dtype=np.float32)
+    _lib.profile(reset=True)
+    g = slk.fused_knn(x, k)
+    assert _lib.profile()["tc_ms"] > 0.0
+    oi, od = oracle.fused_knn(x, k, rows=(0, 1024))
+    assert np.array_equal(g.indices[:1024], oi) and np.array_equal(g.distances[:1024], od)
+
+
+def test_single_linkage_large_d_matches_oracle(slk, oracle):
+    """Cross-colour passes through the chunked kernel (d = 192)."""
+    from paper_2306_16354_b200.synthetic import make_blobs
+
+    x = make_blobs(np.random.default_rng(192), 6000 + 33, 192, 9).astype(np.float32)
+    cfg = slk.LinkageConfig(n_clusters=9, k=4, seed=3)
+    res = slk.single_linkage_result(x, cfg)
+    ref = oracle.single_linkage(x, 9, k=4, seed=3)
+    assert np.array_equal(res.tree.src, ref["tree_src"]) and np.array_equal(res.tree.weight, ref["tree_w"])
+    assert np.array_equal(res.dendrogram.merges, ref["merges"])
+    assert np.array_equal(res.labels.labels, ref["labels"])
