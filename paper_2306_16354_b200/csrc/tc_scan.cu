@@ -279,6 +279,19 @@ __host__ __device__ inline Plan make_plan(int dk, bool aug, int qb, int kc = 0) 
     return p;
 }
 
+// position in a ring of n stages and the mbarrier phase parity of the lap
+struct Ring {
+    int s;
+    uint32_t ph;
+    int n;
+    __device__ __forceinline__ void next() {
+        if (++s == n) {
+            s = 0;
+            ph ^= 1u;
+        }
+    }
+};
+
 struct Misc {
     float part[8];            // per epilogue warp: largest row threshold (a units)
     uint32_t tmem_base;
@@ -481,7 +494,7 @@ __global__ void __launch_bounds__(Cfg<QB>::NTHREADS, 1) tc_scan_kernel(TcArgs a)
         BlockVisitor vis(a.sb_order + qbl * a.nsb, a.sb_lb + qbl * a.nsb, a.flat_lb + qbl * a.nsb * 32,
                          a.nvalid[qbl], lane, split, a.nsplit);
         int64_t computed = 0;
-        int st = 0;  // B stage counter (nck stages per index block)
+        Ring rg{0, 0u, nb};  // B stage ring (nck stages per index block)
         for (int it = 0;; it++) {
             volatile float *part = misc->part;
             float thr = fmaxf(fmaxf(part[0], part[1]), fmaxf(part[2], part[3]));
@@ -496,9 +509,9 @@ __global__ void __launch_bounds__(Cfg<QB>::NTHREADS, 1) tc_scan_kernel(TcArgs a)
 #endif
             if (lane == 0) {
                 // the end marker is one stage; a block is nck stages
-                for (int c = 0; c < (jb < 0 ? 1 : nck); c++, st++) {
-                    const int s = st % nb;
-                    const uint32_t ph = (uint32_t)(st / nb) & 1u;
+                for (int c = 0; c < (jb < 0 ? 1 : nck); c++, rg.next()) {
+                    const int s = rg.s;
+                    const uint32_t ph = rg.ph;
                     mbar_wait(&bempty[s], ph ^ 1u, 1, it);
                     if (c == 0) misc->meta_blk[it % NMETA] = (int)jb;
                     if (jb < 0) {
@@ -534,13 +547,13 @@ __global__ void __launch_bounds__(Cfg<QB>::NTHREADS, 1) tc_scan_kernel(TcArgs a)
                 if (AUG && q == 0) put_norm_terms(sAaug, r, NORM_A, NORM_A);  // shared by the group
             }
         }
-        int st = 0;
+        Ring rg{0, 0u, nb};
         for (int it = 0;; it++) {
             float xx = 0.0f;
             bool end = false;
-            for (int c = 0; c < nck; c++, st++) {
-                const int s = st % nb;
-                const uint32_t ph = (uint32_t)(st / nb) & 1u;
+            for (int c = 0; c < nck; c++, rg.next()) {
+                const int s = rg.s;
+                const uint32_t ph = rg.ph;
                 mbar_wait(&rawfull[s], ph, 3, it);
                 const int jb = misc->meta_blk[it % NMETA];
 #ifdef SLK_WATCHDOG
@@ -571,14 +584,14 @@ __global__ void __launch_bounds__(Cfg<QB>::NTHREADS, 1) tc_scan_kernel(TcArgs a)
         // ===================== MMA issuer (one elected thread)
         if (lane == 0) {
             const uint32_t a_base = smem_u32(sA), b_base = smem_u32(sB);
-            int st = 0;
+            Ring rg{0, 0u, nb};
             for (int it = 0;; it++) {
                 const int ts = it % NT;
                 const uint32_t tph = (uint32_t)(it / NT) & 1u;
                 bool end = false;
-                for (int c = 0; c < nck; c++, st++) {
-                const int s = st % nb;
-                const uint32_t ph = (uint32_t)(st / nb) & 1u;
+                for (int c = 0; c < nck; c++, rg.next()) {
+                const int s = rg.s;
+                const uint32_t ph = rg.ph;
                 mbar_wait(&bfull[s], ph, 4, it);
 #ifdef SLK_WATCHDOG
                 misc->dbg[3] = it;
