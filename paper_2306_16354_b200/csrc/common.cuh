@@ -233,12 +233,27 @@ void csr_solve_mst(int64_t n, const int64_t *offs, const int32_t *cols, const do
                    int32_t *colors, int64_t *n_edges, int64_t *n_components, cudaStream_t s);
 
 // dendro.cu
-void dendrogram_device_sort(const int32_t *src, const int32_t *dst, const double *w, int64_t n,
-                            bool take_sqrt, int32_t *h_a, int32_t *h_b, double *h_w,
-                            cudaStream_t s);
+// Host copy of the sorted spanning tree laid out for the fold
+// (dendro.cu:dendrogram_device_sort).  Positions [0, t) hold the first t
+// merges grouped by the component of the forest they form (group g =
+// positions off[g] .. off[g+1], merge ranks rank[j] increasing within a
+// group); positions [t, n-1) hold merges t .. n-2 in order.  The arrays live
+// in per-thread pinned staging, valid until the next call.
+struct FoldInput {
+    int64_t n = 0;
+    const int32_t *a = nullptr, *b = nullptr;
+    const double *w = nullptr;
+    int64_t t = 0;
+    const int32_t *rank = nullptr;
+    const int64_t *off = nullptr;
+    int64_t ngroups = 0;
+    int threads = 1;
+};
+// cut: merges before the flat cut ((n-1) - (n_clusters-1)), < 0 for none
+FoldInput dendrogram_device_sort(const int32_t *src, const int32_t *dst, const double *w, int64_t n,
+                                 bool take_sqrt, int64_t cut, cudaStream_t s);
 // labels (optional): the flat cut for n_clusters, taken during the fold
-void dendrogram_fold(const int32_t *a, const int32_t *b, const double *w, int64_t n,
-                     double *merges, int64_t n_clusters = 0, int64_t *labels = nullptr,
+void dendrogram_fold(const FoldInput &in, double *merges, int64_t n_clusters = 0, int64_t *labels = nullptr,
                      double *extract_ms = nullptr);
 void extract_labels(const double *merges, int64_t n, int64_t n_clusters, int64_t *labels);
 

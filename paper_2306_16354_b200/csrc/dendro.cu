@@ -16,6 +16,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <thread>
 #include <vector>
 
 #include "common.cuh"
@@ -64,15 +65,105 @@ void sort_pairs(const K *kin, K *kout, const V *vin, V *vout, int64_t m, cudaStr
     SLK_CUDA(cub::DeviceRadixSort::SortPairs(t.get(), tmp, kin, kout, vin, vout, (int)m, 0, end_bit, s));
 }
 
+// ---- components of the forest of the first t merges (hook + pointer jumping)
+__device__ __forceinline__ int32_t cc_find(int32_t *parent, int32_t x) {
+    int32_t p = parent[x];
+    while (p != x) {
+        const int32_t g = parent[p];
+        if (g != p) parent[x] = g;  // halving; a stale write still points at an ancestor
+        x = p;
+        p = g;
+    }
+    return x;
+}
+
+__global__ void cc_init_kernel(int32_t *parent, int64_t n) {
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x)
+        parent[v] = (int32_t)v;
+}
+
+// the larger root hooks under the smaller: every component ends rooted at its
+// smallest vertex, whatever the interleaving
+__global__ void cc_hook_kernel(const int32_t *a, const int32_t *b, int64_t t, int32_t *parent) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < t; e += (int64_t)gridDim.x * blockDim.x) {
+        int32_t u = a[e], v = b[e];
+        while (true) {
+            u = cc_find(parent, u);
+            v = cc_find(parent, v);
+            if (u == v) break;
+            const int32_t hi = u > v ? u : v, lo = u > v ? v : u;
+            if (atomicCAS(&parent[hi], hi, lo) == hi) break;
+        }
+    }
+}
+
+__global__ void cc_key_kernel(const int32_t *a, int64_t t, int32_t *parent, int32_t *key, int32_t *iota) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < t; e += (int64_t)gridDim.x * blockDim.x) {
+        key[e] = cc_find(parent, a[e]);
+        iota[e] = (int32_t)e;
+    }
+}
+
+__global__ void group_gather_kernel(const int32_t *rank, int64_t t, const int32_t *a, const int32_t *b,
+                                    const double *w, int32_t *ga, int32_t *gb, double *gw) {
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < t; j += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t e = rank[j];
+        ga[j] = a[e];
+        gb[j] = b[e];
+        gw[j] = w[e];
+    }
+}
+
+// grow-only pinned host staging for the fold's inputs (one set per host thread)
+template <class T>
+struct PinnedVec {
+    T *p = nullptr;
+    size_t cap = 0;
+    T *get(size_t n) {
+        if (n > cap) {
+            if (p) cudaFreeHost(p);
+            p = nullptr;
+            cap = 0;
+            SLK_CUDA(cudaMallocHost((void **)&p, std::max<size_t>(n, 1) * sizeof(T)));
+            cap = n;
+        }
+        return p;
+    }
+    ~PinnedVec() {
+        if (p) cudaFreeHost(p);
+    }
+};
+struct FoldStaging {
+    PinnedVec<int32_t> a, b, rank;
+    PinnedVec<double> w;
+    std::vector<int64_t> off;
+};
+thread_local FoldStaging staging;
+
+constexpr int64_t FOLD_TOP = 4096;           // merges folded in order after the parallel prefix
+constexpr int64_t FOLD_MIN_PARALLEL = 1 << 17;
+
+int fold_threads() {
+    if (const char *e = getenv("SLK_FOLD_THREADS")) return std::max(1, atoi(e));
+    const unsigned hc = std::thread::hardware_concurrency();
+    return (int)std::min(32u, std::max(1u, hc));
+}
+
 }  // namespace
 
-// Sort the n-1 tree edges by (w', a, b) with w' = sqrt(w) when requested;
-// writes host arrays (a, b, w') in merge order.
-void dendrogram_device_sort(const int32_t *src, const int32_t *dst, const double *w, int64_t n,
-                            bool take_sqrt, int32_t *h_a, int32_t *h_b, double *h_w,
-                            cudaStream_t s) {
-    int64_t m = n - 1;
-    if (m <= 0) return;
+// Sorts the n-1 tree edges by (w', a, b) with w' = sqrt(w) when requested
+// (linkage.py:177, 295-297) and stages them on the host for the fold.  When
+// the tree is large, the first t = min(n-1-FOLD_TOP, cut) merges are grouped
+// by the component of the forest they form (device hook + pointer jumping,
+// stable radix sort by component root, gather), so the host folds the groups
+// in parallel (fold.cu).  cut < 0: no flat cut requested.
+FoldInput dendrogram_device_sort(const int32_t *src, const int32_t *dst, const double *w, int64_t n,
+                                 bool take_sqrt, int64_t cut, cudaStream_t s) {
+    FoldInput in;
+    in.n = n;
+    in.threads = fold_threads();
+    const int64_t m = n - 1;
+    if (m <= 0) return in;
     DevBuf<uint64_t> keys(m, s), ks(m, s);
     DevBuf<double> wt(m, s), w1(m, s), w2(m, s);
     DevBuf<int32_t> iota(m, s), perm1(m, s), iota2(m, s), perm2(m, s), a(m, s), b(m, s);
@@ -87,10 +178,52 @@ void dendrogram_device_sort(const int32_t *src, const int32_t *dst, const double
     sort_pairs(w1.get(), w2.get(), iota2.get(), perm2.get(), m, s);
     dendro_final_kernel<<<grid, 256, 0, s>>>(ks, perm2, m, a, b);
     SLK_CHECK_LAUNCH();
-    SLK_CUDA(cudaMemcpyAsync(h_a, a.get(), m * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-    SLK_CUDA(cudaMemcpyAsync(h_b, b.get(), m * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-    SLK_CUDA(cudaMemcpyAsync(h_w, w2.get(), m * sizeof(double), cudaMemcpyDeviceToHost, s));
+
+    int64_t t = std::min(m - FOLD_TOP, cut >= 0 ? cut : m);
+    if (m < FOLD_MIN_PARALLEL || in.threads < 2 || t < FOLD_MIN_PARALLEL / 2) t = 0;
+    int32_t *ha = staging.a.get(m), *hb = staging.b.get(m);
+    double *hw = staging.w.get(m);
+    if (t > 0) {
+        DevBuf<int32_t> parent(n, s), key(t, s), key2(t, s), rank(t, s), ga(t, s), gb(t, s), cnt(t, s),
+            uniq(t, s), nrun(1, s);
+        DevBuf<double> gw(t, s);
+        cc_init_kernel<<<grid_for(n, 256), 256, 0, s>>>(parent, n);
+        cc_hook_kernel<<<grid_for(t, 256), 256, 0, s>>>(a, b, t, parent);
+        cc_key_kernel<<<grid_for(t, 256), 256, 0, s>>>(a, t, parent, key, iota);
+        SLK_CHECK_LAUNCH();
+        sort_pairs(key.get(), key2.get(), iota.get(), rank.get(), t, s);  // stable: ranks stay increasing
+        group_gather_kernel<<<grid_for(t, 256), 256, 0, s>>>(rank, t, a, b, w2, ga, gb, gw);
+        SLK_CHECK_LAUNCH();
+        size_t tmp = 0;
+        SLK_CUDA(cub::DeviceRunLengthEncode::Encode(nullptr, tmp, key2.get(), uniq.get(), cnt.get(), nrun.get(),
+                                                    (int)t, s));
+        DevBuf<unsigned char> tb(tmp, s);
+        SLK_CUDA(cub::DeviceRunLengthEncode::Encode(tb.get(), tmp, key2.get(), uniq.get(), cnt.get(), nrun.get(),
+                                                    (int)t, s));
+        const int ng = read_scalar<int32_t>(nrun.get(), s);
+        std::vector<int32_t> hc(ng);
+        int32_t *hr = staging.rank.get(t);
+        SLK_CUDA(cudaMemcpyAsync(hc.data(), cnt.get(), ng * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+        SLK_CUDA(cudaMemcpyAsync(hr, rank.get(), t * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+        SLK_CUDA(cudaMemcpyAsync(ha, ga.get(), t * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+        SLK_CUDA(cudaMemcpyAsync(hb, gb.get(), t * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+        SLK_CUDA(cudaMemcpyAsync(hw, gw.get(), t * sizeof(double), cudaMemcpyDeviceToHost, s));
+        SLK_CUDA(cudaStreamSynchronize(s));
+        staging.off.assign(ng + 1, 0);
+        for (int g = 0; g < ng; g++) staging.off[g + 1] = staging.off[g] + hc[g];
+        in.rank = hr;
+        in.off = staging.off.data();
+        in.ngroups = ng;
+    }
+    SLK_CUDA(cudaMemcpyAsync(ha + t, a.get() + t, (m - t) * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    SLK_CUDA(cudaMemcpyAsync(hb + t, b.get() + t, (m - t) * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    SLK_CUDA(cudaMemcpyAsync(hw + t, w2.get() + t, (m - t) * sizeof(double), cudaMemcpyDeviceToHost, s));
     SLK_CUDA(cudaStreamSynchronize(s));
+    in.a = ha;
+    in.b = hb;
+    in.w = hw;
+    in.t = t;
+    return in;
 }
 
 // linkage.py:184-213

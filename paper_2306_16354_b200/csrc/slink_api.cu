@@ -255,13 +255,11 @@ void single_linkage_device(const float *x32, const double *x64, int64_t n, int d
     SLK_CUDA(cudaStreamSynchronize(s));
     double t3 = now_ms();
     // --- dendrogram (linkage.py:295-300)
-    std::vector<int32_t> ha(n - 1), hb(n - 1);
-    std::vector<double> hw(n - 1);
     trace_mark("dendrogram start");
-    dendrogram_device_sort(ts, td, tw, n, metric == 0, ha.data(), hb.data(), hw.data(), s);
+    const FoldInput fin = dendrogram_device_sort(ts, td, tw, n, metric == 0, (n - 1) - (n_clusters - 1), s);
     trace_mark("dendrogram sorted (host)");
     double extract_ms = 0.0;
-    dendrogram_fold(ha.data(), hb.data(), hw.data(), n, h_merges, n_clusters, h_labels, &extract_ms);
+    dendrogram_fold(fin, h_merges, n_clusters, h_labels, &extract_ms);
     trace_mark("dendrogram folded");
     double t5 = now_ms();
     double t4 = t5 - extract_ms;  // the cut is taken inside the fold
@@ -442,10 +440,8 @@ int slk_build_dendrogram(const int32_t *d_src, const int32_t *d_dst, const doubl
     STREAM(s);
     return guarded([&] {
         if (n < 2) throw_invalid("dendrogram needs at least 2 points");
-        std::vector<int32_t> ha(n - 1), hb(n - 1);
-        std::vector<double> hw(n - 1);
-        dendrogram_device_sort(d_src, d_dst, d_w, n, false, ha.data(), hb.data(), hw.data(), s);
-        dendrogram_fold(ha.data(), hb.data(), hw.data(), n, h_merges);
+        const FoldInput in = dendrogram_device_sort(d_src, d_dst, d_w, n, false, -1, s);
+        dendrogram_fold(in, h_merges);
     });
 }
 

@@ -311,3 +311,22 @@ def test_single_linkage_large_d_matches_oracle(slk, oracle):
     assert np.array_equal(res.tree.src, ref["tree_src"]) and np.array_equal(res.tree.weight, ref["tree_w"])
     assert np.array_equal(res.dendrogram.merges, ref["merges"])
     assert np.array_equal(res.labels.labels, ref["labels"])
+
+
+@pytest.mark.parametrize("n_clusters", [1, 30, 5000])
+def test_parallel_fold_matches_sequential(slk, monkeypatch, n_clusters):
+    """Large trees fold their first merges per forest component on several
+    host threads (dendro.cu grouping + fold.cu); the merge table and the cut
+    must equal the single-threaded in-order fold bit for bit."""
+    from paper_2306_16354_b200.synthetic import make_blobs
+
+    x = make_blobs(np.random.default_rng(3), 300_000, 8, 30).astype(np.float32)
+    cfg = slk.LinkageConfig(n_clusters=n_clusters, k=5)
+    monkeypatch.setenv("SLK_FOLD_THREADS", "1")
+    seq = slk.single_linkage_result(x, cfg)
+    monkeypatch.setenv("SLK_FOLD_THREADS", "8")
+    par = slk.single_linkage_result(x, cfg)
+    assert np.array_equal(seq.dendrogram.merges, par.dendrogram.merges)
+    assert np.array_equal(seq.labels.labels, par.labels.labels)
+    d = slk.build_dendrogram(par.tree, len(x))  # standalone entry (no cut), squared weights
+    assert d.merges.shape == (len(x) - 1, 4)
