@@ -257,6 +257,31 @@ def make_roofline(prof, steps, d, sm_mhz):
     }
 
 
+def make_graph_roofline(prof, steps):
+    """HBM roofline of the graph phase ("MST GB/s" in the metric): the Boruvka
+    round loop of every spanning-forest solve in the step (k-NN graph forest +
+    one per connect iteration).  achieved = algorithmic bytes (SURVEY §8d:
+    12 B per directed edge entry + 16 B per vertex, per round) / the loop's
+    CUDA-event time; peak = measured HBM copy bandwidth."""
+    steps = max(steps, 1)
+    peaks, peak_src = measured_peaks()
+    ms, nbytes = prof.get("mst_ms", 0.0), prof.get("mst_bytes", 0.0)
+    if not ms:
+        return None
+    achieved = nbytes / (ms / 1e3) / 1e9
+    peak = float(peaks["hbm_gbs"])
+    return {
+        "kernel": "Boruvka rounds (graph.cu: min_edge / hook / jump / relabel / compact)",
+        "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+        "traffic": None,
+        "algorithmic_bytes_per_step": nbytes / steps,
+        "rounds_per_step": prof.get("mst_rounds", 0.0) / steps,
+        "round_loop_ms_per_step": ms / steps,
+        "forest_solve_ms_per_step": prof.get("msf_ms", 0.0) / steps,
+        "peak_note": f"peak = STREAM-style copy bandwidth, {peak_src} (MEASURED_PEAKS.json)",
+    }
+
+
 def run_gpu(args, c, cfg_name):
     import torch
     import torch.distributed as dist
@@ -369,6 +394,7 @@ def run_gpu(args, c, cfg_name):
         "stage_ms_by_step": step_stages,
         "gpu_launches": int(launches),
         "roofline": roofline,
+        "graph_roofline": make_graph_roofline(prof, args.steps),
         "cpu_baseline": cpu,
         "clocks": clocks,
     }

@@ -209,8 +209,11 @@ int slk_last_scan_stats(int64_t *stats);
  * milliseconds, [7] FLOP of the tiles actually computed (2*128*128*d each),
  * [8] tiles a brute-force scan would compute, [9] tensor-core scan kernel
  * milliseconds, [10] FLOP of the tiles it computed, [11] rows it could not
- * certify.  reset != 0 zeroes the counters after reading.  out must hold 12
- * doubles. */
+ * certify, [12] Boruvka round-loop milliseconds (spanning-forest solves),
+ * [13] its algorithmic bytes (12 B per directed edge entry + 16 B per vertex
+ * per round), [14] rounds, [15] milliseconds of the whole forest
+ * solves (incl. weight alteration and sorts).  reset != 0 zeroes the
+ * counters after reading.  out must hold 16 doubles. */
 int slk_profile(double *out, int reset);
 
 #ifdef __cplusplus

@@ -154,11 +154,11 @@ def scan_stats() -> dict:
 
 def profile(reset: bool = False) -> dict:
     """Cumulative scan-kernel profile (CUDA-event timed inside the library)."""
-    buf = (ctypes.c_double * 12)()
+    buf = (ctypes.c_double * 16)()
     load().slk_profile(buf, int(reset))
     keys = ("scan_ms", "scan_launches", "scan_flops", "scan_tiles", "refine_ms", "rescan_rows",
             "order_ms", "scan_flops_done", "scan_tiles_total", "tc_ms", "tc_flops_done",
-            "tc_uncertified")
+            "tc_uncertified", "mst_ms", "mst_bytes", "mst_rounds", "msf_ms")
     return dict(zip(keys, list(buf)))
 
 

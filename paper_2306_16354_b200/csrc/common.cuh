@@ -141,6 +141,10 @@ struct Profile {
     double scan_ms = 0, scan_launches = 0, scan_flops = 0, scan_tiles = 0, refine_ms = 0,
            rescan_rows = 0, order_ms = 0, scan_flops_done = 0, scan_tiles_total = 0, tc_ms = 0,
            tc_flops_done = 0, tc_uncertified = 0;
+    // graph phase (graph.cu:msf_undirected): Boruvka round loop time, its
+    // algorithmic bytes (12 B per directed entry + 16 B per vertex
+    // per round), rounds, and the whole forest solve incl. its sorts
+    double mst_ms = 0, mst_bytes = 0, mst_rounds = 0, msf_ms = 0;
 };
 Profile &profile();
 

@@ -273,8 +273,12 @@ __global__ void split_keys_kernel(const uint64_t *keys, int64_t m, int32_t *a, i
 
 __global__ void min_member_kernel(int64_t n, const int32_t *color, int32_t *minv, int *roots) {
     GRID_LOOP(v, n) {
-        atomicMin(&minv[color[v]], (int32_t)v);
-        if (color[v] == v) atomicAdd(roots, 1);
+        // a component's vertices all hit one word: one atomic per run of
+        // equal colours in the warp, from its lowest lane (smallest id)
+        const int32_t c = color[v];
+        const unsigned peers = __match_any_sync(__activemask(), c);
+        if ((int)(threadIdx.x & 31) == __ffs(peers) - 1 && minv[c] > (int32_t)v) atomicMin(&minv[c], (int32_t)v);
+        if (c == v) atomicAdd(roots, 1);
     }
 }
 
@@ -505,6 +509,8 @@ void msf_undirected(int64_t n, const int32_t *a_in, const int32_t *b_in, const d
                     int32_t *out_dst, double *out_w, int32_t *colors_out, int64_t *n_edges,
                     int64_t *n_components, cudaStream_t s) {
     if (n <= 0) throw_invalid("empty graph: no vertices");
+    EventPair ev_all, ev_rounds;
+    ev_all.start(s);
     validate_weights(w_in, m, true, s);
     const int32_t *a = a_in, *b = b_in;
     const double *w = w_in;
@@ -562,7 +568,12 @@ void msf_undirected(int64_t n, const int32_t *a_in, const int32_t *b_in, const d
         LAUNCH(iota_kernel, m, (int32_t *)er.get(), m);
         SLK_CUDA(cudaMemsetAsync(accepted.get(), 0, m, s));
         int64_t active = m;
+        double mst_bytes = 0.0;
+        int rounds = 0;
+        ev_rounds.start(s);
         for (int round = 0; round < 64 && active > 0; round++) {
+            mst_bytes += 12.0 * 2.0 * (double)active + 16.0 * (double)n;  // directed entries = 2 x undirected
+            rounds++;
             LAUNCH(fill_u32_kernel, n, best.get(), n, NONE32);
             LAUNCH(min_edge_kernel, active, ea.get(), eb.get(), er.get(), active, color.get(), best.get());
             SLK_CUDA(cudaMemsetAsync(any.get(), 0, sizeof(int), s));
@@ -585,6 +596,10 @@ void msf_undirected(int64_t n, const int32_t *a_in, const int32_t *b_in, const d
             std::swap(er, er2);
             active = next;
         }
+        ev_rounds.stop(s);
+        profile().mst_ms += ev_rounds.ms();
+        profile().mst_bytes += mst_bytes;
+        profile().mst_rounds += rounds;
         // --- accepted edges, sorted by (a, b) with original weights
         LAUNCH(u8_to_i32_kernel, m, accepted.get(), m, flag.get());
         exclusive_sum(flag.get(), pos.get(), m, s);
@@ -612,6 +627,8 @@ void msf_undirected(int64_t n, const int32_t *a_in, const int32_t *b_in, const d
                        (long long)accepted_count, (long long)n, (long long)ncomp);
     *n_edges = accepted_count;
     *n_components = ncomp;
+    ev_all.stop(s);
+    profile().msf_ms += ev_all.ms();
 }
 
 // ------------------------------------------------------- C-ABI helpers

@@ -991,6 +991,59 @@ bool pairs_are_tight(const PointSet &Q, int64_t qb0, int64_t nqb, const QueryGro
 }
 
 // Visit order of every query group against X (colour mode iff xcolor).
+// Per query group: its nsb superblocks by (centroid distance, id), one CTA
+// per group, bitonic sort of packed 64-bit (key bits, id) in shared memory
+// (keys are non-negative or +inf, so their bit patterns order like the
+// floats).  Same order as a stable sort of the id-ordered segment.
+template <int CAP>
+__global__ void __launch_bounds__(256) segment_sort_kernel(const float *__restrict__ key,
+                                                           const int32_t *__restrict__ ids, int64_t nsb,
+                                                           float *__restrict__ skey, int32_t *__restrict__ order) {
+    __shared__ unsigned long long v[CAP];
+    const int64_t base = (int64_t)blockIdx.x * nsb;
+    for (int i = threadIdx.x; i < CAP; i += blockDim.x)
+        v[i] = i < nsb ? ((unsigned long long)__float_as_uint(key[base + i]) << 32) | (uint32_t)ids[base + i]
+                       : ~0ull;
+    __syncthreads();
+    for (int k = 2; k <= CAP; k <<= 1)
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int i = threadIdx.x; i < CAP; i += blockDim.x) {
+                const int l = i ^ j;
+                if (l > i) {
+                    const unsigned long long a = v[i], b = v[l];
+                    if ((a > b) == ((i & k) == 0)) {
+                        v[i] = b;
+                        v[l] = a;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    for (int i = threadIdx.x; i < nsb; i += blockDim.x) {
+        skey[base + i] = __uint_as_float((uint32_t)(v[i] >> 32));
+        order[base + i] = (int32_t)(uint32_t)v[i];
+    }
+}
+
+void sort_segments(const float *key, const int32_t *ids, int64_t nseg, int64_t nsb, const int32_t *seg,
+                   float *skey, int32_t *order, cudaStream_t s) {
+    const unsigned g = (unsigned)nseg;
+    if (nsb <= 256) segment_sort_kernel<256><<<g, 256, 0, s>>>(key, ids, nsb, skey, order);
+    else if (nsb <= 1024) segment_sort_kernel<1024><<<g, 256, 0, s>>>(key, ids, nsb, skey, order);
+    else if (nsb <= 4096) segment_sort_kernel<4096><<<g, 256, 0, s>>>(key, ids, nsb, skey, order);
+    else {
+        const int64_t total = nseg * nsb;
+        size_t tmp = 0;
+        SLK_CUDA(cub::DeviceSegmentedRadixSort::SortPairs(nullptr, tmp, key, skey, ids, order, (int)total,
+                                                          (int)nseg, seg, seg + 1, 0, 32, s));
+        DevBuf<unsigned char> t(tmp, s);
+        SLK_CUDA(cub::DeviceSegmentedRadixSort::SortPairs(t.get(), tmp, key, skey, ids, order, (int)total,
+                                                          (int)nseg, seg, seg + 1, 0, 32, s));
+        return;
+    }
+    SLK_CHECK_LAUNCH();
+}
+
 VisitOrder visit_order(const QueryGroups &G, const PointSet &X, int d, const int32_t *xcolor, cudaStream_t s) {
     const int64_t nqb = G.ng, qb0 = 0;
     const int64_t nxb = X.nb, nsb = X.nsb, stotal = nqb * nsb;
@@ -1013,14 +1066,7 @@ VisitOrder visit_order(const QueryGroups &G, const PointSet &X, int d, const int
         srange.get(), key, sblb_id, ids, seg);
     SLK_CHECK_LAUNCH();
     V.sb_order.alloc(stotal, s);
-    size_t tmp = 0;
-    SLK_CUDA(cub::DeviceSegmentedRadixSort::SortPairs(nullptr, tmp, key.get(), skey.get(), ids.get(),
-                                                      V.sb_order.get(), (int)stotal, (int)nqb, seg.get(),
-                                                      seg.get() + 1, 0, 32, s));
-    DevBuf<unsigned char> t(tmp, s);
-    SLK_CUDA(cub::DeviceSegmentedRadixSort::SortPairs(t.get(), tmp, key.get(), skey.get(), ids.get(),
-                                                      V.sb_order.get(), (int)stotal, (int)nqb, seg.get(),
-                                                      seg.get() + 1, 0, 32, s));
+    sort_segments(key, ids, nqb, nsb, seg, skey, V.sb_order, s);
     DevBuf<float> blk_lb(nqb * nxb, s);
     pair_lb_kernel<<<dim3((unsigned)((nxb + 31) / 32), (unsigned)((nqb + 31) / 32)), 256, 0, s>>>(
         G.cent, G.rad, G.ng, X.centroid, X.radius, nxb, d, qb0, nqb, qrange, xrange.get(), blk_lb);

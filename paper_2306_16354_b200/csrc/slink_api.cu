@@ -312,6 +312,10 @@ int slk_profile(double *out, int reset) {
     out[9] = g_profile.tc_ms;
     out[10] = g_profile.tc_flops_done;
     out[11] = g_profile.tc_uncertified;
+    out[12] = g_profile.mst_ms;
+    out[13] = g_profile.mst_bytes;
+    out[14] = g_profile.mst_rounds;
+    out[15] = g_profile.msf_ms;
     if (reset) g_profile = Profile{};
     return SLK_OK;
 }
