@@ -234,8 +234,29 @@ __global__ void jump_kernel(int64_t n, const int32_t *color, int32_t *parent) {
     }
 }
 
-__global__ void relabel_kernel(int64_t n, int32_t *color, const int32_t *parent) {
-    GRID_LOOP(v, n) color[v] = parent[color[v]];
+// also clears every vertex's best edge for the next round (nothing reads
+// best after the hooks)
+__global__ void relabel_kernel(int64_t n, int32_t *color, const int32_t *parent, uint32_t *best) {
+    GRID_LOOP(v, n) {
+        color[v] = parent[color[v]];
+        best[v] = NONE32;
+    }
+}
+
+// edges still crossing colours after the round, in order (flag / pos from
+// cross_flag_kernel and an exclusive scan)
+__global__ void compact_edges_kernel(const int32_t *ea, const int32_t *eb, const uint32_t *er, const int32_t *flag,
+                                     const int32_t *pos, int64_t m, int32_t *oa, int32_t *ob, uint32_t *orank) {
+    GRID_LOOP(e, m) if (flag[e]) {
+        const int32_t p = pos[e];
+        oa[p] = ea[e];
+        ob[p] = eb[e];
+        orank[p] = er[e];
+    }
+}
+
+__global__ void scan_total_kernel(const int32_t *pos, const int32_t *flag, int64_t m, int64_t *out) {
+    *out = (int64_t)pos[m - 1] + flag[m - 1];
 }
 
 __global__ void cross_flag_kernel(const int32_t *ea, const int32_t *eb, int64_t m,
@@ -571,26 +592,27 @@ void msf_undirected(int64_t n, const int32_t *a_in, const int32_t *b_in, const d
         double mst_bytes = 0.0;
         int rounds = 0;
         ev_rounds.start(s);
+        DevBuf<int64_t> total(1, s);
+        LAUNCH(fill_u32_kernel, n, best.get(), n, NONE32);
+        SLK_CUDA(cudaMemsetAsync(any.get(), 0, sizeof(int), s));
+        // while edges cross colours, every component that has one hooks (so
+        // there is no separate "any hook" check); one host read per round
         for (int round = 0; round < 64 && active > 0; round++) {
             mst_bytes += 12.0 * 2.0 * (double)active + 16.0 * (double)n;  // directed entries = 2 x undirected
             rounds++;
-            LAUNCH(fill_u32_kernel, n, best.get(), n, NONE32);
             LAUNCH(min_edge_kernel, active, ea.get(), eb.get(), er.get(), active, color.get(), best.get());
-            SLK_CUDA(cudaMemsetAsync(any.get(), 0, sizeof(int), s));
             LAUNCH(hook_kernel, n, n, color.get(), best.get(), ra.get(), rb.get(), parent.get(),
                    accepted.get(), any.get());
-            if (!read_scalar(any.get(), s)) break;
             LAUNCH(break_cycles_kernel, n, n, color.get(), parent.get());
             LAUNCH(jump_kernel, n, n, color.get(), parent.get());
-            LAUNCH(relabel_kernel, n, n, color.get(), parent.get());
+            LAUNCH(relabel_kernel, n, n, color.get(), parent.get(), best.get());
             // keep only edges that still cross colours
             LAUNCH(cross_flag_kernel, active, ea.get(), eb.get(), active, color.get(), flag.get());
             exclusive_sum(flag.get(), pos.get(), active, s);
-            int64_t next = (int64_t)read_scalar(pos.get() + active - 1, s) +
-                           read_scalar(flag.get() + active - 1, s);
-            LAUNCH(compact_kernel<int32_t>, active, ea.get(), flag.get(), pos.get(), active, ea2.get());
-            LAUNCH(compact_kernel<int32_t>, active, eb.get(), flag.get(), pos.get(), active, eb2.get());
-            LAUNCH(compact_kernel<uint32_t>, active, er.get(), flag.get(), pos.get(), active, er2.get());
+            scan_total_kernel<<<1, 1, 0, s>>>(pos.get(), flag.get(), active, total.get());
+            LAUNCH(compact_edges_kernel, active, ea.get(), eb.get(), er.get(), flag.get(), pos.get(), active,
+                   ea2.get(), eb2.get(), er2.get());
+            const int64_t next = read_scalar(total.get(), s);
             std::swap(ea, ea2);
             std::swap(eb, eb2);
             std::swap(er, er2);
