@@ -431,18 +431,41 @@ __global__ void prop_apply_kernel(int64_t n, int32_t *colors, const int32_t *nex
 }
 
 // --- symmetric check
-__global__ void sym_keys_kernel(const int32_t *src, const int32_t *cols, const double *w,
-                                int64_t m, uint64_t *kf, uint64_t *kr, unsigned long long *wb) {
+// rows strictly increasing in column: then CSR order is (src, col) order and
+// there are no duplicate entries
+__global__ void rows_sorted_kernel(const int32_t *src, const int32_t *cols, int64_t m, int *unsorted) {
+    GRID_LOOP(e, m) if (e > 0 && src[e] == src[e - 1] && cols[e] <= cols[e - 1]) *unsorted = 1;
+}
+
+// strictly sorted rows: entry (i, j, w) needs (j, i, w); binary search of i in row j
+__global__ void mirror_check_kernel(const int64_t *offs, const int32_t *src, const int32_t *cols, const double *w,
+                                    int64_t m, int *diff) {
     GRID_LOOP(e, m) {
-        uint32_t s = (uint32_t)src[e], d = (uint32_t)cols[e];
-        kf[e] = ((uint64_t)s << 32) | d;
-        kr[e] = ((uint64_t)d << 32) | s;
-        wb[e] = ordered_bits(w[e]);
+        const int32_t i = src[e], j = cols[e];
+        int64_t lo = offs[j], hi = offs[j + 1];
+        while (lo < hi) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (cols[mid] < i) lo = mid + 1;
+            else hi = mid;
+        }
+        if (lo >= offs[j + 1] || cols[lo] != i || !(w[lo] == w[e])) *diff = 1;
     }
 }
-__global__ void compare_kernel(const uint64_t *a, const uint64_t *b, const unsigned long long *wa,
-                               const unsigned long long *wb, int64_t m, int *diff) {
-    GRID_LOOP(e, m) if (a[e] != b[e] || wa[e] != wb[e]) *diff = 1;
+
+// general rows: the reference's pairing (core.py:165-174): entries stably
+// ordered by (src, col) against entries stably ordered by (col, src)
+__global__ void sym_keys2_kernel(const int32_t *src, const int32_t *cols, int64_t m, uint64_t *kf, uint64_t *kr,
+                                 int32_t *iota) {
+    GRID_LOOP(e, m) {
+        const uint32_t a = (uint32_t)src[e], b = (uint32_t)cols[e];
+        kf[e] = ((uint64_t)a << 32) | b;
+        kr[e] = ((uint64_t)b << 32) | a;
+        iota[e] = (int32_t)e;
+    }
+}
+__global__ void sym_compare_kernel(const uint64_t *kf, const uint64_t *kr, const int32_t *pf, const int32_t *pr,
+                                   const double *w, int64_t m, int *diff) {
+    GRID_LOOP(p, m) if (kf[p] != kr[p] || !(w[pf[p]] == w[pr[p]])) *diff = 1;
 }
 
 __global__ void lt_flag_kernel(const int32_t *src, const int32_t *cols, int64_t m, int32_t *flag) {
@@ -674,26 +697,39 @@ void csr_row_sources(int64_t n, const int64_t *offs, int32_t *src, cudaStream_t 
     LAUNCH(row_sources_kernel, n, offs, n, src);
 }
 
+// True iff the rows are strictly increasing in column (CSR order = (src, col)
+// order, no duplicate entries); src = row of every entry.
+static bool rows_strictly_sorted(const int32_t *src, const int32_t *cols, int64_t m, cudaStream_t s) {
+    DevBuf<int> flag(1, s);
+    SLK_CUDA(cudaMemsetAsync(flag.get(), 0, sizeof(int), s));
+    LAUNCH(rows_sorted_kernel, m, src, cols, m, flag.get());
+    return read_scalar(flag.get(), s) == 0;
+}
+
+// core.py:165-174.  Strictly sorted rows (the canonical CSR edge_list_to_csr
+// builds): one binary search per entry for its mirror.  Otherwise the
+// reference's pairing of the two stable orders, by two radix sorts.
 bool csr_symmetric(int64_t n, const int64_t *offs, const int32_t *cols, const double *w,
                    cudaStream_t s) {
     int64_t m = read_scalar(offs + n, s);
     if (m == 0) return true;
     DevBuf<int32_t> src(m, s);
     csr_row_sources(n, offs, src.get(), s);
-    DevBuf<uint64_t> kf(m, s), kr(m, s), k1(m, s), k2(m, s);
-    DevBuf<unsigned long long> wb(m, s), w1(m, s), w2(m, s), wf(m, s), wr(m, s);
-    LAUNCH(sym_keys_kernel, m, src.get(), cols, w, m, kf.get(), kr.get(), wb.get());
-    // lexicographic (key, w): sort by w, then stable by key
-    sort_pairs(wb.get(), w1.get(), kf.get(), k1.get(), m, s);
-    sort_pairs(k1.get(), kf.get(), w1.get(), wf.get(), m, s);
-    sort_pairs(wb.get(), w2.get(), kr.get(), k2.get(), m, s);
-    sort_pairs(k2.get(), kr.get(), w2.get(), wr.get(), m, s);
     DevBuf<int> diff(1, s);
     SLK_CUDA(cudaMemsetAsync(diff.get(), 0, sizeof(int), s));
-    LAUNCH(compare_kernel, m, kf.get(), kr.get(), wf.get(), wr.get(), m, diff.get());
+    if (rows_strictly_sorted(src.get(), cols, m, s)) {
+        LAUNCH(mirror_check_kernel, m, offs, src.get(), cols, w, m, diff.get());
+        return read_scalar(diff.get(), s) == 0;
+    }
+    DevBuf<uint64_t> kf(m, s), kr(m, s), k1(m, s), k2(m, s);
+    DevBuf<int32_t> iota(m, s), pf(m, s), pr(m, s);
+    const int bits = 32 + bits_for(n);
+    LAUNCH(sym_keys2_kernel, m, src.get(), cols, m, kf.get(), kr.get(), iota.get());
+    sort_pairs(kf.get(), k1.get(), iota.get(), pf.get(), m, s, 0, bits);
+    sort_pairs(kr.get(), k2.get(), iota.get(), pr.get(), m, s, 0, bits);
+    LAUNCH(sym_compare_kernel, m, k1.get(), k2.get(), pf.get(), pr.get(), w, m, diff.get());
     return read_scalar(diff.get(), s) == 0;
 }
-
 void csr_validate(int64_t n, const int64_t *offs, const int32_t *cols, const double *w,
                   cudaStream_t s) {
     if (n <= 0) throw_invalid("empty graph: no vertices");
@@ -767,9 +803,10 @@ void csr_solve_mst(int64_t n, const int64_t *offs, const int32_t *cols, const do
                    int32_t *colors, int64_t *n_edges, int64_t *n_components, cudaStream_t s) {
     csr_validate(n, offs, cols, w, s);
     int64_t m = read_scalar(offs + n, s);
-    // undirected entries (src < col) in CSR order, i.e. sorted by (a, b)
+    // undirected entries (src < col) in CSR order
     DevBuf<int32_t> src(m, s), flag(m, s), pos(m, s);
     int64_t mu = 0;
+    bool presorted = true;
     DevBuf<int32_t> ua, ub;
     DevBuf<double> uw;
     if (m > 0) {
@@ -784,8 +821,10 @@ void csr_solve_mst(int64_t n, const int64_t *offs, const int32_t *cols, const do
         LAUNCH(compact_kernel<int32_t>, m, src.get(), flag.get(), pos.get(), m, ua.get());
         LAUNCH(compact_kernel<int32_t>, m, cols, flag.get(), pos.get(), m, ub.get());
         LAUNCH(compact_kernel<double>, m, w, flag.get(), pos.get(), m, uw.get());
+        // strictly sorted rows: the (src < col) entries are already in (a, b) order
+        presorted = rows_strictly_sorted(src.get(), cols, m, s);
     }
-    msf_undirected(n, ua.get(), ub.get(), uw.get(), mu, false, maximize, seed, out_src, out_dst,
+    msf_undirected(n, ua.get(), ub.get(), uw.get(), mu, presorted, maximize, seed, out_src, out_dst,
                    out_w, colors, n_edges, n_components, s);
 }
 

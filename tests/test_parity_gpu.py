@@ -330,3 +330,60 @@ def test_parallel_fold_matches_sequential(slk, monkeypatch, n_clusters):
     assert np.array_equal(seq.labels.labels, par.labels.labels)
     d = slk.build_dendrogram(par.tree, len(x))  # standalone entry (no cut), squared weights
     assert d.merges.shape == (len(x) - 1, 4)
+
+
+def _ref_is_symmetric(g):
+    """core.py:165-174 restated in numpy (stable orders, numeric weight equality)."""
+    src = np.repeat(np.arange(g.n_vertices), np.diff(g.row_offsets))
+    fwd = np.lexsort((g.col_indices, src))
+    rev = np.lexsort((src, g.col_indices))
+    return (np.array_equal(src[fwd], g.col_indices[rev]) and np.array_equal(g.col_indices[fwd], src[rev])
+            and np.array_equal(g.weights[fwd], g.weights[rev]))
+
+
+def test_csr_symmetry_check_sorted_unsorted_and_duplicates(slk):
+    """Strictly sorted rows take the binary-search mirror check, other rows
+    the reference's pairing of the two stable orders (graph.cu:csr_symmetric);
+    both must agree with core.py:165-174, duplicates included."""
+    from paper_2306_16354_b200.synthetic import random_connected_graph
+
+    rng = np.random.default_rng(8)
+    g = slk.edge_list_to_csr(slk.EdgeList(300, *random_connected_graph(rng, 300, 900)))
+    cases = [g]
+    # same graph with every row's entries shuffled (unsorted rows)
+    perm = np.concatenate([g.row_offsets[i] + rng.permutation(g.row_offsets[i + 1] - g.row_offsets[i])
+                           for i in range(g.n_vertices)])
+    cases.append(slk.CsrGraph(g.n_vertices, g.row_offsets, g.col_indices[perm], g.weights[perm]))
+    # one asymmetric weight, sorted rows
+    w = g.weights.copy()
+    w[5] += 1.0
+    cases.append(slk.CsrGraph(g.n_vertices, g.row_offsets, g.col_indices, w))
+    # duplicates: (0,1,w1),(0,1,w2) vs (1,0,w2),(1,0,w1) -- the stable orders disagree
+    cases.append(slk.CsrGraph(2, np.array([0, 2, 4]), np.array([1, 1, 0, 0]), np.array([1.0, 2.0, 2.0, 1.0])))
+    cases.append(slk.CsrGraph(2, np.array([0, 2, 4]), np.array([1, 1, 0, 0]), np.array([1.0, 2.0, 1.0, 2.0])))
+    for c in cases:
+        assert c.is_symmetric() == _ref_is_symmetric(c)
+    assert [c.is_symmetric() for c in cases] == [True, True, False, False, True]
+    # unsorted rows still give the same forest as the canonical CSR
+    a = slk.solve_mst(cases[0], seed=4)
+    b = slk.solve_mst(cases[1], seed=4)
+    assert np.array_equal(a.edges.src, b.edges.src) and np.array_equal(a.edges.weight, b.edges.weight)
+
+
+def test_road_lattice_mst_matches_oracle(slk, oracle):
+    """Road-network-shaped graph with integer weights (many ties), as in
+    scripts/bench_mst.py: the forest, its weights and the components match
+    the oracle's restatement of the reference solver."""
+    import importlib.util
+
+    spec = importlib.util.spec_from_file_location("bench_mst", Path(__file__).resolve().parents[1] / "scripts" / "bench_mst.py")
+    bm = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bm)
+    n, src, dst, wt = bm.road_graph(40_000, 49_000, seed=5)
+    g = slk.edge_list_to_csr(slk.EdgeList(n, src, dst, wt))
+    for maximize in (False, True):
+        r = slk.solve_mst(g, maximize=maximize, seed=2)
+        os_, od, ow, ocol, onc = oracle.solve_mst(n, g.row_offsets, g.col_indices, g.weights, maximize=maximize, seed=2)
+        assert r.n_components == onc
+        assert np.array_equal(r.edges.src, os_) and np.array_equal(r.edges.dst, od)
+        assert np.array_equal(r.edges.weight, ow) and np.array_equal(r.colors.colors, ocol)
