@@ -110,6 +110,26 @@ struct DevBuf {
     operator T *() const { return ptr; }
 };
 
+// Grow-only pinned host staging buffer (keep one per host thread: thread_local).
+template <class T>
+struct PinnedBuf {
+    T *p = nullptr;
+    size_t cap = 0;
+    T *get(size_t n) {
+        if (n > cap) {
+            if (p) cudaFreeHost(p);
+            p = nullptr;
+            cap = 0;
+            SLK_CUDA(cudaMallocHost((void **)&p, (n > 0 ? n : 1) * sizeof(T)));
+            cap = n;
+        }
+        return p;
+    }
+    ~PinnedBuf() {
+        if (p) cudaFreeHost(p);
+    }
+};
+
 inline int grid_for(int64_t n, int block, int64_t cap = 148 * 32) {
     int64_t g = (n + block - 1) / block;
     if (g < 1) g = 1;

@@ -114,28 +114,9 @@ __global__ void group_gather_kernel(const int32_t *rank, int64_t t, const int32_
     }
 }
 
-// grow-only pinned host staging for the fold's inputs (one set per host thread)
-template <class T>
-struct PinnedVec {
-    T *p = nullptr;
-    size_t cap = 0;
-    T *get(size_t n) {
-        if (n > cap) {
-            if (p) cudaFreeHost(p);
-            p = nullptr;
-            cap = 0;
-            SLK_CUDA(cudaMallocHost((void **)&p, std::max<size_t>(n, 1) * sizeof(T)));
-            cap = n;
-        }
-        return p;
-    }
-    ~PinnedVec() {
-        if (p) cudaFreeHost(p);
-    }
-};
 struct FoldStaging {
-    PinnedVec<int32_t> a, b, rank;
-    PinnedVec<double> w;
+    PinnedBuf<int32_t> a, b, rank;
+    PinnedBuf<double> w;
     std::vector<int64_t> off;
 };
 thread_local FoldStaging staging;

@@ -258,22 +258,29 @@ void single_linkage_device(const float *x32, const double *x64, int64_t n, int d
     trace_mark("dendrogram start");
     const FoldInput fin = dendrogram_device_sort(ts, td, tw, n, metric == 0, (n - 1) - (n_clusters - 1), s);
     trace_mark("dendrogram sorted (host)");
+    // the spanning tree goes to pinned staging on the copy engine while the
+    // host folds
+    static thread_local PinnedBuf<int32_t> st_src, st_dst;
+    static thread_local PinnedBuf<double> st_w;
+    const bool want_tree = h_tree_src || h_tree_dst || h_tree_w;
+    if (want_tree) {
+        SLK_CUDA(cudaMemcpyAsync(st_src.get(n - 1), ts.get(), (n - 1) * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+        SLK_CUDA(cudaMemcpyAsync(st_dst.get(n - 1), td.get(), (n - 1) * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+        SLK_CUDA(cudaMemcpyAsync(st_w.get(n - 1), tw.get(), (n - 1) * sizeof(double), cudaMemcpyDeviceToHost, s));
+    }
     double extract_ms = 0.0;
     dendrogram_fold(fin, h_merges, n_clusters, h_labels, &extract_ms);
     trace_mark("dendrogram folded");
     double t5 = now_ms();
     double t4 = t5 - extract_ms;  // the cut is taken inside the fold
-    if (h_tree_src || h_tree_dst || h_tree_w) {
-        std::vector<int32_t> hs(n - 1), hd(n - 1);
-        SLK_CUDA(cudaMemcpyAsync(hs.data(), ts.get(), (n - 1) * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-        SLK_CUDA(cudaMemcpyAsync(hd.data(), td.get(), (n - 1) * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-        if (h_tree_w)
-            SLK_CUDA(cudaMemcpyAsync(h_tree_w, tw.get(), (n - 1) * sizeof(double), cudaMemcpyDeviceToHost, s));
+    if (want_tree) {
         SLK_CUDA(cudaStreamSynchronize(s));
+        const int32_t *hs = st_src.p, *hd = st_dst.p;
         for (int64_t i = 0; i < n - 1; i++) {
             if (h_tree_src) h_tree_src[i] = hs[i];
             if (h_tree_dst) h_tree_dst[i] = hd[i];
         }
+        if (h_tree_w) memcpy(h_tree_w, st_w.p, (n - 1) * sizeof(double));
     }
     if (n_iters) *n_iters = iters;
     if (timings) {
