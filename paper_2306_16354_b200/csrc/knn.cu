@@ -1322,8 +1322,16 @@ int tc_pass(const PointSet &Q, const PointSet &X, const int32_t *qid, int k, int
     while (nsplit < 8 && ngroups * nsplit < 2 * num_sms()) nsplit *= 2;
     if (const char *e = getenv("SLK_TC_SPLIT")) nsplit = std::max(nsplit, std::min(8, atoi(e)));
     if (nsplit & (nsplit - 1)) nsplit = 8;
-    DevBuf<int32_t> cand(rows * 32 * nsplit, s);
-    DevBuf<float> qhat(rows, s), kth_split(rows * nsplit, s);
+    // k-NN pass: two epilogue warps per row, each with its own K' list over
+    // half of every tile's columns (tc_scan.cu HS = 2); the refine unites at
+    // most 8 lists per row
+    int hs = (mode == MODE_SELF && qbn == 1 && tc::halves_supported(d, kp)) ? 2 : 1;
+    if (hs == 2)
+        while (nsplit > 1 && nsplit * hs > 8) nsplit /= 2;
+    if (nsplit * hs > 8) hs = 1;
+    const int nlists = nsplit * hs;
+    DevBuf<int32_t> cand(rows * 32 * nlists, s);
+    DevBuf<float> qhat(rows, s), kth_split(rows * nlists, s);
     DevBuf<unsigned long long> tiles(1, s);
     DevBuf<int> counters(1, s);
     kth.alloc(rows, s);
@@ -1348,13 +1356,14 @@ int tc_pass(const PointSet &Q, const PointSet &X, const int32_t *qid, int k, int
                   cand, kth_split, qhat, q0, q1,
                   V.sb_order, V.sb_lb, V.flat_lb, V.nvalid, X.nsb, tiles, qid, nsplit};
     ev_scan.start(s);
-    tc::launch(mode, kp, qbn, ta, ngroups, s);
+    if (hs == 2) tc::launch_halves(kp, ta, ngroups, s);
+    else tc::launch(mode, kp, qbn, ta, ngroups, s);
     ev_scan.stop(s);
     RefineArgs ra{Q.x32, Q.x64, Q.norms, X.x32, X.x64, X.norms, d, k, nq, nx, q0, q1,
-                  cand, kth_split, nsplit, kth, X.maxn, X.x64 == nullptr && Q.x64 == nullptr, out_idx,
+                  cand, kth_split, nlists, kth, X.maxn, X.x64 == nullptr && Q.x64 == nullptr, out_idx,
                   out_dist, fail, counters, qhat, (double)scale, qid};
     ev_refine.start(s);
-    switch (nsplit) {
+    switch (nlists) {
         case 1: launch_refine<1>(ra, rows, s); break;
         case 2: launch_refine<2>(ra, rows, s); break;
         case 4: launch_refine<4>(ra, rows, s); break;
@@ -1371,8 +1380,8 @@ int tc_pass(const PointSet &Q, const PointSet &X, const int32_t *qid, int k, int
     record_profile(ev_order, ev_scan, ev_refine, rows, nx, d, done, (qb1 - qb0) * X.nb, true);
     const int nfail = read_scalar<int>(counters, s);
     if (trace_on())
-        fprintf(stderr, "[slk] tc_pass mode %d rows %lld (x%d blocks/CTA, split %d): order %.2f scan %.2f refine %.2f ms, tiles %llu, uncertified %d\n",
-                mode, (long long)rows, qbn, nsplit, ev_order.ms(), ev_scan.ms(), ev_refine.ms(), done, nfail);
+        fprintf(stderr, "[slk] tc_pass mode %d rows %lld (x%d blocks/CTA, split %d, halves %d): order %.2f scan %.2f refine %.2f ms, tiles %llu, uncertified %d\n",
+                mode, (long long)rows, qbn, nsplit, hs, ev_order.ms(), ev_scan.ms(), ev_refine.ms(), done, nfail);
     st.rows_uncertified += nfail;
     profile().tc_uncertified += nfail;
     return nfail;

@@ -250,7 +250,7 @@ constexpr uint32_t A_COL = 256;
 
 // aug: the norm rides in the augmented K step (no |x~|^2 array); kc > 0: the
 // chunked large-d layout (A = lo term only, B stages of kc dims)
-__host__ __device__ inline Plan make_plan(int dk, bool aug, int qb, int kc = 0) {
+__host__ __device__ inline Plan make_plan(int dk, bool aug, int qb, int kc = 0, int ew = 0) {
     Plan p{};
     uint32_t off = 0;
     auto take = [&](uint32_t bytes, uint32_t align) {
@@ -266,7 +266,7 @@ __host__ __device__ inline Plan make_plan(int dk, bool aug, int qb, int kc = 0) 
     p.xcol = take(NMETA * BN * 4, 16);
     p.qq = take(qb * BM * 4, 16);
     p.cq = take(dk * 4, 16);
-    p.stg = take(qb * BM * STG_STRIDE * 4, 16);
+    p.stg = take((ew > 0 ? ew : qb) * BM * STG_STRIDE * 4, 16);
     p.misc = take(128, 16);
     p.bars = take(8 * (4 * MAX_NB + 2 * NTMAX + 1), 8);
     off = (off + 1023) / 1024 * 1024;
@@ -408,15 +408,21 @@ __device__ __forceinline__ float convert_query_ck(const float *qblk, unsigned ch
 
 // CK: chunked large-d variant (QB = 1, no augmented step): every index block
 // arrives as dk / KC stages of KC dims that accumulate into one TMEM stage.
-template <int MODE, int KP, bool AUG, int QB, bool CK>
-__global__ void __launch_bounds__(Cfg<QB>::NTHREADS, 1) tc_scan_kernel(TcArgs a) {
+// HS = 2 (QB = 1): two epilogue warps per TMEM lane quarter, each keeping its
+// own K' list over one half of every tile's columns (written out as two
+// splits that the refine unites, like nsplit): twice the epilogue warps to
+// hide the insertion latency of the k-NN pass.
+template <int MODE, int KP, bool AUG, int QB, bool CK, int HS = 1>
+__global__ void __launch_bounds__(Cfg<QB * HS>::NTHREADS, 1) tc_scan_kernel(TcArgs a) {
     extern __shared__ __align__(1024) unsigned char smem[];
     static_assert(!CK || (QB == 1 && !AUG), "chunked kernel: single query block, norms via smem");
-    constexpr int NTHREADS = Cfg<QB>::NTHREADS, NT = CK ? 2 : Cfg<QB>::NT;
+    static_assert(HS == 1 || QB == 1, "column halves only with one query block per CTA");
+    constexpr int EW = QB * HS;  // epilogue warp groups (of 4)
+    constexpr int NTHREADS = Cfg<EW>::NTHREADS, NT = CK ? 2 : Cfg<QB>::NT;
     const int dk = a.dk;
     const int kc = CK ? KC : dk;  // dims per B stage
     const int nck = dk / kc;      // stages per index block
-    const Plan P = make_plan(dk, AUG, QB, CK ? KC : 0);
+    const Plan P = make_plan(dk, AUG, QB, CK ? KC : 0, EW);
     float *s_xx = reinterpret_cast<float *>(smem + P.xx);  // !AUG: |x~|^2 per meta slot
     const int nb = P.nb;
     unsigned char *sA = smem + P.a;
@@ -455,13 +461,13 @@ __global__ void __launch_bounds__(Cfg<QB>::NTHREADS, 1) tc_scan_kernel(TcArgs a)
         }
         for (int s = 0; s < NT; s++) {
             mbar_init(&tfull[s], 1);
-            mbar_init(&tempty[s], 128 * QB);
+            mbar_init(&tempty[s], 128 * EW);
         }
         mbar_init(afull, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         for (int i = 0; i < 8; i++) misc->part[i] = INFINITY;
     }
-    if (warp == Cfg<QB>::WARP_MMA) {
+    if (warp == Cfg<EW>::WARP_MMA) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                          smem_u32(&misc->tmem_base)),
                      "r"(TMEM_COLS)
@@ -484,7 +490,7 @@ __global__ void __launch_bounds__(Cfg<QB>::NTHREADS, 1) tc_scan_kernel(TcArgs a)
     tc_fence_after();
     const uint32_t tmem = misc->tmem_base;
 
-    if (warp == Cfg<QB>::WARP_PROD) {
+    if (warp == Cfg<EW>::WARP_PROD) {
         // ===================== producer: visit order + bulk copies
         if (lane == 0 && !CK) {
             mbar_expect_tx(afull, stage_bytes * nqa);
@@ -498,7 +504,7 @@ __global__ void __launch_bounds__(Cfg<QB>::NTHREADS, 1) tc_scan_kernel(TcArgs a)
         for (int it = 0;; it++) {
             volatile float *part = misc->part;
             float thr = fmaxf(fmaxf(part[0], part[1]), fmaxf(part[2], part[3]));
-            if (QB == 2) thr = fmaxf(thr, fmaxf(fmaxf(part[4], part[5]), fmaxf(part[6], part[7])));
+            if (EW == 2) thr = fmaxf(thr, fmaxf(fmaxf(part[4], part[5]), fmaxf(part[6], part[7])));
             thr *= a.inv_scale2;
             // the visitor's control flow must be warp-uniform: lane 0 (which ran
             // ahead into the barrier wait below) may have read newer thresholds
@@ -580,7 +586,7 @@ __global__ void __launch_bounds__(Cfg<QB>::NTHREADS, 1) tc_scan_kernel(TcArgs a)
             }
             if (end) break;
         }
-    } else if (warp == Cfg<QB>::WARP_MMA) {
+    } else if (warp == Cfg<EW>::WARP_MMA) {
         // ===================== MMA issuer (one elected thread)
         if (lane == 0) {
             const uint32_t a_base = smem_u32(sA), b_base = smem_u32(sB);
@@ -656,9 +662,11 @@ __global__ void __launch_bounds__(Cfg<QB>::NTHREADS, 1) tc_scan_kernel(TcArgs a)
     } else if (warp >= 4) {
         // ===================== epilogue warps: one query row per thread
         const int ew = (warp - 4) & 3;   // TMEM lane quarter
-        const int grp = (warp - 4) >> 2;  // query block of the group
+        const int grp = (warp - 4) >> 2;  // epilogue group: query block of the group, or column half (HS = 2)
+        const int qbi = HS == 2 ? 0 : grp;
+        const int half = HS == 2 ? grp : 0;
         const int row = ew * 32 + lane;
-        const int64_t gi = (qb + grp) * BM + row;
+        const int64_t gi = (qb + qbi) * BM + row;
         // qid (gathered queries): id of the row in the index, -1 for padding
         const int64_t self_id = (gi < a.nq && a.qid) ? (int64_t)a.qid[gi] : gi;
         const bool row_ok = gi < a.nq && self_id >= 0;
@@ -685,7 +693,7 @@ __global__ void __launch_bounds__(Cfg<QB>::NTHREADS, 1) tc_scan_kernel(TcArgs a)
             mbar_wait(&tfull[ts], tph, 6, it);
             tc_fence_after();
             // the convert warps wrote A (and |q~|^2) before their first bfull arrive
-            if (it == 0) qq = s_qq[grp * BM + row];
+            if (it == 0) qq = s_qq[qbi * BM + row];
             const int slot = it % NMETA;
             const int jb = misc->meta_blk[slot];
 #ifdef SLK_WATCHDOG
@@ -693,7 +701,7 @@ __global__ void __launch_bounds__(Cfg<QB>::NTHREADS, 1) tc_scan_kernel(TcArgs a)
 #endif
             if (jb < 0) break;
             const int64_t col0 = (int64_t)jb * BN;
-            const uint32_t taddr = tmem + ((uint32_t)(ew * 32) << 16) + (uint32_t)(ts * QB + grp) * 128;
+            const uint32_t taddr = tmem + ((uint32_t)(ew * 32) << 16) + (uint32_t)(ts * QB + qbi) * 128;
             // columns this row may take from this block: inside the index, not itself
             const int64_t rem = a.nx - col0;
             const int col_limit = row_ok ? (rem < BN ? (int)rem : BN) : 0;
@@ -701,7 +709,7 @@ __global__ void __launch_bounds__(Cfg<QB>::NTHREADS, 1) tc_scan_kernel(TcArgs a)
                 (MODE == MODE_SELF && self_id >= col0 && self_id < col0 + BN) ? (int)(self_id - col0) : -1;
             const int *xcs = s_xcol + slot * BN;
 #pragma unroll 1
-            for (int c0 = 0; c0 < BN; c0 += CH) {
+            for (int c0 = half * (BN / HS); c0 < (half + 1) * (BN / HS); c0 += CH) {
                 float dot[CH];
                 __syncwarp();  // tcgen05.ld is .sync.aligned: reconverge after the insertion loop
                 tmem_ld(taddr + c0, dot);
@@ -791,7 +799,7 @@ __global__ void __launch_bounds__(Cfg<QB>::NTHREADS, 1) tc_scan_kernel(TcArgs a)
         }
         // write this row's candidate list (slots >= KP hold -1)
         if (gi >= a.row0 && gi < a.row1 && row_ok) {
-            const int64_t slot = (gi - a.row0) * a.nsplit + split;
+            const int64_t slot = ((gi - a.row0) * a.nsplit + split) * HS + half;
             int32_t *dst = a.cand + slot * 32;
 #pragma unroll
             for (int q = 0; q < 32; q++) dst[q] = q < KP ? li[q < KP ? q : 0] : -1;
@@ -816,19 +824,19 @@ __global__ void __launch_bounds__(Cfg<QB>::NTHREADS, 1) tc_scan_kernel(TcArgs a)
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
-    if (warp == Cfg<QB>::WARP_MMA) {
+    if (warp == Cfg<EW>::WARP_MMA) {
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS)
                      : "memory");
     }
 }
 
-template <int MODE, int KP, bool AUG, int QB, bool CK>
+template <int MODE, int KP, bool AUG, int QB, bool CK, int HS = 1>
 void launch_mode(const TcArgs &args, int64_t ngroups, cudaStream_t s) {
-    const Plan P = make_plan(args.dk, AUG, QB, CK ? KC : 0);
-    SLK_CUDA(cudaFuncSetAttribute(tc_scan_kernel<MODE, KP, AUG, QB, CK>,
+    const Plan P = make_plan(args.dk, AUG, QB, CK ? KC : 0, QB * HS);
+    SLK_CUDA(cudaFuncSetAttribute(tc_scan_kernel<MODE, KP, AUG, QB, CK, HS>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P.total));
-    tc_scan_kernel<MODE, KP, AUG, QB, CK>
-        <<<(unsigned)(ngroups * args.nsplit), Cfg<QB>::NTHREADS, P.total, s>>>(args);
+    tc_scan_kernel<MODE, KP, AUG, QB, CK, HS>
+        <<<(unsigned)(ngroups * args.nsplit), Cfg<QB * HS>::NTHREADS, P.total, s>>>(args);
     SLK_CHECK_LAUNCH();
 }
 
@@ -848,6 +856,13 @@ void launch_ck(int mode, int kp, const TcArgs &args, int64_t ngroups, cudaStream
     else if (kp <= 8) launch_kp<8, false, 1, true>(mode, args, ngroups, s);
     else if (kp <= 16) launch_kp<16, false, 1, true>(mode, args, ngroups, s);
     else launch_kp<32, false, 1, true>(mode, args, ngroups, s);
+}
+
+// the k-NN pass with column halves (HS = 2)
+template <bool AUG>
+void launch_halves_t(int kp, const TcArgs &args, int64_t ngroups, cudaStream_t s) {
+    if (kp <= 8) launch_mode<MODE_SELF, 8, AUG, 1, false, 2>(args, ngroups, s);
+    else launch_mode<MODE_SELF, 16, AUG, 1, false, 2>(args, ngroups, s);
 }
 
 template <bool AUG>
@@ -907,6 +922,21 @@ int group_blocks(int d, int kp) {
     const char *e = getenv("SLK_TC_QB");
     if ((e && atoi(e) == 1) || kp > 16 || chunked(d)) return 1;
     return make_plan(k_extent(d), use_aug(d), 2).nb >= 2 ? 2 : 1;
+}
+
+// k-NN pass (MODE_SELF) with two column-half lists per row: K' <= 16, the
+// whole-block kernel, and the extra epilogue staging must still leave two B
+// stages (three with the augmented step)
+bool halves_supported(int d, int kp) {
+    if (chunked(d) || kp > 16) return false;
+    if (const char *e = getenv("SLK_TC_HS"))
+        if (atoi(e) == 1) return false;
+    return make_plan(k_extent(d), use_aug(d), 1, 0, 2).nb >= (use_aug(d) ? 3 : 2);
+}
+
+void launch_halves(int kp, const TcArgs &args, int64_t ngroups, cudaStream_t s) {
+    if (use_aug(args.d)) launch_halves_t<true>(kp, args, ngroups, s);
+    else launch_halves_t<false>(kp, args, ngroups, s);
 }
 
 // K' = kp candidates per row (2, 4, 8, 16 or 32; kp > k for the certificate);
