@@ -1322,10 +1322,10 @@ int tc_pass(const PointSet &Q, const PointSet &X, const int32_t *qid, int k, int
     while (nsplit < 8 && ngroups * nsplit < 2 * num_sms()) nsplit *= 2;
     if (const char *e = getenv("SLK_TC_SPLIT")) nsplit = std::max(nsplit, std::min(8, atoi(e)));
     if (nsplit & (nsplit - 1)) nsplit = 8;
-    // k-NN pass: two epilogue warps per row, each with its own K' list over
-    // half of every tile's columns (tc_scan.cu HS = 2); the refine unites at
-    // most 8 lists per row
-    int hs = (mode == MODE_SELF && qbn == 1 && tc::halves_supported(d, kp)) ? 2 : 1;
+    // single query blocks: two epilogue warps per row, each with its own K'
+    // list over half of every tile's columns (tc_scan.cu HS = 2); the refine
+    // unites at most 8 lists per row
+    int hs = (qbn == 1 && tc::halves_supported(mode, d, kp)) ? 2 : 1;
     if (hs == 2)
         while (nsplit > 1 && nsplit * hs > 8) nsplit /= 2;
     if (nsplit * hs > 8) hs = 1;
@@ -1356,7 +1356,7 @@ int tc_pass(const PointSet &Q, const PointSet &X, const int32_t *qid, int k, int
                   cand, kth_split, qhat, q0, q1,
                   V.sb_order, V.sb_lb, V.flat_lb, V.nvalid, X.nsb, tiles, qid, nsplit};
     ev_scan.start(s);
-    if (hs == 2) tc::launch_halves(kp, ta, ngroups, s);
+    if (hs == 2) tc::launch_halves(mode, kp, ta, ngroups, s);
     else tc::launch(mode, kp, qbn, ta, ngroups, s);
     ev_scan.stop(s);
     RefineArgs ra{Q.x32, Q.x64, Q.norms, X.x32, X.x64, X.norms, d, k, nq, nx, q0, q1,

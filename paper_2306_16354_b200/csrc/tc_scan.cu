@@ -860,8 +860,9 @@ void launch_ck(int mode, int kp, const TcArgs &args, int64_t ngroups, cudaStream
 
 // the k-NN pass with column halves (HS = 2)
 template <bool AUG>
-void launch_halves_t(int kp, const TcArgs &args, int64_t ngroups, cudaStream_t s) {
-    if (kp <= 8) launch_mode<MODE_SELF, 8, AUG, 1, false, 2>(args, ngroups, s);
+void launch_halves_t(int mode, int kp, const TcArgs &args, int64_t ngroups, cudaStream_t s) {
+    if (mode == MODE_COLOR) launch_mode<MODE_COLOR, 8, AUG, 1, false, 2>(args, ngroups, s);
+    else if (kp <= 8) launch_mode<MODE_SELF, 8, AUG, 1, false, 2>(args, ngroups, s);
     else launch_mode<MODE_SELF, 16, AUG, 1, false, 2>(args, ngroups, s);
 }
 
@@ -927,16 +928,17 @@ int group_blocks(int d, int kp) {
 // k-NN pass (MODE_SELF) with two column-half lists per row: K' <= 16, the
 // whole-block kernel, and the extra epilogue staging must still leave two B
 // stages (three with the augmented step)
-bool halves_supported(int d, int kp) {
-    if (chunked(d) || kp > 16) return false;
+bool halves_supported(int mode, int d, int kp) {
+    if (chunked(d) || kp > 16 || (mode != MODE_SELF && mode != MODE_COLOR) || (mode == MODE_COLOR && kp > 8))
+        return false;
     if (const char *e = getenv("SLK_TC_HS"))
         if (atoi(e) == 1) return false;
     return make_plan(k_extent(d), use_aug(d), 1, 0, 2).nb >= (use_aug(d) ? 3 : 2);
 }
 
-void launch_halves(int kp, const TcArgs &args, int64_t ngroups, cudaStream_t s) {
-    if (use_aug(args.d)) launch_halves_t<true>(kp, args, ngroups, s);
-    else launch_halves_t<false>(kp, args, ngroups, s);
+void launch_halves(int mode, int kp, const TcArgs &args, int64_t ngroups, cudaStream_t s) {
+    if (use_aug(args.d)) launch_halves_t<true>(mode, kp, args, ngroups, s);
+    else launch_halves_t<false>(mode, kp, args, ngroups, s);
 }
 
 // K' = kp candidates per row (2, 4, 8, 16 or 32; kp > k for the certificate);

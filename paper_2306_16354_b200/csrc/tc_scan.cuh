@@ -51,11 +51,12 @@ int group_blocks(int d, int kp);
 // kp: candidates kept per row (2..32; the certificate needs kp > k); qb query
 // blocks per CTA sharing one centring point (group_blocks)
 void launch(int mode, int kp, int qb, const TcArgs &args, int64_t ngroups, cudaStream_t s);
-// k-NN pass (MODE_SELF, one query block per CTA) with two epilogue warps per
-// TMEM lane quarter, each keeping a K' list over one half of every tile's
-// columns: every CTA writes 2 candidate lists per row (slot split * 2 + half)
-bool halves_supported(int d, int kp);
-void launch_halves(int kp, const TcArgs &args, int64_t ngroups, cudaStream_t s);
+// One query block per CTA with two epilogue warps per TMEM lane quarter, each
+// keeping a K' list over one half of every tile's columns: every CTA writes 2
+// candidate lists per row (slot split * 2 + half).  k-NN (MODE_SELF, K' <= 16)
+// and cross-colour (MODE_COLOR, K' <= 8) passes.
+bool halves_supported(int mode, int d, int kp);
+void launch_halves(int mode, int kp, const TcArgs &args, int64_t ngroups, cudaStream_t s);
 
 }  // namespace tc
 }  // namespace slk
