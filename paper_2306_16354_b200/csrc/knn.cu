@@ -842,11 +842,16 @@ struct ExactArgs {
     const int32_t *qid;  // query row -> id in the index (gathered queries), or null
 };
 
+// nparts > 1: the index is dealt over nparts warps per row (contiguous
+// ranges); each writes its top-k to part_v / part_i for exact_merge_kernel.
 template <int R>
-__global__ void exact_rescan_kernel(ExactArgs a) {
+__global__ void exact_rescan_kernel(ExactArgs a, int nparts, double *part_v, int *part_i) {
     const int lane = threadIdx.x & 31;
-    const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    if (w >= a.nrows) return;
+    const int64_t wg = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    if (wg >= (int64_t)a.nrows * nparts) return;
+    const int64_t w = wg / nparts;
+    const int part = (int)(wg - w * nparts);
+    const int64_t jbeg = a.nx * part / nparts, jend = a.nx * (part + 1) / nparts;
     const int64_t wid = a.rows[w];
     const int64_t gi = a.row0 + wid;
     const double nq = a.qnorm[gi];
@@ -857,9 +862,9 @@ __global__ void exact_rescan_kernel(ExactArgs a) {
         lv[r] = INFINITY;
         li[r] = 0x7fffffff;
     }
-    for (int64_t j0 = 0; j0 < a.nx; j0 += 32) {
+    for (int64_t j0 = jbeg; j0 < jend; j0 += 32) {
         int64_t j = j0 + lane;
-        bool ok = j < a.nx;
+        bool ok = j < jend;
         if (ok && a.mode == MODE_SELF) ok = j != (a.qid ? (int64_t)a.qid[gi] : gi);
         if (ok && a.mode == MODE_COLOR) ok = a.xcolor[j] != a.qcolor[gi];
         if (ok && a.mode == MODE_MASK) ok = a.mask[gi * a.nx + j] != 0;
@@ -872,6 +877,65 @@ __global__ void exact_rescan_kernel(ExactArgs a) {
             m &= m - 1;
             double cv = __shfl_sync(FULL, v, src);
             int cj = __shfl_sync(FULL, (int)j, src);
+            double t2 = __shfl_sync(FULL, lv[R - 1], 31);
+            int i2 = __shfl_sync(FULL, li[R - 1], 31);
+            if (pair_gt(t2, i2, cv, cj)) warp_list_insert<R>(lv, li, cv, cj, lane);
+        }
+    }
+    if (nparts > 1) {
+#pragma unroll
+        for (int r = 0; r < R; r++) {
+            const int p = r * 32 + lane;
+            if (p < a.k) {
+                part_v[wg * a.k + p] = lv[r];
+                part_i[wg * a.k + p] = li[r];
+            }
+        }
+        return;
+    }
+#pragma unroll
+    for (int r = 0; r < R; r++) {
+        int p = r * 32 + lane;
+        if (p < a.k) {
+            a.out_idx[wid * a.k + p] = li[r] == 0x7fffffff ? -1 : li[r];
+            a.out_dist[wid * a.k + p] = lv[r];
+        }
+    }
+    int first = __shfl_sync(FULL, li[0], 0);
+    if (lane == 0 && first == 0x7fffffff) atomicMin(a.missing, (int)gi);
+}
+
+// One warp per row: the top-k of its nparts partial lists, (v, id) order.
+template <int R>
+__global__ void exact_merge_kernel(ExactArgs a, int nparts, const double *part_v, const int *part_i) {
+    const int lane = threadIdx.x & 31;
+    const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    if (w >= a.nrows) return;
+    const int64_t wid = a.rows[w];
+    const int64_t gi = a.row0 + wid;
+    double lv[R];
+    int li[R];
+#pragma unroll
+    for (int r = 0; r < R; r++) {
+        lv[r] = INFINITY;
+        li[r] = 0x7fffffff;
+    }
+    const int64_t total = (int64_t)nparts * a.k;
+    const double *pv = part_v + w * total;
+    const int *pi = part_i + w * total;
+    for (int64_t c0 = 0; c0 < total; c0 += 32) {
+        const int64_t c = c0 + lane;
+        const double v = c < total ? pv[c] : INFINITY;
+        const int id = c < total ? pi[c] : 0x7fffffff;
+        const bool ok = id != 0x7fffffff;
+        double tv = __shfl_sync(FULL, lv[R - 1], 31);
+        int ti = __shfl_sync(FULL, li[R - 1], 31);
+        unsigned m = __ballot_sync(FULL, ok && pair_gt(tv, ti, v, id));
+        while (m) {
+            int src = __ffs(m) - 1;
+            m &= m - 1;
+            double cv = __shfl_sync(FULL, v, src);
+            int cj = __shfl_sync(FULL, id, src);
             double t2 = __shfl_sync(FULL, lv[R - 1], 31);
             int i2 = __shfl_sync(FULL, li[R - 1], 31);
             if (pair_gt(t2, i2, cv, cj)) warp_list_insert<R>(lv, li, cv, cj, lane);
@@ -923,10 +987,25 @@ void launch_refine(const RefineArgs &ra, int64_t rows, cudaStream_t s) {
     SLK_CHECK_LAUNCH();
 }
 
+// Few rows: each row's index is dealt over up to 64 warps (>= 512 index
+// points each) so the fallback fills the GPU, then merged per row.
 template <int R>
 void launch_exact(const ExactArgs &ea, cudaStream_t s) {
-    int64_t threads = (int64_t)ea.nrows * 32;
-    exact_rescan_kernel<R><<<(unsigned)((threads + 127) / 128), 128, 0, s>>>(ea);
+    int64_t parts = std::max<int64_t>(1, (4096 + ea.nrows - 1) / ea.nrows);
+    parts = std::min<int64_t>({parts, 64, std::max<int64_t>(1, ea.nx / 512)});
+    const int np = (int)parts;
+    int64_t threads = (int64_t)ea.nrows * np * 32;
+    if (np == 1) {
+        exact_rescan_kernel<R><<<(unsigned)((threads + 127) / 128), 128, 0, s>>>(ea, 1, nullptr, nullptr);
+        SLK_CHECK_LAUNCH();
+        return;
+    }
+    DevBuf<double> pv((size_t)ea.nrows * np * ea.k, s);
+    DevBuf<int> pi((size_t)ea.nrows * np * ea.k, s);
+    exact_rescan_kernel<R><<<(unsigned)((threads + 127) / 128), 128, 0, s>>>(ea, np, pv, pi);
+    SLK_CHECK_LAUNCH();
+    threads = (int64_t)ea.nrows * 32;
+    exact_merge_kernel<R><<<(unsigned)((threads + 127) / 128), 128, 0, s>>>(ea, np, pv, pi);
     SLK_CHECK_LAUNCH();
 }
 
@@ -1171,7 +1250,11 @@ int64_t search_ffma(const PointSet &Q, const PointSet &X, const int32_t *qid, in
     DevBuf<int> fail_rows(rows, s), counters(2, s);
     SLK_CUDA(cudaMemsetAsync(counters, 0, sizeof(int), s));
     const int Rsel = k < 32 ? 1 : (k < 64 ? 2 : 4);
-    if (k <= 127) {
+    // a handful of rows (the tensor path's last uncertified ones): the
+    // float64 re-scan dealt over many warps beats a pruned scan that would run
+    // on one or two CTAs
+    const bool direct = (double)rows * (double)nx * (double)d <= 4e9;
+    if (k <= 127 && !direct) {
         const int64_t qb0 = q0 / BM, qb1 = (q1 + BM - 1) / BM;
         DevBuf<int32_t> cand(rows * 32 * Rsel, s);
         DevBuf<float> kth(rows, s);
@@ -1205,7 +1288,7 @@ int64_t search_ffma(const PointSet &Q, const PointSet &X, const int32_t *qid, in
         st.tiles_skipped += (qb1 - qb0) * X.nb - (int64_t)done;
         record_profile(ev_order, ev_scan, ev_refine, rows, nx, d, done, (qb1 - qb0) * X.nb, false);
     } else {
-        // k beyond the fused list capacity: every row takes the exact path
+        // k beyond the fused list capacity, or few rows: every row takes the exact path
         if (k > 256) throw_invalid("k=%d exceeds the GPU limit of 256 neighbours", k);
         std::vector<int> all(rows);
         for (int64_t r = 0; r < rows; r++) all[r] = (int)r;

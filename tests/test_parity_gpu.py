@@ -387,3 +387,24 @@ def test_road_lattice_mst_matches_oracle(slk, oracle):
         assert r.n_components == onc
         assert np.array_equal(r.edges.src, os_) and np.array_equal(r.edges.dst, od)
         assert np.array_equal(r.edges.weight, ow) and np.array_equal(r.colors.colors, ocol)
+
+
+def test_exact_fallback_split_over_warps_matches_oracle(slk, oracle):
+    """Rows the certificate rejects (exact distance ties on an integer grid)
+    and k beyond the fused lists go to the float64 re-scan, whose index is
+    dealt over several warps per row and merged (knn.cu:launch_exact)."""
+    from paper_2306_16354_b200 import _lib
+
+    rng = np.random.default_rng(4)
+    x = rng.integers(0, 6, size=(6000, 3)).astype(np.float32)
+    x += np.arange(6000, dtype=np.float32)[:, None] * 1e-3  # distinct points, many near-ties
+    colors = slk.ColorArray(np.repeat(np.arange(6), 1000))
+    got = slk.cross_color_1nn(x, colors)
+    ref = oracle.cross_color_1nn(x.astype(np.float64), colors.colors)
+    assert np.array_equal(got.dst, ref[0]) and np.array_equal(got.weight, ref[1])
+    y = rng.standard_normal((3000, 16)).astype(np.float32)
+    _lib.scan_stats()
+    g = slk.fused_knn(y, 200)
+    assert _lib.scan_stats()["rows_rescanned"] > 0
+    oi, od = oracle.fused_knn(y, 200, rows=(0, 300))
+    assert np.array_equal(g.indices[:300], oi) and np.array_equal(g.distances[:300], od)
