@@ -740,12 +740,11 @@ __global__ void __launch_bounds__(Cfg<QB * HS>::NTHREADS, 1) tc_scan_kernel(TcAr
                 if (!__any_sync(FULL, hit)) continue;  // warp-uniform: nothing to insert
                 uint32_t pass = 0;
                 if (hit) {
-                    if (AUG) {
+                    // AUG: b = -2 acc exactly, so b < thr <=> acc > -thr / 2; the
+                    // chunk is staged as raw accumulators and scaled per insertion
+                    const float nthr = -0.5f * thr;
 #pragma unroll
-                        for (int i = 0; i < CH; i++) av[i] = -2.0f * dot[i];  // b, exact
-                    }
-#pragma unroll
-                    for (int i = 0; i < CH; i++) pass |= (av[i] < thr ? 1u : 0u) << i;
+                    for (int i = 0; i < CH; i++) pass |= ((AUG ? dot[i] > nthr : av[i] < thr) ? 1u : 0u) << i;
                     uint32_t valid = c0 >= col_limit ? 0u
                                      : (col_limit - c0 >= CH ? CH_ALL : ((1u << (col_limit - c0)) - 1u));
                     if (self_col >= c0 && self_col < c0 + CH) valid &= ~(1u << (self_col - c0));
@@ -763,14 +762,16 @@ __global__ void __launch_bounds__(Cfg<QB * HS>::NTHREADS, 1) tc_scan_kernel(TcAr
                         // stage the chunk: a passing value is one LDS away (no
                         // dynamic register indexing)
 #pragma unroll
-                        for (int i = 0; i < CH; i += 4)
-                            *reinterpret_cast<float4 *>(stg + i) = make_float4(av[i], av[i + 1], av[i + 2], av[i + 3]);
+                        for (int i = 0; i < CH; i += 4) {
+                            const float *src = AUG ? dot : av;
+                            *reinterpret_cast<float4 *>(stg + i) = make_float4(src[i], src[i + 1], src[i + 2], src[i + 3]);
+                        }
                     }
                 }
                 while (pass) {
                     const int i = __ffs(pass) - 1;
                     pass &= pass - 1;
-                    const float v = stg[i];
+                    const float v = AUG ? -2.0f * stg[i] : stg[i];
                     if (!(v < thr)) continue;  // the threshold may have dropped
                     const int id = (int)(col0 + c0 + i);
                     // shift-insert: new[p] = v < old[p-1] ? old[p-1] : (v < old[p] ? v : old[p])
