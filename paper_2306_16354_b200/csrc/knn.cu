@@ -1368,14 +1368,19 @@ const float *ensure_tcpack(const PointSet &P, cudaStream_t s) {
 // Writes certified and uncertified rows alike into out_*; returns the
 // uncertified rows (relative to q0) in `fail` and their count, and the
 // approximate K'-th values (scaled units) in `kth`.
+// Xscan / xid (optional): scan a re-blocked copy of the index (Xscan, with
+// xcolor in its order) whose position p holds point xid[p] of X; candidates are
+// mapped to X ids in the kernel and refined against X.
 int tc_pass(const PointSet &Q, const PointSet &X, const int32_t *qid, int k, int kp, int mode,
             const uint8_t *mask, const int32_t *qcolor, const int32_t *xcolor, int64_t q0,
             int64_t q1, float scale, float inv_scale2, int32_t *out_idx, double *out_dist,
-            DevBuf<int> &fail, DevBuf<float> &kth, cudaStream_t s) {
+            DevBuf<int> &fail, DevBuf<float> &kth, cudaStream_t s, const PointSet *Xscan = nullptr,
+            const int32_t *xid = nullptr) {
     ScanStats &st = scan_stats();
+    const PointSet &XS = Xscan ? *Xscan : X;
     const int64_t rows = q1 - q0;
     const int d = X.d;
-    const int64_t nq = Q.n, nx = X.n;
+    const int64_t nq = Q.n, nx = X.n, nxs = XS.n;
     const int64_t qb0 = q0 / BM, qb1 = (q1 + BM - 1) / BM;
     // query blocks per CTA: pairs share every converted index tile, when the
     // launch still fills the GPU with them
@@ -1423,21 +1428,21 @@ int tc_pass(const PointSet &Q, const PointSet &X, const int32_t *qid, int k, int
     SLK_CUDA(cudaMemsetAsync(counters, 0, sizeof(int), s));
     EventPair ev_order, ev_scan, ev_refine;
     ev_order.start(s);
-    VisitOrder V = visit_order(G, X, d, mode == MODE_COLOR ? xcolor : nullptr, s);
+    VisitOrder V = visit_order(G, XS, d, mode == MODE_COLOR ? xcolor : nullptr, s);
     ev_order.stop(s);
     trace_mark("visit_order enqueued");
     // colours of the index padded to whole blocks (one bulk copy per block)
     DevBuf<int32_t> xcolp;
     if (mode == MODE_COLOR) {
-        xcolp.alloc((size_t)X.nb * BN, s);
-        SLK_CUDA(cudaMemsetAsync(xcolp, 0xff, (size_t)X.nb * BN * sizeof(int32_t), s));
-        SLK_CUDA(cudaMemcpyAsync(xcolp, xcolor, (size_t)nx * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+        xcolp.alloc((size_t)XS.nb * BN, s);
+        SLK_CUDA(cudaMemsetAsync(xcolp, 0xff, (size_t)XS.nb * BN * sizeof(int32_t), s));
+        SLK_CUDA(cudaMemcpyAsync(xcolp, xcolor, (size_t)nxs * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
     }
-    const float *qtc = ensure_tcpack(Q, s), *xtc = ensure_tcpack(X, s);
-    tc::TcArgs ta{qtc, xtc, nq, nx, d, X.dp, tc::k_extent(d), qb0, G.cent, G.ng,
+    const float *qtc = ensure_tcpack(Q, s), *xtc = ensure_tcpack(XS, s);
+    tc::TcArgs ta{qtc, xtc, nq, nxs, d, XS.dp, tc::k_extent(d), qb0, G.cent, G.ng,
                   Q.nb, scale, inv_scale2, mask, qcolor, mode == MODE_COLOR ? xcolp.get() : xcolor,
                   cand, kth_split, qhat, q0, q1,
-                  V.sb_order, V.sb_lb, V.flat_lb, V.nvalid, X.nsb, tiles, qid, nsplit};
+                  V.sb_order, V.sb_lb, V.flat_lb, V.nvalid, XS.nsb, tiles, qid, nsplit, xid};
     ev_scan.start(s);
     if (hs == 2) tc::launch_halves(mode, kp, ta, ngroups, s);
     else tc::launch(mode, kp, qbn, ta, ngroups, s);
@@ -1459,8 +1464,8 @@ int tc_pass(const PointSet &Q, const PointSet &X, const int32_t *qid, int k, int
     trace_mark("scan+refine done");
     st.rows_refined += rows;
     st.tiles_computed += (int64_t)done;
-    st.tiles_skipped += (qb1 - qb0) * X.nb - (int64_t)done;
-    record_profile(ev_order, ev_scan, ev_refine, rows, nx, d, done, (qb1 - qb0) * X.nb, true);
+    st.tiles_skipped += (qb1 - qb0) * XS.nb - (int64_t)done;
+    record_profile(ev_order, ev_scan, ev_refine, rows, nx, d, done, (qb1 - qb0) * XS.nb, true);
     const int nfail = read_scalar<int>(counters, s);
     if (trace_on())
         fprintf(stderr, "[slk] tc_pass mode %d rows %lld (x%d blocks/CTA, split %d, halves %d): order %.2f scan %.2f refine %.2f ms, tiles %llu, uncertified %d\n",
@@ -1556,6 +1561,78 @@ Gathered gather_queries(const PointSet &Q, const std::vector<int32_t> &src,
     return G;
 }
 
+__global__ void iota_ids_kernel(int32_t *v, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        v[i] = (int32_t)i;
+}
+
+__global__ void colour_changes_kernel(const int32_t *colors, int64_t n, unsigned long long *count) {
+    unsigned long long c = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i + 1 < n; i += (int64_t)gridDim.x * blockDim.x)
+        c += colors[i] != colors[i + 1];
+    for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(FULL, c, o);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(count, c);
+}
+
+__global__ void map_failed_kernel(const int *gfail, const float *gkth, int nfail, const int32_t *gqid, int64_t q0,
+                                  int *fail, float *kth) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nfail; i += gridDim.x * blockDim.x) {
+        const int64_t rel = (int64_t)gqid[gfail[i]] - q0;
+        fail[i] = (int)rel;
+        kth[rel] = gkth[gfail[i]];
+    }
+}
+
+// Cross-colour passes whose colour segments straddle the 128-point blocks
+// (clusters not aligned to blocks, e.g. C5's 1000 clusters of 500 points):
+// the block spheres of straddling blocks span two clusters and prune
+// nothing.  Plan a colour-sorted copy (stable: original order within a
+// colour) in which every colour segment of >= 64 points starts a fresh
+// block; pad rows repeat the previous segment's first point (query id -1).
+// Returns false when few blocks straddle (C3: 49 boundaries in 7813 blocks).
+bool plan_colour_blocks(const PointSet &Q, const int32_t *colors, std::vector<int32_t> &src,
+                        std::vector<int32_t> &qid, cudaStream_t s) {
+    const int64_t n = Q.n;
+    DevBuf<unsigned long long> changes(1, s);
+    SLK_CUDA(cudaMemsetAsync(changes, 0, sizeof(unsigned long long), s));
+    colour_changes_kernel<<<grid_for(n, 256), 256, 0, s>>>(colors, n, changes);
+    SLK_CHECK_LAUNCH();
+    const unsigned long long nchg = read_scalar(changes.get(), s);
+    if ((double)nchg < 0.05 * (double)Q.nb) return false;
+    DevBuf<int32_t> iota(n, s), keys(n, s), ids(n, s);
+    iota_ids_kernel<<<grid_for(n, 256), 256, 0, s>>>(iota, n);
+    SLK_CHECK_LAUNCH();
+    size_t tmp = 0;
+    SLK_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, colors, keys.get(), iota.get(), ids.get(), (int)n, 0, 32, s));
+    DevBuf<unsigned char> t(tmp, s);
+    SLK_CUDA(cub::DeviceRadixSort::SortPairs(t.get(), tmp, colors, keys.get(), iota.get(), ids.get(), (int)n, 0, 32, s));
+    std::vector<int32_t> hk(n), hi(n);
+    SLK_CUDA(cudaMemcpyAsync(hk.data(), keys.get(), n * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    SLK_CUDA(cudaMemcpyAsync(hi.data(), ids.get(), n * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    SLK_CUDA(cudaStreamSynchronize(s));
+    src.clear();
+    qid.clear();
+    src.reserve(n + n / 4);
+    qid.reserve(n + n / 4);
+    int32_t prev_first = hi[0];
+    for (int64_t i = 0; i < n;) {
+        int64_t j = i + 1;
+        while (j < n && hk[j] == hk[i]) j++;
+        if (j - i >= BM / 2 && !src.empty())
+            while (src.size() % BM) {
+                src.push_back(prev_first);
+                qid.push_back(-1);
+            }
+        for (int64_t r = i; r < j; r++) {
+            src.push_back(hi[r]);
+            qid.push_back(hi[r]);
+        }
+        prev_first = hi[i];
+        i = j;
+    }
+    return true;
+}
+
 // Full neighbour search for query rows [q0, q1) of Q against X; k results per row.
 void search(const PointSet &Q, const PointSet &X, int k, int mode, const uint8_t *mask,
             const int32_t *qcolor, const int32_t *xcolor, int64_t q0, int64_t q1,
@@ -1578,8 +1655,37 @@ void search(const PointSet &Q, const PointSet &X, int k, int mode, const uint8_t
     } else {
         DevBuf<int> fail;
         DevBuf<float> kth;
-        const int nfail = tc_pass(Q, X, nullptr, k, tc_kp(k, false), mode, mask, qcolor, xcolor, q0, q1, scale,
-                                  inv_scale2, out_idx, out_dist, fail, kth, s);
+        int nfail = -1;
+        std::vector<int32_t> csrc, cqid;
+        if (mode == MODE_COLOR && k == 1 && &Q == &X && qcolor == xcolor && q0 == 0 && q1 == Q.n &&
+            !getenv("SLK_NO_COLOUR_REBLOCK") && plan_colour_blocks(Q, qcolor, csrc, cqid, s)) {
+            // scan the colour-blocked copy against itself (candidates mapped back to
+            // X ids in the kernel), refine against X, scatter rows back
+            Gathered CG = gather_queries(Q, csrc, cqid, mode, qcolor, nullptr, nx, s);
+            DevBuf<int32_t> xid(CG.n, s);
+            SLK_CUDA(cudaMemcpyAsync(xid.get(), csrc.data(), CG.n * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+            DevBuf<int32_t> gidx(CG.n * k, s);
+            DevBuf<double> gdist(CG.n * k, s);
+            DevBuf<int> gfail;
+            DevBuf<float> gkth;
+            trace_mark("colour blocks");
+            const int gn = tc_pass(*CG.P, X, CG.qid, k, tc_kp(k, false), mode, nullptr, CG.qcolor.get(),
+                                   CG.qcolor.get(), 0, CG.n, scale, inv_scale2, gidx, gdist, gfail, gkth, s,
+                                   CG.P.get(), xid.get());
+            scatter_gathered_kernel<<<grid_for(CG.n * k, 256), 256, 0, s>>>(gidx, gdist, CG.qid, CG.n, k, q0,
+                                                                             out_idx, out_dist);
+            SLK_CHECK_LAUNCH();
+            fail.alloc(std::max(gn, 1), s);
+            kth.alloc(rows, s);
+            if (gn > 0) {
+                map_failed_kernel<<<grid_for(gn, 256), 256, 0, s>>>(gfail, gkth, gn, CG.qid, q0, fail, kth);
+                SLK_CHECK_LAUNCH();
+            }
+            nfail = gn;
+        }
+        if (nfail < 0)
+            nfail = tc_pass(Q, X, nullptr, k, tc_kp(k, false), mode, mask, qcolor, xcolor, q0, q1, scale,
+                            inv_scale2, out_idx, out_dist, fail, kth, s);
         (void)Rsel;
         if (nfail > 0) {
             // Uncertified rows mostly sit in query blocks that straddle two

@@ -803,7 +803,11 @@ __global__ void __launch_bounds__(Cfg<QB * HS>::NTHREADS, 1) tc_scan_kernel(TcAr
             const int64_t slot = ((gi - a.row0) * a.nsplit + split) * HS + half;
             int32_t *dst = a.cand + slot * 32;
 #pragma unroll
-            for (int q = 0; q < 32; q++) dst[q] = q < KP ? li[q < KP ? q : 0] : -1;
+#pragma unroll
+            for (int q = 0; q < 32; q++) {
+                const int id = q < KP ? li[q < KP ? q : 0] : -1;
+                dst[q] = (a.xid && id >= 0) ? a.xid[id] : id;
+            }
             // a = |q~|^2 + b rounded down: a lower bound keeps the certificate rigorous
             a.kth[slot] = li[KP - 1] >= 0 ? __fadd_rd(lv[KP - 1], qq) : INFINITY;
             a.qhat[gi - a.row0] = qq;

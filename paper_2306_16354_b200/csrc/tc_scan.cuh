@@ -33,6 +33,7 @@ struct TcArgs {
     unsigned long long *tiles_done;
     const int32_t *qid;      // query row -> id in the index, -1 = padding (or null)
     int nsplit;              // CTAs per query block, each scanning 1/nsplit of the visit order
+    const int32_t *xid;      // index position -> id written to cand (re-blocked index), or null
 };
 
 // MMA K extent for d dims: d rounded up to 16, plus the augmented norm step

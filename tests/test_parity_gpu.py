@@ -408,3 +408,45 @@ def test_exact_fallback_split_over_warps_matches_oracle(slk, oracle):
     assert _lib.scan_stats()["rows_rescanned"] > 0
     oi, od = oracle.fused_knn(y, 200, rows=(0, 300))
     assert np.array_equal(g.indices[:300], oi) and np.array_equal(g.distances[:300], od)
+
+
+@pytest.mark.parametrize("layout", ["clusters", "interleaved", "mixed_sizes"])
+def test_cross_colour_colour_blocked_matches_oracle(slk, oracle, monkeypatch, layout):
+    """When colour segments straddle the 128-point blocks, the cross-colour
+    pass scans a colour-sorted, block-aligned copy (knn.cu:plan_colour_blocks)
+    and maps candidates back; results must equal the oracle's (and the
+    unblocked scan's) exactly."""
+    from paper_2306_16354_b200.synthetic import make_blobs
+
+    rng = np.random.default_rng(len(layout))
+    if layout == "clusters":
+        x = make_blobs(rng, 60 * 333, 16, 60).astype(np.float32)
+        col = np.repeat(np.arange(60), 333)
+    elif layout == "interleaved":
+        x = rng.standard_normal((9000, 8)).astype(np.float32)
+        col = rng.integers(0, 7, size=9000)
+    else:  # clusters of 3 .. 700 points: small segments pack without padding
+        sizes = rng.integers(3, 700, size=40)
+        x = make_blobs(rng, int(sizes.sum()), 12, 40).astype(np.float32)
+        col = np.repeat(np.arange(40), sizes)[: len(x)]
+    colors = slk.ColorArray(col)
+    got = slk.cross_color_1nn(x, colors)
+    ref = oracle.cross_color_1nn(x.astype(np.float64), col)
+    assert np.array_equal(got.dst, ref[0]) and np.array_equal(got.weight, ref[1])
+    monkeypatch.setenv("SLK_NO_COLOUR_REBLOCK", "1")
+    plain = slk.cross_color_1nn(x, colors)
+    assert np.array_equal(plain.dst, got.dst) and np.array_equal(plain.weight, got.weight)
+
+
+def test_single_linkage_unaligned_clusters_matches_oracle(slk, oracle):
+    """C5-shaped (many clusters not aligned to blocks, k = 2): the connect
+    passes take the colour-blocked scan."""
+    from paper_2306_16354_b200.synthetic import make_blobs
+
+    x = make_blobs(np.random.default_rng(55), 150 * 200 + 7, 24, 150).astype(np.float32)
+    cfg = slk.LinkageConfig(n_clusters=150, k=2, seed=5)
+    res = slk.single_linkage_result(x, cfg)
+    ref = oracle.single_linkage(x, 150, k=2, seed=5)
+    assert np.array_equal(res.tree.src, ref["tree_src"]) and np.array_equal(res.tree.weight, ref["tree_w"])
+    assert np.array_equal(res.dendrogram.merges, ref["merges"])
+    assert np.array_equal(res.labels.labels, ref["labels"])
