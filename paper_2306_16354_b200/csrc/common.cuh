@@ -202,6 +202,9 @@ struct PointSet {
     DevBuf<double> norms, maxn;
     // tensor-core scan operand layout (knn.cu:tcpack_kernel), built on first use
     mutable DevBuf<float> tcpack;
+    // optional finest cluster labels (the k-NN graph's components): the
+    // cross-colour re-blocking keeps their segments contiguous and aligned
+    const int32_t *block_hint = nullptr;
 };
 std::shared_ptr<PointSet> make_pointset(const float *x32, const double *x64, int64_t n, int d,
                                         cudaStream_t s);

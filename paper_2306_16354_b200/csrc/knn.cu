@@ -1566,6 +1566,11 @@ __global__ void iota_ids_kernel(int32_t *v, int64_t n) {
         v[i] = (int32_t)i;
 }
 
+__global__ void colour_keys_kernel(const int32_t *colors, const int32_t *hint, int64_t n, uint64_t *key) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        key[i] = ((uint64_t)(uint32_t)colors[i] << 32) | (uint32_t)(hint ? hint[i] : 0);
+}
+
 __global__ void colour_changes_kernel(const int32_t *colors, int64_t n, unsigned long long *count) {
     unsigned long long c = 0;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i + 1 < n; i += (int64_t)gridDim.x * blockDim.x)
@@ -1599,15 +1604,20 @@ bool plan_colour_blocks(const PointSet &Q, const int32_t *colors, std::vector<in
     SLK_CHECK_LAUNCH();
     const unsigned long long nchg = read_scalar(changes.get(), s);
     if ((double)nchg < 0.05 * (double)Q.nb) return false;
-    DevBuf<int32_t> iota(n, s), keys(n, s), ids(n, s);
+    // key (colour, finest label): colours are unions of the hint's clusters,
+    // which stay contiguous and block-aligned inside each colour
+    DevBuf<int32_t> iota(n, s), ids(n, s);
+    DevBuf<uint64_t> key(n, s), keys(n, s);
     iota_ids_kernel<<<grid_for(n, 256), 256, 0, s>>>(iota, n);
+    colour_keys_kernel<<<grid_for(n, 256), 256, 0, s>>>(colors, Q.block_hint, n, key);
     SLK_CHECK_LAUNCH();
     size_t tmp = 0;
-    SLK_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, colors, keys.get(), iota.get(), ids.get(), (int)n, 0, 32, s));
+    SLK_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, key.get(), keys.get(), iota.get(), ids.get(), (int)n, 0, 64, s));
     DevBuf<unsigned char> t(tmp, s);
-    SLK_CUDA(cub::DeviceRadixSort::SortPairs(t.get(), tmp, colors, keys.get(), iota.get(), ids.get(), (int)n, 0, 32, s));
-    std::vector<int32_t> hk(n), hi(n);
-    SLK_CUDA(cudaMemcpyAsync(hk.data(), keys.get(), n * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    SLK_CUDA(cub::DeviceRadixSort::SortPairs(t.get(), tmp, key.get(), keys.get(), iota.get(), ids.get(), (int)n, 0, 64, s));
+    std::vector<uint64_t> hk(n);
+    std::vector<int32_t> hi(n);
+    SLK_CUDA(cudaMemcpyAsync(hk.data(), keys.get(), n * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
     SLK_CUDA(cudaMemcpyAsync(hi.data(), ids.get(), n * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
     SLK_CUDA(cudaStreamSynchronize(s));
     src.clear();

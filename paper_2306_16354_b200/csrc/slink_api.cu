@@ -226,7 +226,13 @@ void single_linkage_device(const float *x32, const double *x64, int64_t n, int d
     // --- connect loop (linkage.py:222-254)
     int64_t budget = max_iters >= 0 ? max_iters : (int64_t)ceil(log2((double)std::max<int64_t>(n, 2))) + 8;
     int64_t iters = 0;
+    DevBuf<int32_t> base_colors;
     if (nc > 1) {
+        // the k-NN graph's components: every later colour is a union of them,
+        // and the cross-colour re-blocking keeps them contiguous
+        base_colors.alloc(n, s);
+        SLK_CUDA(cudaMemcpyAsync(base_colors.get(), colors.get(), n * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+        P->block_hint = base_colors.get();
         DevBuf<int32_t> usrc(2 * n, s), udst(2 * n, s);
         DevBuf<double> uw(2 * n, s);
         while (nc > 1) {
