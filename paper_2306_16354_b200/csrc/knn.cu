@@ -1375,7 +1375,7 @@ int tc_pass(const PointSet &Q, const PointSet &X, const int32_t *qid, int k, int
             const uint8_t *mask, const int32_t *qcolor, const int32_t *xcolor, int64_t q0,
             int64_t q1, float scale, float inv_scale2, int32_t *out_idx, double *out_dist,
             DevBuf<int> &fail, DevBuf<float> &kth, cudaStream_t s, const PointSet *Xscan = nullptr,
-            const int32_t *xid = nullptr) {
+            const int32_t *xid = nullptr, bool self_pos = false) {
     ScanStats &st = scan_stats();
     const PointSet &XS = Xscan ? *Xscan : X;
     const int64_t rows = q1 - q0;
@@ -1433,16 +1433,16 @@ int tc_pass(const PointSet &Q, const PointSet &X, const int32_t *qid, int k, int
     trace_mark("visit_order enqueued");
     // colours of the index padded to whole blocks (one bulk copy per block)
     DevBuf<int32_t> xcolp;
-    if (mode == MODE_COLOR) {
+    if (mode == MODE_COLOR || (mode == MODE_SELF && xcolor)) {
         xcolp.alloc((size_t)XS.nb * BN, s);
         SLK_CUDA(cudaMemsetAsync(xcolp, 0xff, (size_t)XS.nb * BN * sizeof(int32_t), s));
         SLK_CUDA(cudaMemcpyAsync(xcolp, xcolor, (size_t)nxs * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
     }
     const float *qtc = ensure_tcpack(Q, s), *xtc = ensure_tcpack(XS, s);
     tc::TcArgs ta{qtc, xtc, nq, nxs, d, XS.dp, tc::k_extent(d), qb0, G.cent, G.ng,
-                  Q.nb, scale, inv_scale2, mask, qcolor, mode == MODE_COLOR ? xcolp.get() : xcolor,
+                  Q.nb, scale, inv_scale2, mask, qcolor, xcolp.get() ? xcolp.get() : xcolor,
                   cand, kth_split, qhat, q0, q1,
-                  V.sb_order, V.sb_lb, V.flat_lb, V.nvalid, XS.nsb, tiles, qid, nsplit, xid};
+                  V.sb_order, V.sb_lb, V.flat_lb, V.nvalid, XS.nsb, tiles, qid, nsplit, xid, self_pos ? 1 : 0};
     ev_scan.start(s);
     if (hs == 2) tc::launch_halves(mode, kp, ta, ngroups, s);
     else tc::launch(mode, kp, qbn, ta, ngroups, s);
@@ -1643,6 +1643,75 @@ bool plan_colour_blocks(const PointSet &Q, const int32_t *colors, std::vector<in
     return true;
 }
 
+void search(const PointSet &Q, const PointSet &X, int k, int mode, const uint8_t *mask,
+            const int32_t *qcolor, const int32_t *xcolor, int64_t q0, int64_t q1,
+            int32_t *out_idx, double *out_dist, cudaStream_t s);
+
+// k-NN pass over data whose clusters straddle the 128-point blocks (many
+// blocks with radii far above the typical block's, e.g. C5's 500-point
+// clusters): order the points by their nearest pivot (every 256th point of
+// the input order, exact 1-NN on the device) and start every pivot cell of
+// >= 64 points on a fresh block, so blocks stay inside one cell.  Pad rows
+// repeat the previous cell's first point: query id -1, index mark -1 (the
+// scan never takes them).  Returns false when few blocks are oversized (C3).
+bool plan_pivot_blocks(const PointSet &X, std::vector<int32_t> &src, std::vector<int32_t> &qid,
+                       std::vector<int32_t> &mark, cudaStream_t s) {
+    const int64_t n = X.n, nb = X.nb;
+    if (nb < 64 || getenv("SLK_NO_PIVOT_REBLOCK")) return false;
+    std::vector<float> r(nb);
+    SLK_CUDA(cudaMemcpyAsync(r.data(), X.radius.get(), nb * sizeof(float), cudaMemcpyDeviceToHost, s));
+    SLK_CUDA(cudaStreamSynchronize(s));
+    std::vector<float> sorted(r);
+    std::nth_element(sorted.begin(), sorted.begin() + nb / 2, sorted.end());
+    const float med = sorted[nb / 2];
+    int64_t big = 0;
+    for (float v : r) big += v > 2.0f * med;
+    if ((double)big < 0.08 * (double)nb) return false;
+    const int64_t np = std::max<int64_t>(2, n / 256);
+    std::vector<int32_t> pid(np);
+    for (int64_t j = 0; j < np; j++) pid[j] = (int32_t)(j * n / np);
+    Gathered PV = gather_queries(X, pid, pid, MODE_NONE, nullptr, nullptr, 0, s);
+    DevBuf<int32_t> near(n, s);
+    DevBuf<double> nd(n, s);
+    search(X, *PV.P, 1, MODE_NONE, nullptr, nullptr, nullptr, 0, n, near, nd, s);
+    DevBuf<int32_t> iota(n, s), keys(n, s), ids(n, s);
+    iota_ids_kernel<<<grid_for(n, 256), 256, 0, s>>>(iota, n);
+    SLK_CHECK_LAUNCH();
+    size_t tmp = 0;
+    SLK_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, near.get(), keys.get(), iota.get(), ids.get(), (int)n, 0, 32, s));
+    DevBuf<unsigned char> t(tmp, s);
+    SLK_CUDA(cub::DeviceRadixSort::SortPairs(t.get(), tmp, near.get(), keys.get(), iota.get(), ids.get(), (int)n, 0, 32, s));
+    std::vector<int32_t> hk(n), hi(n);
+    SLK_CUDA(cudaMemcpyAsync(hk.data(), keys.get(), n * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    SLK_CUDA(cudaMemcpyAsync(hi.data(), ids.get(), n * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    SLK_CUDA(cudaStreamSynchronize(s));
+    src.clear();
+    qid.clear();
+    mark.clear();
+    src.reserve(n + n / 2);
+    qid.reserve(n + n / 2);
+    mark.reserve(n + n / 2);
+    int32_t prev_first = hi[0];
+    for (int64_t i = 0; i < n;) {
+        int64_t j = i + 1;
+        while (j < n && hk[j] == hk[i]) j++;
+        if (j - i >= BM / 2 && !src.empty())
+            while (src.size() % BM) {
+                src.push_back(prev_first);
+                qid.push_back(-1);
+                mark.push_back(-1);
+            }
+        for (int64_t q = i; q < j; q++) {
+            src.push_back(hi[q]);
+            qid.push_back(hi[q]);
+            mark.push_back(0);
+        }
+        prev_first = hi[i];
+        i = j;
+    }
+    return true;
+}
+
 // Full neighbour search for query rows [q0, q1) of Q against X; k results per row.
 void search(const PointSet &Q, const PointSet &X, int k, int mode, const uint8_t *mask,
             const int32_t *qcolor, const int32_t *xcolor, int64_t q0, int64_t q1,
@@ -1689,6 +1758,34 @@ void search(const PointSet &Q, const PointSet &X, int k, int mode, const uint8_t
             kth.alloc(rows, s);
             if (gn > 0) {
                 map_failed_kernel<<<grid_for(gn, 256), 256, 0, s>>>(gfail, gkth, gn, CG.qid, q0, fail, kth);
+                SLK_CHECK_LAUNCH();
+            }
+            nfail = gn;
+        }
+        std::vector<int32_t> psrc, pqid, pmark;
+        if (nfail < 0 && mode == MODE_SELF && &Q == &X && q0 == 0 && q1 == Q.n &&
+            plan_pivot_blocks(Q, psrc, pqid, pmark, s)) {
+            // scan the pivot-ordered copy against itself; candidates map back to
+            // X ids in the kernel, a row's own point sits at its own position,
+            // pad entries (mark -1) are never taken
+            Gathered PG = gather_queries(Q, psrc, pqid, mode, nullptr, nullptr, nx, s);
+            DevBuf<int32_t> xid(PG.n, s), xmark(PG.n, s);
+            SLK_CUDA(cudaMemcpyAsync(xid.get(), psrc.data(), PG.n * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+            SLK_CUDA(cudaMemcpyAsync(xmark.get(), pmark.data(), PG.n * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+            DevBuf<int32_t> gidx(PG.n * k, s);
+            DevBuf<double> gdist(PG.n * k, s);
+            DevBuf<int> gfail;
+            DevBuf<float> gkth;
+            trace_mark("pivot blocks");
+            const int gn = tc_pass(*PG.P, X, PG.qid, k, tc_kp(k, false), mode, nullptr, nullptr, xmark.get(), 0,
+                                   PG.n, scale, inv_scale2, gidx, gdist, gfail, gkth, s, PG.P.get(), xid.get(), true);
+            scatter_gathered_kernel<<<grid_for(PG.n * k, 256), 256, 0, s>>>(gidx, gdist, PG.qid, PG.n, k, q0,
+                                                                             out_idx, out_dist);
+            SLK_CHECK_LAUNCH();
+            fail.alloc(std::max(gn, 1), s);
+            kth.alloc(rows, s);
+            if (gn > 0) {
+                map_failed_kernel<<<grid_for(gn, 256), 256, 0, s>>>(gfail, gkth, gn, PG.qid, q0, fail, kth);
                 SLK_CHECK_LAUNCH();
             }
             nfail = gn;

@@ -523,7 +523,8 @@ __global__ void __launch_bounds__(Cfg<QB * HS>::NTHREADS, 1) tc_scan_kernel(TcAr
                     if (jb < 0) {
                         mbar_arrive(&rawfull[s]);
                     } else {
-                        const bool col = MODE == MODE_COLOR && c == 0;
+                        // MODE_SELF with xcolor: re-blocked index whose pad entries are marked < 0
+                        const bool col = (MODE == MODE_COLOR || (MODE == MODE_SELF && a.xcolor)) && c == 0;
                         mbar_expect_tx(&rawfull[s], stage_bytes + (col ? BN * 4 : 0));
                         bulk_g2s(sB + (size_t)s * stage_bytes, a.xp + (jb * nck + c) * (int64_t)kc * BN,
                                  stage_bytes, &rawfull[s]);
@@ -705,8 +706,9 @@ __global__ void __launch_bounds__(Cfg<QB * HS>::NTHREADS, 1) tc_scan_kernel(TcAr
             // columns this row may take from this block: inside the index, not itself
             const int64_t rem = a.nx - col0;
             const int col_limit = row_ok ? (rem < BN ? (int)rem : BN) : 0;
+            const int64_t self_at = a.self_pos ? gi : self_id;
             const int self_col =
-                (MODE == MODE_SELF && self_id >= col0 && self_id < col0 + BN) ? (int)(self_id - col0) : -1;
+                (MODE == MODE_SELF && self_at >= col0 && self_at < col0 + BN) ? (int)(self_at - col0) : -1;
             const int *xcs = s_xcol + slot * BN;
 #pragma unroll 1
             for (int c0 = half * (BN / HS); c0 < (half + 1) * (BN / HS); c0 += CH) {
@@ -753,6 +755,11 @@ __global__ void __launch_bounds__(Cfg<QB * HS>::NTHREADS, 1) tc_scan_kernel(TcAr
 #pragma unroll
                         for (int i = 0; i < CH; i++)
                             if (xcs[c0 + i] == qc) pass &= ~(1u << i);
+                    }
+                    if (MODE == MODE_SELF && a.xcolor && pass) {
+#pragma unroll
+                        for (int i = 0; i < CH; i++)
+                            if (xcs[c0 + i] < 0) pass &= ~(1u << i);
                     }
                     if (MODE == MODE_MASK && pass) {
                         for (int i = 0; i < CH; i++)

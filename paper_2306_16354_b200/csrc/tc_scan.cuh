@@ -34,6 +34,7 @@ struct TcArgs {
     const int32_t *qid;      // query row -> id in the index, -1 = padding (or null)
     int nsplit;              // CTAs per query block, each scanning 1/nsplit of the visit order
     const int32_t *xid;      // index position -> id written to cand (re-blocked index), or null
+    int self_pos;            // MODE_SELF over one re-blocked set: a row's own point sits at its position
 };
 
 // MMA K extent for d dims: d rounded up to 16, plus the augmented norm step

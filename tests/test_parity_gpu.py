@@ -450,3 +450,21 @@ def test_single_linkage_unaligned_clusters_matches_oracle(slk, oracle):
     assert np.array_equal(res.tree.src, ref["tree_src"]) and np.array_equal(res.tree.weight, ref["tree_w"])
     assert np.array_equal(res.dendrogram.merges, ref["merges"])
     assert np.array_equal(res.labels.labels, ref["labels"])
+
+
+@pytest.mark.parametrize("k", [2, 15])
+def test_knn_pivot_blocked_matches_oracle(slk, oracle, monkeypatch, k):
+    """Clusters that straddle the 128-point blocks: the k-NN pass scans a
+    pivot-ordered copy (knn.cu:plan_pivot_blocks, self excluded by position,
+    candidates mapped back); identical to the oracle and to the plain scan."""
+    from paper_2306_16354_b200 import _lib
+    from paper_2306_16354_b200.synthetic import make_blobs
+
+    x = make_blobs(np.random.default_rng(k), 90 * 210, 20, 90).astype(np.float32)
+    _lib.profile(reset=True)
+    g = slk.fused_knn(x, k)
+    oi, od = oracle.fused_knn(x, k, rows=(0, 2500))
+    assert np.array_equal(g.indices[:2500], oi) and np.array_equal(g.distances[:2500], od)
+    monkeypatch.setenv("SLK_NO_PIVOT_REBLOCK", "1")
+    p = slk.fused_knn(x, k)
+    assert np.array_equal(p.indices, g.indices) and np.array_equal(p.distances, g.distances)
