@@ -493,7 +493,8 @@ __global__ void __launch_bounds__(256) pair_lb_kernel(const float *__restrict__ 
                                                       const float *__restrict__ xr, int64_t nxb, int d,
                                                       int64_t qb0, int64_t nqb, const int2 *__restrict__ qcol,
                                                       const int2 *__restrict__ xcol, float *__restrict__ lb) {
-    __shared__ float sq[64][33], sx[64][33];
+    // staged as float64 (exact conversions): no float->double conversion in the inner loop
+    __shared__ double sq[64][33], sx[64][33];
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // ty: 0..7
     const int64_t b = (int64_t)blockIdx.x * 32 + tx;
     const int64_t ql0 = (int64_t)blockIdx.y * 32;
@@ -504,15 +505,15 @@ __global__ void __launch_bounds__(256) pair_lb_kernel(const float *__restrict__ 
         for (int e = threadIdx.x; e < tn * 32; e += 256) {
             const int t = e >> 5, j = e & 31;
             const int64_t qg = qb0 + ql0 + j, xg = (int64_t)blockIdx.x * 32 + j;
-            sq[t][j] = ql0 + j < nqb ? qc[(int64_t)(t0 + t) * nqb_total + qg] : 0.0f;
-            sx[t][j] = xg < nxb ? xc[(int64_t)(t0 + t) * nxb + xg] : 0.0f;
+            sq[t][j] = ql0 + j < nqb ? (double)qc[(int64_t)(t0 + t) * nqb_total + qg] : 0.0;
+            sx[t][j] = xg < nxb ? (double)xc[(int64_t)(t0 + t) * nxb + xg] : 0.0;
         }
         __syncthreads();
         for (int t = 0; t < tn; t++) {
-            const double xv = (double)sx[t][tx];
+            const double xv = sx[t][tx];
 #pragma unroll
             for (int i = 0; i < 4; i++) {
-                const double df = (double)sq[t][ty * 4 + i] - xv;
+                const double df = sq[t][ty * 4 + i] - xv;
                 acc[i] += df * df;
             }
         }
