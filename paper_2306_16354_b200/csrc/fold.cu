@@ -15,6 +15,7 @@
 #include <algorithm>
 #include <atomic>
 #include <chrono>
+#include <memory>
 #include <thread>
 #include <vector>
 
@@ -98,16 +99,30 @@ void parallel_slices(int64_t n, int threads, F body) {
 // threads.
 void cut_labels(const Node *nd, int64_t n, int64_t n_clusters, int64_t *labels, int threads) {
     std::vector<std::pair<int32_t, int32_t>> roots;  // (cluster id, root vertex)
-    roots.reserve(n_clusters);
-    for (int32_t v = 0; v < (int32_t)n; v++)
-        if (nd[v].parent == v) roots.emplace_back(nd[v].cid, v);
+    {
+        // roots found per slice in parallel, concatenated (sorted below)
+        const int nt = (int)std::max<int64_t>(1, std::min<int64_t>(threads, n / 65536 + 1));
+        std::vector<std::vector<std::pair<int32_t, int32_t>>> part(nt);
+        std::vector<std::thread> pool;
+        auto scan = [&](int k) {
+            const int64_t lo = n * k / nt, hi = n * (k + 1) / nt;
+            for (int64_t v = lo; v < hi; v++)
+                if (nd[v].parent == (int32_t)v) part[k].emplace_back(nd[v].cid, (int32_t)v);
+        };
+        for (int k = 1; k < nt; k++) pool.emplace_back(scan, k);
+        scan(0);
+        for (auto &t : pool) t.join();
+        roots.reserve(n_clusters);
+        for (auto &p : part) roots.insert(roots.end(), p.begin(), p.end());
+    }
     if ((int64_t)roots.size() != n_clusters)
         throw_invalid("internal: found %lld label roots for %lld clusters", (long long)roots.size(),
                       (long long)n_clusters);
     std::sort(roots.begin(), roots.end());
-    std::vector<int32_t> lab(n);
+    // label of each root vertex (only roots are read)
+    std::unique_ptr<int32_t[]> lab(new int32_t[n]);
     for (size_t r = 0; r < roots.size(); r++) lab[roots[r].second] = (int32_t)r;
-    const int32_t *lp = lab.data();
+    const int32_t *lp = lab.get();
     parallel_slices(n, threads, [&](int64_t lo, int64_t hi) {
         for (int64_t p = lo; p < hi; p++) {
             int32_t x = (int32_t)p;
