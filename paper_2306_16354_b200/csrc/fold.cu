@@ -148,8 +148,9 @@ void cut_labels(const Node *nd, int64_t n, int64_t n_clusters, int64_t *labels, 
 void dendrogram_fold(const FoldInput &in, double *merges, int64_t n_clusters, int64_t *labels, double *extract_ms) {
     const int64_t n = in.n;
     if (n >= (1ll << 30)) throw_invalid("n=%lld too large for the dendrogram fold", (long long)n);
-    std::vector<Node> nodes(n);
-    Node *nd = nodes.data();
+    // uninitialised: the threads below write every node (first touch in parallel)
+    std::unique_ptr<Node[]> nodes(new Node[n]);
+    Node *nd = nodes.get();
     parallel_slices(n, in.threads, [&](int64_t lo, int64_t hi) {
         for (int64_t v = lo; v < hi; v++) nd[v] = Node{(int32_t)v, (int32_t)v, 1, 0};
     });
