@@ -14,6 +14,7 @@
 #include <chrono>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "common.cuh"
@@ -282,11 +283,23 @@ void single_linkage_device(const float *x32, const double *x64, int64_t n, int d
     if (want_tree) {
         SLK_CUDA(cudaStreamSynchronize(s));
         const int32_t *hs = st_src.p, *hd = st_dst.p;
-        for (int64_t i = 0; i < n - 1; i++) {
-            if (h_tree_src) h_tree_src[i] = hs[i];
-            if (h_tree_dst) h_tree_dst[i] = hd[i];
-        }
-        if (h_tree_w) memcpy(h_tree_w, st_w.p, (n - 1) * sizeof(double));
+        const double *hw = st_w.p;
+        // widen / copy out of the pinned staging in parallel slices (the caller's
+        // fresh arrays are first touched here)
+        const int64_t m = n - 1;
+        const int nt = (int)std::max<int64_t>(1, std::min<int64_t>(fin.threads, m / 65536 + 1));
+        auto copy = [&](int k) {
+            const int64_t lo = m * k / nt, hi = m * (k + 1) / nt;
+            for (int64_t i = lo; i < hi; i++) {
+                if (h_tree_src) h_tree_src[i] = hs[i];
+                if (h_tree_dst) h_tree_dst[i] = hd[i];
+            }
+            if (h_tree_w) memcpy(h_tree_w + lo, hw + lo, (hi - lo) * sizeof(double));
+        };
+        std::vector<std::thread> pool;
+        for (int k = 1; k < nt; k++) pool.emplace_back(copy, k);
+        copy(0);
+        for (auto &t : pool) t.join();
     }
     if (n_iters) *n_iters = iters;
     if (timings) {
