@@ -198,7 +198,9 @@ struct PointSet {
     int64_t n = 0, nb = 0, nsb = 0;
     int d = 0, dp = 0;
     float maxabs = 0.0f;  // max |x| of the float32 values (tensor-path scaling)
-    DevBuf<float> packed, centroid, radius, sb_centroid, sb_radius;
+    DevBuf<float> centroid, radius, sb_centroid, sb_radius;
+    // dims-major block layout of the exact-fp32 FFMA scan, built on first use
+    mutable DevBuf<float> packed;
     DevBuf<double> norms, maxn;
     // tensor-core scan operand layout (knn.cu:tcpack_kernel), built on first use
     mutable DevBuf<float> tcpack;

@@ -386,10 +386,10 @@ __global__ void block_sphere_kernel(const float *__restrict__ xp, int64_t n, int
     const int64_t b = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     if (b >= nb) return;
     const int cnt = (int)(n - b * BN < BN ? n - b * BN : BN);
-    const float *blk = xp + b * (int64_t)dp * BN;
+    const float *blk = xp + b * (int64_t)BN * d;  // row-major points of the block
     for (int t = 0; t < d; t++) {
         double s = 0.0;
-        for (int j = lane; j < cnt; j += 32) s += (double)blk[(int64_t)t * BN + j];
+        for (int j = lane; j < cnt; j += 32) s += (double)blk[(int64_t)j * d + t];
         for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(FULL, s, o);
         if (lane == 0) centroid[(int64_t)t * nb + b] = (float)(s / cnt);
     }
@@ -398,7 +398,7 @@ __global__ void block_sphere_kernel(const float *__restrict__ xp, int64_t n, int
     for (int j = lane; j < cnt; j += 32) {
         double acc = 0.0;
         for (int t = 0; t < d; t++) {
-            double df = (double)blk[(int64_t)t * BN + j] - (double)centroid[(int64_t)t * nb + b];
+            double df = (double)blk[(int64_t)j * d + t] - (double)centroid[(int64_t)t * nb + b];
             acc += df * df;
         }
         r2 = fmax(r2, acc);
@@ -1240,6 +1240,16 @@ void record_profile(const EventPair &ev_order, const EventPair &ev_scan, const E
 // rows [q0, q1) of Q; `qid` (nullable) maps a query row to its id in X for
 // self-exclusion (gathered queries).  Returns the first query row without an
 // admissible candidate, or -1.
+const float *ensure_packed(const PointSet &P, cudaStream_t s) {
+    if (!P.packed) {
+        P.packed.alloc((size_t)P.nb * BN * P.dp, s);
+        const int64_t total = P.nb * BN * (int64_t)P.dp;
+        pack_blocks_kernel<<<grid_for(total, 256), 256, 0, s>>>(P.x32, P.n, P.d, P.dp, P.nb, P.packed);
+        SLK_CHECK_LAUNCH();
+    }
+    return P.packed;
+}
+
 int64_t search_ffma(const PointSet &Q, const PointSet &X, const int32_t *qid, int k, int mode,
                     const uint8_t *mask, const int32_t *qcolor, const int32_t *xcolor, int64_t q0,
                     int64_t q1, int32_t *out_idx, double *out_dist, cudaStream_t s) {
@@ -1266,7 +1276,7 @@ int64_t search_ffma(const PointSet &Q, const PointSet &X, const int32_t *qid, in
         VisitOrder V = visit_order(Q, X, qb0, qb1 - qb0, mode == MODE_COLOR ? qcolor : nullptr,
                                    xcolor, s);
         ev_order.stop(s);
-        ScanArgs sa{Q.packed, X.packed, nq, nx, X.dp, qb0, mask, qcolor, xcolor, cand, kth,
+        ScanArgs sa{ensure_packed(Q, s), ensure_packed(X, s), nq, nx, X.dp, qb0, mask, qcolor, xcolor, cand, kth,
                     q0, q1, V.sb_order, V.sb_lb, V.flat_lb, V.nvalid, X.nsb, tiles, qid};
         ev_scan.start(s);
         if (Rsel == 1) dispatch_scan<1>(mode, sa, qb1 - qb0, s);
@@ -1886,10 +1896,6 @@ std::shared_ptr<PointSet> make_pointset(const float *x32, const double *x64, int
     P->d = d;
     P->dp = ((d + KC - 1) / KC) * KC;
     P->nb = (n + BN - 1) / BN;
-    P->packed.alloc((size_t)P->nb * BN * P->dp, s);
-    int64_t total = P->nb * BN * (int64_t)P->dp;
-    pack_blocks_kernel<<<grid_for(total, 256), 256, 0, s>>>(x32, n, d, P->dp, P->nb, P->packed);
-    SLK_CHECK_LAUNCH();
     P->norms.alloc(n, s);
     norms_kernel<<<grid_for(n, 256), 256, 0, s>>>(x32, x64, n, d, P->norms);
     SLK_CHECK_LAUNCH();
@@ -1909,7 +1915,7 @@ std::shared_ptr<PointSet> make_pointset(const float *x32, const double *x64, int
     P->centroid.alloc((size_t)P->dp * P->nb, s);
     P->radius.alloc(P->nb, s);
     block_sphere_kernel<<<(unsigned)((P->nb * 32 + 255) / 256), 256, 0, s>>>(
-        P->packed, n, d, P->dp, P->nb, P->centroid, P->radius);
+        x32, n, d, P->dp, P->nb, P->centroid, P->radius);
     SLK_CHECK_LAUNCH();
     P->nsb = (P->nb + 31) / 32;
     P->sb_centroid.alloc((size_t)P->dp * P->nsb, s);
