@@ -485,8 +485,8 @@ __device__ __forceinline__ bool same_colour(const int2 *qcol, const int2 *xcol, 
 }
 
 // Bounds for every (query block, index block) pair of the launch, tiled: a
-// 32 x 32 pair tile per CTA stages both centroid sets in shared memory in
-// 64-dim slices; each thread accumulates 4 pairs.  Same arithmetic as
+// 64 x 32 pair tile per CTA stages both centroid sets in shared memory in
+// 32-dim slices; each thread accumulates 8 pairs.  Same arithmetic as
 // sphere_lb (float64 squared differences summed in dimension order).
 __global__ void __launch_bounds__(256) pair_lb_kernel(const float *__restrict__ qc, const float *__restrict__ qr,
                                                       int64_t nqb_total, const float *__restrict__ xc,
@@ -494,34 +494,38 @@ __global__ void __launch_bounds__(256) pair_lb_kernel(const float *__restrict__ 
                                                       int64_t qb0, int64_t nqb, const int2 *__restrict__ qcol,
                                                       const int2 *__restrict__ xcol, float *__restrict__ lb) {
     // staged as float64 (exact conversions): no float->double conversion in the inner loop
-    __shared__ double sq[64][33], sx[64][33];
+    __shared__ double sq[32][65], sx[32][33];
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // ty: 0..7
     const int64_t b = (int64_t)blockIdx.x * 32 + tx;
-    const int64_t ql0 = (int64_t)blockIdx.y * 32;
-    double acc[4] = {0.0, 0.0, 0.0, 0.0};
-    for (int t0 = 0; t0 < d; t0 += 64) {
-        const int tn = min(64, d - t0);
+    const int64_t ql0 = (int64_t)blockIdx.y * 64;
+    double acc[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+    for (int t0 = 0; t0 < d; t0 += 32) {
+        const int tn = min(32, d - t0);
         __syncthreads();
+        for (int e = threadIdx.x; e < tn * 64; e += 256) {
+            const int t = e >> 6, j = e & 63;
+            const int64_t qg = qb0 + ql0 + j;
+            sq[t][j] = ql0 + j < nqb ? (double)qc[(int64_t)(t0 + t) * nqb_total + qg] : 0.0;
+        }
         for (int e = threadIdx.x; e < tn * 32; e += 256) {
             const int t = e >> 5, j = e & 31;
-            const int64_t qg = qb0 + ql0 + j, xg = (int64_t)blockIdx.x * 32 + j;
-            sq[t][j] = ql0 + j < nqb ? (double)qc[(int64_t)(t0 + t) * nqb_total + qg] : 0.0;
+            const int64_t xg = (int64_t)blockIdx.x * 32 + j;
             sx[t][j] = xg < nxb ? (double)xc[(int64_t)(t0 + t) * nxb + xg] : 0.0;
         }
         __syncthreads();
         for (int t = 0; t < tn; t++) {
             const double xv = sx[t][tx];
 #pragma unroll
-            for (int i = 0; i < 4; i++) {
-                const double df = sq[t][ty * 4 + i] - xv;
+            for (int i = 0; i < 8; i++) {
+                const double df = sq[t][ty * 8 + i] - xv;
                 acc[i] += df * df;
             }
         }
     }
     if (b >= nxb) return;
 #pragma unroll
-    for (int i = 0; i < 4; i++) {
-        const int64_t ql = ql0 + ty * 4 + i;
+    for (int i = 0; i < 8; i++) {
+        const int64_t ql = ql0 + ty * 8 + i;
         if (ql >= nqb) continue;
         const int64_t q = qb0 + ql;
         float v = INFINITY;
@@ -1148,7 +1152,7 @@ VisitOrder visit_order(const QueryGroups &G, const PointSet &X, int d, const int
     V.sb_order.alloc(stotal, s);
     sort_segments(key, ids, nqb, nsb, seg, skey, V.sb_order, s);
     DevBuf<float> blk_lb(nqb * nxb, s);
-    pair_lb_kernel<<<dim3((unsigned)((nxb + 31) / 32), (unsigned)((nqb + 31) / 32)), 256, 0, s>>>(
+    pair_lb_kernel<<<dim3((unsigned)((nxb + 31) / 32), (unsigned)((nqb + 63) / 64)), 256, 0, s>>>(
         G.cent, G.rad, G.ng, X.centroid, X.radius, nxb, d, qb0, nqb, qrange, xrange.get(), blk_lb);
     SLK_CHECK_LAUNCH();
     V.flat_lb.alloc(stotal * 32, s);
