@@ -273,3 +273,30 @@ def test_adjusted_rand_index_properties():
     assert checkers.adjusted_rand_index(a, a + 7) == 1.0
     assert checkers.adjusted_rand_index(a, [0, 1, 0, 1, 0, 1]) < 0.5
     assert checkers.adjusted_rand_index([0], [3]) == 1.0
+
+
+def test_kruskal_checker_matches_oracle_kruskal(oracle, rng):
+    """The CLI's Kruskal checker agrees with the oracle's restatement on
+    random graphs with tied integer weights (forest edges and total weight)."""
+    from paper_2306_16354_b200.synthetic import random_connected_graph
+
+    for n, extra in ((50, 80), (400, 1500)):
+        s, d, w = random_connected_graph(rng, n, extra, weights="ties")
+        a, b, kw = checkers.kruskal_forest(n, s, d, w)
+        oa, ob, ow = oracle.kruskal_mst(n, s, d, w)
+        assert len(a) == len(oa) == n - 1
+        assert np.array_equal(np.sort(kw), np.sort(ow)) and kw.sum() == ow.sum()
+
+
+def test_road_graph_generator_is_deterministic():
+    import importlib.util
+
+    spec = importlib.util.spec_from_file_location(
+        "bench_mst", Path(__file__).resolve().parents[1] / "scripts" / "bench_mst.py")
+    bm = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bm)
+    n1, s1, d1, w1 = bm.road_graph(10_000, 12_000, seed=3)
+    n2, s2, d2, w2 = bm.road_graph(10_000, 12_000, seed=3)
+    assert n1 == n2 and np.array_equal(s1, s2) and np.array_equal(d1, d2) and np.array_equal(w1, w2)
+    assert abs(len(s1) - 12_000) < 600 and (w1 >= 1).all() and (w1 <= 100_000).all()
+    assert (s1 != d1).all() and d1.max() < n1
