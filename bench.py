@@ -46,16 +46,32 @@ CONFIGS = {
     "C1": dict(n=10_000, d=16, c=10, k=15, n_clusters=10),
     "C2": dict(n=100_000, d=128, c=50, k=15, n_clusters=50),
     "C3": dict(n=1_000_000, d=64, c=50, k=15, n_clusters=50),
+    # configs[3]: k-NN graph only, N(0,1) points, d in {32,128,512}, k in {8,32,64}
+    # (--d / --k pick the cell; a step is one fused_knn over all N rows)
+    "C4": dict(n=1_000_000, d=128, c=None, k=8, n_clusters=None),
     "C5": dict(n=500_000, d=32, c=1000, k=2, n_clusters=1000),
 }
+DTYPE = ("fp16x2 tcgen05 scan (hi.hi + hi.lo + lo.hi products, fp32 accumulate) + "
+         "f64 refine/certificate")
 METRIC = "end-to-end SLINK seconds at 1M×64 (k=15), 1/2/4/8 B200; kNN-tile % of peak; MST GB/s"
 SM_COUNT = 148
 FP32_LANES = 128
 
 
 def workload_name(cfg_name, c):
+    if c["c"] is None:
+        return f"{cfg_name}: k-NN graph only, N(0,1) N={c['n']} d={c['d']} k={c['k']} seed=0"
     return (f"{cfg_name}: blobs N={c['n']} d={c['d']} c={c['c']} k={c['k']} "
             f"n_clusters={c['n_clusters']} euclidean seed=0")
+
+
+def run_config(cfg_name, c, world):
+    """The config object both arms print (identical dicts)."""
+    return {"workload": workload_name(cfg_name, c),
+            "parallelism": f"query-row shards x{world}" if world > 1 else "single GPU",
+            "l2": f"inputs {c['n'] * c['d'] * 4 / 1e6:.0f} MB float32"
+                  + (" > 126 MB L2 (no explicit flush)" if c["n"] * c["d"] * 4 > 126e6
+                     else "; 200 MB L2 flush buffer rewritten before every timed step")}
 
 
 def make_points(c):
@@ -130,17 +146,19 @@ def cpu_slab_seconds(x, c, rows, threads, n_iters=2):
 
     x64 = x.astype(np.float64)
     n = len(x)
+    t0 = time.perf_counter()
+    orc.fused_knn(x64, c["k"], rows=(0, rows), threads=threads)
+    t_knn = time.perf_counter() - t0
+    scale = n / rows
+    if c["c"] is None:  # C4: k-NN graph only
+        return dict(total=scale * t_knn, knn=scale * t_knn, nn1=0.0, sample_s=t_knn)
     counts = np.full(c["c"], n // c["c"])
     counts[: n % c["c"]] += 1
     starts = np.concatenate([[0], np.cumsum(counts)[:-1]])
     colors = np.repeat(starts, counts)
     t0 = time.perf_counter()
-    orc.fused_knn(x64, c["k"], rows=(0, rows), threads=threads)
-    t_knn = time.perf_counter() - t0
-    t0 = time.perf_counter()
     orc.cross_color_1nn(x64, colors, rows=(0, rows), threads=threads)
     t_nn1 = time.perf_counter() - t0
-    scale = n / rows
     return dict(total=scale * (t_knn + n_iters * t_nn1), knn=scale * t_knn, nn1=scale * t_nn1,
                 sample_s=t_knn + t_nn1)
 
@@ -169,14 +187,17 @@ def run_reference(args, c, cfg_name):
     for _ in range(args.steps):
         vals.append(cpu_slab_seconds(x, c, rows, cores)["total"])
     v = float(np.mean(vals))
-    sample = (f"k-NN + cross-colour 1-NN of query rows [0,{rows}) against all {c['n']} points "
-              f"(BASELINE.md §3 P2), extrapolated x{c['n'] / rows:.0f}; end-to-end = kNN + 2 "
-              f"connect passes (graph stages excluded, <1% at C2)")
+    what = "k-NN" if c["c"] is None else "k-NN + cross-colour 1-NN"
+    tail = ("" if c["c"] is None else "; end-to-end = kNN + 2 connect passes (graph stages "
+            "excluded, <1% at C2)")
+    sample = (f"slab-extrapolated: {what} of query rows [0,{rows}) against all {c['n']} points "
+              f"(BASELINE.md §3 P2), extrapolated x{c['n'] / rows:.0f}{tail}")
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": "s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": v * 1e3,
         "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": {"workload": workload_name(cfg_name, c)},
+        "data": "synthetic", "config": run_config(cfg_name, c, args.gpus),
+        "extrapolated": {"slab_rows": rows, "factor": c["n"] / rows},
         "cpu_baseline": {"value": v, "unit": "s", "cores": cores, "kind": "port",
                          "sample": sample},
         "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -297,13 +318,34 @@ def run_gpu(args, c, cfg_name):
     distributed = world > 1
     if distributed:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    cfg = slk.LinkageConfig(n_clusters=c["n_clusters"], k=c["k"], seed=0)
+    knn_only = c["c"] is None
+    cfg = None if knn_only else slk.LinkageConfig(n_clusters=c["n_clusters"], k=c["k"], seed=0)
     x = make_points(c)
     x_pinned = torch.from_numpy(x).pin_memory()
     x_dev = x_pinned.to("cuda", non_blocking=False)
     pts = DevicePoints.from_tensors(x_dev)
+    flush = None
+    if x.nbytes <= 126e6:  # inputs fit in L2: overwrite a 200 MB buffer between steps
+        flush = torch.empty(50_000_000, dtype=torch.float32, device="cuda")
 
-    if distributed:
+    if knn_only:
+        from paper_2306_16354_b200.neighbors import knn_device
+
+        if distributed:
+            from paper_2306_16354_b200 import parallel
+
+            def value_step():
+                return parallel.knn_distributed(pts, c["k"])
+
+            def e2e_step():
+                return parallel.knn_distributed(x_pinned.numpy(), c["k"], to_host=True)
+        else:
+            def value_step():
+                return knn_device(pts, c["k"])
+
+            def e2e_step():
+                return slk.fused_knn(x_pinned.numpy(), c["k"])
+    elif distributed:
         from paper_2306_16354_b200 import parallel
 
         def value_step():
@@ -328,6 +370,8 @@ def run_gpu(args, c, cfg_name):
     def timed(fn, steps):
         times = []
         for _ in range(steps):
+            if flush is not None:
+                flush.fill_(1.0)
             barrier()
             s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             s.record()
@@ -360,7 +404,8 @@ def run_gpu(args, c, cfg_name):
     e2e = float(np.mean(e2e_times))
     n = c["n"]
     h2d = x.nbytes
-    d2h = (n - 1) * 4 * 8 + n * 8 + (n - 1) * 3 * 8
+    # merges (n-1)x4 f64 + labels n i64 + tree (n-1) x (2 i64 + f64); k-NN: idx i32 + dist f64
+    d2h = n * c["k"] * 12 if knn_only else (n - 1) * 4 * 8 + n * 8 + (n - 1) * 3 * 8
 
     if rank != 0:
         if distributed:
@@ -371,23 +416,23 @@ def run_gpu(args, c, cfg_name):
     roofline = make_roofline(prof, args.steps, c["d"], sm_mhz)
     cpu = None
     if not args.no_cpu_baseline and world == 1:
-        b = cpu_slab_seconds(x, c, args.cpu_rows, cpu_cores(), n_iters=max(res.connect_iters, 1)
-                             if hasattr(res, "connect_iters") else 2)
+        iters = getattr(res, "connect_iters", 2)
+        rows = args.cpu_rows if c["d"] <= 128 else max(64, args.cpu_rows // 4)
+        b = cpu_slab_seconds(x, c, rows, cpu_cores(), n_iters=max(iters, 1))
+        what = "kNN slab" if knn_only else f"kNN slab + cross-colour slab, kNN + {iters} connect passes"
         cpu = {"value": b["total"], "unit": "s", "cores": cpu_cores(), "kind": "port",
-               "sample": (f"oracle port (C restatement of the reference, OpenMP) on query rows "
-                          f"[0,{args.cpu_rows}) vs all {n} points: kNN slab + cross-colour slab, "
-                          f"extrapolated x{n / args.cpu_rows:.0f}, kNN + {getattr(res, 'connect_iters', 2)} "
-                          f"connect passes; {b['sample_s']:.1f} s of CPU work")}
+               "extrapolated": True,
+               "sample": (f"slab-extrapolated oracle port (C restatement of the reference, OpenMP) on "
+                          f"query rows [0,{rows}) vs all {n} points: {what}, extrapolated "
+                          f"x{n / rows:.0f}; {b['sample_s']:.1f} s of CPU work")}
     line = {
         "metric": METRIC, "value": value, "unit": "s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": value * 1e3, "higher_is_better": False,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f32 scan / f64 refine",
-        "data": "synthetic",
-        "config": {"workload": workload_name(cfg_name, c),
-                   "parallelism": f"query-row shards x{world}" if world > 1 else "single GPU",
-                   "l2": "inputs 256 MB > 126 MB L2 (no explicit flush)",
-                   "connect_iters": getattr(res, "connect_iters", None),
-                   "stage_ms": getattr(res, "timings", None)},
+        "scaling": "strong", "vs_baseline": None, "dtype": DTYPE,
+        "data": "synthetic" + (" N(0,1) float32" if knn_only else " Gaussian blobs float32"),
+        "config": run_config(cfg_name, c, world),
+        "connect_iters": getattr(res, "connect_iters", None),
+        "stage_ms": getattr(res, "timings", None),
         "e2e": {"value": e2e, "unit": "s", "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h), "steps_s": [round(t, 5) for t in e2e_times]},
         "value_steps_s": [round(t, 5) for t in times],
@@ -413,8 +458,15 @@ def main():
     ap.add_argument("--cpu-rows", type=int, default=1024)
     ap.add_argument("--ref-rows", type=int, default=512)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--d", type=int, default=None, help="C4: dimension (32, 128 or 512)")
+    ap.add_argument("--k", type=int, default=None, help="C4: neighbours (8, 32 or 64)")
     args = ap.parse_args()
-    c = CONFIGS[args.config]
+    c = dict(CONFIGS[args.config])
+    if args.config == "C4":
+        c["d"] = args.d or c["d"]
+        c["k"] = args.k or c["k"]
+    elif args.d or args.k:
+        ap.error("--d / --k select the C4 cell only")
     if args.impl == "reference":
         run_reference(args, c, args.config)
     else:

@@ -15,7 +15,8 @@
  *    SLK_ERR_INTERNAL / SLK_ERR_CUDA -> LinkageError.
  *  - "d_" pointers are device pointers (cudaMalloc / torch tensors) on the
  *    current device; "h_" pointers are host pointers.  Vertex / point ids are
- *    int32 on the device (N < 2^31); distances and weights are float64 with
+ *    int32 on the device (N < 2^30: merge-table node ids n + i stay below
+ *    2^31); distances and weights are float64 with
  *    the reference's exact values.  The library never frees caller memory;
  *    its scratch comes from the stream-ordered pool of the current device.
  *  - `stream` is a cudaStream_t (NULL = legacy default stream).  Calls return
@@ -215,6 +216,13 @@ int slk_last_scan_stats(int64_t *stats);
  * solves (incl. weight alteration and sorts).  reset != 0 zeroes the
  * counters after reading.  out must hold 16 doubles. */
 int slk_profile(double *out, int reset);
+
+/* Diagnostic (scripts/tc_debug.py): only the tensor-core k-NN scan over all n
+ * points, without refine: per row its raw candidate list d_cand (n x 32 int32,
+ * unused slots -1), the K'-th approximate value d_kth (n floats, scaled
+ * units), |q~|^2 d_qhat (n floats) and the power-of-two operand scale. */
+int slk_debug_tc_scan(const float *d_x32, int64_t n, int d, int k, int32_t *d_cand,
+                      float *d_kth, float *d_qhat, float *scale, void *stream);
 
 #ifdef __cplusplus
 }

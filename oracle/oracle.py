@@ -59,6 +59,8 @@ def _load():
         "orc_pairwise_l2": (None, [P, I64, P, I64, I, I, P]),
         "orc_knn": (I, [P, P, I64, I, I, I64, I64, P, P, I]),
         "orc_nn1": (I, [P, P, I64, P, P, I64, I, I, P, P, P, I64, I64, P, P, I]),
+        "orc_knn_rows": (I, [P, P, I64, I, I, P, I64, P, P, I]),
+        "orc_nn1_rows": (I, [P, P, I64, P, P, I64, I, I, P, P, P, P, I64, P, P, I]),
         "orc_edge_list_to_csr": (I64, [I64, P, P, P, I64, P, P, P]),
         "orc_csr_is_symmetric": (I, [I64, P, P, P]),
         "orc_hash_unit": (D, [I64, I64, I64]),
@@ -130,6 +132,34 @@ def fused_knn(x, k, *, squared=True, rows=None, threads=0):
     _check(_load().orc_knn(_p(x), _p(norms), n, d, k, q0, q1, _p(idx), _p(dist), threads))
     if not squared:
         dist = np.sqrt(dist)
+    return idx, dist
+
+
+def knn_rows(x, k, rows, *, threads=0):
+    """fused_knn (ref neighbors.py:246-298) for an explicit list of query rows
+    → (indices, distances), one output row per entry of ``rows``."""
+    x = _f64(x)
+    n, d = x.shape
+    rows = _i64(rows)
+    norms = row_sq_norms(x)
+    idx = np.empty((len(rows), k), dtype=np.int64)
+    dist = np.empty((len(rows), k))
+    _check(_load().orc_knn_rows(_p(x), _p(norms), n, d, k, _p(rows), len(rows), _p(idx), _p(dist),
+                                threads))
+    return idx, dist
+
+
+def cross_color_1nn_rows(x, colors, rows, *, threads=0):
+    """cross_color_1nn (ref neighbors.py:375-391) for an explicit list of
+    query rows → (dst, squared weight) per entry of ``rows``."""
+    x = _f64(x)
+    n, d = x.shape
+    rows, col = _i64(rows), _i64(colors)
+    norms = row_sq_norms(x)
+    idx = np.empty(len(rows), dtype=np.int64)
+    dist = np.empty(len(rows))
+    _check(_load().orc_nn1_rows(_p(x), _p(norms), n, _p(x), _p(norms), n, d, 2, _p(np.zeros(1, np.uint8)),
+                                _p(col), _p(col), _p(rows), len(rows), _p(idx), _p(dist), threads))
     return idx, dist
 
 

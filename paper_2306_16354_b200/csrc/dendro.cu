@@ -212,6 +212,15 @@ void extract_labels(const double *merges, int64_t n, int64_t n_clusters, int64_t
     if (n_clusters < 1 || n_clusters > n)
         throw_invalid("n_clusters must be in [1, %lld], got %lld", (long long)n, (long long)n_clusters);
     int64_t cut = (n - 1) - (n_clusters - 1), total = 2 * n - 1;
+    // row i may only reference points and the clusters of earlier rows
+    // (ref linkage.py:103-129 builds exactly such tables; a forward reference
+    // raises IndexError there and must not index out of bounds here)
+    for (int64_t i = 0; i < n - 1; i++)
+        for (int c = 0; c < 2; c++) {
+            const double v = merges[4 * i + c];
+            if (!(v >= 0.0 && v < (double)(n + i)) || v != (double)(int64_t)v)
+                throw_invalid("merge row %lld references cluster %g before it exists", (long long)i, v);
+        }
     std::vector<uint8_t> consumed(n + cut, 0);
     for (int64_t i = 0; i < cut; i++) {
         consumed[(int64_t)merges[4 * i]] = 1;

@@ -500,7 +500,7 @@ int slk_single_linkage(const float *h_x32, const double *h_x64, int64_t n, int d
         if (n_clusters > n) throw_invalid("n_clusters=%lld exceeds %lld points", (long long)n_clusters, (long long)n);
         if (k < 1) throw_invalid("k must be >= 1, got %d", k);
         if (k > n - 1) throw_invalid("k=%d exceeds N-1=%lld", k, (long long)(n - 1));
-        if (n >= (1ll << 31)) throw_invalid("n=%lld exceeds the 2^31-1 point limit", (long long)n);
+        if (n >= (1ll << 30)) throw_invalid("n=%lld exceeds the 2^30-1 point limit", (long long)n);
         StreamGuard g;
         cudaStream_t s = g.s;
         DevBuf<float> x32(n * (int64_t)d, s);
@@ -534,6 +534,7 @@ int slk_single_linkage_device(const float *d_x32, const double *d_x64, int64_t n
         if (n_clusters > n) throw_invalid("n_clusters=%lld exceeds %lld points", (long long)n_clusters, (long long)n);
         if (k < 1) throw_invalid("k must be >= 1, got %d", k);
         if (k > n - 1) throw_invalid("k=%d exceeds N-1=%lld", k, (long long)(n - 1));
+        if (n >= (1ll << 30)) throw_invalid("n=%lld exceeds the 2^30-1 point limit", (long long)n);
         single_linkage_device(d_x32, d_x64, n, d, k, n_clusters, metric, seed, max_connect_iters,
                               h_merges, h_labels, h_tree_src, h_tree_dst, h_tree_w,
                               n_connect_iters, h_timings, s);

@@ -502,12 +502,20 @@ __global__ void __launch_bounds__(Cfg<QB * HS>::NTHREADS, 1) tc_scan_kernel(TcAr
         int64_t computed = 0;
         Ring rg{0, 0u, nb};  // B stage ring (nck stages per index block)
         for (int it = 0;; it++) {
-            volatile float *part = misc->part;
-            float thr = fmaxf(fmaxf(part[0], part[1]), fmaxf(part[2], part[3]));
-            if (EW == 2) thr = fmaxf(thr, fmaxf(fmaxf(part[4], part[5]), fmaxf(part[6], part[7])));
-            thr *= a.inv_scale2;
-            // the visitor's control flow must be warp-uniform: lane 0 (which ran
-            // ahead into the barrier wait below) may have read newer thresholds
+            // the epilogue warps publish their largest row threshold with an
+            // atomic exchange and lane 0 reads them atomically: thresholds only
+            // shrink, so any value read is a valid (conservative) bound
+            float thr = 0.0f;
+            if (lane == 0) {
+                float *part = misc->part;
+                thr = fmaxf(fmaxf(atomicAdd(&part[0], 0.0f), atomicAdd(&part[1], 0.0f)),
+                            fmaxf(atomicAdd(&part[2], 0.0f), atomicAdd(&part[3], 0.0f)));
+                if (EW == 2)
+                    thr = fmaxf(thr, fmaxf(fmaxf(atomicAdd(&part[4], 0.0f), atomicAdd(&part[5], 0.0f)),
+                                           fmaxf(atomicAdd(&part[6], 0.0f), atomicAdd(&part[7], 0.0f))));
+                thr *= a.inv_scale2;
+            }
+            // the visitor's control flow must be warp-uniform
             thr = __shfl_sync(FULL, thr, 0);
             const int64_t jb = vis.next(thr, lane);
 #ifdef SLK_WATCHDOG
@@ -803,7 +811,7 @@ __global__ void __launch_bounds__(Cfg<QB * HS>::NTHREADS, 1) tc_scan_kernel(TcAr
             // largest row threshold in a units, rounded up (pruning stays conservative)
             float wm = row_ok ? __fadd_ru(thr, qq) : -INFINITY;
             for (int o = 16; o; o >>= 1) wm = fmaxf(wm, __shfl_xor_sync(FULL, wm, o));
-            if (lane == 0) ((volatile float *)misc->part)[grp * 4 + ew] = wm;
+            if (lane == 0) atomicExch(&misc->part[grp * 4 + ew], wm);
         }
         // write this row's candidate list (slots >= KP hold -1)
         if (gi >= a.row0 && gi < a.row1 && row_ok) {

@@ -26,6 +26,7 @@ from .core import (
     ValidationError,
     _trusted,
     as_point_matrix,
+    unscale_sq,
 )
 from .neighbors import DevicePoints, TileSpec, nn1_device
 
@@ -175,7 +176,8 @@ def connect_graph(x, mst_edges: EdgeList, colors: ColorArray, cfg: LinkageConfig
     torch = _lib.torch_cuda()
     pts = DevicePoints(pm)
     t_src, t_dst = _lib.ids_to_device(mst_edges.src), _lib.ids_to_device(mst_edges.dst)
-    t_w = _lib.to_device(mst_edges.weight, np.float64)
+    # forest weights in the device's (possibly power-of-two scaled) units: exact
+    t_w = _lib.to_device(np.ldexp(mst_edges.weight, -2 * pm.scale_exp), np.float64)
     col = _lib.ids_to_device(colors.colors)
     ncomp, iters, ne = colors.n_components, 0, len(mst_edges)
     iota = torch.arange(n, dtype=torch.int32, device=_lib.device())
@@ -192,11 +194,17 @@ def connect_graph(x, mst_edges: EdgeList, colors: ColorArray, cfg: LinkageConfig
         t_src, t_dst, t_w, col, ne, ncomp = msf_of_edges(n, u_src, u_dst, u_w, ne + n, cfg.seed)
         iters += 1
     return EdgeList(n, _lib.to_host(t_src[:ne]).astype(np.int64),
-                    _lib.to_host(t_dst[:ne]).astype(np.int64), _lib.to_host(t_w[:ne]))
+                    _lib.to_host(t_dst[:ne]).astype(np.int64),
+                    unscale_sq(_lib.to_host(t_w[:ne]), pm.scale_exp))
+
+
+MAX_POINTS = (1 << 30) - 1  # int32 node ids of the merge table (n + i < 2^31)
 
 
 def _validate_run(pm, cfg: LinkageConfig):
     n = pm.n_rows
+    if n > MAX_POINTS:
+        raise ValidationError(f"n={n} exceeds the {MAX_POINTS} point limit")
     if n < 2:
         raise ValidationError(f"need at least 2 points, got {n}")
     if cfg.n_clusters > n:
@@ -220,7 +228,7 @@ def _run(pm, cfg: LinkageConfig, device_points=None) -> SingleLinkageResult:
     p = lambda a: a.ctypes.data_as(ctypes.c_void_p)  # noqa: E731
     if device_points is None:
         x32 = np.ascontiguousarray(pm.float32)
-        x64 = None if pm.exact_f32 else np.ascontiguousarray(pm.data)
+        x64 = None if pm.exact_f32 else np.ascontiguousarray(pm.device_f64)
         _lib.torch_cuda()
         _lib.call("slk_single_linkage", p(x32), None if x64 is None else p(x64), n, d, cfg.k,
                   cfg.n_clusters, metric, int(cfg.seed), budget, p(merges), p(labels), p(ts),
@@ -230,6 +238,10 @@ def _run(pm, cfg: LinkageConfig, device_points=None) -> SingleLinkageResult:
         _lib.call("slk_single_linkage_device", _lib.ptr(dp.x32), _lib.ptr(dp.x64), n, d, cfg.k,
                   cfg.n_clusters, metric, int(cfg.seed), budget, p(merges), p(labels), p(ts),
                   p(td), p(tw), ctypes.byref(iters), p(tim), _lib.stream_handle())
+    e = pm.scale_exp if pm is not None else 0
+    if e:  # back from the device's power-of-two scaled units (exact)
+        tw[: n - 1] = np.ldexp(tw[: n - 1], 2 * e)
+        merges[: n - 1, 2] = np.ldexp(merges[: n - 1, 2], e if metric == 0 else 2 * e)
     # outputs of the library itself: skip re-validating 1M-row arrays
     dendro = _trusted(Dendrogram, n_points=n, merges=merges[: n - 1])
     lab = _trusted(LabelArray, labels=labels, n_clusters=cfg.n_clusters)
@@ -249,6 +261,8 @@ def single_linkage_result(x, cfg: LinkageConfig) -> SingleLinkageResult:
 
 def single_linkage_on_device(points: DevicePoints, cfg: LinkageConfig) -> SingleLinkageResult:
     """Pipeline over points already resident on the GPU (bench ``value`` leg)."""
+    if points.n > MAX_POINTS:
+        raise ValidationError(f"n={points.n} exceeds the {MAX_POINTS} point limit")
     if points.n < 2:
         raise ValidationError(f"need at least 2 points, got {points.n}")
     if cfg.n_clusters > points.n:

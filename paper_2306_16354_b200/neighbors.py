@@ -17,7 +17,8 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _lib
-from .core import ColorArray, EdgeList, NeighborPair, PointMatrix, ValidationError, as_point_matrix
+from .core import (ColorArray, EdgeList, NeighborPair, PointMatrix, ValidationError, as_point_matrix,
+                   common_scale, unscale_sq)
 
 
 @dataclass(frozen=True)
@@ -77,14 +78,16 @@ class DevicePoints:
 
     def __init__(self, pm: PointMatrix):
         self.n, self.d = pm.n_rows, pm.n_cols
+        self.scale_exp = pm.scale_exp
         self.x32 = _lib.to_device(pm.float32, np.float32)
-        self.x64 = None if pm.exact_f32 else _lib.to_device(pm.data, np.float64)
+        self.x64 = None if pm.exact_f32 else _lib.to_device(pm.device_f64, np.float64)
 
     @classmethod
     def from_tensors(cls, x32, x64=None):
         self = cls.__new__(cls)
         self.n, self.d = int(x32.shape[0]), int(x32.shape[1])
         self.x32, self.x64 = x32, x64
+        self.scale_exp = 0
         return self
 
 
@@ -139,7 +142,7 @@ def fused_knn(x, k: int, tile: TileSpec | None = None, *, squared: bool = True,
     pm = as_point_matrix(x)
     _check_k(pm.n_rows, k)
     idx, dist = knn_device(DevicePoints(pm), k)
-    out_d = _lib.to_host(dist)
+    out_d = unscale_sq(_lib.to_host(dist), pm.scale_exp)
     if not squared:
         out_d = np.sqrt(out_d)
     return KnnGraph(_lib.to_host(idx).astype(np.int64), out_d)
@@ -154,10 +157,11 @@ def fused_1nn(queries, index, mask: np.ndarray | None = None, *, squared: bool =
     if mask is not None and mask.shape != (qm.n_rows, xm.n_rows):
         raise ValidationError(
             f"mask shape {mask.shape} does not match ({qm.n_rows}, {xm.n_rows})")
+    qm, xm = common_scale(qm, xm)
     q, xx = DevicePoints(qm), DevicePoints(xm)
     dmask = None if mask is None else _lib.to_device(np.asarray(mask, dtype=bool), np.uint8)
     idx, dist = nn1_device(q, xx, mode=0 if mask is None else 1, mask=dmask)
-    d = _lib.to_host(dist)
+    d = unscale_sq(_lib.to_host(dist), qm.scale_exp)
     if not squared:
         d = np.sqrt(d)
     return [NeighborPair(int(i), float(v)) for i, v in zip(_lib.to_host(idx), d)]
@@ -175,7 +179,7 @@ def cross_color_1nn(x, colors: ColorArray, *, squared: bool = True, tile: TileSp
     pts = DevicePoints(pm)
     dcol = _lib.ids_to_device(labels)
     idx, dist = nn1_device(pts, pts, mode=2, qcolor=dcol, xcolor=dcol)
-    d = _lib.to_host(dist)
+    d = unscale_sq(_lib.to_host(dist), pm.scale_exp)
     if not squared:
         d = np.sqrt(d)
     return EdgeList(pm.n_rows, np.arange(pm.n_rows, dtype=np.int64),

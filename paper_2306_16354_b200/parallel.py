@@ -22,7 +22,8 @@ import os
 
 import numpy as np
 
-from .core import ConvergenceError, Dendrogram, EdgeList, ValidationError, as_point_matrix
+from .core import (ConvergenceError, Dendrogram, EdgeList, LinkageError, ValidationError, as_point_matrix,
+                   unscale_sq)
 from .linkage import STAGES, LabelArray, LinkageConfig, SingleLinkageResult
 
 ROW_ALIGN = 128  # query-block granularity of the scan kernel
@@ -88,11 +89,15 @@ class DeviceEngine:
 
         return msf_of_edges(n, src, dst, w, m, seed)
 
-    def finish(self, n, t_src, t_dst, t_w, cfg):
+    def scale_exp(self, pts) -> int:
+        return getattr(pts, "scale_exp", 0)
+
+    def finish(self, n, t_src, t_dst, t_w, cfg, scale_exp=0):
         from .linkage import build_dendrogram, extract_clusters
 
         tree = EdgeList(n, self._lib.to_host(t_src).astype(np.int64),
-                        self._lib.to_host(t_dst).astype(np.int64), self._lib.to_host(t_w))
+                        self._lib.to_host(t_dst).astype(np.int64),
+                        unscale_sq(self._lib.to_host(t_w), scale_exp))
         w = np.sqrt(tree.weight) if cfg.metric == "euclidean" else tree.weight
         dendro = build_dendrogram(EdgeList(n, tree.src, tree.dst, w), n)
         return tree, dendro, extract_clusters(dendro, cfg.n_clusters)
@@ -132,6 +137,33 @@ def _broadcast(dist, group, t):
         dist.broadcast(t, 0, group=group)
 
 
+_ERRORS = (ValidationError, ConvergenceError, LinkageError)  # status -1, -2, -3
+
+
+def _rank0_step(dist, group, rank, ncomp_t, fn):
+    """Runs ``fn`` (rank-0-only work returning the new component count) on rank
+    0 and broadcasts the count; a failure there is broadcast as a negative
+    status plus its message so EVERY rank raises the same exception class
+    instead of waiting in the next collective."""
+    err = None
+    if rank == 0:
+        try:
+            ncomp_t.fill_(int(fn()))
+        except _ERRORS as exc:
+            err = exc
+            code = next(i for i, cls in enumerate(_ERRORS) if isinstance(exc, cls))
+            ncomp_t.fill_(-1 - code)
+    _broadcast(dist, group, ncomp_t)
+    status = int(ncomp_t.item())
+    if status < 0:
+        msg = [str(err) if err is not None else None]
+        dist.broadcast_object_list(msg, src=0, group=group)
+        if err is not None:
+            raise err
+        raise _ERRORS[-1 - status](msg[0])
+    return status
+
+
 def single_linkage_distributed(x, cfg: LinkageConfig, *, engine=None, group=None):
     """single_linkage over all ranks of ``group``; returns the result on rank 0, None elsewhere.
 
@@ -167,13 +199,16 @@ def single_linkage_distributed(x, cfg: LinkageConfig, *, engine=None, group=None
     ncomp_t = torch.zeros(1, dtype=torch.int64, device=dev)
     colors = torch.empty(n, dtype=torch.int32, device=dev)
     state = None
-    if rank == 0:
+
+    def first_forest():
+        nonlocal state
         src = torch.arange(n, dtype=torch.int32, device=dev).repeat_interleave(cfg.k)
         state = engine.msf(n, src, idx_all.reshape(-1), dst_all.reshape(-1), n * cfg.k, cfg.seed)
-        ncomp_t.fill_(state[5])
         colors.copy_(state[3][:n])
+        return state[5]
+
+    ncomp = _rank0_step(dist, group, rank, ncomp_t, first_forest)
     del idx_all, dst_all
-    _broadcast(dist, group, ncomp_t)
     marks.append(time.perf_counter())
 
     # --- connect loop: colours broadcast, sharded cross-colour 1-NN, gather bridges
@@ -181,24 +216,27 @@ def single_linkage_distributed(x, cfg: LinkageConfig, *, engine=None, group=None
         math.ceil(math.log2(max(n, 2))) + 8
     iters = 0
     iota = torch.arange(n, dtype=torch.int32, device=dev)
-    while int(ncomp_t.item()) > 1:
+    while ncomp > 1:
         if iters >= budget:
             raise ConvergenceError(
                 f"reconnection did not converge within {budget} iterations: "
-                f"{int(ncomp_t.item())} components remain")
+                f"{ncomp} components remain")
         _broadcast(dist, group, colors)
         bidx, bw = engine.nn1_shard(pts, colors, ranges[rank])
         bidx_all = _gather_rows(torch, dist, group, bidx, rows_per_rank, world)
         bw_all = _gather_rows(torch, dist, group, bw, rows_per_rank, world)
-        if rank == 0:
+
+        def resolve():
+            nonlocal state
             ne = state[4]
             u_src = torch.cat([state[0][:ne], iota])
             u_dst = torch.cat([state[1][:ne], bidx_all])
             u_w = torch.cat([state[2][:ne], bw_all])
             state = engine.msf(n, u_src, u_dst, u_w, ne + n, cfg.seed)
-            ncomp_t.fill_(state[5])
             colors.copy_(state[3][:n])
-        _broadcast(dist, group, ncomp_t)
+            return state[5]
+
+        ncomp = _rank0_step(dist, group, rank, ncomp_t, resolve)
         iters += 1
     engine.sync()
     marks.append(time.perf_counter())
@@ -207,11 +245,41 @@ def single_linkage_distributed(x, cfg: LinkageConfig, *, engine=None, group=None
 
     # --- dendrogram + cut on rank 0
     ne = state[4]
-    tree, dendro, labels = engine.finish(n, state[0][:ne], state[1][:ne], state[2][:ne], cfg)
+    tree, dendro, labels = engine.finish(n, state[0][:ne], state[1][:ne], state[2][:ne], cfg,
+                                         engine.scale_exp(pts))
     marks.append(time.perf_counter())
     timings = {STAGES[i]: (marks[i + 1] - marks[i]) * 1e3 for i in range(4)}
     timings["extract"] = 0.0
     return SingleLinkageResult(dendro, labels, tree, iters, timings)
 
 
-__all__ = ["DeviceEngine", "shard_rows", "single_linkage_distributed", "Dendrogram", "LabelArray"]
+def knn_distributed(x, k: int, *, engine=None, group=None, to_host: bool = False):
+    """fused_knn over all ranks of ``group`` (BASELINE configs[3] sharded):
+    each rank scans its query-row shard against the replicated index, rank 0
+    gathers the lists.  Returns (idx, dist) on rank 0 (device tensors, or a
+    KnnGraph with ``to_host``), None elsewhere."""
+    import torch
+    import torch.distributed as dist
+
+    engine = engine or DeviceEngine()
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    pts = engine.upload(x)
+    n = engine.n_points(pts)
+    ranges = [shard_rows(n, world, r) for r in range(world)]
+    rows_per_rank = [b - a for a, b in ranges]
+    idx, dst = engine.knn_shard(pts, k, ranges[rank])
+    idx_all = _gather_rows(torch, dist, group, idx, rows_per_rank, world)
+    dst_all = _gather_rows(torch, dist, group, dst, rows_per_rank, world)
+    engine.sync()
+    if rank != 0:
+        return None
+    if not to_host:
+        return idx_all, dst_all
+    from .neighbors import KnnGraph
+
+    return KnnGraph(idx_all.cpu().numpy().astype(np.int64),
+                    unscale_sq(dst_all.cpu().numpy(), engine.scale_exp(pts)))
+
+
+__all__ = ["DeviceEngine", "knn_distributed", "shard_rows", "single_linkage_distributed", "Dendrogram",
+           "LabelArray"]

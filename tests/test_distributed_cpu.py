@@ -41,12 +41,20 @@ class OracleEngine:
         return torch.from_numpy(idx.astype(np.int32)), torch.from_numpy(d)
 
     def msf(self, n, src, dst, w, m, seed):
+        from paper_2306_16354_b200 import ValidationError
+
         offs, cols, ww = self.orc.edge_list_to_csr(n, src.numpy()[:m], dst.numpy()[:m], w.numpy()[:m])
-        s, d, wt, colors, nc = self.orc.solve_mst(n, offs, cols, ww, seed=seed)
+        try:
+            s, d, wt, colors, nc = self.orc.solve_mst(n, offs, cols, ww, seed=seed)
+        except self.orc.OracleError as exc:  # the device engine raises the package's classes
+            raise ValidationError(str(exc)) from None
         return (torch.from_numpy(s.astype(np.int32)), torch.from_numpy(d.astype(np.int32)),
                 torch.from_numpy(wt), torch.from_numpy(colors.astype(np.int32)), len(s), nc)
 
-    def finish(self, n, t_src, t_dst, t_w, cfg):
+    def scale_exp(self, x):
+        return 0
+
+    def finish(self, n, t_src, t_dst, t_w, cfg, scale_exp=0):
         from paper_2306_16354_b200 import Dendrogram, EdgeList, LabelArray
 
         w = t_w.numpy()
@@ -70,6 +78,16 @@ def _worker(rank, world, port, name, out):
         import paper_2306_16354_b200 as slk
         from paper_2306_16354_b200.parallel import single_linkage_distributed
 
+        if name == "duplicates":
+            # duplicate points -> zero-weight edge: rank 0's forest solve raises
+            # (ref mst.py:209-210); every rank must raise the same class
+            x = np.concatenate([np.random.default_rng(0).standard_normal((40, 3))] * 2)
+            try:
+                single_linkage_distributed(x, slk.LinkageConfig(n_clusters=2, k=3), engine=OracleEngine())
+                out.put((rank, "no error", ""))
+            except slk.LinkageError as exc:
+                out.put((rank, type(exc).__name__, str(exc)))
+            return
         g = load_golden(name)
         cfg = slk.LinkageConfig(n_clusters=int(g["n_clusters"]), k=int(g["k"]), seed=int(g["seed"]))
         res = single_linkage_distributed(g["x"], cfg, engine=OracleEngine())
@@ -80,6 +98,20 @@ def _worker(rank, world, port, name, out):
             assert res is None
     finally:
         dist.destroy_process_group()
+
+
+def _run_ranks(world, name, n_results):
+    ctx = mp.get_context("spawn")
+    out = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, name, out)) for r in range(world)]
+    for p in procs:
+        p.start()
+    results = [out.get(timeout=300) for _ in range(n_results)]
+    for p in procs:
+        p.join(timeout=300)
+        assert p.exitcode == 0
+    return results
 
 
 def _free_port():
@@ -100,20 +132,20 @@ def test_shard_rows_cover_exactly():
             assert all(a % 128 == 0 for a, _ in ranges if a < n)
 
 
-@pytest.mark.parametrize("name", ["slink_blobs_2k_d32_k2", "slink_tiny_k2"])
-def test_two_rank_pipeline_matches_reference(oracle, name):
-    ctx = mp.get_context("spawn")
-    out = ctx.Queue()
-    port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, name, out)) for r in range(2)]
-    for p in procs:
-        p.start()
-    result = out.get(timeout=300)
-    for p in procs:
-        p.join(timeout=300)
-        assert p.exitcode == 0
+@pytest.mark.parametrize("world,name", [(2, "slink_blobs_2k_d32_k2"), (2, "slink_tiny_k2"),
+                                        (3, "slink_blobs_2k_d32_k2")])
+def test_multi_rank_pipeline_matches_reference(oracle, world, name):
+    """World sizes 2 and 3 (ragged last shard: 2000 rows = 6 + 6 + 4 blocks)."""
+    (result,) = _run_ranks(world, name, 1)
     src, w, merges, labels, iters = result
     g = load_golden(name)
     assert np.array_equal(src, g["tree_src"]) and np.array_equal(w, g["tree_w"])
     assert np.array_equal(merges, g["merges"]) and np.array_equal(labels, g["labels"])
     assert iters == int(g["connect_iters"])
+
+
+def test_rank0_failure_raises_on_every_rank(oracle):
+    """A ValidationError in rank 0's forest solve is broadcast: no rank hangs."""
+    results = _run_ranks(2, "duplicates", 2)
+    assert sorted(r[0] for r in results) == [0, 1]
+    assert all(r[1] == "ValidationError" and "zero" in r[2] for r in results), results

@@ -101,3 +101,33 @@ def test_config_and_containers():
     assert d.sizes.tolist() == [2]
     with pytest.raises(slk.ValidationError):
         slk.Dendrogram(3, np.array([[0.0, 1.0, 0.5, 2.0], [0.0, 2.0, 1.0, 3.0]]))
+
+
+def test_every_exported_symbol_is_declared():
+    """No undeclared entry points: the .so's slk_* exports == include/slink.h."""
+    import subprocess
+
+    from paper_2306_16354_b200 import _lib, build
+
+    _lib.load()
+    out = subprocess.run(["nm", "-D", "--defined-only", str(build.LIB)], capture_output=True, text=True).stdout
+    exported = sorted({ln.split()[-1] for ln in out.splitlines() if ln.split()[-1].startswith("slk_")})
+    assert exported == declared_symbols()
+
+
+def test_huge_float64_points_scale_exactly():
+    """float64 inputs beyond float32 range go to the device as x * 2^-e (core.py
+    PointMatrix): the float32 copy is finite, the float64 copy is the exact
+    power-of-two scaling, and distances scale back exactly."""
+    from paper_2306_16354_b200.core import PointMatrix, unscale_sq
+
+    x = np.random.default_rng(0).standard_normal((50, 4)) * 1e40
+    pm = PointMatrix(x)
+    assert pm.scale_exp > 0 and np.isfinite(pm.float32).all()
+    assert np.abs(pm.float32).max() < 2.0 ** 64
+    assert np.array_equal(np.ldexp(pm.device_f64, pm.scale_exp), x)
+    assert np.array_equal(pm.data, x)
+    d2 = ((pm.device_f64[0] - pm.device_f64[1]) ** 2).sum()
+    assert unscale_sq(d2, pm.scale_exp) == ((x[0] - x[1]) ** 2).sum()
+    small = PointMatrix(np.ones((3, 2)))
+    assert small.scale_exp == 0 and small.exact_f32

@@ -468,3 +468,26 @@ def test_knn_pivot_blocked_matches_oracle(slk, oracle, monkeypatch, k):
     monkeypatch.setenv("SLK_NO_PIVOT_REBLOCK", "1")
     p = slk.fused_knn(x, k)
     assert np.array_equal(p.indices, g.indices) and np.array_equal(p.distances, g.distances)
+
+
+def test_huge_float64_points_match_oracle(slk, oracle):
+    """Finite float64 values beyond float32 range (ref PointMatrix accepts any
+    finite float64): the device computes on x * 2^-e and every distance,
+    weight and height scales back exactly (core.py:PointMatrix)."""
+    from paper_2306_16354_b200.synthetic import make_blobs
+
+    x = make_blobs(np.random.default_rng(21), 3000, 12, 6) * 3e38
+    for metric in ("euclidean", "sqeuclidean"):
+        cfg = slk.LinkageConfig(n_clusters=6, k=5, seed=1, metric=metric)
+        res = slk.single_linkage_result(x, cfg)
+        ref = oracle.single_linkage(x, 6, k=5, seed=1, metric=metric)
+        assert np.array_equal(res.tree.src, ref["tree_src"]) and np.array_equal(res.tree.weight, ref["tree_w"])
+        assert np.array_equal(res.dendrogram.merges, ref["merges"])
+        assert np.array_equal(res.labels.labels, ref["labels"])
+    g = slk.fused_knn(x, 7)
+    oi, od = oracle.fused_knn(x, 7, rows=(0, 500))
+    assert np.array_equal(g.indices[:500], oi) and np.array_equal(g.distances[:500], od)
+    colors = slk.ColorArray(np.repeat(np.arange(6), 500))
+    e = slk.cross_color_1nn(x, colors)
+    ci, cd = oracle.cross_color_1nn(x, colors.colors, rows=(0, 500))
+    assert np.array_equal(e.dst[:500], ci) and np.array_equal(e.weight[:500], cd)
