@@ -9,6 +9,7 @@ PyTorch only provides device memory and the current stream.
 from __future__ import annotations
 
 import ctypes
+import os
 import threading
 import warnings
 
@@ -64,7 +65,9 @@ def load():
     global _lib
     with _lock:
         if _lib is None:
-            path = _build.build()
+            # SLK_LIB_VARIANT=timeline: a diagnostic build (build.py VARIANTS)
+            variant = os.environ.get("SLK_LIB_VARIANT") or None
+            path = _build.build(variant=variant)
             lib = ctypes.CDLL(str(path))
             for name, (res, args) in SIGNATURES.items():
                 fn = getattr(lib, name)

@@ -25,27 +25,38 @@ FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxe
          "-Xptxas", "-warn-spills"]
 
 
+# Diagnostic variants (never loaded unless SLK_LIB_VARIANT names one):
+# "timeline" stamps the scan's warp-role hand-offs (tc_scan.cu, SLK_TIMELINE).
+VARIANTS = {"timeline": ["-DSLK_TIMELINE"]}
+
+
+def variant_path(name: str) -> Path:
+    return OUT_DIR / f"libslink_{name}.so"
+
+
 def sources():
     return sorted(CSRC.glob("*.cu"))
 
 
-def _stale() -> bool:
-    if not LIB.exists():
+def _stale(lib: Path = LIB) -> bool:
+    if not lib.exists():
         return True
-    t = LIB.stat().st_mtime
+    t = lib.stat().st_mtime
     deps = list(CSRC.glob("*.cu")) + list(CSRC.glob("*.cuh")) + [PKG.parent / "include" / "slink.h"]
     return any(p.stat().st_mtime > t for p in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    if not force and not _stale():
-        return LIB
+def build(force: bool = False, verbose: bool = False, variant: str | None = None) -> Path:
+    lib = variant_path(variant) if variant else LIB
+    extra = VARIANTS[variant] if variant else []
+    if not force and not _stale(lib):
+        return lib
     OUT_DIR.mkdir(exist_ok=True)
     objs = []
 
     def compile_one(src: Path):
-        obj = OUT_DIR / (src.stem + ".o")
-        cmd = [NVCC, *ARCH, *FLAGS, "-c", str(src), "-o", str(obj)]
+        obj = OUT_DIR / (src.stem + (f"_{variant}" if variant else "") + ".o")
+        cmd = [NVCC, *ARCH, *FLAGS, *extra, "-c", str(src), "-o", str(obj)]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed for {src.name}:\n{r.stdout}\n{r.stderr}")
@@ -55,16 +66,17 @@ def build(force: bool = False, verbose: bool = False) -> Path:
 
     with ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
         objs = list(ex.map(compile_one, sources()))
-    tmp = OUT_DIR / "libslink.so.tmp"
+    tmp = lib.with_suffix(".so.tmp")
     cmd = [NVCC, *ARCH, "-shared", "-o", str(tmp), *map(str, objs), "-lcudart"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
-    os.replace(tmp, LIB)
+    os.replace(tmp, lib)
     for o in objs:
         o.unlink(missing_ok=True)
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True))
+    var = next((a.split("=", 1)[1] for a in sys.argv if a.startswith("--variant=")), None)
+    print(build(force="--force" in sys.argv, verbose=True, variant=var))

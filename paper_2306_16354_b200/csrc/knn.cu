@@ -669,6 +669,7 @@ struct RefineArgs {
     // tensor-core scan (tc_scan.cu): kth in scaled units, |q^|^2 per row
     const float *qhat;        // nullptr for the exact-fp32 scan
     double scale;             // power of two applied after centring
+    int nprod;                // fp16 products per 16 dims of that scan (1 or 3)
     const int32_t *qid;       // gathered queries: -1 marks padding rows (skipped)
 };
 
@@ -733,19 +734,31 @@ __device__ double certified_floor(float a, int d, double nq, double max_xn, bool
 //   sqrt(D) >= sqrt(D~) - eta (|q'| + |x'|) - 2 sqrt(d) 2^-25
 // (eta: fp32 centring + two-term fp16 representation, 2^-25: fp16 subnormal
 // spacing / 2 of the low term).
+//
+// One-product scans (nprod = 1: hi.hi only, tc_scan.cu) represent each operand
+// by its fp16 rounding h, |v - h| <= 2^-11 |v| + 2^-25 per component, so
+//   |2<v_q,v_x> - 2<h_q,h_x>| <= 2^-9 (1 + 2^-12) |q~||x~| + 2^-24 sqrt(d) (|q~| + |x~|) + tiny
+//                             <= 2^-11 (1 + 2^-12) (|q~| + |x~|)^2 + 2^-24 sqrt(d) ((|q~| + |x~|)^2 + 1/4)
+// and D~ is the distance of the unsplit (fp32 centred) values themselves:
+// g gains 2^-11 (1 + 2^-10) + 2^-24 sqrt(d), c0 gains 2^-26 sqrt(d), and the
+// accumulation covers d (not 3d) products.
 __device__ double certified_floor_tc(float a, float qhat2, double scale, int d, double nq,
-                                     double max_xn, bool exact_f32) {
+                                     double max_xn, bool exact_f32, int nprod = 3) {
     const double sd_ = sqrt((double)d);
     // c0: + 2^-10 for the fp16 low term of the augmented norm (subnormal
     // spacing 2^-25, times 2^14 (A side) times 2 (b = -2 acc))
-    const double A = (double)a - (0x1p-25 * sd_ + 0x1p-45 * d + 0x1p-10);
+    const double c0 = 0x1p-25 * sd_ + 0x1p-45 * d + 0x1p-10 + (nprod == 1 ? 0x1p-26 * sd_ : 0.0);
+    const double A = (double)a - c0;
     if (!(A > 0.0) || !((double)a < INFINITY)) return -INFINITY;
     // |q~| of the represented query from the fp32-accumulated |v|^2 (relative
     // accumulation error <= (d + 4) 2^-24, representation 2^-22 |v| + 2^-25 sqrt(d))
     const double r = sqrt((double)qhat2 * (1.0 + (d + 4) * 0x1p-24)) * (1.0 + 0x1p-21) + 0x1p-25 * sd_;
     // + 2^-21: two-term fp16 split of the augmented norm (2^-22 relative, x2);
     // + 4 2^-23: its accumulation (one more MMA step, two products)
-    const double g = (3.0 * d + 12.0) * 0x1p-23 * 1.1 + 0x1p-21 + 0x1p-20 + 0x1p-21 + 0x1p-23 * sd_;
+    const double g = nprod == 1
+                         ? (d + 12.0) * 0x1p-23 * 1.1 + 0x1p-11 * (1.0 + 0x1p-10) + 0x1p-24 * sd_ + 0x1p-20 +
+                               0x1p-21 + 0x1p-23 * sd_
+                         : (3.0 * d + 12.0) * 0x1p-23 * 1.1 + 0x1p-21 + 0x1p-20 + 0x1p-21 + 0x1p-23 * sd_;
     const double ca = 1.0 + g, cb = 4.0 * g * r, cc = 4.0 * g * r * r - A;
     const double disc = cb * cb - 4.0 * ca * cc;
     if (!(disc > 0.0)) return -INFINITY;
@@ -814,7 +827,7 @@ __global__ void refine_kernel(RefineArgs a) {
             ok = true;  // list never filled: every admissible candidate was kept
         } else {
             double floor = a.qhat ? certified_floor_tc(kth, a.qhat[wid], a.scale, a.d, nq,
-                                                       *a.max_xnorm, a.exact_f32)
+                                                       *a.max_xnorm, a.exact_f32, a.nprod)
                                   : certified_floor(kth, a.d, nq, *a.max_xnorm, a.exact_f32);
             ok = floor > vk;
         }
@@ -1289,7 +1302,7 @@ int64_t search_ffma(const PointSet &Q, const PointSet &X, const int32_t *qid, in
         ev_scan.stop(s);
         RefineArgs ra{Q.x32, Q.x64, Q.norms, X.x32, X.x64, X.norms, d, k, nq, nx, q0, q1,
                       cand, kth, 1, nullptr, X.maxn, X.x64 == nullptr && Q.x64 == nullptr, out_idx, out_dist,
-                      fail_rows, counters, nullptr, 1.0, qid};
+                      fail_rows, counters, nullptr, 1.0, 3, qid};
         ev_refine.start(s);
         if (Rsel == 1) launch_refine<1>(ra, rows, s);
         else if (Rsel == 2) launch_refine<2>(ra, rows, s);
@@ -1390,7 +1403,7 @@ int tc_pass(const PointSet &Q, const PointSet &X, const int32_t *qid, int k, int
             const uint8_t *mask, const int32_t *qcolor, const int32_t *xcolor, int64_t q0,
             int64_t q1, float scale, float inv_scale2, int32_t *out_idx, double *out_dist,
             DevBuf<int> &fail, DevBuf<float> &kth, cudaStream_t s, const PointSet *Xscan = nullptr,
-            const int32_t *xid = nullptr, bool self_pos = false) {
+            const int32_t *xid = nullptr, bool self_pos = false, bool rerun = false) {
     ScanStats &st = scan_stats();
     const PointSet &XS = Xscan ? *Xscan : X;
     const int64_t rows = q1 - q0;
@@ -1457,14 +1470,17 @@ int tc_pass(const PointSet &Q, const PointSet &X, const int32_t *qid, int k, int
     tc::TcArgs ta{qtc, xtc, nq, nxs, d, XS.dp, tc::k_extent(d), qb0, G.cent, G.ng,
                   Q.nb, scale, inv_scale2, mask, qcolor, xcolp.get() ? xcolp.get() : xcolor,
                   cand, kth_split, qhat, q0, q1,
-                  V.sb_order, V.sb_lb, V.flat_lb, V.nvalid, XS.nsb, tiles, qid, nsplit, xid, self_pos ? 1 : 0};
+                  V.sb_order, V.sb_lb, V.flat_lb, V.nvalid, XS.nsb, tiles, qid, nsplit, xid, self_pos ? 1 : 0,
+                  tc::nprod_for(rerun)};
+    tc::timeline_arm(s);
     ev_scan.start(s);
     if (hs == 2) tc::launch_halves(mode, kp, ta, ngroups, s);
     else tc::launch(mode, kp, qbn, ta, ngroups, s);
     ev_scan.stop(s);
+    tc::timeline_dump(mode, rows, s);
     RefineArgs ra{Q.x32, Q.x64, Q.norms, X.x32, X.x64, X.norms, d, k, nq, nx, q0, q1,
                   cand, kth_split, nlists, kth, X.maxn, X.x64 == nullptr && Q.x64 == nullptr, out_idx,
-                  out_dist, fail, counters, qhat, (double)scale, qid};
+                  out_dist, fail, counters, qhat, (double)scale, ta.nprod, qid};
     ev_refine.start(s);
     switch (nlists) {
         case 1: launch_refine<1>(ra, rows, s); break;
@@ -1483,8 +1499,8 @@ int tc_pass(const PointSet &Q, const PointSet &X, const int32_t *qid, int k, int
     record_profile(ev_order, ev_scan, ev_refine, rows, nx, d, done, (qb1 - qb0) * XS.nb, true);
     const int nfail = read_scalar<int>(counters, s);
     if (trace_on())
-        fprintf(stderr, "[slk] tc_pass mode %d rows %lld (x%d blocks/CTA, split %d, halves %d): order %.2f scan %.2f refine %.2f ms, tiles %llu, uncertified %d\n",
-                mode, (long long)rows, qbn, nsplit, hs, ev_order.ms(), ev_scan.ms(), ev_refine.ms(), done, nfail);
+        fprintf(stderr, "[slk] tc_pass mode %d rows %lld (x%d blocks/CTA, split %d, halves %d, nprod %d): order %.2f scan %.2f refine %.2f ms, tiles %llu, uncertified %d\n",
+                mode, (long long)rows, qbn, nsplit, hs, ta.nprod, ev_order.ms(), ev_scan.ms(), ev_refine.ms(), done, nfail);
     st.rows_uncertified += nfail;
     profile().tc_uncertified += nfail;
     return nfail;
@@ -1851,7 +1867,8 @@ void search(const PointSet &Q, const PointSet &X, int k, int mode, const uint8_t
             DevBuf<int> fail2;
             DevBuf<float> kth2;
             const int nfail2 = tc_pass(*G.P, X, G.qid, k, tc_kp(k, true), mode, G.mask.get(), G.qcolor.get(),
-                                       xcolor, 0, G.n, scale, inv_scale2, gidx, gdist, fail2, kth2, s);
+                                       xcolor, 0, G.n, scale, inv_scale2, gidx, gdist, fail2, kth2, s, nullptr, nullptr,
+                                       false, true);
             // global query ids in the gathered set are Q row ids: scatter to q0-relative rows
             scatter_gathered_kernel<<<grid_for(G.n * k, 256), 256, 0, s>>>(gidx, gdist, G.qid, G.n,
                                                                             k, q0, out_idx, out_dist);

@@ -55,6 +55,24 @@ namespace {
 
 using namespace scan;
 
+// ------------------------------------------------------------ timeline probe
+// Diagnostic build only (-DSLK_TIMELINE, build.py variant "timeline"): each
+// warp role stamps clock64() at its hand-offs for the first TL_IT tiles of
+// CTAs 0..TL_CTAS-1; tc_pass dumps them (SLK_TIMELINE=<file>).
+#ifdef SLK_TIMELINE
+constexpr int TL_CTAS = 16, TL_EV = 12, TL_IT = 512;
+__device__ unsigned long long *g_tl;
+#define TL(ev, it)                                                                                  \
+    do {                                                                                            \
+        if (g_tl && blockIdx.x < TL_CTAS && (it) < TL_IT)                                           \
+            g_tl[((size_t)blockIdx.x * TL_EV + (ev)) * TL_IT + (it)] = clock64();                   \
+    } while (0)
+#else
+#define TL(ev, it) \
+    do {           \
+    } while (0)
+#endif
+
 // ------------------------------------------------------------ PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
     return (uint32_t)__cvta_generic_to_shared(p);
@@ -118,25 +136,6 @@ __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint
 // Instruction descriptor: F32 accumulate, F16 A and B, both K-major, M=128, N=128.
 constexpr uint32_t IDESC = (1u << 4) | (0u << 7) | (0u << 10) | ((128u >> 3) << 17) | ((128u >> 4) << 24);
 
-__device__ __forceinline__ void umma_f16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t accumulate) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-        "l"(a), "l"(b), "r"(IDESC), "r"(accumulate)
-        : "memory");
-}
-// A operand from tensor memory (lane = query row, 32-bit column c = fp16
-// elements 2c, 2c+1 of the K step): the chunked large-d kernel keeps the hi
-// term of its query tile there
-__device__ __forceinline__ void umma_f16_ta(uint32_t tmem_d, uint32_t tmem_a, uint64_t b, uint32_t accumulate) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
-        "r"(tmem_a), "l"(b), "r"(IDESC), "r"(accumulate)
-        : "memory");
-}
 __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
     asm volatile(
         "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
@@ -149,10 +148,34 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32
         "r"(r[29]), "r"(r[30]), "r"(r[31])
         : "memory");
 }
-__device__ __forceinline__ void umma_commit(uint64_t *bar) {
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                     smem_u32(bar))
-                 : "memory");
+// Warp-collective forms for the MMA warp: every lane runs the issue loop and
+// elect.sync picks one lane (always the same: the lowest active one) to issue,
+// so ptxas emits no per-instruction ELECT retry loop around a divergent issue.
+__device__ __forceinline__ void umma_f16_w(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(a), "l"(b), "r"(IDESC), "r"(accumulate)
+        : "memory");
+}
+__device__ __forceinline__ void umma_f16_ta_w(uint32_t tmem_d, uint32_t tmem_a, uint64_t b, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "r"(tmem_a), "l"(b), "r"(IDESC), "r"(accumulate)
+        : "memory");
+}
+__device__ __forceinline__ void umma_commit_w(uint64_t *bar) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(
+            smem_u32(bar))
+        : "memory");
 }
 
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
@@ -331,7 +354,7 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
 // 128-point operand tile in place (raw tc-packed fp32 -> fp16 hi/lo canonical
 // layout, K extent dk = dkm) and returns |v|^2 of the unsplit values.
 __device__ __forceinline__ float convert_tile(unsigned char *tile, int r, int dkm, int dk, float sc,
-                                              const float *s_cq) {
+                                              const float *s_cq, bool one = false) {
     const uint32_t half_bytes = (uint32_t)BM * dk * 2;
     unsigned char *row = tile + (r >> 3) * (dk * 16) + (r & 7) * 16;
     // four independent partial norms: the accumulation chain would otherwise
@@ -348,10 +371,21 @@ __device__ __forceinline__ float convert_tile(unsigned char *tile, int r, int dk
                             __fmaf_rn(u.w, sc, c0.w), __fmaf_rn(w.x, sc, c1.x), __fmaf_rn(w.y, sc, c1.y),
                             __fmaf_rn(w.z, sc, c1.z), __fmaf_rn(w.w, sc, c1.w)};
         __half2 h[4], l[4];
+        if (one) {
+            // one-product scan: the hi term only (the lo tile is never read)
 #pragma unroll
-        for (int q = 0; q < 4; q++) split2(v[2 * q], v[2 * q + 1], h[q], l[q], nrm4[q]);
-        *reinterpret_cast<uint4 *>(ph) = *reinterpret_cast<uint4 *>(h);
-        *reinterpret_cast<uint4 *>(pl) = *reinterpret_cast<uint4 *>(l);
+            for (int q = 0; q < 4; q++) {
+                h[q] = __floats2half2_rn(v[2 * q], v[2 * q + 1]);
+                nrm4[q] = __fmaf_rn(v[2 * q], v[2 * q], nrm4[q]);
+                nrm4[q] = __fmaf_rn(v[2 * q + 1], v[2 * q + 1], nrm4[q]);
+            }
+            *reinterpret_cast<uint4 *>(ph) = *reinterpret_cast<uint4 *>(h);
+        } else {
+#pragma unroll
+            for (int q = 0; q < 4; q++) split2(v[2 * q], v[2 * q + 1], h[q], l[q], nrm4[q]);
+            *reinterpret_cast<uint4 *>(ph) = *reinterpret_cast<uint4 *>(h);
+            *reinterpret_cast<uint4 *>(pl) = *reinterpret_cast<uint4 *>(l);
+        }
     }
     return __fadd_rn(__fadd_rn(nrm4[0], nrm4[1]), __fadd_rn(nrm4[2], nrm4[3]));
 }
@@ -451,6 +485,7 @@ __global__ void __launch_bounds__(Cfg<QB * HS>::NTHREADS, 1) tc_scan_kernel(TcAr
     const int dkm = dk;                      // dims (d rounded up to 16); the norm step is separate
     unsigned char *sAaug = smem + P.aaug;    // AUG: norm-step tiles of A and of each B stage
     unsigned char *sBaug = smem + P.baug;
+    const bool one = a.nprod == 1;    // one fp16 product per 16 dims (hi.hi)
 
     // ---- setup: barriers, TMEM, centring constants
     if (tid == 0) {
@@ -523,10 +558,12 @@ __global__ void __launch_bounds__(Cfg<QB * HS>::NTHREADS, 1) tc_scan_kernel(TcAr
 #endif
             if (lane == 0) {
                 // the end marker is one stage; a block is nck stages
+                TL(0, it);
                 for (int c = 0; c < (jb < 0 ? 1 : nck); c++, rg.next()) {
                     const int s = rg.s;
                     const uint32_t ph = rg.ph;
                     mbar_wait(&bempty[s], ph ^ 1u, 1, it);
+                    if (c == 0) TL(1, it);
                     if (c == 0) misc->meta_blk[it % NMETA] = (int)jb;
                     if (jb < 0) {
                         mbar_arrive(&rawfull[s]);
@@ -540,6 +577,7 @@ __global__ void __launch_bounds__(Cfg<QB * HS>::NTHREADS, 1) tc_scan_kernel(TcAr
                             bulk_g2s(s_xcol + (it % NMETA) * BN, a.xcolor + jb * BN, BN * 4, &rawfull[s]);
                     }
                 }
+                TL(2, it);
                 if (jb >= 0) computed++;
             }
             if (jb < 0) break;
@@ -558,7 +596,7 @@ __global__ void __launch_bounds__(Cfg<QB * HS>::NTHREADS, 1) tc_scan_kernel(TcAr
 #pragma unroll
             for (int q = 0; q < QB; q++) {
                 // a missing second block (odd count) converts stale smem: its rows are never output
-                s_qq[q * BM + r] = convert_tile(sA + q * stage_bytes, r, dkm, dk, sc, s_cq);
+                s_qq[q * BM + r] = convert_tile(sA + q * stage_bytes, r, dkm, dk, sc, s_cq, one);
                 if (AUG && q == 0) put_norm_terms(sAaug, r, NORM_A, NORM_A);  // shared by the group
             }
         }
@@ -570,6 +608,7 @@ __global__ void __launch_bounds__(Cfg<QB * HS>::NTHREADS, 1) tc_scan_kernel(TcAr
                 const int s = rg.s;
                 const uint32_t ph = rg.ph;
                 mbar_wait(&rawfull[s], ph, 3, it);
+                if (r == 0 && c == 0) TL(3, it);
                 const int jb = misc->meta_blk[it % NMETA];
 #ifdef SLK_WATCHDOG
                 if (r == 100) misc->dbg[1] = it * 100000 + (jb < 0 ? 99999 : jb % 100000);
@@ -580,7 +619,7 @@ __global__ void __launch_bounds__(Cfg<QB * HS>::NTHREADS, 1) tc_scan_kernel(TcAr
                     break;
                 }
                 unsigned char *tile = sB + (size_t)s * stage_bytes;
-                xx = __fadd_rn(xx, convert_tile(tile, r, kc, kc, sc, s_cq + c * kc));
+                xx = __fadd_rn(xx, convert_tile(tile, r, kc, kc, sc, s_cq + c * kc, one));
                 if (c == nck - 1) {
                     if (AUG) {
                         float t0, t1;
@@ -592,13 +631,17 @@ __global__ void __launch_bounds__(Cfg<QB * HS>::NTHREADS, 1) tc_scan_kernel(TcAr
                 }
                 fence_async_smem();  // generic-proxy smem writes -> visible to the tensor core
                 mbar_arrive(&bfull[s]);
+                if (r == 0 && c == nck - 1) TL(4, it);
             }
             if (end) break;
         }
     } else if (warp == Cfg<EW>::WARP_MMA) {
-        // ===================== MMA issuer (one elected thread)
-        if (lane == 0) {
+        // ===================== MMA issuer (the whole warp; elect.sync issues)
+        {
             const uint32_t a_base = smem_u32(sA), b_base = smem_u32(sB);
+            // descriptors advance by 256 B (one 16-dim K step) = 16 in the
+            // address field (bits 0-13, addr >> 4; shared addresses < 2^18)
+            const uint64_t aug_a = umma_desc(smem_u32(sAaug), 128, 256);
             Ring rg{0, 0u, nb};
             for (int it = 0;; it++) {
                 const int ts = it % NT;
@@ -607,17 +650,20 @@ __global__ void __launch_bounds__(Cfg<QB * HS>::NTHREADS, 1) tc_scan_kernel(TcAr
                 for (int c = 0; c < nck; c++, rg.next()) {
                 const int s = rg.s;
                 const uint32_t ph = rg.ph;
+                if (c == 0) TL(5, it);
                 mbar_wait(&bfull[s], ph, 4, it);
 #ifdef SLK_WATCHDOG
                 misc->dbg[3] = it;
 #endif
                 if (c == 0) {
+                    TL(6, it);
                     // the accumulator stage must be drained even for the end marker:
                     // two completions of tfull[ts] ahead of the epilogue would alias
                     // its phase parity
                     mbar_wait(&tempty[ts], tph ^ 1u, 5, it);
+                    TL(7, it);
                     if (misc->meta_blk[it % NMETA] < 0) {
-                        mbar_arrive(&tfull[ts]);
+                        if (lane == 0) mbar_arrive(&tfull[ts]);
                         end = true;
                         break;
                     }
@@ -627,41 +673,47 @@ __global__ void __launch_bounds__(Cfg<QB * HS>::NTHREADS, 1) tc_scan_kernel(TcAr
                 if (CK) {
                     // <q~, x~> over this chunk's K steps: hi from TMEM, lo from smem
                     const uint32_t d_tmem = tmem + (uint32_t)ts * 128;
+                    const int kg0 = c * (kc / 16);
+                    const uint64_t al0 = umma_desc(a_base + kg0 * 256, 128, (uint32_t)dk * 16);
+                    const uint64_t bh0 = umma_desc(bs, 128, sbo);
+                    const uint64_t bl0 = umma_desc(bs + half_bytes, 128, sbo);
+#pragma unroll 2
                     for (int k = 0; k < kc / 16; k++) {
-                        const int kg = c * (kc / 16) + k;
-                        const uint32_t ta = tmem + A_COL + (uint32_t)kg * 8;
-                        const uint64_t al = umma_desc(a_base + kg * 256, 128, (uint32_t)dk * 16);
-                        const uint64_t bh = umma_desc(bs + k * 256, 128, sbo);
-                        const uint64_t bl = umma_desc(bs + half_bytes + k * 256, 128, sbo);
-                        umma_f16_ta(d_tmem, ta, bh, kg > 0 ? 1u : 0u);
-                        umma_f16_ta(d_tmem, ta, bl, 1u);
-                        umma_f16(d_tmem, al, bh, 1u);
+                        const uint32_t ta = tmem + A_COL + (uint32_t)(kg0 + k) * 8;
+                        umma_f16_ta_w(d_tmem, ta, bh0 + 16u * k, (kg0 + k) > 0 ? 1u : 0u);
+                        if (!one) {
+                            umma_f16_ta_w(d_tmem, ta, bl0 + 16u * k, 1u);
+                            umma_f16_w(d_tmem, al0 + 16u * k, bh0 + 16u * k, 1u);
+                        }
                     }
                 } else {
+                const uint64_t bh0 = umma_desc(bs, 128, sbo);
+                const uint64_t bl0 = umma_desc(bs + half_bytes, 128, sbo);
+                const uint64_t aug_b = umma_desc(smem_u32(sBaug) + s * AUG_TILE, 128, 256);
 #pragma unroll
                 for (int q = 0; q < QB; q++) {
                     const uint32_t d_tmem = tmem + (uint32_t)(ts * QB + q) * 128;
                     const uint32_t aq = a_base + q * stage_bytes;
+                    const uint64_t ah0 = umma_desc(aq, 128, sbo);
+                    const uint64_t al0 = umma_desc(aq + half_bytes, 128, sbo);
                     // <q~, x~> = hi.hi + hi.lo + lo.hi (the lo.lo term, <= 2^-22 |q~||x~|, is dropped)
+#pragma unroll 4
                     for (int k = 0; k < dkm / 16; k++) {
-                        const uint64_t ah = umma_desc(aq + k * 256, 128, sbo);
-                        const uint64_t al = umma_desc(aq + half_bytes + k * 256, 128, sbo);
-                        const uint64_t bh = umma_desc(bs + k * 256, 128, sbo);
-                        const uint64_t bl = umma_desc(bs + half_bytes + k * 256, 128, sbo);
-                        umma_f16(d_tmem, ah, bh, k > 0 ? 1u : 0u);
-                        umma_f16(d_tmem, ah, bl, 1u);
-                        umma_f16(d_tmem, al, bh, 1u);
+                        umma_f16_w(d_tmem, ah0 + 16u * k, bh0 + 16u * k, k > 0 ? 1u : 0u);
+                        if (!one) {
+                            umma_f16_w(d_tmem, ah0 + 16u * k, bl0 + 16u * k, 1u);
+                            umma_f16_w(d_tmem, al0 + 16u * k, bh0 + 16u * k, 1u);
+                        }
                     }
                     // augmented step: + 2^14 (-|x~|^2 2^-15) = -|x~|^2 / 2
-                    if (AUG)
-                        umma_f16(d_tmem, umma_desc(smem_u32(sAaug), 128, 256),
-                                 umma_desc(smem_u32(sBaug) + s * AUG_TILE, 128, 256), 1u);
+                    if (AUG) umma_f16_w(d_tmem, aug_a, aug_b, 1u);
                 }
                 }
-                umma_commit(&bempty[s]);  // operands consumed: the producer may refill stage s
+                umma_commit_w(&bempty[s]);  // operands consumed: the producer may refill stage s
                 }
                 if (end) break;
-                umma_commit(&tfull[ts]);  // accumulator ready
+                umma_commit_w(&tfull[ts]);  // accumulator ready
+                TL(8, it);
             }
 #ifdef SLK_WATCHDOG
             ((volatile int *)misc->dbg)[3] = -2;
@@ -699,8 +751,10 @@ __global__ void __launch_bounds__(Cfg<QB * HS>::NTHREADS, 1) tc_scan_kernel(TcAr
         for (int it = 0;; it++) {
             const int ts = it % NT;
             const uint32_t tph = (uint32_t)(it / NT) & 1u;
+            if (warp == 4 && lane == 0) TL(9, it);
             mbar_wait(&tfull[ts], tph, 6, it);
             tc_fence_after();
+            if (warp == 4 && lane == 0) TL(10, it);
             // the convert warps wrote A (and |q~|^2) before their first bfull arrive
             if (it == 0) qq = s_qq[qbi * BM + row];
             const int slot = it % NMETA;
@@ -808,6 +862,7 @@ __global__ void __launch_bounds__(Cfg<QB * HS>::NTHREADS, 1) tc_scan_kernel(TcAr
             __syncwarp();
             tc_fence_before();
             mbar_arrive(&tempty[ts]);  // accumulator stage free (xx/xcol slots: see NMETA)
+            if (warp == 4 && lane == 0) TL(11, it);
             // largest row threshold in a units, rounded up (pruning stays conservative)
             float wm = row_ok ? __fadd_ru(thr, qq) : -INFINITY;
             for (int o = 16; o; o >>= 1) wm = fmaxf(wm, __shfl_xor_sync(FULL, wm, o));
@@ -903,6 +958,50 @@ void launch_aug(int mode, int kp, int qb, const TcArgs &args, int64_t ngroups, c
 }
 
 }  // namespace
+
+#ifdef SLK_TIMELINE
+// SLK_TIMELINE=<file>: arm the probe before a scan launch, append the stamps after it
+static unsigned long long *tl_buf = nullptr;
+void timeline_arm(cudaStream_t s) {
+    if (!getenv("SLK_TIMELINE")) return;
+    const size_t bytes = sizeof(unsigned long long) * TL_CTAS * TL_EV * TL_IT;
+    if (!tl_buf) SLK_CUDA(cudaMalloc(&tl_buf, bytes));
+    SLK_CUDA(cudaMemsetAsync(tl_buf, 0, bytes, s));
+    SLK_CUDA(cudaMemcpyToSymbolAsync(g_tl, &tl_buf, sizeof(tl_buf), 0, cudaMemcpyHostToDevice, s));
+}
+void timeline_dump(int mode, int64_t rows, cudaStream_t s) {
+    const char *path = getenv("SLK_TIMELINE");
+    if (!path || !tl_buf) return;
+    const size_t n = (size_t)TL_CTAS * TL_EV * TL_IT;
+    unsigned long long *h = (unsigned long long *)malloc(n * sizeof(unsigned long long));
+    SLK_CUDA(cudaMemcpyAsync(h, tl_buf, n * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+    SLK_CUDA(cudaStreamSynchronize(s));
+    unsigned long long *z = nullptr;
+    SLK_CUDA(cudaMemcpyToSymbol(g_tl, &z, sizeof(z)));
+    FILE *f = fopen(path, "ab");
+    if (f) {
+        const long long hdr[5] = {mode, rows, TL_CTAS, TL_EV, TL_IT};
+        fwrite(hdr, sizeof(hdr), 1, f);
+        fwrite(h, sizeof(unsigned long long), n, f);
+        fclose(f);
+    }
+    free(h);
+}
+#else
+void timeline_arm(cudaStream_t) {}
+void timeline_dump(int, int64_t, cudaStream_t) {}
+#endif
+
+int nprod_for(bool rerun) {
+    if (const char *e = getenv("SLK_TC_NPROD")) {
+        const int v = atoi(e);
+        if (v == 1 || v == 3) return v;
+    }
+    (void)rerun;
+    // measured at C3 (round 2): one product leaves 5 % of the cross-colour rows
+    // uncertified and its K' = 32 reruns cost more than the scan saves
+    return 3;
+}
 
 static int round16(int d) { return ((d + 15) / 16) * 16; }
 static bool aug_fits(int d) { return make_plan(round16(d), true, 1).nb >= 3; }

@@ -35,7 +35,16 @@ struct TcArgs {
     int nsplit;              // CTAs per query block, each scanning 1/nsplit of the visit order
     const int32_t *xid;      // index position -> id written to cand (re-blocked index), or null
     int self_pos;            // MODE_SELF over one re-blocked set: a row's own point sits at its position
+    int nprod;               // fp16 products per 16 dims: 1 (hi.hi) or 3 (hi.hi + hi.lo + lo.hi); see nprod_for
 };
+
+// fp16 products per 16 dims for a pass: 3 (certificate
+// slack 2^-22 relative to |q~||x~|); SLK_TC_NPROD=1 selects one product
+// (2^-11) for every pass.
+int nprod_for(bool rerun);
+// diagnostic timeline probe (no-ops unless built with -DSLK_TIMELINE)
+void timeline_arm(cudaStream_t s);
+void timeline_dump(int mode, int64_t rows, cudaStream_t s);
 
 // MMA K extent for d dims: d rounded up to 16, plus the augmented norm step
 // when use_aug(d) (tc_scan.cu)
