@@ -220,7 +220,10 @@ int slk_profile(double *out, int reset);
 /* Diagnostic (scripts/tc_debug.py): only the tensor-core k-NN scan over all n
  * points, without refine: per row its raw candidate list d_cand (n x 32 int32,
  * unused slots -1), the K'-th approximate value d_kth (n floats, scaled
- * units), |q~|^2 d_qhat (n floats) and the power-of-two operand scale. */
+ * units), |q~|^2 d_qhat (n floats) and the power-of-two operand scale.
+ * With SLK_DEBUG_BC=1 in the environment it runs the block-centred kernel
+ * instead: d_cand n x 64 (two column-half lists), d_kth n x 2, d_qhat = the
+ * largest visited block radius (scaled). */
 int slk_debug_tc_scan(const float *d_x32, int64_t n, int d, int k, int32_t *d_cand,
                       float *d_kth, float *d_qhat, float *scale, void *stream);
 

@@ -56,7 +56,7 @@ SIGNATURES = {
     "slk_single_linkage_device": (_I, [_P, _P, _I64, _I, _I, _I64, _I, _I64, _I64, _P, _P, _P,
                                        _P, _P, _PI64, _P, _P]),
     "slk_msf_edges": (_I, [_I64, _P, _P, _P, _I64, _I64, _P, _P, _P, _P, _PI64, _PI64, _P]),
-    "slk_debug_tc_scan": (_I, [_P, _I64, _I, _I, _P, _P, _P, _PD, _P]),
+    "slk_debug_tc_scan": (_I, [_P, _I64, _I, _I, _P, _P, _P, ctypes.POINTER(ctypes.c_float), _P]),
 }
 
 

@@ -192,6 +192,7 @@ struct EventPair {
 // knn.cu
 // A point matrix prepared for the scans: dims-major 128-point blocks, fp64
 // norms (reference order), max norm, and per-block bounding spheres.
+struct SplitIndex;  // knn.cu: tight-block copy of an index for the block-centred scan
 struct PointSet {
     const float *x32 = nullptr;
     const double *x64 = nullptr;
@@ -204,6 +205,16 @@ struct PointSet {
     DevBuf<double> norms, maxn;
     // tensor-core scan operand layout (knn.cu:tcpack_kernel), built on first use
     mutable DevBuf<float> tcpack;
+    // block-centred fp16 index records (tc_bc.cu), built on first use for one scale
+    mutable DevBuf<unsigned char> bcpack;
+    mutable float bcpack_scale = 0.0f;
+    // knn.cu:split_index: -1 not planned, 0 every block tight, 1 `split` built,
+    // 2 too many wide blocks (the block-centred scan is not used)
+    mutable std::shared_ptr<SplitIndex> split;
+    mutable int split_state = -1;
+    // virtual re-blocked index (knn.cu:split_index): position p holds row
+    // rowmap[p] of x32; spheres and the block-centred records read through it
+    const int32_t *rowmap = nullptr;
     // optional finest cluster labels (the k-NN graph's components): the
     // cross-colour re-blocking keeps their segments contiguous and aligned
     const int32_t *block_hint = nullptr;

@@ -381,15 +381,16 @@ __global__ void __launch_bounds__(NT, (R == 1 ? 2 : 1)) scan_kernel(ScanArgs a) 
 // float64 so the bound is rigorous for the values the scan sees.
 __global__ void block_sphere_kernel(const float *__restrict__ xp, int64_t n, int d, int dp,
                                     int64_t nb, float *__restrict__ centroid,
-                                    float *__restrict__ radius) {
+                                    float *__restrict__ radius, const int32_t *__restrict__ rowmap = nullptr) {
     const int lane = threadIdx.x & 31;
     const int64_t b = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     if (b >= nb) return;
     const int cnt = (int)(n - b * BN < BN ? n - b * BN : BN);
-    const float *blk = xp + b * (int64_t)BN * d;  // row-major points of the block
+    // row-major points of the block (through rowmap for a virtual re-blocked index)
+    auto row = [&](int j) { return xp + (rowmap ? (int64_t)rowmap[b * BN + j] : b * BN + j) * d; };
     for (int t = 0; t < d; t++) {
         double s = 0.0;
-        for (int j = lane; j < cnt; j += 32) s += (double)blk[(int64_t)j * d + t];
+        for (int j = lane; j < cnt; j += 32) s += (double)row(j)[t];
         for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(FULL, s, o);
         if (lane == 0) centroid[(int64_t)t * nb + b] = (float)(s / cnt);
     }
@@ -397,8 +398,9 @@ __global__ void block_sphere_kernel(const float *__restrict__ xp, int64_t n, int
     double r2 = 0.0;
     for (int j = lane; j < cnt; j += 32) {
         double acc = 0.0;
+        const float *xr = row(j);
         for (int t = 0; t < d; t++) {
-            double df = (double)blk[(int64_t)j * d + t] - (double)centroid[(int64_t)t * nb + b];
+            double df = (double)xr[t] - (double)centroid[(int64_t)t * nb + b];
             acc += df * df;
         }
         r2 = fmax(r2, acc);
@@ -670,6 +672,8 @@ struct RefineArgs {
     const float *qhat;        // nullptr for the exact-fp32 scan
     double scale;             // power of two applied after centring
     int nprod;                // fp16 products per 16 dims of that scan (1 or 3)
+    int bc;                   // block-centred scan (tc_bc.cu): qhat holds the largest visited block radius
+    int debug;                // SLK_DEBUG_CERT: print the first uncertified rows
     const int32_t *qid;       // gathered queries: -1 marks padding rows (skipped)
 };
 
@@ -774,6 +778,45 @@ __device__ double certified_floor_tc(float a, float qhat2, double scale, int d, 
     return dlo - ev;
 }
 
+// Block-centred one-product scan (tc_bc.cu).  The kernel keeps, per row, the
+// K' smallest T = fl_down(aa - 2 acc), where aa = fp32 |a|^2 of the row
+// centred on the visited block's centroid c_b (a = fl(q s - c_b s)), acc = the
+// fp32 tensor-core sum <h(a), h(x~)> - |x~|^2 / 2 (h = fp16 rounding, x~ =
+// fl(x s - c_b s), the norm through the augmented step); every dropped
+// candidate has exact aa - 2 acc >= T.  With S = |a - x~|, |x~| <= rho (the
+// largest radius of the blocks this CTA visited, scaled) and |a| <= S + rho:
+//   |aa - 2 acc - S^2| <= k1 rho (S + rho) + gam rho^2 + an ((S + rho)^2 + rho^2)
+//                         + 2^-21 rho^2 + 2^-24 sqrt(d) 1.001 (S + 2 rho) + c0,
+//   k1 = 2 (2u + u^2) + 2 gam (1 + u)^2   (u = 2^-11: fp16 rounding of both operands),
+//   gam = (d + 4) 2^-23 1.1 (accumulation), an = (d + 4) 2^-24 (fp32 norms),
+//   2^-21: two-term fp16 norm term, 2^-24 sqrt(d): fp16 subnormal spacing,
+//   c0 = 2^-10 + 2^-45 d (low norm term's spacing x 2^14 x 2; tiny products),
+// so S >= the root of S^2 + E(S) = T; then |(q - x) s| >= S (1 - 2^-24) -
+// 2^-23 rho (fp32 centring of both operands) and the float64 steps as below.
+__device__ double certified_floor_bc(float T, float rho_s, double scale, int d, double nq, double max_xn,
+                                     bool exact_f32) {
+    if (!(T < INFINITY)) return -INFINITY;
+    const double sd = sqrt((double)d);
+    const double rho = (double)rho_s * (1.0 + 0x1p-20);
+    const double u = 0x1p-11;
+    const double gam = (d + 4.0) * 0x1p-23 * 1.1;
+    const double an = (d + 4.0) * 0x1p-24;
+    const double k1 = 2.0 * (2.0 * u + u * u) + 2.0 * gam * (1.0 + u) * (1.0 + u);
+    const double c0 = 0x1p-10 + 0x1p-45 * d;
+    const double qa = 1.0 + an;
+    const double qb = k1 * rho + 2.0 * an * rho + 0x1p-24 * sd * 1.001;
+    const double qc = (k1 + gam + 2.0 * an + 0x1p-21) * rho * rho + 0x1p-23 * sd * 1.001 * rho + c0 - (double)T;
+    if (!(qc < 0.0)) return -INFINITY;
+    const double S = (-qb + sqrt(qb * qb - 4.0 * qa * qc)) / (2.0 * qa) * (1.0 - 1e-12);
+    double sdd = S * (1.0 - 0x1p-24 * 1.0001) - 0x1p-23 * 1.0001 * rho;
+    sdd = sdd / scale;  // back to data units (scale is a power of two)
+    if (!exact_f32) sdd -= 0x1p-24 * 1.01 * (sqrt(nq) + sqrt(max_xn));
+    if (!(sdd > 0.0)) return -INFINITY;
+    const double dlo = sdd * sdd * (1.0 - 1e-15);
+    const double ev = (d + 4) * 0x1p-52 * (nq + max_xn) * 1.01 + 0x1p-1074;
+    return dlo - ev;
+}
+
 template <int R>
 __global__ void refine_kernel(RefineArgs a) {
     const int lane = threadIdx.x & 31;
@@ -826,7 +869,9 @@ __global__ void refine_kernel(RefineArgs a) {
         } else if (kth == INFINITY && cand[32 * R - 1] < 0) {
             ok = true;  // list never filled: every admissible candidate was kept
         } else {
-            double floor = a.qhat ? certified_floor_tc(kth, a.qhat[wid], a.scale, a.d, nq,
+            double floor = a.bc     ? certified_floor_bc(kth, a.qhat[wid], a.scale, a.d, nq, *a.max_xnorm,
+                                                         a.exact_f32)
+                           : a.qhat ? certified_floor_tc(kth, a.qhat[wid], a.scale, a.d, nq,
                                                        *a.max_xnorm, a.exact_f32, a.nprod)
                                   : certified_floor(kth, a.d, nq, *a.max_xnorm, a.exact_f32);
             ok = floor > vk;
@@ -834,6 +879,11 @@ __global__ void refine_kernel(RefineArgs a) {
         if (!ok) {
             int slot = atomicAdd(a.fail_count, 1);
             a.fail_rows[slot] = (int)wid;
+            if (a.debug && slot < 4)
+                printf("[slk] uncertified row %lld: kth %.9g qhat %.9g vk %.17g floor %.17g bc %d nprod %d\n",
+                       (long long)gi, (double)kth, a.qhat ? (double)a.qhat[wid] : -1.0, vk,
+                       a.bc ? certified_floor_bc(kth, a.qhat[wid], a.scale, a.d, nq, *a.max_xnorm, a.exact_f32)
+                       : -1.0, a.bc, a.nprod);
         }
     }
 }
@@ -1302,7 +1352,7 @@ int64_t search_ffma(const PointSet &Q, const PointSet &X, const int32_t *qid, in
         ev_scan.stop(s);
         RefineArgs ra{Q.x32, Q.x64, Q.norms, X.x32, X.x64, X.norms, d, k, nq, nx, q0, q1,
                       cand, kth, 1, nullptr, X.maxn, X.x64 == nullptr && Q.x64 == nullptr, out_idx, out_dist,
-                      fail_rows, counters, nullptr, 1.0, 3, qid};
+                      fail_rows, counters, nullptr, 1.0, 3, 0, 0, qid};
         ev_refine.start(s);
         if (Rsel == 1) launch_refine<1>(ra, rows, s);
         else if (Rsel == 2) launch_refine<2>(ra, rows, s);
@@ -1381,6 +1431,15 @@ bool tensor_scale(const PointSet &Q, const PointSet &X, float *scale, float *inv
     return true;
 }
 
+const unsigned char *ensure_bcpack(const PointSet &P, float scale, cudaStream_t s) {
+    if (!P.bcpack || P.bcpack_scale != scale) {
+        P.bcpack.alloc((size_t)P.nb * tc::bc_record_bytes(P.d), s);
+        tc::bc_pack(P.x32, P.rowmap, P.n, P.d, P.nb, P.centroid, P.radius, scale, P.bcpack, s);
+        P.bcpack_scale = scale;
+    }
+    return P.bcpack;
+}
+
 const float *ensure_tcpack(const PointSet &P, cudaStream_t s) {
     if (!P.tcpack) {
         const int dk = tc::k_extent(P.d);
@@ -1403,7 +1462,8 @@ int tc_pass(const PointSet &Q, const PointSet &X, const int32_t *qid, int k, int
             const uint8_t *mask, const int32_t *qcolor, const int32_t *xcolor, int64_t q0,
             int64_t q1, float scale, float inv_scale2, int32_t *out_idx, double *out_dist,
             DevBuf<int> &fail, DevBuf<float> &kth, cudaStream_t s, const PointSet *Xscan = nullptr,
-            const int32_t *xid = nullptr, bool self_pos = false, bool rerun = false) {
+            const int32_t *xid = nullptr, bool self_pos = false, bool rerun = false, bool bc_ok = true,
+            const int32_t *xpos = nullptr) {
     ScanStats &st = scan_stats();
     const PointSet &XS = Xscan ? *Xscan : X;
     const int64_t rows = q1 - q0;
@@ -1412,7 +1472,10 @@ int tc_pass(const PointSet &Q, const PointSet &X, const int32_t *qid, int k, int
     const int64_t qb0 = q0 / BM, qb1 = (q1 + BM - 1) / BM;
     // query blocks per CTA: pairs share every converted index tile, when the
     // launch still fills the GPU with them
-    int qbn = tc::group_blocks(d, kp);
+    // block-centred one-product kernel for the first pass (tc_bc.cu); the
+    // re-blocked rerun keeps the query-centred three-product kernel
+    const bool bc = !rerun && bc_ok && tc::bc_supported(mode, d, kp);
+    int qbn = bc ? 1 : tc::group_blocks(d, kp);
     // pairs pay in the 1-NN passes (conversion-bound); the k-NN pass is
     // insertion-bound and only sees the extra tiles (C3: +18 %)
     const char *force_qb = getenv("SLK_TC_QB");  // 1 / 2: force singles / pairs (tests)
@@ -1441,10 +1504,10 @@ int tc_pass(const PointSet &Q, const PointSet &X, const int32_t *qid, int k, int
     // single query blocks: two epilogue warps per row, each with its own K'
     // list over half of every tile's columns (tc_scan.cu HS = 2); the refine
     // unites at most 8 lists per row
-    int hs = (qbn == 1 && tc::halves_supported(mode, d, kp)) ? 2 : 1;
+    int hs = bc ? 2 : (qbn == 1 && tc::halves_supported(mode, d, kp)) ? 2 : 1;
     if (hs == 2)
         while (nsplit > 1 && nsplit * hs > 8) nsplit /= 2;
-    if (nsplit * hs > 8) hs = 1;
+    if (nsplit * hs > 8 && !bc) hs = 1;
     const int nlists = nsplit * hs;
     DevBuf<int32_t> cand(rows * 32 * nlists, s);
     DevBuf<float> qhat(rows, s), kth_split(rows * nlists, s);
@@ -1466,21 +1529,26 @@ int tc_pass(const PointSet &Q, const PointSet &X, const int32_t *qid, int k, int
         SLK_CUDA(cudaMemsetAsync(xcolp, 0xff, (size_t)XS.nb * BN * sizeof(int32_t), s));
         SLK_CUDA(cudaMemcpyAsync(xcolp, xcolor, (size_t)nxs * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
     }
-    const float *qtc = ensure_tcpack(Q, s), *xtc = ensure_tcpack(XS, s);
+    const float *qtc = bc ? Q.x32 : ensure_tcpack(Q, s), *xtc = bc ? nullptr : ensure_tcpack(XS, s);
+    if (bc) SLK_CUDA(cudaMemsetAsync(qhat, 0, rows * sizeof(float), s));
     tc::TcArgs ta{qtc, xtc, nq, nxs, d, XS.dp, tc::k_extent(d), qb0, G.cent, G.ng,
                   Q.nb, scale, inv_scale2, mask, qcolor, xcolp.get() ? xcolp.get() : xcolor,
                   cand, kth_split, qhat, q0, q1,
                   V.sb_order, V.sb_lb, V.flat_lb, V.nvalid, XS.nsb, tiles, qid, nsplit, xid, self_pos ? 1 : 0,
-                  tc::nprod_for(rerun)};
-    tc::timeline_arm(s);
+                  bc ? 1 : tc::nprod_for(rerun), bc ? ensure_bcpack(XS, scale, s) : nullptr, xpos};
+    if (bc) tc::bc_timeline_arm(s);
+    else tc::timeline_arm(s);
     ev_scan.start(s);
-    if (hs == 2) tc::launch_halves(mode, kp, ta, ngroups, s);
+    if (bc) tc::bc_launch(mode, kp, ta, ngroups, s);
+    else if (hs == 2) tc::launch_halves(mode, kp, ta, ngroups, s);
     else tc::launch(mode, kp, qbn, ta, ngroups, s);
     ev_scan.stop(s);
-    tc::timeline_dump(mode, rows, s);
+    if (bc) tc::bc_timeline_dump(mode, rows, s);
+    else tc::timeline_dump(mode, rows, s);
     RefineArgs ra{Q.x32, Q.x64, Q.norms, X.x32, X.x64, X.norms, d, k, nq, nx, q0, q1,
                   cand, kth_split, nlists, kth, X.maxn, X.x64 == nullptr && Q.x64 == nullptr, out_idx,
-                  out_dist, fail, counters, qhat, (double)scale, ta.nprod, qid};
+                  out_dist, fail, counters, qhat, (double)scale, ta.nprod, bc ? 1 : 0,
+                  getenv("SLK_DEBUG_CERT") ? 1 : 0, qid};
     ev_refine.start(s);
     switch (nlists) {
         case 1: launch_refine<1>(ra, rows, s); break;
@@ -1500,7 +1568,7 @@ int tc_pass(const PointSet &Q, const PointSet &X, const int32_t *qid, int k, int
     const int nfail = read_scalar<int>(counters, s);
     if (trace_on())
         fprintf(stderr, "[slk] tc_pass mode %d rows %lld (x%d blocks/CTA, split %d, halves %d, nprod %d): order %.2f scan %.2f refine %.2f ms, tiles %llu, uncertified %d\n",
-                mode, (long long)rows, qbn, nsplit, hs, ta.nprod, ev_order.ms(), ev_scan.ms(), ev_refine.ms(), done, nfail);
+                mode, (long long)rows, qbn, nsplit, hs, bc ? -1 : ta.nprod, ev_order.ms(), ev_scan.ms(), ev_refine.ms(), done, nfail);
     st.rows_uncertified += nfail;
     profile().tc_uncertified += nfail;
     return nfail;
@@ -1590,6 +1658,232 @@ Gathered gather_queries(const PointSet &Q, const std::vector<int32_t> &src,
     }
     G.P = make_pointset(G.x32, G.x64.get(), G.n, d, s);
     return G;
+}
+
+// ---------------------------------------------------------------- split index
+// The block-centred scan (tc_bc.cu) bounds its error by the radius of the
+// index blocks it visits, so a block that straddles two clusters (radius far
+// above the median) would spoil the certificate of every query block near it.
+// split_index gives such an index a copy whose wide blocks are split in two by
+// 2-means (two_means_kernel, one CTA per wide block), each part padded to a whole
+// block with marked repeats of a real point; every other block keeps its
+// place.  Queries are not re-blocked: the block-centred kernel centres them on
+// the visited index block.  (2-means in float32 on the device; any split is
+// valid, a good one only keeps the new blocks tight.)
+}  // namespace
+struct SplitIndex {
+    PointSet P;                    // virtual re-blocked index over the same x32 (P.rowmap = xid)
+    DevBuf<int32_t> xid, xmark, xpos;
+    std::vector<int32_t> src;      // position -> id (pads repeat a real id)
+};
+namespace {
+
+__global__ void gather_ids_kernel(const int32_t *v, const int32_t *src, int64_t m, int32_t *out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = v[src[i]];
+}
+
+// id -> position of a re-blocked index (pads, mark < 0, skipped)
+__global__ void xpos_kernel(const int32_t *xid, const int32_t *mark, int64_t m, int32_t *xpos) {
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < m; p += (int64_t)gridDim.x * blockDim.x)
+        if (mark[p] == 0) xpos[xid[p]] = (int32_t)p;
+}
+
+// 2-means split of one wide block per CTA (128 threads, thread j = point j):
+// seeds = the point farthest from the centroid and the point farthest from
+// that one, six Lloyd steps; part[j] in {0, 1}, or all 2 if a part empties.
+__global__ void __launch_bounds__(BM) two_means_kernel(const float *__restrict__ x, int64_t n, int d,
+                                                      const int32_t *__restrict__ blocks,
+                                                      int8_t *__restrict__ part) {
+    extern __shared__ float sh[];  // c0[d], c1[d]
+    float *c0 = sh, *c1 = sh + d;
+    __shared__ float best_v[BM / 32];
+    __shared__ int best_i[BM / 32], cnt1, seed[2];
+    const int64_t b = blocks[blockIdx.x];
+    const int j = threadIdx.x, lane = j & 31, w = j >> 5;
+    const int cnt = (int)min((int64_t)BM, n - b * BM);
+    const float *xb = x + b * BM * (int64_t)d;
+    const bool real = j < cnt;
+    auto dist_to = [&](const float *c) {
+        float s2 = 0.0f;
+        if (real)
+            for (int t = 0; t < d; t++) {
+                const float df = xb[(int64_t)j * d + t] - c[t];
+                s2 = fmaf(df, df, s2);
+            }
+        return real ? s2 : -1.0f;
+    };
+    auto argmax = [&](float v) {
+        int i = j;
+        for (int o = 16; o; o >>= 1) {
+            const float ov = __shfl_xor_sync(FULL, v, o);
+            const int oi = __shfl_xor_sync(FULL, i, o);
+            if (ov > v || (ov == v && oi < i)) v = ov, i = oi;
+        }
+        if (lane == 0) best_v[w] = v, best_i[w] = i;
+        __syncthreads();
+        float bv = best_v[0];
+        int bi = best_i[0];
+        for (int q = 1; q < BM / 32; q++)
+            if (best_v[q] > bv) bv = best_v[q], bi = best_i[q];
+        __syncthreads();
+        return bi;
+    };
+    // centroid
+    for (int t = j; t < d; t += BM) {
+        float s2 = 0.0f;
+        for (int r = 0; r < cnt; r++) s2 += xb[(int64_t)r * d + t];
+        c0[t] = s2 / cnt;
+    }
+    __syncthreads();
+    const int a0 = argmax(dist_to(c0));
+    for (int t = j; t < d; t += BM) c0[t] = xb[(int64_t)a0 * d + t];
+    __syncthreads();
+    const int a1 = argmax(dist_to(c0));
+    for (int t = j; t < d; t += BM) c1[t] = xb[(int64_t)a1 * d + t];
+    __syncthreads();
+    int my = 0;
+    bool ok = true;
+    for (int iter = 0; iter < 6 && ok; iter++) {
+        my = dist_to(c1) < dist_to(c0) ? 1 : 0;
+        if (j == 0) cnt1 = 0;
+        __syncthreads();
+        if (real && my) atomicAdd(&cnt1, 1);
+        __syncthreads();
+        const int n1 = cnt1;
+        ok = n1 > 0 && n1 < cnt;
+        __syncthreads();
+        if (!ok) break;
+        part[blockIdx.x * (int64_t)BM + j] = (int8_t)my;
+        __syncthreads();
+        for (int t = j; t < d; t += BM) {
+            float s0 = 0.0f, s1 = 0.0f;
+            for (int r = 0; r < cnt; r++) {
+                const float v = xb[(int64_t)r * d + t];
+                if (part[blockIdx.x * (int64_t)BM + r]) s1 += v;
+                else s0 += v;
+            }
+            c0[t] = s0 / (cnt - n1);
+            c1[t] = s1 / n1;
+        }
+        __syncthreads();
+    }
+    (void)seed;
+    part[blockIdx.x * (int64_t)BM + j] = ok ? (int8_t)my : (int8_t)2;
+}
+
+// blocks whose radius exceeds twice the median radius
+std::vector<int64_t> wide_blocks(const PointSet &X, float &lim, cudaStream_t s) {
+    const int64_t nb = X.nb;
+    std::vector<float> r(nb);
+    SLK_CUDA(cudaMemcpyAsync(r.data(), X.radius.get(), nb * sizeof(float), cudaMemcpyDeviceToHost, s));
+    SLK_CUDA(cudaStreamSynchronize(s));
+    std::vector<float> sorted(r);
+    std::nth_element(sorted.begin(), sorted.begin() + nb / 2, sorted.end());
+    lim = 2.0f * sorted[nb / 2];
+    std::vector<int64_t> wide;
+    for (int64_t b = 0; b < nb; b++)
+        if (r[b] > lim) wide.push_back(b);
+    return wide;
+}
+
+int split_index(const PointSet &X, cudaStream_t s) {
+    if (X.split_state >= 0) return X.split_state;
+    trace_mark("split index: plan");
+    const int64_t n = X.n, nb = X.nb;
+    const int d = X.d;
+    float lim = 0.0f;
+    const std::vector<int64_t> wide = wide_blocks(X, lim, s);
+    if (wide.empty() || getenv("SLK_NO_SPLIT_INDEX")) return X.split_state = 0;
+    if ((double)wide.size() > 0.25 * (double)nb) return X.split_state = 2;
+    // 2-means of the wide blocks on the device; the host reads the parts
+    const int nw = (int)wide.size();
+    thread_local PinnedBuf<int32_t> wstage;
+    thread_local PinnedBuf<int8_t> pstage;
+    int32_t *hwb = wstage.get(nw);
+    for (int w = 0; w < nw; w++) hwb[w] = (int32_t)wide[w];
+    DevBuf<int32_t> dwide(nw, s);
+    DevBuf<int8_t> dpart((size_t)nw * BM, s);
+    SLK_CUDA(cudaMemcpyAsync(dwide.get(), hwb, nw * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+    two_means_kernel<<<nw, BM, 2 * d * sizeof(float), s>>>(X.x32, n, d, dwide, dpart);
+    SLK_CHECK_LAUNCH();
+    int8_t *hpart = pstage.get((size_t)nw * BM);
+    SLK_CUDA(cudaMemcpyAsync(hpart, dpart.get(), (size_t)nw * BM, cudaMemcpyDeviceToHost, s));
+    SLK_CUDA(cudaStreamSynchronize(s));
+    auto SI = std::make_shared<SplitIndex>();
+    std::vector<int32_t> mark;
+    SI->src.reserve(n + 2 * BM * wide.size());
+    size_t wi = 0;
+    std::vector<int> part(BM);
+    auto pad = [&](int32_t rep) {
+        while (SI->src.size() % BM) {
+            SI->src.push_back(rep);
+            mark.push_back(-1);
+        }
+    };
+    for (int64_t b = 0; b < nb; b++) {
+        const int cnt = (int)std::min<int64_t>(BM, n - b * BM);
+        bool split = false;
+        if (wi < wide.size() && wide[wi] == b) {
+            split = hpart[wi * BM] != 2;
+            for (int j = 0; j < cnt; j++) part[j] = hpart[wi * BM + j];
+            wi++;
+        }
+        for (int h = 0; h < (split ? 2 : 1); h++) {
+            int32_t first = -1;
+            for (int j = 0; j < cnt; j++) {
+                if (split && part[j] != h) continue;
+                const int32_t id = (int32_t)(b * BM + j);
+                if (first < 0) first = id;
+                SI->src.push_back(id);
+                mark.push_back(0);
+            }
+            if (split) pad(first);
+        }
+    }
+    const int64_t m = (int64_t)SI->src.size();
+    trace_mark("split index: 2-means");
+    SI->xid.alloc(m, s);
+    SI->xmark.alloc(m, s);
+    SI->xpos.alloc(n, s);
+    {
+        thread_local PinnedBuf<int32_t> stage;
+        int32_t *h = stage.get(2 * (size_t)m);
+        memcpy(h, SI->src.data(), m * sizeof(int32_t));
+        memcpy(h + m, mark.data(), m * sizeof(int32_t));
+        SLK_CUDA(cudaMemcpyAsync(SI->xid.get(), h, m * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+        SLK_CUDA(cudaMemcpyAsync(SI->xmark.get(), h + m, m * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+        xpos_kernel<<<grid_for(m, 256), 256, 0, s>>>(SI->xid, SI->xmark, m, SI->xpos);
+        SLK_CHECK_LAUNCH();
+    }
+    // the virtual point set: same matrix, positions through xid, its own spheres
+    PointSet &V = SI->P;
+    V.x32 = X.x32;
+    V.x64 = X.x64;
+    V.rowmap = SI->xid;
+    V.n = m;
+    V.d = d;
+    V.dp = X.dp;
+    V.nb = (m + BN - 1) / BN;
+    V.maxabs = X.maxabs;
+    V.centroid.alloc((size_t)V.dp * V.nb, s);
+    V.radius.alloc(V.nb, s);
+    block_sphere_kernel<<<(unsigned)((V.nb * 32 + 255) / 256), 256, 0, s>>>(X.x32, m, d, V.dp, V.nb, V.centroid,
+                                                                          V.radius, SI->xid);
+    SLK_CHECK_LAUNCH();
+    V.nsb = (V.nb + 31) / 32;
+    V.sb_centroid.alloc((size_t)V.dp * V.nsb, s);
+    V.sb_radius.alloc(V.nsb, s);
+    superblock_sphere_kernel<<<(unsigned)((V.nsb * 32 + 255) / 256), 256, 0, s>>>(
+        V.centroid, V.radius, V.nb, d, V.nsb, V.sb_centroid, V.sb_radius);
+    SLK_CHECK_LAUNCH();
+    SLK_CUDA(cudaStreamSynchronize(s));  // host vectors go out of scope
+    trace_mark("split index: built");
+    if (trace_on())
+        fprintf(stderr, "[slk] split index: %zu wide blocks (radius > %.3g), %lld -> %lld positions\n", wide.size(),
+                (double)lim, (long long)n, (long long)m);
+    X.split = SI;
+    return X.split_state = 1;
 }
 
 __global__ void iota_ids_kernel(int32_t *v, int64_t n) {
@@ -1779,9 +2073,12 @@ void search(const PointSet &Q, const PointSet &X, int k, int mode, const uint8_t
             DevBuf<int> gfail;
             DevBuf<float> gkth;
             trace_mark("colour blocks");
+            // the block-centred scan needs tight index blocks (no straddling segments)
+            float lim;
+            const bool bc_ok = tc::bc_supported(mode, d, tc_kp(k, false)) && wide_blocks(*CG.P, lim, s).empty();
             const int gn = tc_pass(*CG.P, X, CG.qid, k, tc_kp(k, false), mode, nullptr, CG.qcolor.get(),
                                    CG.qcolor.get(), 0, CG.n, scale, inv_scale2, gidx, gdist, gfail, gkth, s,
-                                   CG.P.get(), xid.get());
+                                   CG.P.get(), xid.get(), false, false, bc_ok);
             scatter_gathered_kernel<<<grid_for(CG.n * k, 256), 256, 0, s>>>(gidx, gdist, CG.qid, CG.n, k, q0,
                                                                              out_idx, out_dist);
             SLK_CHECK_LAUNCH();
@@ -1808,8 +2105,11 @@ void search(const PointSet &Q, const PointSet &X, int k, int mode, const uint8_t
             DevBuf<int> gfail;
             DevBuf<float> gkth;
             trace_mark("pivot blocks");
+            float lim;
+            const bool bc_ok = tc::bc_supported(mode, d, tc_kp(k, false)) && wide_blocks(*PG.P, lim, s).empty();
             const int gn = tc_pass(*PG.P, X, PG.qid, k, tc_kp(k, false), mode, nullptr, nullptr, xmark.get(), 0,
-                                   PG.n, scale, inv_scale2, gidx, gdist, gfail, gkth, s, PG.P.get(), xid.get(), true);
+                                   PG.n, scale, inv_scale2, gidx, gdist, gfail, gkth, s, PG.P.get(), xid.get(), true,
+                                   false, bc_ok);
             scatter_gathered_kernel<<<grid_for(PG.n * k, 256), 256, 0, s>>>(gidx, gdist, PG.qid, PG.n, k, q0,
                                                                              out_idx, out_dist);
             SLK_CHECK_LAUNCH();
@@ -1821,9 +2121,27 @@ void search(const PointSet &Q, const PointSet &X, int k, int mode, const uint8_t
             }
             nfail = gn;
         }
-        if (nfail < 0)
-            nfail = tc_pass(Q, X, nullptr, k, tc_kp(k, false), mode, mask, qcolor, xcolor, q0, q1, scale,
-                            inv_scale2, out_idx, out_dist, fail, kth, s);
+        if (nfail < 0) {
+            // block-centred scan: its index blocks must be tight (split_index)
+            const int st = tc::bc_supported(mode, d, tc_kp(k, false)) ? split_index(X, s) : 2;
+            if (st == 1) {
+                SplitIndex &SI = *X.split;
+                const int64_t m = SI.P.n;
+                DevBuf<int32_t> xcs;
+                if (mode == MODE_COLOR) {
+                    // pads repeat a real point: same colour, harmless duplicates for k = 1
+                    xcs.alloc(m, s);
+                    gather_ids_kernel<<<grid_for(m, 256), 256, 0, s>>>(xcolor, SI.xid, m, xcs);
+                    SLK_CHECK_LAUNCH();
+                }
+                nfail = tc_pass(Q, X, nullptr, k, tc_kp(k, false), mode, mask, qcolor,
+                                mode == MODE_COLOR ? xcs.get() : SI.xmark.get(), q0, q1, scale, inv_scale2,
+                                out_idx, out_dist, fail, kth, s, &SI.P, SI.xid, false, false, true, SI.xpos);
+            } else {
+                nfail = tc_pass(Q, X, nullptr, k, tc_kp(k, false), mode, mask, qcolor, xcolor, q0, q1, scale,
+                                inv_scale2, out_idx, out_dist, fail, kth, s, nullptr, nullptr, false, false, st == 0);
+            }
+        }
         (void)Rsel;
         if (nfail > 0) {
             // Uncertified rows mostly sit in query blocks that straddle two
@@ -2037,7 +2355,15 @@ void debug_tc_scan(const float *x32, int64_t n, int d, int k, int32_t *cand, flo
     tc::TcArgs ta{tcp, tcp, n, n, d, P->dp, tc::k_extent(d), 0, G.cent, G.ng,
                   P->nb, scale, inv2, nullptr, nullptr, nullptr, cand, kth, qhat, 0, n,
                   V.sb_order, V.sb_lb, V.flat_lb, V.nvalid, P->nsb, tiles, nullptr, 1};
-    tc::launch(scan::MODE_SELF, tc_kp(k, false), 1, ta, nqb, s);
+    if (getenv("SLK_DEBUG_BC")) {
+        // block-centred kernel: cand [n][2][32], kth [n][2], qhat = visited radius bits
+        ta.qp = x32;
+        ta.bcx = ensure_bcpack(*P, scale, s);
+        SLK_CUDA(cudaMemsetAsync(qhat, 0, n * sizeof(float), s));
+        tc::bc_launch(scan::MODE_SELF, tc_kp(k, false), ta, nqb, s);
+    } else {
+        tc::launch(scan::MODE_SELF, tc_kp(k, false), 1, ta, nqb, s);
+    }
     SLK_CUDA(cudaStreamSynchronize(s));
     *scale_out = scale;
 }

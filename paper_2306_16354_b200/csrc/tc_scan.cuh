@@ -36,12 +36,27 @@ struct TcArgs {
     const int32_t *xid;      // index position -> id written to cand (re-blocked index), or null
     int self_pos;            // MODE_SELF over one re-blocked set: a row's own point sits at its position
     int nprod;               // fp16 products per 16 dims: 1 (hi.hi) or 3 (hi.hi + hi.lo + lo.hi); see nprod_for
+    const unsigned char *bcx;  // block-centred kernel (tc_bc.cu): bc-packed index records; qp = raw query rows
+    const int32_t *xpos;     // block-centred kernel over a re-blocked index: id -> position (self exclusion), or null
 };
 
 // fp16 products per 16 dims for a pass: 3 (certificate
 // slack 2^-22 relative to |q~||x~|); SLK_TC_NPROD=1 selects one product
 // (2^-11) for every pass.
 int nprod_for(bool rerun);
+// Block-centred one-product kernel (tc_bc.cu): index
+// converted once per call (bc_pack, bc_record_bytes per 128-point block),
+// queries re-centred per tile into tensor memory; two column-half lists per
+// row, the refine's certificate takes the largest visited block radius from
+// qhat (float bits, zero-initialised).
+bool bc_supported(int mode, int d, int kp);
+size_t bc_record_bytes(int d);
+// rowmap (optional): position p of the index is row rowmap[p] of x32
+void bc_pack(const float *x32, const int32_t *rowmap, int64_t n, int d, int64_t nb, const float *centroid,
+             const float *radius, float scale, unsigned char *out, cudaStream_t s);
+void bc_launch(int mode, int kp, const TcArgs &args, int64_t ngroups, cudaStream_t s);
+void bc_timeline_arm(cudaStream_t s);
+void bc_timeline_dump(int mode, int64_t rows, cudaStream_t s);
 // diagnostic timeline probe (no-ops unless built with -DSLK_TIMELINE)
 void timeline_arm(cudaStream_t s);
 void timeline_dump(int mode, int64_t rows, cudaStream_t s);

@@ -1,0 +1,9 @@
+O=gpurun_out/${TAG:-bc}
+mkdir -p $O
+rm -f $O/*.tl
+SLK_TRACE=1 timeout 300 python bench.py --config C3 --no-cpu-baseline --steps 2 > $O/bench_C3.log 2>&1
+SLK_LIB_VARIANT=timeline SLK_TIMELINE=$O/knn.tl timeout 300 python scripts/profile_scan.py knn 1000000 64 50 15 > $O/knn.log 2>&1
+SLK_LIB_VARIANT=timeline SLK_TIMELINE=$O/cc.tl timeout 300 python scripts/profile_scan.py cc 1000000 64 50 1 > $O/cc.log 2>&1
+for f in $O/*.tl; do echo $f; python scripts/timeline.py $f; done > $O/summary.txt 2>&1
+timeout 1200 python -m pytest tests -m gpu -q -x --deselect "tests/test_configs_gpu.py::test_pipeline_digest[C3]" --deselect "tests/test_configs_gpu.py::test_pipeline_digest[C5]" > $O/pytest_gpu.log 2>&1; echo "rc=$?" >> $O/pytest_gpu.log
+for cfg in C5 C2 C1; do SLK_TRACE=1 timeout 300 python bench.py --config $cfg --no-cpu-baseline --steps 2 > $O/bench_${cfg}.log 2>&1; done
