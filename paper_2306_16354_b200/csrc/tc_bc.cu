@@ -271,12 +271,12 @@ __global__ void __launch_bounds__(Shape<DK, KP>::NTHREADS, 1) tc_bc_kernel(TcArg
             mbar_init(&empty[s], 1);
         }
         for (int s = 0; s < NA; s++) {
-            mbar_init(&afull[s], 128 * NCG);
+            mbar_init(&afull[s], 4 * NCG);  // one arrival per convert warp
             mbar_init(&aempty[s], 1);
         }
         for (int s = 0; s < NT; s++) {
             mbar_init(&tfull[s], 1);
-            mbar_init(&tempty[s], 256);
+            mbar_init(&tempty[s], 8);  // one arrival per epilogue warp
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         for (int i = 0; i < 8; i++) misc->part[i] = INFINITY;
@@ -395,7 +395,8 @@ __global__ void __launch_bounds__(Shape<DK, KP>::NTHREADS, 1) tc_bc_kernel(TcArg
             if (r == 0 && g == 0)
                 atomicMax(&misc->rho_bits, __float_as_uint(*reinterpret_cast<const float *>(rec + rec_rho(DK))));
             tc_fence_before();
-            mbar_arrive(&afull[slot]);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&afull[slot]);
             if (r == 0 && g == 0) TL(4, it);
         }
     } else if (warp == WARP_MMA) {
@@ -549,9 +550,9 @@ __global__ void __launch_bounds__(Shape<DK, KP>::NTHREADS, 1) tc_bc_kernel(TcArg
                     chunk(dot, c0);
                 }
             }
-            __syncwarp();
             tc_fence_before();
-            mbar_arrive(&tempty[ts]);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[ts]);
             if (warp == WARP_EPI && lane == 0) TL(11, it);
             // warp maximum of the row thresholds in one REDUX (order-preserving
             // float -> uint map), published for the producer's pruning

@@ -309,12 +309,12 @@ __global__ void __launch_bounds__(Cfg<QB * HS>::NTHREADS, 1) tc_scan_kernel(TcAr
     if (tid == 0) {
         for (int s = 0; s < MAX_NB; s++) {
             mbar_init(&rawfull[s], 1);
-            mbar_init(&bfull[s], 128);
+            mbar_init(&bfull[s], 4);  // one arrival per convert warp
             mbar_init(&bempty[s], 1);
         }
         for (int s = 0; s < NT; s++) {
             mbar_init(&tfull[s], 1);
-            mbar_init(&tempty[s], 128 * EW);
+            mbar_init(&tempty[s], 4 * EW);  // one arrival per epilogue warp
         }
         mbar_init(afull, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -432,7 +432,8 @@ __global__ void __launch_bounds__(Cfg<QB * HS>::NTHREADS, 1) tc_scan_kernel(TcAr
                 if (r == 100) misc->dbg[1] = it * 100000 + (jb < 0 ? 99999 : jb % 100000);
 #endif
                 if (jb < 0) {
-                    mbar_arrive(&bfull[s]);
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&bfull[s]);
                     end = true;
                     break;
                 }
@@ -448,7 +449,8 @@ __global__ void __launch_bounds__(Cfg<QB * HS>::NTHREADS, 1) tc_scan_kernel(TcAr
                     }
                 }
                 fence_async_smem();  // generic-proxy smem writes -> visible to the tensor core
-                mbar_arrive(&bfull[s]);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&bfull[s]);
                 if (r == 0 && c == nck - 1) TL(4, it);
             }
             if (end) break;
@@ -677,9 +679,9 @@ __global__ void __launch_bounds__(Cfg<QB * HS>::NTHREADS, 1) tc_scan_kernel(TcAr
                     thr = lv[KP - 1];
                 }
             }
-            __syncwarp();
             tc_fence_before();
-            mbar_arrive(&tempty[ts]);  // accumulator stage free (xx/xcol slots: see NMETA)
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[ts]);  // accumulator stage free (xx/xcol slots: see NMETA)
             if (warp == 4 && lane == 0) TL(11, it);
             // largest row threshold in a units, rounded up (pruning stays conservative)
             float wm = row_ok ? __fadd_ru(thr, qq) : -INFINITY;
