@@ -376,6 +376,9 @@ __global__ void __launch_bounds__(Shape<DK, KP>::NTHREADS, 1) tc_bc_kernel(TcArg
             const float *cneg = reinterpret_cast<const float *>(rec + rec_cneg(DK)) + g * DC;
             uint32_t h[DC / 2];
             float n4[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+#ifdef SLK_ABL_NOCONV
+            if (false)
+#endif
 #pragma unroll
             for (int t = 0; t < DC; t += 4) {
                 const float4 c = *reinterpret_cast<const float4 *>(cneg + t);
@@ -424,10 +427,16 @@ __global__ void __launch_bounds__(Shape<DK, KP>::NTHREADS, 1) tc_bc_kernel(TcArg
             const uint32_t d_tmem = tmem + (uint32_t)ts * 128;
             const uint32_t a_tmem = tmem + ACOL + (uint32_t)slot * (DK / 2);
             const uint64_t b0 = umma_desc(bs, 128, SBO);
+#ifndef SLK_ABL_NOMMA
 #pragma unroll
             for (int k = 0; k < DK / 16; k++) umma_f16_ta_w(d_tmem, a_tmem + 8u * k, b0 + 16u * k, k > 0 ? 1u : 0u);
             // augmented step: + 2^14 (-|x~|^2 2^-15) = -|x~|^2 / 2
             umma_f16_w(d_tmem, aug_a, umma_desc(bs + rec_hi(DK), 128, 256), 1u);
+#else
+            (void)a_tmem;
+            (void)b0;
+            (void)aug_a;
+#endif
             umma_commit_w(&empty[rg.s]);
             umma_commit_w(&aempty[slot]);
             umma_commit_w(&tfull[ts]);
@@ -458,7 +467,11 @@ __global__ void __launch_bounds__(Shape<DK, KP>::NTHREADS, 1) tc_bc_kernel(TcArg
             const int ts = it % NT;
             const uint32_t tph = (uint32_t)(it / NT) & 1u;
             if (warp == WARP_EPI && lane == 0) TL(9, it);
+#ifdef SLK_EPI_SPIN
+            mbar_wait_spin(&tfull[ts], tph);
+#else
             mbar_wait(&tfull[ts], tph, 6, it);
+#endif
             tc_fence_after();
             if (warp == WARP_EPI && lane == 0) TL(10, it);
             const int slot = it % NMETA;
@@ -534,6 +547,9 @@ __global__ void __launch_bounds__(Shape<DK, KP>::NTHREADS, 1) tc_bc_kernel(TcArg
                 }
                 nthr = 0.5f * __fsub_rd(aa, thr);
             };
+#ifdef SLK_ABL_NOEPI
+            if (false)
+#endif
             if (KP <= 8) {
                 // K' = 8: both chunks of the half in one TMEM round trip
                 float da[CH], db[CH];
@@ -556,6 +572,9 @@ __global__ void __launch_bounds__(Shape<DK, KP>::NTHREADS, 1) tc_bc_kernel(TcArg
             if (warp == WARP_EPI && lane == 0) TL(11, it);
             // warp maximum of the row thresholds in one REDUX (order-preserving
             // float -> uint map), published for the producer's pruning
+#ifdef SLK_PUB2
+            if (it & 1)
+#endif
             {
                 const uint32_t b = __float_as_uint(row_ok ? thr : -INFINITY);
                 const uint32_t key = (b & 0x80000000u) ? ~b : (b | 0x80000000u);

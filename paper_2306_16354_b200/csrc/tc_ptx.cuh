@@ -60,6 +60,20 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity, int ta
 #endif
     } while (!done);
 }
+// spin form (no suspend hint): for a warp on the critical path whose
+// barrier usually completes within a few hundred cycles
+__device__ __forceinline__ void mbar_wait_spin(uint64_t *bar, uint32_t parity) {
+    uint32_t done;
+    do {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(smem_u32(bar)), "r"(parity)
+            : "memory");
+    } while (!done);
+}
 __device__ __forceinline__ void fence_async_smem() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }

@@ -1,0 +1,7 @@
+O=gpurun_out/${TAG:-var}
+mkdir -p $O
+for v in base spin pub2 spinpub2; do
+  if [ $v = base ]; then L=""; else L=$v; fi
+  SLK_LIB_VARIANT=$L SLK_TRACE=1 timeout 300 python scripts/profile_scan.py cc 1000000 64 50 1 > $O/cc_$v.log 2>&1
+  SLK_LIB_VARIANT=$L SLK_TRACE=1 timeout 300 python scripts/profile_scan.py cc 1000000 64 50 1 >> $O/cc_$v.log 2>&1
+done
