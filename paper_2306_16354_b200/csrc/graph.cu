@@ -15,6 +15,7 @@
 // the edge list is compacted to the edges that still cross colours.  The
 // minimum spanning forest under a strict total order is unique, so the
 // accepted edge set equals the reference's exactly.
+#include <cooperative_groups.h>
 #include <cub/cub.cuh>
 #include <cuda_runtime.h>
 #include <math.h>
@@ -253,6 +254,116 @@ __global__ void compact_edges_kernel(const int32_t *ea, const int32_t *eb, const
         ob[p] = eb[e];
         orank[p] = er[e];
     }
+}
+
+// ------------------------------------------------- persistent Boruvka
+// All rounds in ONE cooperative launch (grid-wide barriers between phases, no
+// host round trip): per round min_edge -> hook -> break 2-cycles -> pointer
+// jumping -> relabel -> compaction of the edges that still cross colours.
+// Compaction appends with warp-aggregated atomics, so the order of the active
+// list changes between rounds; nothing depends on it (ranks are unique and
+// min_edge is an atomicMin), so the accepted set is the same unique MSF.
+// counts[r] = active edges at round r (counts[0] = m, the rest zero on entry).
+struct BoruvkaArgs {
+    int64_t n;
+    int32_t *color, *parent;
+    uint32_t *best;
+    const int32_t *ra, *rb;  // endpoints by rank
+    uint8_t *accepted;
+    int32_t *ea[2], *eb[2];
+    uint32_t *er[2];
+    unsigned long long *counts;  // [MAX_ROUNDS + 1]
+    int *rounds;
+};
+constexpr int MAX_ROUNDS = 64;
+
+__global__ void __launch_bounds__(256) boruvka_coop_kernel(BoruvkaArgs a) {
+    namespace cg = cooperative_groups;
+    cg::grid_group grid = cg::this_grid();
+    const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t nth = (int64_t)gridDim.x * blockDim.x;
+    const int lane = threadIdx.x & 31;
+    const int64_t n = a.n;
+    int32_t *color = a.color, *parent = a.parent;
+    uint32_t *best = a.best;
+    for (int r = 0; r < MAX_ROUNDS; r++) {
+        const int64_t active = (int64_t)a.counts[r];
+        if (active == 0) {
+            if (tid == 0) *a.rounds = r;
+            return;  // uniform: every thread read the same count after the last barrier
+        }
+        const int32_t *ea = a.ea[r & 1], *eb = a.eb[r & 1];
+        const uint32_t *er = a.er[r & 1];
+        for (int64_t e = tid; e < active; e += nth) {
+            const int32_t ca = color[ea[e]], cb = color[eb[e]];
+            if (ca == cb) continue;
+            const uint32_t rk = er[e];
+            if (best[ca] > rk) atomicMin(&best[ca], rk);
+            if (best[cb] > rk) atomicMin(&best[cb], rk);
+        }
+        grid.sync();
+        for (int64_t v = tid; v < n; v += nth) {  // hook every root along its minimum edge
+            if (color[v] != v) continue;
+            const uint32_t e = best[v];
+            if (e == NONE32) {
+                parent[v] = (int32_t)v;
+                continue;
+            }
+            a.accepted[e] = 1;
+            const int32_t ca = color[a.ra[e]], cb = color[a.rb[e]];
+            parent[v] = ca == v ? cb : ca;
+        }
+        grid.sync();
+        for (int64_t v = tid; v < n; v += nth) {  // a 2-cycle keeps its smaller root
+            if (color[v] != v) continue;
+            const int32_t p = parent[v];
+            if (p != v && p > v && parent[p] == v) parent[v] = (int32_t)v;
+        }
+        grid.sync();
+        for (int64_t v = tid; v < n; v += nth) {  // pointer jumping (in place: writes are ancestors)
+            if (color[v] != v) continue;
+            int32_t p = parent[v];
+            while (true) {
+                const int32_t pp = parent[p];
+                if (pp == p) break;
+                p = pp;
+            }
+            parent[v] = p;
+        }
+        grid.sync();
+        for (int64_t v = tid; v < n; v += nth) {
+            color[v] = parent[color[v]];
+            best[v] = NONE32;
+        }
+        grid.sync();
+        // edges that still cross colours -> the other buffer
+        int32_t *oa = a.ea[(r + 1) & 1], *ob = a.eb[(r + 1) & 1];
+        uint32_t *orank = a.er[(r + 1) & 1];
+        for (int64_t base = tid - lane; base < active; base += nth) {
+            const int64_t e = base + lane;
+            bool keep = false;
+            int32_t xa = 0, xb = 0;
+            uint32_t xr = 0;
+            if (e < active) {
+                xa = ea[e];
+                xb = eb[e];
+                xr = er[e];
+                keep = color[xa] != color[xb];
+            }
+            const unsigned m = __ballot_sync(0xffffffffu, keep);
+            unsigned long long at = 0;
+            if (lane == 0 && m) at = atomicAdd(&a.counts[r + 1], (unsigned long long)__popc(m));
+            at = __shfl_sync(0xffffffffu, at, 0);
+            if (keep) {
+                const int64_t p = (int64_t)at + __popc(m & ((1u << lane) - 1u));
+                oa[p] = xa;
+                ob[p] = xb;
+                orank[p] = xr;
+            }
+        }
+        grid.sync();
+    }
+    if (tid == 0) *a.rounds = MAX_ROUNDS;
 }
 
 __global__ void scan_total_kernel(const int32_t *pos, const int32_t *flag, int64_t m, int64_t *out) {
@@ -601,47 +712,50 @@ void msf_undirected(int64_t n, const int32_t *a_in, const int32_t *b_in, const d
         alt_sorted.release();
         ww.release();
 
-        // --- Boruvka rounds on ranks
-        DevBuf<int32_t> ea(m, s), eb(m, s), ea2(m, s), eb2(m, s), flag(m, s), pos(m, s);
+        // --- Boruvka rounds on ranks: one persistent cooperative launch
+        DevBuf<int32_t> ea2(m, s), eb2(m, s), flag(m, s), pos(m, s);
         DevBuf<uint32_t> er(m, s), er2(m, s), best(n, s);
         DevBuf<int32_t> parent(n, s);
         DevBuf<uint8_t> accepted(m, s);
-        DevBuf<int> any(1, s);
-        SLK_CUDA(cudaMemcpyAsync(ea.get(), ra.get(), m * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
-        SLK_CUDA(cudaMemcpyAsync(eb.get(), rb.get(), m * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+        DevBuf<unsigned long long> counts(MAX_ROUNDS + 1, s);
+        DevBuf<int> nrounds(1, s);
         LAUNCH(iota_kernel, m, (int32_t *)er.get(), m);
         SLK_CUDA(cudaMemsetAsync(accepted.get(), 0, m, s));
-        int64_t active = m;
-        double mst_bytes = 0.0;
-        int rounds = 0;
-        ev_rounds.start(s);
-        DevBuf<int64_t> total(1, s);
-        LAUNCH(fill_u32_kernel, n, best.get(), n, NONE32);
-        SLK_CUDA(cudaMemsetAsync(any.get(), 0, sizeof(int), s));
-        // while edges cross colours, every component that has one hooks (so
-        // there is no separate "any hook" check); one host read per round
-        for (int round = 0; round < 64 && active > 0; round++) {
-            mst_bytes += 12.0 * 2.0 * (double)active + 16.0 * (double)n;  // directed entries = 2 x undirected
-            rounds++;
-            LAUNCH(min_edge_kernel, active, ea.get(), eb.get(), er.get(), active, color.get(), best.get());
-            LAUNCH(hook_kernel, n, n, color.get(), best.get(), ra.get(), rb.get(), parent.get(),
-                   accepted.get(), any.get());
-            LAUNCH(break_cycles_kernel, n, n, color.get(), parent.get());
-            LAUNCH(jump_kernel, n, n, color.get(), parent.get());
-            LAUNCH(relabel_kernel, n, n, color.get(), parent.get(), best.get());
-            // keep only edges that still cross colours
-            LAUNCH(cross_flag_kernel, active, ea.get(), eb.get(), active, color.get(), flag.get());
-            exclusive_sum(flag.get(), pos.get(), active, s);
-            scan_total_kernel<<<1, 1, 0, s>>>(pos.get(), flag.get(), active, total.get());
-            LAUNCH(compact_edges_kernel, active, ea.get(), eb.get(), er.get(), flag.get(), pos.get(), active,
-                   ea2.get(), eb2.get(), er2.get());
-            const int64_t next = read_scalar(total.get(), s);
-            std::swap(ea, ea2);
-            std::swap(eb, eb2);
-            std::swap(er, er2);
-            active = next;
+        SLK_CUDA(cudaMemsetAsync(counts.get(), 0, (MAX_ROUNDS + 1) * sizeof(unsigned long long), s));
+        {
+            const unsigned long long m0 = (unsigned long long)m;
+            SLK_CUDA(cudaMemcpyAsync(counts.get(), &m0, sizeof(m0), cudaMemcpyHostToDevice, s));
         }
+        LAUNCH(fill_u32_kernel, n, best.get(), n, NONE32);
+        ev_rounds.start(s);
+        BoruvkaArgs ba{n, color.get(), parent.get(), best.get(), ra.get(), rb.get(), accepted.get(),
+                       {ra.get(), ea2.get()}, {rb.get(), eb2.get()}, {er.get(), er2.get()}, counts.get(),
+                       nrounds.get()};
+        // the active edge lists alternate between two buffers; ra / rb stay
+        // intact (hook reads endpoints by rank), so buffer 0 starts as a copy
+        DevBuf<int32_t> ea0(m, s), eb0(m, s);
+        SLK_CUDA(cudaMemcpyAsync(ea0.get(), ra.get(), m * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+        SLK_CUDA(cudaMemcpyAsync(eb0.get(), rb.get(), m * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+        ba.ea[0] = ea0.get();
+        ba.eb[0] = eb0.get();
+        static int coop_blocks = 0;
+        if (!coop_blocks) {
+            int per_sm = 0;
+            SLK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, boruvka_coop_kernel, 256, 0));
+            coop_blocks = std::max(1, per_sm) * num_sms();
+        }
+        void *kargs[] = {&ba};
+        SLK_CUDA(cudaLaunchCooperativeKernel((void *)boruvka_coop_kernel, dim3(coop_blocks), dim3(256), kargs, 0, s));
+        SLK_CHECK_LAUNCH();
         ev_rounds.stop(s);
+        unsigned long long hc[MAX_ROUNDS + 1];
+        int rounds = 0;
+        SLK_CUDA(cudaMemcpyAsync(hc, counts.get(), sizeof(hc), cudaMemcpyDeviceToHost, s));
+        SLK_CUDA(cudaMemcpyAsync(&rounds, nrounds.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
+        SLK_CUDA(cudaStreamSynchronize(s));
+        double mst_bytes = 0.0;
+        for (int r = 0; r < rounds; r++)
+            mst_bytes += 12.0 * 2.0 * (double)hc[r] + 16.0 * (double)n;  // directed entries = 2 x undirected
         profile().mst_ms += ev_rounds.ms();
         profile().mst_bytes += mst_bytes;
         profile().mst_rounds += rounds;
