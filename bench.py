@@ -51,8 +51,9 @@ CONFIGS = {
     "C4": dict(n=1_000_000, d=128, c=None, k=8, n_clusters=None),
     "C5": dict(n=500_000, d=32, c=1000, k=2, n_clusters=1000),
 }
-DTYPE = ("fp16x2 tcgen05 scan (hi.hi + hi.lo + lo.hi products, fp32 accumulate) + "
-         "f64 refine/certificate")
+DTYPE = ("fp16 tcgen05 distance tiles, fp32 accumulate: block-centred one-product scan for the "
+         "cross-colour passes at d >= 64, query-centred three-product (hi.hi + hi.lo + lo.hi) scan "
+         "otherwise; f64 refine + certificate (outputs bit-identical to the f64 reference)")
 METRIC = "end-to-end SLINK seconds at 1M×64 (k=15), 1/2/4/8 B200; kNN-tile % of peak; MST GB/s"
 SM_COUNT = 148
 FP32_LANES = 128
@@ -163,6 +164,14 @@ def cpu_slab_seconds(x, c, rows, threads, n_iters=2):
                 sample_s=t_knn + t_nn1)
 
 
+def cpu_rows_for(x, c, cores, target_s=12.0):
+    """Query rows whose oracle slab takes about target_s seconds on these cores
+    (a 128-row probe, scaled linearly; whole multiples of 128, at most N)."""
+    probe = cpu_slab_seconds(x, c, 128, cores)["sample_s"]
+    rows = int(128 * target_s / max(probe, 1e-3)) // 128 * 128
+    return max(128, min(len(x), rows))
+
+
 def cpu_cores():
     try:
         return len(os.sched_getaffinity(0))
@@ -180,7 +189,7 @@ def run_reference(args, c, cfg_name):
     orc.build()
     x = make_points(c)
     cores = cpu_cores()
-    rows = args.ref_rows
+    rows = args.ref_rows or cpu_rows_for(x, c, cores)
     for _ in range(args.warmup):
         cpu_slab_seconds(x, c, 64, cores)
     vals = []
@@ -417,7 +426,7 @@ def run_gpu(args, c, cfg_name):
     cpu = None
     if not args.no_cpu_baseline and world == 1:
         iters = getattr(res, "connect_iters", 2)
-        rows = args.cpu_rows if c["d"] <= 128 else max(64, args.cpu_rows // 4)
+        rows = args.cpu_rows or cpu_rows_for(x, c, cpu_cores())
         b = cpu_slab_seconds(x, c, rows, cpu_cores(), n_iters=max(iters, 1))
         what = "kNN slab" if knn_only else f"kNN slab + cross-colour slab, kNN + {iters} connect passes"
         cpu = {"value": b["total"], "unit": "s", "cores": cpu_cores(), "kind": "port",
@@ -455,8 +464,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C3", choices=sorted(CONFIGS))
-    ap.add_argument("--cpu-rows", type=int, default=1024)
-    ap.add_argument("--ref-rows", type=int, default=512)
+    ap.add_argument("--cpu-rows", type=int, default=0, help="oracle slab rows (0: ~12 s of CPU work)")
+    ap.add_argument("--ref-rows", type=int, default=0, help="reference-arm slab rows (0: ~12 s per step)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--d", type=int, default=None, help="C4: dimension (32, 128 or 512)")
     ap.add_argument("--k", type=int, default=None, help="C4: neighbours (8, 32 or 64)")

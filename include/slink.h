@@ -173,16 +173,25 @@ int slk_extract_clusters(const double *h_merges, int64_t n, int64_t n_clusters,
  */
 int slk_single_linkage(const float *h_x32, const double *h_x64, int64_t n, int d, int k,
                        int64_t n_clusters, int metric, int64_t seed, int64_t max_connect_iters,
-                       double *h_merges, int64_t *h_labels, int64_t *h_tree_src,
+                       int n_gpus, double *h_merges, int64_t *h_labels, int64_t *h_tree_src,
                        int64_t *h_tree_dst, double *h_tree_w, int64_t *n_connect_iters,
                        double *h_timings);
 
-/* As slk_single_linkage with the points already resident on the device. */
+/* As slk_single_linkage with the points already resident on the device.
+ *
+ * n_gpus (both entry points): the replacement of the reference's threads=
+ * knob (parallel.py:16-48).  The k-NN pass and every cross-colour pass are
+ * dealt to n_gpus shards in 128-row chunks, round-robin; shard g runs on
+ * device (current + g) % device_count with a replica of the points, one host
+ * thread per shard, and its rows return to the current device by peer copies
+ * over NVLink.  The spanning forests, dendrogram and cut run on the current
+ * device.  Results do not depend on n_gpus. */
 int slk_single_linkage_device(const float *d_x32, const double *d_x64, int64_t n, int d, int k,
                               int64_t n_clusters, int metric, int64_t seed,
-                              int64_t max_connect_iters, double *h_merges, int64_t *h_labels,
-                              int64_t *h_tree_src, int64_t *h_tree_dst, double *h_tree_w,
-                              int64_t *n_connect_iters, double *h_timings, void *stream);
+                              int64_t max_connect_iters, int n_gpus, double *h_merges,
+                              int64_t *h_labels, int64_t *h_tree_src, int64_t *h_tree_dst,
+                              double *h_tree_w, int64_t *n_connect_iters, double *h_timings,
+                              void *stream);
 
 /*
  * Spanning forest of the union of two edge lists (used by the connect loop

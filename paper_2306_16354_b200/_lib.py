@@ -51,9 +51,9 @@ SIGNATURES = {
     "slk_solve_mst": (_I, [_I64, _P, _P, _P, _I, _I64, _P, _P, _P, _P, _PI64, _PI64, _P]),
     "slk_build_dendrogram": (_I, [_P, _P, _P, _I64, _P, _P]),
     "slk_extract_clusters": (_I, [_P, _I64, _I64, _P]),
-    "slk_single_linkage": (_I, [_P, _P, _I64, _I, _I, _I64, _I, _I64, _I64, _P, _P, _P, _P, _P,
+    "slk_single_linkage": (_I, [_P, _P, _I64, _I, _I, _I64, _I, _I64, _I64, _I, _P, _P, _P, _P, _P,
                                 _PI64, _P]),
-    "slk_single_linkage_device": (_I, [_P, _P, _I64, _I, _I, _I64, _I, _I64, _I64, _P, _P, _P,
+    "slk_single_linkage_device": (_I, [_P, _P, _I64, _I, _I, _I64, _I, _I64, _I64, _I, _P, _P, _P,
                                        _P, _P, _PI64, _P, _P]),
     "slk_msf_edges": (_I, [_I64, _P, _P, _P, _I64, _I64, _P, _P, _P, _P, _PI64, _PI64, _P]),
     "slk_debug_tc_scan": (_I, [_P, _I64, _I, _I, _P, _P, _P, ctypes.POINTER(ctypes.c_float), _P]),

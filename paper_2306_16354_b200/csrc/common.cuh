@@ -165,7 +165,14 @@ struct Profile {
     // algorithmic bytes (12 B per directed entry + 16 B per vertex
     // per round), rounds, and the whole forest solve incl. its sorts
     double mst_ms = 0, mst_bytes = 0, mst_rounds = 0, msf_ms = 0;
+    Profile &operator+=(const Profile &o) {
+        double *a = &scan_ms;
+        const double *b = &o.scan_ms;
+        for (size_t i = 0; i < sizeof(Profile) / sizeof(double); i++) a[i] += b[i];
+        return *this;
+    }
 };
+// per host thread (the multi-GPU driver's shard threads merge theirs into the caller's)
 Profile &profile();
 
 // CUDA-event pair on one stream.

@@ -103,7 +103,7 @@ void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 ScanStats &scan_stats() { return g_scan_stats; }
 
-static Profile g_profile;
+static thread_local Profile g_profile;
 Profile &profile() { return g_profile; }
 
 int num_sms() {
@@ -181,12 +181,119 @@ std::string largest_sizes(const std::vector<int32_t> &colors) {
 
 }  // namespace
 
-// Pipeline state on one device (used by slk_single_linkage).
+namespace {
+
+// ------------------------------------------------------------ multi-GPU
+// The two neighbour searches are the only sharded stages (SURVEY §8e,
+// north_star): query rows are dealt to G shards in 128-aligned chunks
+// round-robin (4 chunks per shard, so clusters of unequal pruning cost
+// spread over the shards), the index is replicated, and each shard's rows
+// come back to the main device with peer copies over NVLink; the spanning
+// forests, dendrogram and cut stay on the main device.  One host thread per
+// shard drives its device (the search has host synchronisation points);
+// shard g uses device (main + g) % device_count, so G > device_count places
+// several shards on one device (the multi-shard logic is testable on one GPU).
+struct Shard {
+    int dev = 0;
+    cudaStream_t s = nullptr;
+    DevBuf<float> x32;
+    DevBuf<double> x64;
+    const float *px32 = nullptr;
+    const double *px64 = nullptr;
+    std::shared_ptr<PointSet> P;
+    DevBuf<int32_t> idx, colors;
+    DevBuf<double> dist;
+    Profile prof;
+};
+
+struct ShardSet {
+    int main_dev = 0;
+    cudaStream_t main_s = nullptr;
+    std::vector<std::unique_ptr<Shard>> sh;
+    std::vector<std::pair<int64_t, int64_t>> chunks;  // row ranges; chunk j -> shard j % G
+
+    ShardSet(int G, int64_t n, cudaStream_t s) : main_s(s) {
+        SLK_CUDA(cudaGetDevice(&main_dev));
+        int ndev = 1;
+        SLK_CUDA(cudaGetDeviceCount(&ndev));
+        for (int g = 0; g < G; g++) {
+            auto S = std::make_unique<Shard>();
+            S->dev = (main_dev + g) % ndev;
+            if (S->dev != main_dev) {
+                const cudaError_t e = cudaDeviceEnablePeerAccess(S->dev, 0);
+                if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) SLK_CUDA(e);
+                (void)cudaGetLastError();
+            }
+            sh.push_back(std::move(S));
+        }
+        const int64_t nb = (n + 127) / 128;
+        const int64_t nc = std::min<int64_t>(nb, 4 * (int64_t)G);
+        for (int64_t j = 0; j < nc; j++) chunks.push_back({std::min(n, nb * j / nc * 128), std::min(n, nb * (j + 1) / nc * 128)});
+    }
+    ~ShardSet() {
+        for (auto &S : sh)
+            if (S->s) {
+                cudaSetDevice(S->dev);
+                cudaStreamSynchronize(S->s);
+                S->x32.release();
+                S->x64.release();
+                S->idx.release();
+                S->dist.release();
+                S->colors.release();
+                S->P.reset();
+                cudaStreamDestroy(S->s);
+            }
+        cudaSetDevice(main_dev);
+    }
+    int size() const { return (int)sh.size(); }
+    // fn(g, shard) on every shard concurrently (shard 0 on this thread)
+    template <class F>
+    void run(F fn) {
+        std::vector<std::exception_ptr> err(sh.size());
+        auto body = [&](int g) {
+            try {
+                SLK_CUDA(cudaSetDevice(sh[g]->dev));
+                if (!sh[g]->s) SLK_CUDA(cudaStreamCreateWithFlags(&sh[g]->s, cudaStreamNonBlocking));
+                fn(g, *sh[g]);
+                SLK_CUDA(cudaStreamSynchronize(sh[g]->s));
+                if (g > 0) sh[g]->prof += profile();  // worker threads hand their profile to the caller
+            } catch (...) {
+                err[g] = std::current_exception();
+            }
+        };
+        std::vector<std::thread> th;
+        for (int g = 1; g < size(); g++) th.emplace_back(body, g);
+        body(0);
+        for (auto &t : th) t.join();
+        SLK_CUDA(cudaSetDevice(main_dev));
+        for (int g = 1; g < size(); g++) {
+            profile() += sh[g]->prof;
+            sh[g]->prof = Profile{};
+        }
+        for (auto &e : err)
+            if (e) std::rethrow_exception(e);
+    }
+    // copy rows [r0, r1) x width elements of T from shard g's buffer to dst (main device)
+    template <class T>
+    void gather(T *dst, const T *src, int g, int64_t r0, int64_t r1, int64_t width) {
+        const size_t bytes = (size_t)(r1 - r0) * width * sizeof(T);
+        if (!bytes) return;
+        if (sh[g]->dev == main_dev)
+            SLK_CUDA(cudaMemcpyAsync(dst + r0 * width, src + r0 * width, bytes, cudaMemcpyDeviceToDevice, main_s));
+        else
+            SLK_CUDA(cudaMemcpyPeerAsync(dst + r0 * width, main_dev, src + r0 * width, sh[g]->dev, bytes, main_s));
+    }
+};
+
+}  // namespace
+
+// Pipeline state on one device (used by slk_single_linkage); n_gpus > 1
+// shards the two neighbour searches (ShardSet above).
 void single_linkage_device(const float *x32, const double *x64, int64_t n, int d, int k,
                            int64_t n_clusters, int metric, int64_t seed, int64_t max_iters,
                            double *h_merges, int64_t *h_labels, int64_t *h_tree_src,
                            int64_t *h_tree_dst, double *h_tree_w, int64_t *n_iters,
-                           double *timings, cudaStream_t s) {
+                           double *timings, cudaStream_t s, int n_gpus = 1) {
     // peak scratch of the pipeline, x2 headroom: operand copies (packed,
     // tc-packed, f64), per-query-block visit bounds, k-NN lists, edge lists
     {
@@ -197,15 +304,51 @@ void single_linkage_device(const float *x32, const double *x64, int64_t n, int d
     }
     double t0 = now_ms();
     // --- k-NN graph (linkage.py:287)
-    auto P = make_pointset(x32, x64, n, d, s);
-    if (trace_on()) {
-        SLK_CUDA(cudaStreamSynchronize(s));
-        fprintf(stderr, "[slk] pointset %.1f ms\n", now_ms() - t0);
-    }
-    trace_mark("pointset");
+    std::unique_ptr<ShardSet> shards;
+    std::shared_ptr<PointSet> P;
     DevBuf<int32_t> idx(n * k, s);
     DevBuf<double> dist(n * k, s);
-    knn_ps(*P, k, 0, n, idx, dist, s);
+    if (n_gpus > 1) {
+        // every shard holds the points and its own PointSet (spheres, packs)
+        // for the k-NN and all connect passes
+        SLK_CUDA(cudaStreamSynchronize(s));  // the caller's points are ready
+        shards = std::make_unique<ShardSet>(n_gpus, n, s);
+        ShardSet &SS = *shards;
+        SS.run([&](int g, Shard &S) {
+            if (S.dev == SS.main_dev) {
+                S.px32 = x32;
+                S.px64 = x64;
+            } else {
+                S.x32.alloc(n * (int64_t)d, S.s);
+                SLK_CUDA(cudaMemcpyPeerAsync(S.x32.get(), S.dev, x32, SS.main_dev, n * (int64_t)d * sizeof(float), S.s));
+                S.px32 = S.x32.get();
+                if (x64) {
+                    S.x64.alloc(n * (int64_t)d, S.s);
+                    SLK_CUDA(cudaMemcpyPeerAsync(S.x64.get(), S.dev, x64, SS.main_dev, n * (int64_t)d * sizeof(double), S.s));
+                    S.px64 = S.x64.get();
+                }
+            }
+            S.P = make_pointset(S.px32, S.px64, n, d, S.s);
+            S.idx.alloc(n * k, S.s);
+            S.dist.alloc(n * k, S.s);
+            for (size_t j = g; j < SS.chunks.size(); j += SS.size())
+                knn_ps(*S.P, k, SS.chunks[j].first, SS.chunks[j].second, S.idx.get() + SS.chunks[j].first * k,
+                       S.dist.get() + SS.chunks[j].first * k, S.s);
+        });
+        for (size_t j = 0; j < SS.chunks.size(); j++) {
+            const int g = (int)(j % SS.size());
+            SS.gather(idx.get(), (const int32_t *)SS.sh[g]->idx.get(), g, SS.chunks[j].first, SS.chunks[j].second, k);
+            SS.gather(dist.get(), (const double *)SS.sh[g]->dist.get(), g, SS.chunks[j].first, SS.chunks[j].second, k);
+        }
+    } else {
+        P = make_pointset(x32, x64, n, d, s);
+        if (trace_on()) {
+            SLK_CUDA(cudaStreamSynchronize(s));
+            fprintf(stderr, "[slk] pointset %.1f ms\n", now_ms() - t0);
+        }
+        trace_mark("pointset");
+        knn_ps(*P, k, 0, n, idx, dist, s);
+    }
     trace_mark("knn returned");
     SLK_CUDA(cudaStreamSynchronize(s));
     trace_mark("knn synced");
@@ -233,7 +376,7 @@ void single_linkage_device(const float *x32, const double *x64, int64_t n, int d
         // and the cross-colour re-blocking keeps them contiguous
         base_colors.alloc(n, s);
         SLK_CUDA(cudaMemcpyAsync(base_colors.get(), colors.get(), n * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
-        P->block_hint = base_colors.get();
+        if (P) P->block_hint = base_colors.get();
         DevBuf<int32_t> usrc(2 * n, s), udst(2 * n, s);
         DevBuf<double> uw(2 * n, s);
         while (nc > 1) {
@@ -253,7 +396,31 @@ void single_linkage_device(const float *x32, const double *x64, int64_t n, int d
             SLK_CUDA(cudaMemcpyAsync(uw.get(), tw.get(), ne * sizeof(double), cudaMemcpyDeviceToDevice, s));
             iota32_kernel<<<grid_for(n, 256), 256, 0, s>>>(n, usrc.get() + ne);
             SLK_CHECK_LAUNCH();
-            nn1_ps(*P, *P, 2, nullptr, colors, colors, 0, n, udst.get() + ne, uw.get() + ne, s);
+            if (shards) {
+                // every shard scans its chunks against the replicated index
+                // with this iteration's colours; bridges come back by rows
+                ShardSet &SS = *shards;
+                SLK_CUDA(cudaStreamSynchronize(s));  // colours final on the main device
+                SS.run([&](int g, Shard &S) {
+                    S.colors.alloc(n, S.s);
+                    if (S.dev == SS.main_dev)
+                        SLK_CUDA(cudaMemcpyAsync(S.colors.get(), colors.get(), n * sizeof(int32_t), cudaMemcpyDeviceToDevice, S.s));
+                    else
+                        SLK_CUDA(cudaMemcpyPeerAsync(S.colors.get(), S.dev, colors.get(), SS.main_dev, n * sizeof(int32_t), S.s));
+                    for (size_t j = g; j < SS.chunks.size(); j += SS.size())
+                        nn1_ps(*S.P, *S.P, 2, nullptr, S.colors, S.colors, SS.chunks[j].first, SS.chunks[j].second,
+                               S.idx.get() + SS.chunks[j].first, S.dist.get() + SS.chunks[j].first, S.s);
+                });
+                for (size_t j = 0; j < SS.chunks.size(); j++) {
+                    const int g = (int)(j % SS.size());
+                    SS.gather(udst.get() + ne, (const int32_t *)SS.sh[g]->idx.get(), g, SS.chunks[j].first,
+                              SS.chunks[j].second, 1);
+                    SS.gather(uw.get() + ne, (const double *)SS.sh[g]->dist.get(), g, SS.chunks[j].first,
+                              SS.chunks[j].second, 1);
+                }
+            } else {
+                nn1_ps(*P, *P, 2, nullptr, colors, colors, 0, n, udst.get() + ne, uw.get() + ne, s);
+            }
             EdgeSet U = dedup_undirected(n, usrc, udst, uw, m, s);
             msf_undirected(n, U.a, U.b, U.w, U.m, true, false, seed, ts, td, tw, colors, &ne, &nc, s);
             iters++;
@@ -489,12 +656,17 @@ int slk_pairwise_l2(const double *d_q, int64_t nq, const double *d_x, int64_t nx
     });
 }
 
+static void check_gpus(int n_gpus) {
+    if (n_gpus < 1 || n_gpus > 64) throw_invalid("n_gpus must be in [1, 64], got %d", n_gpus);
+}
+
 int slk_single_linkage(const float *h_x32, const double *h_x64, int64_t n, int d, int k,
                        int64_t n_clusters, int metric, int64_t seed, int64_t max_connect_iters,
-                       double *h_merges, int64_t *h_labels, int64_t *h_tree_src,
+                       int n_gpus, double *h_merges, int64_t *h_labels, int64_t *h_tree_src,
                        int64_t *h_tree_dst, double *h_tree_w, int64_t *n_connect_iters,
                        double *h_timings) {
     return guarded([&] {
+        check_gpus(n_gpus);
         if (n < 2) throw_invalid("need at least 2 points, got %lld", (long long)n);
         if (n_clusters < 1) throw_invalid("n_clusters must be >= 1, got %lld", (long long)n_clusters);
         if (n_clusters > n) throw_invalid("n_clusters=%lld exceeds %lld points", (long long)n_clusters, (long long)n);
@@ -517,18 +689,20 @@ int slk_single_linkage(const float *h_x32, const double *h_x64, int64_t n, int d
         }
         single_linkage_device(x32, h_x64 ? x64.get() : nullptr, n, d, k, n_clusters, metric, seed,
                               max_connect_iters, h_merges, h_labels, h_tree_src, h_tree_dst,
-                              h_tree_w, n_connect_iters, h_timings, s);
+                              h_tree_w, n_connect_iters, h_timings, s, n_gpus);
         SLK_CUDA(cudaStreamSynchronize(s));
     });
 }
 
 int slk_single_linkage_device(const float *d_x32, const double *d_x64, int64_t n, int d, int k,
                               int64_t n_clusters, int metric, int64_t seed,
-                              int64_t max_connect_iters, double *h_merges, int64_t *h_labels,
-                              int64_t *h_tree_src, int64_t *h_tree_dst, double *h_tree_w,
-                              int64_t *n_connect_iters, double *h_timings, void *stream_) {
+                              int64_t max_connect_iters, int n_gpus, double *h_merges,
+                              int64_t *h_labels, int64_t *h_tree_src, int64_t *h_tree_dst,
+                              double *h_tree_w, int64_t *n_connect_iters, double *h_timings,
+                              void *stream_) {
     STREAM(s);
     return guarded([&] {
+        check_gpus(n_gpus);
         if (n < 2) throw_invalid("need at least 2 points, got %lld", (long long)n);
         if (n_clusters < 1) throw_invalid("n_clusters must be >= 1, got %lld", (long long)n_clusters);
         if (n_clusters > n) throw_invalid("n_clusters=%lld exceeds %lld points", (long long)n_clusters, (long long)n);
@@ -537,7 +711,7 @@ int slk_single_linkage_device(const float *d_x32, const double *d_x64, int64_t n
         if (n >= (1ll << 30)) throw_invalid("n=%lld exceeds the 2^30-1 point limit", (long long)n);
         single_linkage_device(d_x32, d_x64, n, d, k, n_clusters, metric, seed, max_connect_iters,
                               h_merges, h_labels, h_tree_src, h_tree_dst, h_tree_w,
-                              n_connect_iters, h_timings, s);
+                              n_connect_iters, h_timings, s, n_gpus);
         SLK_CUDA(cudaStreamSynchronize(s));
     });
 }

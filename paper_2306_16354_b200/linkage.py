@@ -213,7 +213,14 @@ def _validate_run(pm, cfg: LinkageConfig):
         raise ValidationError(f"k={cfg.k} exceeds N-1={n - 1}")
 
 
-def _run(pm, cfg: LinkageConfig, device_points=None) -> SingleLinkageResult:
+def _check_gpus(n_gpus) -> int:
+    g = 1 if n_gpus is None else n_gpus
+    if isinstance(g, bool) or not isinstance(g, (int, np.integer)) or not 1 <= g <= 64:
+        raise ValidationError(f"n_gpus must be an integer in [1, 64], got {n_gpus!r}")
+    return int(g)
+
+
+def _run(pm, cfg: LinkageConfig, device_points=None, n_gpus: int = 1) -> SingleLinkageResult:
     n, d = pm.n_rows if pm is not None else device_points.n, (
         pm.n_cols if pm is not None else device_points.d)
     merges = np.empty((max(n - 1, 1), 4))
@@ -231,13 +238,13 @@ def _run(pm, cfg: LinkageConfig, device_points=None) -> SingleLinkageResult:
         x64 = None if pm.exact_f32 else np.ascontiguousarray(pm.device_f64)
         _lib.torch_cuda()
         _lib.call("slk_single_linkage", p(x32), None if x64 is None else p(x64), n, d, cfg.k,
-                  cfg.n_clusters, metric, int(cfg.seed), budget, p(merges), p(labels), p(ts),
-                  p(td), p(tw), ctypes.byref(iters), p(tim))
+                  cfg.n_clusters, metric, int(cfg.seed), budget, n_gpus, p(merges), p(labels),
+                  p(ts), p(td), p(tw), ctypes.byref(iters), p(tim))
     else:
         dp = device_points
         _lib.call("slk_single_linkage_device", _lib.ptr(dp.x32), _lib.ptr(dp.x64), n, d, cfg.k,
-                  cfg.n_clusters, metric, int(cfg.seed), budget, p(merges), p(labels), p(ts),
-                  p(td), p(tw), ctypes.byref(iters), p(tim), _lib.stream_handle())
+                  cfg.n_clusters, metric, int(cfg.seed), budget, n_gpus, p(merges), p(labels),
+                  p(ts), p(td), p(tw), ctypes.byref(iters), p(tim), _lib.stream_handle())
     e = pm.scale_exp if pm is not None else 0
     if e:  # back from the device's power-of-two scaled units (exact)
         tw[: n - 1] = np.ldexp(tw[: n - 1], 2 * e)
@@ -249,18 +256,21 @@ def _run(pm, cfg: LinkageConfig, device_points=None) -> SingleLinkageResult:
     return SingleLinkageResult(dendro, lab, tree, int(iters.value), dict(zip(STAGES, tim.tolist())))
 
 
-def single_linkage_result(x, cfg: LinkageConfig) -> SingleLinkageResult:
+def single_linkage_result(x, cfg: LinkageConfig, *, n_gpus: int | None = None) -> SingleLinkageResult:
     """single_linkage plus the spanning tree, connect iterations and stage timings."""
+    g = _check_gpus(n_gpus)
     if isinstance(x, np.ndarray) and x.dtype == np.float32 and x.ndim == 2:
         pm = PointMatrix._float32_device_checked(x)  # finiteness checked on the GPU
     else:
         pm = as_point_matrix(x)
     _validate_run(pm, cfg)
-    return _run(pm, cfg)
+    return _run(pm, cfg, n_gpus=g)
 
 
-def single_linkage_on_device(points: DevicePoints, cfg: LinkageConfig) -> SingleLinkageResult:
+def single_linkage_on_device(points: DevicePoints, cfg: LinkageConfig, *,
+                             n_gpus: int | None = None) -> SingleLinkageResult:
     """Pipeline over points already resident on the GPU (bench ``value`` leg)."""
+    g = _check_gpus(n_gpus)
     if points.n > MAX_POINTS:
         raise ValidationError(f"n={points.n} exceeds the {MAX_POINTS} point limit")
     if points.n < 2:
@@ -269,19 +279,22 @@ def single_linkage_on_device(points: DevicePoints, cfg: LinkageConfig) -> Single
         raise ValidationError(f"n_clusters={cfg.n_clusters} exceeds {points.n} points")
     if cfg.k > points.n - 1:
         raise ValidationError(f"k={cfg.k} exceeds N-1={points.n - 1}")
-    return _run(None, cfg, device_points=points)
+    return _run(None, cfg, device_points=points, n_gpus=g)
 
 
 def single_linkage(x, cfg: LinkageConfig, *, tile: TileSpec | None = None,
-                   threads: int | None = None,
-                   timings: dict | None = None) -> tuple[Dendrogram, LabelArray]:
+                   threads: int | None = None, timings: dict | None = None,
+                   n_gpus: int | None = None) -> tuple[Dendrogram, LabelArray]:
     """End-to-end single-linkage clustering (linkage.py:257-311).
 
     Returns the full dendrogram and the flat labels for cfg.n_clusters.
     ``timings`` (optional dict) receives per-stage milliseconds under the
     reference's keys.  ``tile`` / ``threads`` are accepted and ignored.
+    ``n_gpus`` (extension; the GPU counterpart of ``threads``, parallel.py:16-48)
+    shards the neighbour searches over that many devices of this process
+    (include/slink.h: slk_single_linkage); results do not depend on it.
     """
-    res = single_linkage_result(x, cfg)
+    res = single_linkage_result(x, cfg, n_gpus=n_gpus)
     if timings is not None:
         timings.update(res.timings)
     return res.dendrogram, res.labels
