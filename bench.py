@@ -165,10 +165,17 @@ def cpu_slab_seconds(x, c, rows, threads, n_iters=2):
 
 
 def cpu_rows_for(x, c, cores, target_s=12.0):
-    """Query rows whose oracle slab takes about target_s seconds on these cores
-    (a 128-row probe, scaled linearly; whole multiples of 128, at most N)."""
-    probe = cpu_slab_seconds(x, c, 128, cores)["sample_s"]
-    rows = int(128 * target_s / max(probe, 1e-3)) // 128 * 128
+    """Query rows whose oracle slab takes about target_s seconds on these cores:
+    a small probe scaled linearly, refined once more on a larger slab (fixed
+    per-call costs make the probe underestimate the rate); whole multiples of
+    128, at most N."""
+    rows = 128
+    for _ in range(3):
+        t = cpu_slab_seconds(x, c, rows, cores)["sample_s"]
+        if t >= 0.5 * target_s or rows >= len(x):
+            break
+        rows = max(rows + 128, int(rows * target_s / max(t, 1e-3)) // 128 * 128)
+        rows = min(len(x), rows)
     return max(128, min(len(x), rows))
 
 

@@ -194,6 +194,22 @@ int slk_single_linkage_device(const float *d_x32, const double *d_x64, int64_t n
                               void *stream);
 
 /*
+ * Point-set handles (the distributed driver, parallel.py): the per-matrix
+ * search state (block spheres, tensor operand packs, split index) built once
+ * over device-resident points and reused by every search on them.  The
+ * caller keeps d_x32 / d_x64 alive until slk_pointset_destroy.
+ *   slk_knn_ps: fused_knn rows [q0, q1) (neighbors.py:246-298), outputs as slk_knn.
+ *   slk_nn1_colour_ps: cross_color_1nn rows [q0, q1) (neighbors.py:375-391)
+ *     with colours d_colors (n int32), outputs as slk_nn1.
+ */
+int slk_pointset_create(const float *d_x32, const double *d_x64, int64_t n, int d, void **handle,
+                        void *stream);
+int slk_pointset_destroy(void *handle);
+int slk_knn_ps(void *handle, int k, int64_t q0, int64_t q1, int32_t *d_idx, double *d_dist, void *stream);
+int slk_nn1_colour_ps(void *handle, const int32_t *d_colors, int64_t q0, int64_t q1, int32_t *d_idx,
+                      double *d_dist, void *stream);
+
+/*
  * Spanning forest of the union of two edge lists (used by the connect loop
  * and the multi-GPU driver): symmetrise + min-dedup (core.py:264-286) then
  * solve_mst (mst.py:292-344) with the given seed, without materialising the

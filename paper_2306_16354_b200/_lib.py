@@ -56,6 +56,10 @@ SIGNATURES = {
     "slk_single_linkage_device": (_I, [_P, _P, _I64, _I, _I, _I64, _I, _I64, _I64, _I, _P, _P, _P,
                                        _P, _P, _PI64, _P, _P]),
     "slk_msf_edges": (_I, [_I64, _P, _P, _P, _I64, _I64, _P, _P, _P, _P, _PI64, _PI64, _P]),
+    "slk_pointset_create": (_I, [_P, _P, _I64, _I, ctypes.POINTER(ctypes.c_void_p), _P]),
+    "slk_pointset_destroy": (_I, [_P]),
+    "slk_knn_ps": (_I, [_P, _I, _I64, _I64, _P, _P, _P]),
+    "slk_nn1_colour_ps": (_I, [_P, _P, _I64, _I64, _P, _P, _P]),
     "slk_debug_tc_scan": (_I, [_P, _I64, _I, _I, _P, _P, _P, ctypes.POINTER(ctypes.c_float), _P]),
 }
 

@@ -531,6 +531,51 @@ int slk_knn(const float *d_x32, const double *d_x64, int64_t n, int d, int k, in
     });
 }
 
+// Point-set handles: the block spheres, operand packs and split index of one
+// device-resident matrix, built once and reused by every search over it
+// (a rank's k-NN chunks and all its cross-colour passes).
+int slk_pointset_create(const float *d_x32, const double *d_x64, int64_t n, int d, void **handle,
+                        void *stream_) {
+    STREAM(s);
+    return guarded([&] {
+        if (!handle) throw_invalid("handle pointer is NULL");
+        auto *P = new std::shared_ptr<PointSet>(make_pointset(d_x32, d_x64, n, d, s));
+        SLK_CUDA(cudaStreamSynchronize(s));
+        *handle = P;
+    });
+}
+
+int slk_pointset_destroy(void *handle) {
+    return guarded([&] { delete static_cast<std::shared_ptr<PointSet> *>(handle); });
+}
+
+int slk_knn_ps(void *handle, int k, int64_t q0, int64_t q1, int32_t *d_idx, double *d_dist, void *stream_) {
+    STREAM(s);
+    return guarded([&] {
+        if (!handle) throw_invalid("NULL point-set handle");
+        const PointSet &P = **static_cast<std::shared_ptr<PointSet> *>(handle);
+        if (k < 1 || k > P.n - 1) throw_invalid("k must be in [1, %lld] for %lld points, got %d",
+                                                (long long)(P.n - 1), (long long)P.n, k);
+        if (q0 < 0 || q1 > P.n || q0 > q1) throw_invalid("row range [%lld, %lld) outside [0, %lld)",
+                                                          (long long)q0, (long long)q1, (long long)P.n);
+        knn_ps(P, k, q0, q1, d_idx, d_dist, s);
+        SLK_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+int slk_nn1_colour_ps(void *handle, const int32_t *d_colors, int64_t q0, int64_t q1, int32_t *d_idx,
+                      double *d_dist, void *stream_) {
+    STREAM(s);
+    return guarded([&] {
+        if (!handle) throw_invalid("NULL point-set handle");
+        const PointSet &P = **static_cast<std::shared_ptr<PointSet> *>(handle);
+        if (q0 < 0 || q1 > P.n || q0 > q1) throw_invalid("row range [%lld, %lld) outside [0, %lld)",
+                                                          (long long)q0, (long long)q1, (long long)P.n);
+        nn1_ps(P, P, 2, nullptr, d_colors, d_colors, q0, q1, d_idx, d_dist, s);
+        SLK_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
 int slk_nn1(const float *d_q32, const double *d_q64, int64_t nq, const float *d_x32,
             const double *d_x64, int64_t nx, int d, int mode, const uint8_t *d_mask,
             const int32_t *d_qcolor, const int32_t *d_xcolor, int64_t q0, int64_t q1,

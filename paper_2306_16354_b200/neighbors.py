@@ -90,20 +90,57 @@ class DevicePoints:
         self.scale_exp = 0
         return self
 
+    def handle(self):
+        """The library's search state over these points (slk_pointset_create),
+        built on first use and reused by every later search on them."""
+        h = getattr(self, "_handle", None)
+        if h is None:
+            import ctypes
+
+            out = ctypes.c_void_p()
+            _lib.call("slk_pointset_create", _lib.ptr(self.x32), _lib.ptr(self.x64), self.n, self.d,
+                      ctypes.byref(out), _lib.stream_handle())
+            h = self._handle = out
+        return h
+
+    def __del__(self):
+        h = getattr(self, "_handle", None)
+        if h is not None and _lib is not None:
+            try:
+                _lib.load().slk_pointset_destroy(h)
+            except Exception:  # interpreter shutdown
+                pass
+
 
 def _check_k(n: int, k: int):
     if not 1 <= k <= n - 1:
         raise ValidationError(f"k must be in [1, {n - 1}] for {n} points, got {k}")
 
 
-def knn_device(pts: DevicePoints, k: int, rows=None):
-    """Device tensors (idx int32, dist float64) of rows [q0, q1)."""
+def knn_device(pts: DevicePoints, k: int, rows=None, *, reuse: bool = False):
+    """Device tensors (idx int32, dist float64) of rows [q0, q1).
+
+    ``reuse``: search through the points' persistent handle (DevicePoints.handle)
+    instead of building the search state for this call only."""
     _check_k(pts.n, k)
     q0, q1 = rows if rows is not None else (0, pts.n)
     idx = _lib.empty((q1 - q0, k), np.int32)
     dist = _lib.empty((q1 - q0, k), np.float64)
-    _lib.call("slk_knn", _lib.ptr(pts.x32), _lib.ptr(pts.x64), pts.n, pts.d, k, q0, q1,
-              _lib.ptr(idx), _lib.ptr(dist), _lib.stream_handle())
+    if reuse:
+        _lib.call("slk_knn_ps", pts.handle(), k, q0, q1, _lib.ptr(idx), _lib.ptr(dist), _lib.stream_handle())
+    else:
+        _lib.call("slk_knn", _lib.ptr(pts.x32), _lib.ptr(pts.x64), pts.n, pts.d, k, q0, q1,
+                  _lib.ptr(idx), _lib.ptr(dist), _lib.stream_handle())
+    return idx, dist
+
+
+def nn1_colour_device(pts: DevicePoints, colors, rows=None):
+    """cross_color_1nn rows [q0, q1) through the points' persistent handle."""
+    q0, q1 = rows if rows is not None else (0, pts.n)
+    idx = _lib.empty(q1 - q0, np.int32)
+    dist = _lib.empty(q1 - q0, np.float64)
+    _lib.call("slk_nn1_colour_ps", pts.handle(), _lib.ptr(colors), q0, q1, _lib.ptr(idx), _lib.ptr(dist),
+              _lib.stream_handle())
     return idx, dist
 
 

@@ -3,8 +3,8 @@
 One process per GPU (torchrun), ``torch.distributed`` over NCCL.  Following
 the north star, only the brute-force k-NN scan and the cross-colour 1-NN
 scans shard: every rank holds the full point matrix (the index is
-replicated), scans the query rows ``[q0, q1)`` of its shard, and the
-per-shard results are all-gathered.  Boruvka, the dendrogram and the cut run
+replicated), scans its round-robin chunks of query rows (``shard_chunks``),
+and rank 0 gathers the per-chunk results (the only consumer).  Boruvka, the dendrogram and the cut run
 on rank 0; the colours rank 0 produces are broadcast before each connect
 pass.  The reference has no distributed path (its parallelism is the thread
 pool of /root/reference/pkg/src/parlink/parallel.py:36-48 over the same
@@ -45,13 +45,21 @@ def resolve_threads(threads: int | None = None) -> int:
     return threads
 
 
-def shard_rows(n: int, world: int, rank: int, align: int = ROW_ALIGN) -> tuple[int, int]:
-    """Contiguous, block-aligned query-row range of one rank (covers [0, n) exactly)."""
-    blocks = math.ceil(n / align)
-    per = math.ceil(blocks / world)
-    q0 = min(n, rank * per * align)
-    q1 = min(n, (rank + 1) * per * align)
-    return q0, q1
+CHUNKS_PER_RANK = 4  # round-robin chunks per rank (balances clusters of unequal pruning cost)
+
+
+def shard_chunks(n: int, world: int, rank: int, per_rank: int = CHUNKS_PER_RANK,
+                 align: int = ROW_ALIGN) -> list[tuple[int, int]]:
+    """Block-aligned query-row chunks of one rank: [0, n) is cut into
+    min(blocks, per_rank * world) near-equal chunks and chunk j goes to rank
+    j % world, so every rank samples the whole row order (pruning makes the
+    cost of a query block depend on its cluster; contiguous shards would
+    inherit that imbalance).  The same rule as the single-process driver
+    (slink_api.cu:ShardSet)."""
+    blocks = max(1, math.ceil(n / align))
+    c = max(1, min(blocks, per_rank * world))
+    chunks = [(min(n, blocks * j // c * align), min(n, blocks * (j + 1) // c * align)) for j in range(c)]
+    return [chunks[j] for j in range(rank, c, world)]
 
 
 class DeviceEngine:
@@ -74,15 +82,18 @@ class DeviceEngine:
     def n_points(self, pts) -> int:
         return pts.n
 
+    # both searches go through the points' persistent handle: one PointSet
+    # (spheres, operand packs, split index) per rank for the k-NN chunks and
+    # every connect pass
     def knn_shard(self, pts, k, rows):
         from .neighbors import knn_device
 
-        return knn_device(pts, k, rows)
+        return knn_device(pts, k, rows, reuse=True)
 
     def nn1_shard(self, pts, colors, rows):
-        from .neighbors import nn1_device
+        from .neighbors import nn1_colour_device
 
-        return nn1_device(pts, pts, mode=2, qcolor=colors, xcolor=colors, rows=rows)
+        return nn1_colour_device(pts, colors, rows)
 
     def msf(self, n, src, dst, w, m, seed):
         from .linkage import msf_of_edges
@@ -112,19 +123,29 @@ def _host_staged(dist, group, t) -> bool:
     return t.is_cuda and dist.get_backend(group) == "gloo"
 
 
-def _gather_rows(torch, dist, group, t, rows_per_rank, world):
-    """All-gather variable-length row shards (padded to the largest) → concatenated."""
-    cap = max(rows_per_rank)
-    dev = t.device
+def _gather_chunks(torch, dist, group, parts, n, world, rank, row_shape, dtype, dev):
+    """Rank 0 receives every rank's chunk results (row blocks, concatenated in
+    chunk order, padded to the largest rank) and reassembles rows [0, n);
+    other ranks only send (a rank may hold no chunk when n is small).
+    Returns the full tensor on rank 0, None elsewhere."""
+    per_rank = [sum(b - a for a, b in shard_chunks(n, world, r)) for r in range(world)]
+    cap = max(per_rank)
+    t = torch.cat([p for _, p in parts]) if parts else torch.empty((0,) + tuple(row_shape), dtype=dtype, device=dev)
     if _host_staged(dist, group, t):
         t = t.cpu()
-    shape = (cap,) + tuple(t.shape[1:])
-    pad = torch.zeros(shape, dtype=t.dtype, device=t.device)
+    pad = torch.zeros((cap,) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
     pad[: t.shape[0]] = t
-    out = torch.empty((world * cap,) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
-    dist.all_gather_into_tensor(out, pad, group=group)
-    parts = [out[r * cap: r * cap + rows_per_rank[r]] for r in range(world)]
-    return torch.cat(parts).to(dev)
+    bufs = [torch.empty_like(pad) for _ in range(world)] if rank == 0 else None
+    dist.gather(pad, bufs, dst=0, group=group)
+    if rank != 0:
+        return None
+    out = torch.empty((n,) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
+    for r in range(world):
+        at = 0
+        for a, b in shard_chunks(n, world, r):
+            out[a:b] = bufs[r][at: at + (b - a)]
+            at += b - a
+    return out.to(dev)
 
 
 def _broadcast(dist, group, t):
@@ -184,18 +205,19 @@ def single_linkage_distributed(x, cfg: LinkageConfig, *, engine=None, group=None
         raise ValidationError(f"n_clusters={cfg.n_clusters} exceeds {n} points")
     if cfg.k > n - 1:
         raise ValidationError(f"k={cfg.k} exceeds N-1={n - 1}")
-    ranges = [shard_rows(n, world, r) for r in range(world)]
-    rows_per_rank = [b - a for a, b in ranges]
+    chunks = shard_chunks(n, world, rank)
     marks = [time.perf_counter()]
 
-    # --- sharded k-NN, gathered on every rank (rank 0 consumes it)
-    idx, dst = engine.knn_shard(pts, cfg.k, ranges[rank])
-    idx_all = _gather_rows(torch, dist, group, idx, rows_per_rank, world)
-    dst_all = _gather_rows(torch, dist, group, dst, rows_per_rank, world)
+    # --- sharded k-NN (round-robin chunks), gathered on rank 0 only
+    dev = getattr(engine, "device", torch.device("cpu"))
+    res = [engine.knn_shard(pts, cfg.k, c) for c in chunks]
+    idx_all = _gather_chunks(torch, dist, group, [(c, r[0]) for c, r in zip(chunks, res)], n, world, rank,
+                             (cfg.k,), torch.int32, dev)
+    dst_all = _gather_chunks(torch, dist, group, [(c, r[1]) for c, r in zip(chunks, res)], n, world, rank,
+                             (cfg.k,), torch.float64, dev)
     engine.sync()
     marks.append(time.perf_counter())
-
-    dev = idx.device
+    del res
     ncomp_t = torch.zeros(1, dtype=torch.int64, device=dev)
     colors = torch.empty(n, dtype=torch.int32, device=dev)
     state = None
@@ -222,9 +244,12 @@ def single_linkage_distributed(x, cfg: LinkageConfig, *, engine=None, group=None
                 f"reconnection did not converge within {budget} iterations: "
                 f"{ncomp} components remain")
         _broadcast(dist, group, colors)
-        bidx, bw = engine.nn1_shard(pts, colors, ranges[rank])
-        bidx_all = _gather_rows(torch, dist, group, bidx, rows_per_rank, world)
-        bw_all = _gather_rows(torch, dist, group, bw, rows_per_rank, world)
+        res = [engine.nn1_shard(pts, colors, c) for c in chunks]
+        bidx_all = _gather_chunks(torch, dist, group, [(c, r[0]) for c, r in zip(chunks, res)], n, world, rank,
+                                  (), torch.int32, dev)
+        bw_all = _gather_chunks(torch, dist, group, [(c, r[1]) for c, r in zip(chunks, res)], n, world, rank,
+                                (), torch.float64, dev)
+        del res
 
         def resolve():
             nonlocal state
@@ -265,11 +290,13 @@ def knn_distributed(x, k: int, *, engine=None, group=None, to_host: bool = False
     rank, world = dist.get_rank(group), dist.get_world_size(group)
     pts = engine.upload(x)
     n = engine.n_points(pts)
-    ranges = [shard_rows(n, world, r) for r in range(world)]
-    rows_per_rank = [b - a for a, b in ranges]
-    idx, dst = engine.knn_shard(pts, k, ranges[rank])
-    idx_all = _gather_rows(torch, dist, group, idx, rows_per_rank, world)
-    dst_all = _gather_rows(torch, dist, group, dst, rows_per_rank, world)
+    chunks = shard_chunks(n, world, rank)
+    dev = getattr(engine, "device", torch.device("cpu"))
+    res = [engine.knn_shard(pts, k, c) for c in chunks]
+    idx_all = _gather_chunks(torch, dist, group, [(c, r[0]) for c, r in zip(chunks, res)], n, world, rank,
+                             (k,), torch.int32, dev)
+    dst_all = _gather_chunks(torch, dist, group, [(c, r[1]) for c, r in zip(chunks, res)], n, world, rank,
+                             (k,), torch.float64, dev)
     engine.sync()
     if rank != 0:
         return None
@@ -281,5 +308,5 @@ def knn_distributed(x, k: int, *, engine=None, group=None, to_host: bool = False
                     unscale_sq(dst_all.cpu().numpy(), engine.scale_exp(pts)))
 
 
-__all__ = ["DeviceEngine", "knn_distributed", "shard_rows", "single_linkage_distributed", "Dendrogram",
+__all__ = ["DeviceEngine", "knn_distributed", "shard_chunks", "single_linkage_distributed", "Dendrogram",
            "LabelArray"]

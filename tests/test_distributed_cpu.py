@@ -120,22 +120,29 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def test_shard_rows_cover_exactly():
-    from paper_2306_16354_b200.parallel import shard_rows
+def test_shard_chunks_cover_exactly():
+    """Round-robin chunks: disjoint, 128-aligned, covering [0, n), every rank
+    holding chunks spread over the whole row order."""
+    from paper_2306_16354_b200.parallel import shard_chunks
 
     for n in (1, 127, 128, 129, 1000, 10_000, 1_000_000):
         for world in (1, 2, 3, 4, 8):
-            ranges = [shard_rows(n, world, r) for r in range(world)]
-            assert ranges[0][0] == 0 and ranges[-1][1] == n
-            for (a0, a1), (b0, b1) in zip(ranges, ranges[1:]):
+            per = [shard_chunks(n, world, r) for r in range(world)]
+            allc = sorted(c for p in per for c in p)
+            assert allc[0][0] == 0 and allc[-1][1] == n
+            for (a0, a1), (b0, b1) in zip(allc, allc[1:]):
                 assert a1 == b0 and a0 <= a1
-            assert all(a % 128 == 0 for a, _ in ranges if a < n)
+            assert all(a % 128 == 0 for a, _ in allc if a < n)
+            blocks = -(-n // 128)
+            if blocks >= 4 * world:
+                assert all(len(p) == 4 for p in per)
 
 
 @pytest.mark.parametrize("world,name", [(2, "slink_blobs_2k_d32_k2"), (2, "slink_tiny_k2"),
                                         (3, "slink_blobs_2k_d32_k2")])
 def test_multi_rank_pipeline_matches_reference(oracle, world, name):
-    """World sizes 2 and 3 (ragged last shard: 2000 rows = 6 + 6 + 4 blocks)."""
+    """World sizes 2 and 3 (2000 rows = 16 blocks in 12 round-robin chunks of
+    1-2 blocks: ragged per-rank row counts, padded in the gather)."""
     (result,) = _run_ranks(world, name, 1)
     src, w, merges, labels, iters = result
     g = load_golden(name)
