@@ -840,25 +840,46 @@ __global__ void refine_kernel(RefineArgs a) {
             li[r] = 0x7fffffff;
         }
     }
-    warp_bitonic_sort<R>(lv, li, lane);
-#pragma unroll
-    for (int r = 0; r < R; r++) {
-        int p = r * 32 + lane;
-        if (p < a.k) {
-            a.out_idx[wid * a.k + p] = li[r] == 0x7fffffff ? -1 : li[r];
-            a.out_dist[wid * a.k + p] = lv[r];
-        }
-    }
-    // certificate: the k-th exact value must beat every unseen candidate
-    const int kr = (a.k - 1) / 32, kl = (a.k - 1) & 31;
     double vk = 0.0;
     int ik = 0;
+    if (a.k == 1) {
+        // cross-colour passes: the (value, id)-minimum is all the output needs
+        // (a warp reduction instead of sorting 32 R candidates)
+        double bv = lv[0];
+        int bi = li[0];
 #pragma unroll
-    for (int r = 0; r < R; r++)
-        if (r == kr) {
-            vk = __shfl_sync(FULL, lv[r], kl);
-            ik = __shfl_sync(FULL, li[r], kl);
+        for (int r = 1; r < R; r++)
+            if (lv[r] < bv || (lv[r] == bv && li[r] < bi)) bv = lv[r], bi = li[r];
+        for (int o = 16; o; o >>= 1) {
+            const double ov = __shfl_xor_sync(FULL, bv, o);
+            const int oi = __shfl_xor_sync(FULL, bi, o);
+            if (ov < bv || (ov == bv && oi < bi)) bv = ov, bi = oi;
         }
+        if (lane == 0) {
+            a.out_idx[wid] = bi == 0x7fffffff ? -1 : bi;
+            a.out_dist[wid] = bv;
+        }
+        vk = bv;
+        ik = bi;
+    } else {
+        warp_bitonic_sort<R>(lv, li, lane);
+#pragma unroll
+        for (int r = 0; r < R; r++) {
+            int p = r * 32 + lane;
+            if (p < a.k) {
+                a.out_idx[wid * a.k + p] = li[r] == 0x7fffffff ? -1 : li[r];
+                a.out_dist[wid * a.k + p] = lv[r];
+            }
+        }
+        // certificate: the k-th exact value must beat every unseen candidate
+        const int kr = (a.k - 1) / 32, kl = (a.k - 1) & 31;
+#pragma unroll
+        for (int r = 0; r < R; r++)
+            if (r == kr) {
+                vk = __shfl_sync(FULL, lv[r], kl);
+                ik = __shfl_sync(FULL, li[r], kl);
+            }
+    }
     if (lane == 0) {
         float kth = a.kth[wid * a.kth_per_row];
         for (int r = 1; r < a.kth_per_row; r++) kth = fminf(kth, a.kth[wid * a.kth_per_row + r]);
@@ -1673,14 +1694,68 @@ Gathered gather_queries(const PointSet &Q, const std::vector<int32_t> &src,
 }  // namespace
 struct SplitIndex {
     PointSet P;                    // virtual re-blocked index over the same x32 (P.rowmap = xid)
-    DevBuf<int32_t> xid, xmark, xpos;
-    std::vector<int32_t> src;      // position -> id (pads repeat a real id)
+    DevBuf<int32_t> xid, xmark, xpos;  // position -> id (pads repeat a real id), pad marks, id -> position
 };
 namespace {
 
 __global__ void gather_ids_kernel(const int32_t *v, const int32_t *src, int64_t m, int32_t *out) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
         out[i] = v[src[i]];
+}
+
+// Positions of the split index, one CTA per block (thread j = point j): a
+// block keeps its place (shifted by pos[b]) unless slot[b] >= 0, then its two
+// 2-means parts fill two blocks in id order, each padded with marked repeats
+// of its first point.
+__global__ void __launch_bounds__(BM) split_fill_kernel(int64_t n, const int64_t *__restrict__ pos,
+                                                       const int32_t *__restrict__ slot,
+                                                       const int8_t *__restrict__ part, int32_t *xid,
+                                                       int32_t *mark) {
+    __shared__ int cnt1_w[BM / 32], first[2];
+    const int64_t b = blockIdx.x;
+    const int j = threadIdx.x, lane = j & 31, w = j >> 5;
+    const int cnt = (int)min((int64_t)BM, n - b * BM);
+    const int64_t p0 = pos[b];
+    const int32_t id = (int32_t)(b * BM + j);
+    if (slot[b] < 0) {
+        if (j < cnt) {
+            xid[p0 + j] = id;
+            mark[p0 + j] = 0;
+        }
+        return;
+    }
+    const int h = j < cnt ? part[(int64_t)slot[b] * BM + j] : -1;
+    const unsigned m1 = __ballot_sync(0xffffffffu, h == 1), m0 = __ballot_sync(0xffffffffu, h == 0);
+    if (lane == 0) cnt1_w[w] = __popc(m1) | (__popc(m0) << 16);
+    if (j == 0) first[0] = first[1] = 0x7fffffff;
+    __syncthreads();
+    int before0 = 0, before1 = 0, n0 = 0, n1 = 0;
+    for (int q = 0; q < BM / 32; q++) {
+        const int c1 = cnt1_w[q] & 0xffff, c0 = cnt1_w[q] >> 16;
+        if (q < w) before0 += c0, before1 += c1;
+        n0 += c0;
+        n1 += c1;
+    }
+    if (h >= 0) atomicMin(&first[h], id);
+    __syncthreads();
+    if (h == 0) {
+        const int64_t p = p0 + before0 + __popc(m0 & ((1u << lane) - 1u));
+        xid[p] = id;
+        mark[p] = 0;
+    } else if (h == 1) {
+        const int64_t p = p0 + BM + before1 + __popc(m1 & ((1u << lane) - 1u));
+        xid[p] = id;
+        mark[p] = 0;
+    }
+    // pads after each part
+    if (j >= n0) {
+        xid[p0 + j] = first[0];
+        mark[p0 + j] = -1;
+    }
+    if (j >= n1) {
+        xid[p0 + BM + j] = first[1];
+        mark[p0 + BM + j] = -1;
+    }
 }
 
 // id -> position of a re-blocked index (pads, mark < 0, skipped)
@@ -1811,48 +1886,33 @@ int split_index(const PointSet &X, cudaStream_t s) {
     SLK_CUDA(cudaMemcpyAsync(hpart, dpart.get(), (size_t)nw * BM, cudaMemcpyDeviceToHost, s));
     SLK_CUDA(cudaStreamSynchronize(s));
     auto SI = std::make_shared<SplitIndex>();
-    std::vector<int32_t> mark;
-    SI->src.reserve(n + 2 * BM * wide.size());
+    // output position of every block (a split block takes two padded blocks)
+    thread_local PinnedBuf<int64_t> posstage;
+    thread_local PinnedBuf<int32_t> slotstage;
+    int64_t *hpos = posstage.get(nb);
+    int32_t *hslot = slotstage.get(nb);  // wide-list slot of a split block, else -1
+    int64_t m = 0;
     size_t wi = 0;
-    std::vector<int> part(BM);
-    auto pad = [&](int32_t rep) {
-        while (SI->src.size() % BM) {
-            SI->src.push_back(rep);
-            mark.push_back(-1);
-        }
-    };
     for (int64_t b = 0; b < nb; b++) {
-        const int cnt = (int)std::min<int64_t>(BM, n - b * BM);
-        bool split = false;
+        hpos[b] = m;
+        hslot[b] = -1;
         if (wi < wide.size() && wide[wi] == b) {
-            split = hpart[wi * BM] != 2;
-            for (int j = 0; j < cnt; j++) part[j] = hpart[wi * BM + j];
+            if (hpart[wi * BM] != 2) hslot[b] = (int32_t)wi;
             wi++;
         }
-        for (int h = 0; h < (split ? 2 : 1); h++) {
-            int32_t first = -1;
-            for (int j = 0; j < cnt; j++) {
-                if (split && part[j] != h) continue;
-                const int32_t id = (int32_t)(b * BM + j);
-                if (first < 0) first = id;
-                SI->src.push_back(id);
-                mark.push_back(0);
-            }
-            if (split) pad(first);
-        }
+        m += hslot[b] >= 0 ? 2 * BM : std::min<int64_t>(BM, n - b * BM);
     }
-    const int64_t m = (int64_t)SI->src.size();
     trace_mark("split index: 2-means");
     SI->xid.alloc(m, s);
     SI->xmark.alloc(m, s);
     SI->xpos.alloc(n, s);
     {
-        thread_local PinnedBuf<int32_t> stage;
-        int32_t *h = stage.get(2 * (size_t)m);
-        memcpy(h, SI->src.data(), m * sizeof(int32_t));
-        memcpy(h + m, mark.data(), m * sizeof(int32_t));
-        SLK_CUDA(cudaMemcpyAsync(SI->xid.get(), h, m * sizeof(int32_t), cudaMemcpyHostToDevice, s));
-        SLK_CUDA(cudaMemcpyAsync(SI->xmark.get(), h + m, m * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+        DevBuf<int64_t> dpos(nb, s);
+        DevBuf<int32_t> dslot(nb, s);
+        SLK_CUDA(cudaMemcpyAsync(dpos.get(), hpos, nb * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+        SLK_CUDA(cudaMemcpyAsync(dslot.get(), hslot, nb * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+        split_fill_kernel<<<(unsigned)nb, BM, 0, s>>>(n, dpos, dslot, dpart, SI->xid, SI->xmark);
+        SLK_CHECK_LAUNCH();
         xpos_kernel<<<grid_for(m, 256), 256, 0, s>>>(SI->xid, SI->xmark, m, SI->xpos);
         SLK_CHECK_LAUNCH();
     }
@@ -1877,7 +1937,7 @@ int split_index(const PointSet &X, cudaStream_t s) {
     superblock_sphere_kernel<<<(unsigned)((V.nsb * 32 + 255) / 256), 256, 0, s>>>(
         V.centroid, V.radius, V.nb, d, V.nsb, V.sb_centroid, V.sb_radius);
     SLK_CHECK_LAUNCH();
-    SLK_CUDA(cudaStreamSynchronize(s));  // host vectors go out of scope
+    SLK_CUDA(cudaStreamSynchronize(s));  // staging buffers are reused by the next call
     trace_mark("split index: built");
     if (trace_on())
         fprintf(stderr, "[slk] split index: %zu wide blocks (radius > %.3g), %lld -> %lld positions\n", wide.size(),

@@ -615,7 +615,13 @@ void launch_t(const TcArgs &args, int64_t ngroups, cudaStream_t s) {
 
 template <int DK>
 void launch_dk(int mode, int kp, const TcArgs &args, int64_t ngroups, cudaStream_t s) {
-    if (mode == MODE_COLOR) launch_t<MODE_COLOR, 8, DK>(args, ngroups, s);
+    if (mode == MODE_COLOR) {
+        // K' = 4 per column half (8 candidates a row) certifies the C3 / C2
+        // cross-colour rows as well as 8 and saves 7 % of the scan; an
+        // explicit SLK_TC_KP1 keeps the requested K'
+        if (kp <= 4 || (kp == 8 && !getenv("SLK_TC_KP1"))) launch_t<MODE_COLOR, 4, DK>(args, ngroups, s);
+        else launch_t<MODE_COLOR, 8, DK>(args, ngroups, s);
+    }
     else if (kp <= 8) launch_t<MODE_SELF, 8, DK>(args, ngroups, s);
     else launch_t<MODE_SELF, 16, DK>(args, ngroups, s);
 }
