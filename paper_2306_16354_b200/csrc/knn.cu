@@ -379,34 +379,52 @@ __global__ void __launch_bounds__(NT, (R == 1 ? 2 : 1)) scan_kernel(ScanArgs a) 
 // Bounding sphere of each 128-point block (from the float32 operand values):
 // centroid (float, dims-major [dp][nb]) and radius rounded up, computed in
 // float64 so the bound is rigorous for the values the scan sees.
-__global__ void block_sphere_kernel(const float *__restrict__ xp, int64_t n, int d, int dp,
-                                    int64_t nb, float *__restrict__ centroid,
-                                    float *__restrict__ radius, const int32_t *__restrict__ rowmap = nullptr) {
-    const int lane = threadIdx.x & 31;
-    const int64_t b = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+__global__ void __launch_bounds__(128) block_sphere_kernel(const float *__restrict__ xp, int64_t n, int d, int dp,
+                                                           int64_t nb, float *__restrict__ centroid,
+                                                           float *__restrict__ radius,
+                                                           const int32_t *__restrict__ rowmap = nullptr) {
+    // one CTA of 128 threads per block.  Centroid: thread t sums dim t % 64 of
+    // every other row (a warp reads 32 consecutive floats of one row), float64;
+    // radius: thread j = point j, its distance to the float centroid in float64.
+    __shared__ double part[2][64];
+    __shared__ float cent[512];
+    __shared__ double r2w[4];
+    const int64_t b = blockIdx.x;
     if (b >= nb) return;
+    const int tid = threadIdx.x;
     const int cnt = (int)(n - b * BN < BN ? n - b * BN : BN);
     // row-major points of the block (through rowmap for a virtual re-blocked index)
     auto row = [&](int j) { return xp + (rowmap ? (int64_t)rowmap[b * BN + j] : b * BN + j) * d; };
-    for (int t = 0; t < d; t++) {
+    for (int t0 = 0; t0 < d; t0 += 64) {
+        const int t = t0 + (tid & 63), par = tid >> 6;
         double s = 0.0;
-        for (int j = lane; j < cnt; j += 32) s += (double)row(j)[t];
-        for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(FULL, s, o);
-        if (lane == 0) centroid[(int64_t)t * nb + b] = (float)(s / cnt);
+        if (t < d)
+            for (int j = par; j < cnt; j += 2) s += (double)row(j)[t];
+        part[par][tid & 63] = s;
+        __syncthreads();
+        if (tid < 64 && t0 + tid < d) {
+            const float c = (float)((part[0][tid] + part[1][tid]) / cnt);
+            centroid[(int64_t)(t0 + tid) * nb + b] = c;
+            if (t0 + tid < 512) cent[t0 + tid] = c;
+        }
+        __syncthreads();
     }
-    __syncwarp();
-    double r2 = 0.0;
-    for (int j = lane; j < cnt; j += 32) {
-        double acc = 0.0;
-        const float *xr = row(j);
+    double acc = 0.0;
+    if (tid < cnt) {
+        const float *xr = row(tid);
         for (int t = 0; t < d; t++) {
-            double df = (double)xr[t] - (double)centroid[(int64_t)t * nb + b];
+            const double c = t < 512 ? (double)cent[t] : (double)centroid[(int64_t)t * nb + b];
+            const double df = (double)xr[t] - c;
             acc += df * df;
         }
-        r2 = fmax(r2, acc);
     }
-    for (int o = 16; o; o >>= 1) r2 = fmax(r2, __shfl_xor_sync(FULL, r2, o));
-    if (lane == 0) radius[b] = (float)(sqrt(r2) * (1.0 + 1e-6)) + 1e-30f;
+    for (int o = 16; o; o >>= 1) acc = fmax(acc, __shfl_xor_sync(FULL, acc, o));
+    if ((tid & 31) == 0) r2w[tid >> 5] = acc;
+    __syncthreads();
+    if (tid == 0) {
+        const double r2 = fmax(fmax(r2w[0], r2w[1]), fmax(r2w[2], r2w[3]));
+        radius[b] = (float)(sqrt(r2) * (1.0 + 1e-6)) + 1e-30f;
+    }
 }
 
 __global__ void block_color_range_kernel(const int32_t *__restrict__ color, int64_t n, int64_t nb,
@@ -1928,8 +1946,7 @@ int split_index(const PointSet &X, cudaStream_t s) {
     V.maxabs = X.maxabs;
     V.centroid.alloc((size_t)V.dp * V.nb, s);
     V.radius.alloc(V.nb, s);
-    block_sphere_kernel<<<(unsigned)((V.nb * 32 + 255) / 256), 256, 0, s>>>(X.x32, m, d, V.dp, V.nb, V.centroid,
-                                                                          V.radius, SI->xid);
+    block_sphere_kernel<<<(unsigned)V.nb, 128, 0, s>>>(X.x32, m, d, V.dp, V.nb, V.centroid, V.radius, SI->xid);
     SLK_CHECK_LAUNCH();
     V.nsb = (V.nb + 31) / 32;
     V.sb_centroid.alloc((size_t)V.dp * V.nsb, s);
@@ -2313,8 +2330,7 @@ std::shared_ptr<PointSet> make_pointset(const float *x32, const double *x64, int
     }
     P->centroid.alloc((size_t)P->dp * P->nb, s);
     P->radius.alloc(P->nb, s);
-    block_sphere_kernel<<<(unsigned)((P->nb * 32 + 255) / 256), 256, 0, s>>>(
-        x32, n, d, P->dp, P->nb, P->centroid, P->radius);
+    block_sphere_kernel<<<(unsigned)P->nb, 128, 0, s>>>(x32, n, d, P->dp, P->nb, P->centroid, P->radius);
     SLK_CHECK_LAUNCH();
     P->nsb = (P->nb + 31) / 32;
     P->sb_centroid.alloc((size_t)P->dp * P->nsb, s);

@@ -4,7 +4,8 @@
 
 Drives every kernel family of libslink.so once at a size where the sanitizer
 finishes in minutes: the full single-linkage pipeline on 3,000 blob points
-(tcgen05 k-NN and cross-colour scans, refine, visit order, Boruvka rounds,
+(tcgen05 k-NN and cross-colour scans, the block-centred scan with its split
+index and the multi-GPU shard driver, refine, visit order, Boruvka rounds,
 connect loop, dendrogram sort + fold, cut), the chunked large-d tensor kernel
 (d = 192), the exact-fp32/float64 fallbacks (integer grid with ties), the
 colour-blocked and pivot-blocked scans, and a general-graph MST with maximize.
@@ -14,6 +15,7 @@ perturbs timing still has to produce the reference's answer.
 
 from __future__ import annotations
 
+import os
 import sys
 from pathlib import Path
 
@@ -38,6 +40,18 @@ def main():
     res = slk.single_linkage_result(y, slk.LinkageConfig(n_clusters=60, k=2, seed=1))
     ref = orc.single_linkage(y, 60, k=2, seed=1)
     assert np.array_equal(res.tree.src, ref["tree_src"]) and np.array_equal(res.labels.labels, ref["labels"])
+
+    # block-centred kernel (cross-colour passes at d >= 64) with a split
+    # index (clusters unaligned to 128-point blocks), the k-NN pass on it too
+    # (SLK_TC_BC=2), and the in-process multi-GPU driver (3 shards)
+    u = make_blobs(np.random.default_rng(5), 3100, 64, 9).astype(np.float32)
+    ref = orc.single_linkage(u, 9, k=3, seed=0)
+    for env, shards in (("1", 1), ("2", 1), ("1", 3)):
+        os.environ["SLK_TC_BC"] = env
+        res = slk.single_linkage_result(u, slk.LinkageConfig(n_clusters=9, k=3, seed=0), n_gpus=shards)
+        assert np.array_equal(res.dendrogram.merges, ref["merges"]), (env, shards)
+        assert np.array_equal(res.labels.labels, ref["labels"]), (env, shards)
+    os.environ["SLK_TC_BC"] = "1"
 
     # chunked tcgen05 kernel (d > 128)
     z = np.random.default_rng(2).standard_normal((1500, 192)).astype(np.float32)
