@@ -73,7 +73,7 @@ __host__ __device__ constexpr uint32_t rec_bytes(int dk) { return rec_rho(dk) + 
 __host__ __device__ constexpr uint32_t stage_stride(int dk) { return (rec_bytes(dk) + 1023) / 1024 * 1024; }
 
 struct Plan {
-    uint32_t aaug, xcol, aa, stg, misc, thr, bars, b, total;
+    uint32_t aaug, xcol, aa, stg, misc, bars, b, total;
     int nb;
 };
 __host__ __device__ inline Plan make_plan(int dk, int ncg) {
@@ -90,7 +90,6 @@ __host__ __device__ inline Plan make_plan(int dk, int ncg) {
     p.aa = take(NMETA * ncg * BM * 4, 16);
     p.stg = take(2 * BM * STG_STRIDE * 4, 16);
     p.misc = take(256, 16);
-    p.thr = take(2 * BM * 4, 16);  // each column half's current K'-th value per row
     p.bars = take(8 * (2 * MAX_NB + 2 * NA_MAX + 2 * NT), 8);
     off = (off + 1023) / 1024 * 1024;
     const uint32_t st = stage_stride(dk);
@@ -254,7 +253,6 @@ __global__ void __launch_bounds__(Shape<DK, KP>::NTHREADS, 1) tc_bc_kernel(TcArg
     float *s_aa = reinterpret_cast<float *>(smem + P.aa);
     float *s_stg = reinterpret_cast<float *>(smem + P.stg);
     Misc *misc = reinterpret_cast<Misc *>(smem + P.misc);
-    float *s_thr = reinterpret_cast<float *>(smem + P.thr);
     uint64_t *full = reinterpret_cast<uint64_t *>(smem + P.bars);  // producer (bulk copy) -> MMA / convert
     uint64_t *empty = full + MAX_NB;                                // MMA commit -> producer
     uint64_t *afull = empty + MAX_NB;                               // convert -> MMA (A slot written)
@@ -273,16 +271,15 @@ __global__ void __launch_bounds__(Shape<DK, KP>::NTHREADS, 1) tc_bc_kernel(TcArg
             mbar_init(&empty[s], 1);
         }
         for (int s = 0; s < NA; s++) {
-            mbar_init(&afull[s], 4 * NCG);  // one arrival per convert warp
+            mbar_init(&afull[s], 128 * NCG);
             mbar_init(&aempty[s], 1);
         }
         for (int s = 0; s < NT; s++) {
             mbar_init(&tfull[s], 1);
-            mbar_init(&tempty[s], 8);  // one arrival per epilogue warp
+            mbar_init(&tempty[s], 256);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         for (int i = 0; i < 8; i++) misc->part[i] = INFINITY;
-        for (int i = 0; i < 2 * BM; i++) s_thr[i] = INFINITY;
         misc->rho_bits = 0u;
     }
     if (warp == WARP_MMA) {
@@ -401,8 +398,7 @@ __global__ void __launch_bounds__(Shape<DK, KP>::NTHREADS, 1) tc_bc_kernel(TcArg
             if (r == 0 && g == 0)
                 atomicMax(&misc->rho_bits, __float_as_uint(*reinterpret_cast<const float *>(rec + rec_rho(DK))));
             tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&afull[slot]);
+            mbar_arrive(&afull[slot]);  // every thread arrives: its writes are released by its own arrive
             if (r == 0 && g == 0) TL(4, it);
         }
     } else if (warp == WARP_MMA) {
@@ -466,10 +462,6 @@ __global__ void __launch_bounds__(Shape<DK, KP>::NTHREADS, 1) tc_bc_kernel(TcArg
             li[p] = -1;
         }
         float thr = row_ok ? INFINITY : -INFINITY;
-        // the other column half's K'-th value also cuts this half (tc_scan.cu)
-        float tcut = thr;
-        volatile float *other_thr = s_thr + (half ^ 1) * BM + row;
-        volatile float *my_thr = s_thr + half * BM + row;
         for (int it = 0;; it++) {
             const int ts = it % NT;
             const uint32_t tph = (uint32_t)(it / NT) & 1u;
@@ -496,8 +488,7 @@ __global__ void __launch_bounds__(Shape<DK, KP>::NTHREADS, 1) tc_bc_kernel(TcArg
             const int *xcs = s_xcol + slot * BN;
             // acc > nthr <=> |a|^2 - 2 acc < thr; nthr rounded down, so every
             // dropped column has exact |a|^2 - 2 acc >= thr
-            tcut = fminf(thr, *other_thr);
-            float nthr = 0.5f * __fsub_rd(aa, tcut);
+            float nthr = 0.5f * __fsub_rd(aa, thr);
             // one 32-column chunk: fast max filter, exact pass mask, insertion
             auto chunk = [&](const float (&dot)[CH], const int c0) {
                 float mx[CH / 2];
@@ -537,7 +528,7 @@ __global__ void __launch_bounds__(Shape<DK, KP>::NTHREADS, 1) tc_bc_kernel(TcArg
                     const int i = __ffs(pass) - 1;
                     pass &= pass - 1;
                     const float v = __fmaf_rd(-2.0f, stg[i], aa);
-                    if (!(v < tcut)) continue;
+                    if (!(v < thr)) continue;
                     const int id = (int)(col0 + c0 + i);
                     bool c_next = v < lv[KP - 1];
 #pragma unroll
@@ -552,10 +543,8 @@ __global__ void __launch_bounds__(Shape<DK, KP>::NTHREADS, 1) tc_bc_kernel(TcArg
                         li[0] = id;
                     }
                     thr = lv[KP - 1];
-                    tcut = fminf(tcut, thr);
                 }
-                *my_thr = thr;
-                nthr = 0.5f * __fsub_rd(aa, tcut);
+                nthr = 0.5f * __fsub_rd(aa, thr);
             };
 #ifdef SLK_ABL_NOEPI
             if (false)
@@ -576,9 +565,9 @@ __global__ void __launch_bounds__(Shape<DK, KP>::NTHREADS, 1) tc_bc_kernel(TcArg
                     chunk(dot, c0);
                 }
             }
-            tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&tempty[ts]);
+            tc_fence_before();
+            mbar_arrive(&tempty[ts]);
             if (warp == WARP_EPI && lane == 0) TL(11, it);
             // warp maximum of the row thresholds in one REDUX (order-preserving
             // float -> uint map), published for the producer's pruning
@@ -586,7 +575,7 @@ __global__ void __launch_bounds__(Shape<DK, KP>::NTHREADS, 1) tc_bc_kernel(TcArg
             if (it & 1)
 #endif
             {
-                const uint32_t b = __float_as_uint(row_ok ? tcut : -INFINITY);
+                const uint32_t b = __float_as_uint(row_ok ? thr : -INFINITY);
                 const uint32_t key = (b & 0x80000000u) ? ~b : (b | 0x80000000u);
                 const uint32_t mk = __reduce_max_sync(FULL, key);
                 const uint32_t mb = (mk & 0x80000000u) ? (mk & 0x7fffffffu) : ~mk;

@@ -89,7 +89,7 @@ constexpr int STG_STRIDE = CH + 4;  // per-row chunk staging (CH + 4 floats: con
 constexpr uint32_t SMEM_LIMIT = 227 * 1024;
 
 struct Plan {
-    uint32_t a, b, aaug, baug, xx, xcol, qq, cq, stg, misc, thr, bars, total;
+    uint32_t a, b, aaug, baug, xx, xcol, qq, cq, stg, misc, bars, total;
     int nb;  // B stages that fit
 };
 
@@ -122,7 +122,6 @@ __host__ __device__ inline Plan make_plan(int dk, bool aug, int qb, int kc = 0, 
     p.cq = take(dk * 4, 16);
     p.stg = take((ew > 0 ? ew : qb) * BM * STG_STRIDE * 4, 16);
     p.misc = take(128, 16);
-    p.thr = take(2 * BM * 4, 16);  // HS = 2: each column half's current K'-th value per row
     p.bars = take(8 * (4 * MAX_NB + 2 * NTMAX + 1), 8);
     off = (off + 1023) / 1024 * 1024;
     const uint32_t per = stage + (aug ? AUG_TILE : 0u);
@@ -285,7 +284,6 @@ __global__ void __launch_bounds__(Cfg<QB * HS>::NTHREADS, 1) tc_scan_kernel(TcAr
     float *s_cq = reinterpret_cast<float *>(smem + P.cq);
     float *s_stg = reinterpret_cast<float *>(smem + P.stg);
     Misc *misc = reinterpret_cast<Misc *>(smem + P.misc);
-    float *s_thr = reinterpret_cast<float *>(smem + P.thr);
     uint64_t *rawfull = reinterpret_cast<uint64_t *>(smem + P.bars);  // producer -> convert
     uint64_t *bfull = rawfull + MAX_NB;                                 // convert -> MMA
     uint64_t *bempty = bfull + MAX_NB;                                  // MMA commit -> producer
@@ -311,12 +309,12 @@ __global__ void __launch_bounds__(Cfg<QB * HS>::NTHREADS, 1) tc_scan_kernel(TcAr
     if (tid == 0) {
         for (int s = 0; s < MAX_NB; s++) {
             mbar_init(&rawfull[s], 1);
-            mbar_init(&bfull[s], 4);  // one arrival per convert warp
+            mbar_init(&bfull[s], 128);
             mbar_init(&bempty[s], 1);
         }
         for (int s = 0; s < NT; s++) {
             mbar_init(&tfull[s], 1);
-            mbar_init(&tempty[s], 4 * EW);  // one arrival per epilogue warp
+            mbar_init(&tempty[s], 128 * EW);
         }
         mbar_init(afull, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -329,7 +327,6 @@ __global__ void __launch_bounds__(Cfg<QB * HS>::NTHREADS, 1) tc_scan_kernel(TcAr
                      : "memory");
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     }
-    for (int i = tid; i < 2 * BM; i += NTHREADS) s_thr[i] = INFINITY;
     // s_cq[t] = -c_t * s (exact: s is a power of two), so x~ = fma(x, s, s_cq[t])
     for (int t = tid; t < dk; t += NTHREADS)
         s_cq[t] = t < a.d ? -a.gcentroid[(int64_t)t * a.ngroups + qbl] * a.scale : 0.0f;
@@ -435,8 +432,7 @@ __global__ void __launch_bounds__(Cfg<QB * HS>::NTHREADS, 1) tc_scan_kernel(TcAr
                 if (r == 100) misc->dbg[1] = it * 100000 + (jb < 0 ? 99999 : jb % 100000);
 #endif
                 if (jb < 0) {
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(&bfull[s]);
+                    mbar_arrive(&bfull[s]);
                     end = true;
                     break;
                 }
@@ -452,8 +448,7 @@ __global__ void __launch_bounds__(Cfg<QB * HS>::NTHREADS, 1) tc_scan_kernel(TcAr
                     }
                 }
                 fence_async_smem();  // generic-proxy smem writes -> visible to the tensor core
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&bfull[s]);
+                mbar_arrive(&bfull[s]);  // every thread arrives: its writes are released by its own arrive
                 if (r == 0 && c == nck - 1) TL(4, it);
             }
             if (end) break;
@@ -570,13 +565,6 @@ __global__ void __launch_bounds__(Cfg<QB * HS>::NTHREADS, 1) tc_scan_kernel(TcAr
             li[p] = -1;
         }
         float thr = row_ok ? INFINITY : -INFINITY;
-        // HS = 2: a candidate at or above the OTHER half's K'-th value is not
-        // among the row's K' best either, so each half filters with the
-        // smaller of the two (tcut); every dropped candidate stays >= the
-        // smaller final K'-th value, which is what the certificate uses
-        float tcut = thr;
-        volatile float *other_thr = s_thr + (half ^ 1) * BM + row;
-        volatile float *my_thr = s_thr + half * BM + row;
 
         for (int it = 0;; it++) {
             const int ts = it % NT;
@@ -605,7 +593,6 @@ __global__ void __launch_bounds__(Cfg<QB * HS>::NTHREADS, 1) tc_scan_kernel(TcAr
 #pragma unroll 1
             for (int c0 = half * (BN / HS); c0 < (half + 1) * (BN / HS); c0 += CH) {
                 float dot[CH];
-                if (HS == 2) tcut = fminf(thr, *other_thr);
                 __syncwarp();  // tcgen05.ld is .sync.aligned: reconverge after the insertion loop
                 tmem_ld(taddr + c0, dot);
                 // fast path.  AUG: acc = -b / 2, hit iff max(acc) > -thr / 2 (exact
@@ -631,15 +618,15 @@ __global__ void __launch_bounds__(Cfg<QB * HS>::NTHREADS, 1) tc_scan_kernel(TcAr
                 for (int w = CH / 4; w; w >>= 1)
 #pragma unroll
                     for (int i = 0; i < w; i++) mx[i] = AUG ? fmaxf(mx[i], mx[i + w]) : fminf(mx[i], mx[i + w]);
-                const bool hit = AUG ? mx[0] > -0.5f * tcut : mx[0] < tcut;
+                const bool hit = AUG ? mx[0] > -0.5f * thr : mx[0] < thr;
                 if (!__any_sync(FULL, hit)) continue;  // warp-uniform: nothing to insert
                 uint32_t pass = 0;
                 if (hit) {
                     // AUG: b = -2 acc exactly, so b < thr <=> acc > -thr / 2; the
                     // chunk is staged as raw accumulators and scaled per insertion
-                    const float nthr = -0.5f * tcut;
+                    const float nthr = -0.5f * thr;
 #pragma unroll
-                    for (int i = 0; i < CH; i++) pass |= ((AUG ? dot[i] > nthr : av[i] < tcut) ? 1u : 0u) << i;
+                    for (int i = 0; i < CH; i++) pass |= ((AUG ? dot[i] > nthr : av[i] < thr) ? 1u : 0u) << i;
                     uint32_t valid = c0 >= col_limit ? 0u
                                      : (col_limit - c0 >= CH ? CH_ALL : ((1u << (col_limit - c0)) - 1u));
                     if (self_col >= c0 && self_col < c0 + CH) valid &= ~(1u << (self_col - c0));
@@ -672,7 +659,7 @@ __global__ void __launch_bounds__(Cfg<QB * HS>::NTHREADS, 1) tc_scan_kernel(TcAr
                     const int i = __ffs(pass) - 1;
                     pass &= pass - 1;
                     const float v = AUG ? -2.0f * stg[i] : stg[i];
-                    if (!(v < tcut)) continue;  // the threshold may have dropped
+                    if (!(v < thr)) continue;  // the threshold may have dropped
                     const int id = (int)(col0 + c0 + i);
                     // shift-insert: new[p] = v < old[p-1] ? old[p-1] : (v < old[p] ? v : old[p])
                     bool c_next = v < lv[KP - 1];
@@ -688,16 +675,14 @@ __global__ void __launch_bounds__(Cfg<QB * HS>::NTHREADS, 1) tc_scan_kernel(TcAr
                         li[0] = id;
                     }
                     thr = lv[KP - 1];
-                    tcut = fminf(tcut, thr);
                 }
-                if (HS == 2) *my_thr = thr;
             }
-            tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&tempty[ts]);  // accumulator stage free (xx/xcol slots: see NMETA)
+            tc_fence_before();
+            mbar_arrive(&tempty[ts]);  // accumulator stage free (xx/xcol slots: see NMETA)
             if (warp == 4 && lane == 0) TL(11, it);
             // largest row threshold in a units, rounded up (pruning stays conservative)
-            float wm = row_ok ? __fadd_ru(tcut, qq) : -INFINITY;
+            float wm = row_ok ? __fadd_ru(thr, qq) : -INFINITY;
             for (int o = 16; o; o >>= 1) wm = fmaxf(wm, __shfl_xor_sync(FULL, wm, o));
             if (lane == 0) atomicExch(&misc->part[grp * 4 + ew], wm);
         }
