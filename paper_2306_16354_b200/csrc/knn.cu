@@ -506,43 +506,48 @@ __device__ __forceinline__ bool same_colour(const int2 *qcol, const int2 *xcol, 
 
 // Bounds for every (query block, index block) pair of the launch, tiled: a
 // 64 x 32 pair tile per CTA stages both centroid sets in shared memory in
-// 32-dim slices; each thread accumulates 8 pairs.  Same arithmetic as
-// sphere_lb (float64 squared differences summed in dimension order).
+// 32-dim slices; each thread accumulates 8 pairs.  float32 arithmetic rounded
+// toward a LOWER bound: the fp32 sum of d squared differences (positive terms,
+// FMA) is within (d + 3) 2^-24 1.01 relative of the exact one, so
+// s (1 - (d + 8) 2^-23) <= |c_q - c_b|^2; the square root, the radius
+// subtractions and the final square round down.  A bound below the exact one
+// only admits more blocks, never fewer (measured: the float64 version of this
+// kernel took 2.4x longer at C3).
 __global__ void __launch_bounds__(256) pair_lb_kernel(const float *__restrict__ qc, const float *__restrict__ qr,
                                                       int64_t nqb_total, const float *__restrict__ xc,
                                                       const float *__restrict__ xr, int64_t nxb, int d,
                                                       int64_t qb0, int64_t nqb, const int2 *__restrict__ qcol,
                                                       const int2 *__restrict__ xcol, float *__restrict__ lb) {
-    // staged as float64 (exact conversions): no float->double conversion in the inner loop
-    __shared__ double sq[32][65], sx[32][33];
+    __shared__ float sq[32][65], sx[32][33];
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // ty: 0..7
     const int64_t b = (int64_t)blockIdx.x * 32 + tx;
     const int64_t ql0 = (int64_t)blockIdx.y * 64;
-    double acc[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+    float acc[8] = {0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f};
     for (int t0 = 0; t0 < d; t0 += 32) {
         const int tn = min(32, d - t0);
         __syncthreads();
         for (int e = threadIdx.x; e < tn * 64; e += 256) {
             const int t = e >> 6, j = e & 63;
             const int64_t qg = qb0 + ql0 + j;
-            sq[t][j] = ql0 + j < nqb ? (double)qc[(int64_t)(t0 + t) * nqb_total + qg] : 0.0;
+            sq[t][j] = ql0 + j < nqb ? qc[(int64_t)(t0 + t) * nqb_total + qg] : 0.0f;
         }
         for (int e = threadIdx.x; e < tn * 32; e += 256) {
             const int t = e >> 5, j = e & 31;
             const int64_t xg = (int64_t)blockIdx.x * 32 + j;
-            sx[t][j] = xg < nxb ? (double)xc[(int64_t)(t0 + t) * nxb + xg] : 0.0;
+            sx[t][j] = xg < nxb ? xc[(int64_t)(t0 + t) * nxb + xg] : 0.0f;
         }
         __syncthreads();
         for (int t = 0; t < tn; t++) {
-            const double xv = sx[t][tx];
+            const float xv = sx[t][tx];
 #pragma unroll
             for (int i = 0; i < 8; i++) {
-                const double df = sq[t][ty * 8 + i] - xv;
-                acc[i] += df * df;
+                const float df = sq[t][ty * 8 + i] - xv;
+                acc[i] = __fmaf_rn(df, df, acc[i]);
             }
         }
     }
     if (b >= nxb) return;
+    const float shrink = 1.0f - (float)(d + 8) * 0x1p-23f;
 #pragma unroll
     for (int i = 0; i < 8; i++) {
         const int64_t ql = ql0 + ty * 8 + i;
@@ -550,8 +555,8 @@ __global__ void __launch_bounds__(256) pair_lb_kernel(const float *__restrict__ 
         const int64_t q = qb0 + ql;
         float v = INFINITY;
         if (!same_colour(qcol, xcol, q, b)) {
-            const double g = sqrt(acc[i]) * (1.0 - 1e-12) - (double)qr[q] - (double)xr[b];
-            v = g > 0.0 ? (float)(g * g * (1.0 - 1e-6)) : 0.0f;
+            const float g = __fsub_rd(__fsub_rd(__fsqrt_rd(__fmul_rd(acc[i], shrink)), qr[q]), xr[b]);
+            v = g > 0.0f ? __fmul_rd(__fmul_rd(g, g), 1.0f - 0x1p-22f) : 0.0f;
         }
         lb[ql * nxb + b] = v;
     }
