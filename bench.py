@@ -330,10 +330,17 @@ def run_gpu(args, c, cfg_name):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
+    ndev = torch.cuda.device_count()
+    # more ranks than devices (a one-GPU smoke test of the torchrun path):
+    # ranks share devices and talk over gloo (NCCL needs one device per rank)
+    shared = world > ndev
+    torch.cuda.set_device(local % ndev)
     distributed = world > 1
     if distributed:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     knn_only = c["c"] is None
     cfg = None if knn_only else slk.LinkageConfig(n_clusters=c["n_clusters"], k=c["k"], seed=0)
     x = make_points(c)
@@ -474,8 +481,8 @@ def main():
     ap.add_argument("--cpu-rows", type=int, default=0, help="oracle slab rows (0: ~12 s of CPU work)")
     ap.add_argument("--ref-rows", type=int, default=0, help="reference-arm slab rows (0: ~12 s per step)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--d", type=int, default=None, help="C4: dimension (32, 128 or 512)")
-    ap.add_argument("--k", type=int, default=None, help="C4: neighbours (8, 32 or 64)")
+    ap.add_argument("--d", "--dim", dest="d", type=int, default=None, help="C4: dimension (32, 128 or 512)")
+    ap.add_argument("--k", "--neighbours", dest="k", type=int, default=None, help="C4: neighbours (8, 32 or 64)")
     args = ap.parse_args()
     c = dict(CONFIGS[args.config])
     if args.config == "C4":
