@@ -210,6 +210,17 @@ int slk_nn1_colour_ps(void *handle, const int32_t *d_colors, int64_t q0, int64_t
                       double *d_dist, void *stream);
 
 /*
+ * The tail of single_linkage (linkage.py:295-311) on a device spanning tree
+ * (n-1 edges, squared-L2 weights): device (w, a, b) sort, the union-find fold
+ * and the cut, as the single-process driver runs them; the torchrun driver's
+ * rank 0 calls it after its connect loop.  Outputs as slk_single_linkage;
+ * h_ms[2] (may be NULL) = dendrogram and cut milliseconds.
+ */
+int slk_finish_tree(const int32_t *d_src, const int32_t *d_dst, const double *d_w, int64_t n, int metric,
+                    int64_t n_clusters, double *h_merges, int64_t *h_labels, int64_t *h_tree_src,
+                    int64_t *h_tree_dst, double *h_tree_w, double *h_ms, void *stream);
+
+/*
  * Spanning forest of the union of two edge lists (used by the connect loop
  * and the multi-GPU driver): symmetrise + min-dedup (core.py:264-286) then
  * solve_mst (mst.py:292-344) with the given seed, without materialising the

@@ -60,6 +60,7 @@ SIGNATURES = {
     "slk_pointset_destroy": (_I, [_P]),
     "slk_knn_ps": (_I, [_P, _I, _I64, _I64, _P, _P, _P]),
     "slk_nn1_colour_ps": (_I, [_P, _P, _I64, _I64, _P, _P, _P]),
+    "slk_finish_tree": (_I, [_P, _P, _P, _I64, _I, _I64, _P, _P, _P, _P, _P, _P, _P]),
     "slk_debug_tc_scan": (_I, [_P, _I64, _I, _I, _P, _P, _P, ctypes.POINTER(ctypes.c_float), _P]),
 }
 

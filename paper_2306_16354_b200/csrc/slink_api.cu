@@ -287,6 +287,57 @@ struct ShardSet {
 
 }  // namespace
 
+// Dendrogram + cut + spanning-tree copy-out of a device spanning tree
+// (linkage.py:295-311): device sort, parallel host fold, cut; returns the
+// dendrogram and extract milliseconds.  Shared by the single-process driver
+// and slk_finish_tree (the torchrun driver's rank 0).
+static void finish_tree(const int32_t *ts, const int32_t *td, const double *tw, int64_t n, int metric,
+                        int64_t n_clusters, double *h_merges, int64_t *h_labels, int64_t *h_tree_src,
+                        int64_t *h_tree_dst, double *h_tree_w, double *dendro_ms, double *extract_ms_out,
+                        cudaStream_t s) {
+    const double t3 = now_ms();
+    trace_mark("dendrogram start");
+    const FoldInput fin = dendrogram_device_sort(ts, td, tw, n, metric == 0, (n - 1) - (n_clusters - 1), s);
+    trace_mark("dendrogram sorted (host)");
+    // the spanning tree goes to pinned staging on the copy engine while the
+    // host folds
+    static thread_local PinnedBuf<int32_t> st_src, st_dst;
+    static thread_local PinnedBuf<double> st_w;
+    const bool want_tree = h_tree_src || h_tree_dst || h_tree_w;
+    if (want_tree) {
+        SLK_CUDA(cudaMemcpyAsync(st_src.get(n - 1), ts, (n - 1) * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+        SLK_CUDA(cudaMemcpyAsync(st_dst.get(n - 1), td, (n - 1) * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+        SLK_CUDA(cudaMemcpyAsync(st_w.get(n - 1), tw, (n - 1) * sizeof(double), cudaMemcpyDeviceToHost, s));
+    }
+    double extract_ms = 0.0;
+    dendrogram_fold(fin, h_merges, n_clusters, h_labels, &extract_ms);
+    trace_mark("dendrogram folded");
+    const double t5 = now_ms();
+    if (want_tree) {
+        SLK_CUDA(cudaStreamSynchronize(s));
+        const int32_t *hs = st_src.p, *hd = st_dst.p;
+        const double *hw = st_w.p;
+        // widen / copy out of the pinned staging in parallel slices (the caller's
+        // fresh arrays are first touched here)
+        const int64_t m = n - 1;
+        const int nt = (int)std::max<int64_t>(1, std::min<int64_t>(fin.threads, m / 65536 + 1));
+        auto copy = [&](int k) {
+            const int64_t lo = m * k / nt, hi = m * (k + 1) / nt;
+            for (int64_t i = lo; i < hi; i++) {
+                if (h_tree_src) h_tree_src[i] = hs[i];
+                if (h_tree_dst) h_tree_dst[i] = hd[i];
+            }
+            if (h_tree_w) memcpy(h_tree_w + lo, hw + lo, (hi - lo) * sizeof(double));
+        };
+        std::vector<std::thread> pool;
+        for (int k = 1; k < nt; k++) pool.emplace_back(copy, k);
+        copy(0);
+        for (auto &t : pool) t.join();
+    }
+    if (dendro_ms) *dendro_ms = t5 - t3 - extract_ms;  // the cut is taken inside the fold
+    if (extract_ms_out) *extract_ms_out = extract_ms;
+}
+
 // Pipeline state on one device (used by slk_single_linkage); n_gpus > 1
 // shards the two neighbour searches (ShardSet above).
 void single_linkage_device(const float *x32, const double *x64, int64_t n, int d, int k,
@@ -428,46 +479,10 @@ void single_linkage_device(const float *x32, const double *x64, int64_t n, int d
     }
     SLK_CUDA(cudaStreamSynchronize(s));
     double t3 = now_ms();
-    // --- dendrogram (linkage.py:295-300)
-    trace_mark("dendrogram start");
-    const FoldInput fin = dendrogram_device_sort(ts, td, tw, n, metric == 0, (n - 1) - (n_clusters - 1), s);
-    trace_mark("dendrogram sorted (host)");
-    // the spanning tree goes to pinned staging on the copy engine while the
-    // host folds
-    static thread_local PinnedBuf<int32_t> st_src, st_dst;
-    static thread_local PinnedBuf<double> st_w;
-    const bool want_tree = h_tree_src || h_tree_dst || h_tree_w;
-    if (want_tree) {
-        SLK_CUDA(cudaMemcpyAsync(st_src.get(n - 1), ts.get(), (n - 1) * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-        SLK_CUDA(cudaMemcpyAsync(st_dst.get(n - 1), td.get(), (n - 1) * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-        SLK_CUDA(cudaMemcpyAsync(st_w.get(n - 1), tw.get(), (n - 1) * sizeof(double), cudaMemcpyDeviceToHost, s));
-    }
-    double extract_ms = 0.0;
-    dendrogram_fold(fin, h_merges, n_clusters, h_labels, &extract_ms);
-    trace_mark("dendrogram folded");
-    double t5 = now_ms();
-    double t4 = t5 - extract_ms;  // the cut is taken inside the fold
-    if (want_tree) {
-        SLK_CUDA(cudaStreamSynchronize(s));
-        const int32_t *hs = st_src.p, *hd = st_dst.p;
-        const double *hw = st_w.p;
-        // widen / copy out of the pinned staging in parallel slices (the caller's
-        // fresh arrays are first touched here)
-        const int64_t m = n - 1;
-        const int nt = (int)std::max<int64_t>(1, std::min<int64_t>(fin.threads, m / 65536 + 1));
-        auto copy = [&](int k) {
-            const int64_t lo = m * k / nt, hi = m * (k + 1) / nt;
-            for (int64_t i = lo; i < hi; i++) {
-                if (h_tree_src) h_tree_src[i] = hs[i];
-                if (h_tree_dst) h_tree_dst[i] = hd[i];
-            }
-            if (h_tree_w) memcpy(h_tree_w + lo, hw + lo, (hi - lo) * sizeof(double));
-        };
-        std::vector<std::thread> pool;
-        for (int k = 1; k < nt; k++) pool.emplace_back(copy, k);
-        copy(0);
-        for (auto &t : pool) t.join();
-    }
+    double dendro_ms = 0.0, extract_ms = 0.0;
+    finish_tree(ts, td, tw, n, metric, n_clusters, h_merges, h_labels, h_tree_src, h_tree_dst, h_tree_w,
+                &dendro_ms, &extract_ms, s);
+    const double t4 = t3 + dendro_ms, t5 = t4 + extract_ms;
     if (n_iters) *n_iters = iters;
     if (timings) {
         timings[0] = t1 - t0;
@@ -573,6 +588,25 @@ int slk_nn1_colour_ps(void *handle, const int32_t *d_colors, int64_t q0, int64_t
                                                           (long long)q0, (long long)q1, (long long)P.n);
         nn1_ps(P, P, 2, nullptr, d_colors, d_colors, q0, q1, d_idx, d_dist, s);
         SLK_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+int slk_finish_tree(const int32_t *d_src, const int32_t *d_dst, const double *d_w, int64_t n, int metric,
+                    int64_t n_clusters, double *h_merges, int64_t *h_labels, int64_t *h_tree_src,
+                    int64_t *h_tree_dst, double *h_tree_w, double *h_ms, void *stream_) {
+    STREAM(s);
+    return guarded([&] {
+        if (n < 2) throw_invalid("need at least 2 points, got %lld", (long long)n);
+        if (n_clusters < 1 || n_clusters > n)
+            throw_invalid("n_clusters=%lld outside [1, %lld]", (long long)n_clusters, (long long)n);
+        double dm = 0.0, em = 0.0;
+        finish_tree(d_src, d_dst, d_w, n, metric, n_clusters, h_merges, h_labels, h_tree_src, h_tree_dst,
+                    h_tree_w, &dm, &em, s);
+        SLK_CUDA(cudaStreamSynchronize(s));
+        if (h_ms) {
+            h_ms[0] = dm;
+            h_ms[1] = em;
+        }
     });
 }
 

@@ -104,14 +104,29 @@ class DeviceEngine:
         return getattr(pts, "scale_exp", 0)
 
     def finish(self, n, t_src, t_dst, t_w, cfg, scale_exp=0):
-        from .linkage import build_dendrogram, extract_clusters
+        """Dendrogram + cut of the device tree in one native call (slk_finish_tree:
+        the single-process pipeline's own tail, no host round trip of the tree
+        before the fold); the library's outputs skip re-validation."""
+        import ctypes
 
-        tree = EdgeList(n, self._lib.to_host(t_src).astype(np.int64),
-                        self._lib.to_host(t_dst).astype(np.int64),
-                        unscale_sq(self._lib.to_host(t_w), scale_exp))
-        w = np.sqrt(tree.weight) if cfg.metric == "euclidean" else tree.weight
-        dendro = build_dendrogram(EdgeList(n, tree.src, tree.dst, w), n)
-        return tree, dendro, extract_clusters(dendro, cfg.n_clusters)
+        from .core import _trusted
+
+        merges = np.empty((max(n - 1, 1), 4))
+        labels = np.empty(n, dtype=np.int64)
+        ts = np.empty(max(n - 1, 1), dtype=np.int64)
+        td = np.empty(max(n - 1, 1), dtype=np.int64)
+        tw = np.empty(max(n - 1, 1))
+        p = lambda a: a.ctypes.data_as(ctypes.c_void_p)  # noqa: E731
+        metric = 0 if cfg.metric == "euclidean" else 1
+        self._lib.call("slk_finish_tree", self._lib.ptr(t_src), self._lib.ptr(t_dst), self._lib.ptr(t_w), n,
+                       metric, cfg.n_clusters, p(merges), p(labels), p(ts), p(td), p(tw), None,
+                       self._lib.stream_handle())
+        if scale_exp:  # back from the device's power-of-two scaled units (exact)
+            tw[: n - 1] = np.ldexp(tw[: n - 1], 2 * scale_exp)
+            merges[: n - 1, 2] = np.ldexp(merges[: n - 1, 2], scale_exp if metric == 0 else 2 * scale_exp)
+        tree = _trusted(EdgeList, n_vertices=n, src=ts[: n - 1], dst=td[: n - 1], weight=tw[: n - 1])
+        dendro = _trusted(Dendrogram, n_points=n, merges=merges[: n - 1])
+        return tree, dendro, _trusted(LabelArray, labels=labels, n_clusters=cfg.n_clusters)
 
     def sync(self):
         self.torch.cuda.synchronize()
