@@ -250,6 +250,12 @@ struct EdgeSet {
     DevBuf<double> w;
     int64_t m = 0;
 };
+// The same undirected edge sets without sorting (graph.cu), in arbitrary
+// order: a k-NN graph's (rows of k ids, symmetric weights), and a spanning
+// forest united with one cross-colour bridge per point.
+EdgeSet knn_undirected(int64_t n, int k, const int32_t *idx, const double *dist, cudaStream_t s);
+EdgeSet forest_plus_bridges(int64_t n, const int32_t *fa, const int32_t *fb, const double *fw, int64_t ne,
+                            const int32_t *bdst, const double *bw, cudaStream_t s);
 EdgeSet dedup_undirected(int64_t n, const int32_t *src, const int32_t *dst, const double *w,
                          int64_t m, cudaStream_t s);
 // Spanning forest of an undirected edge set (alteration + Boruvka).  Outputs

@@ -616,6 +616,144 @@ int64_t unique_min(const uint64_t *keys_in, const double *w_in, int64_t m, int k
         SLK_CHECK_LAUNCH();                                           \
     } while (0)
 
+// ---------------------------------------------------- sort-free dedups
+// Undirected edges of a k-NN graph without sorting (core.py:264-286 keeps
+// the minimum weight per pair; both directions of a pair carry bit-identical
+// weights, knn.cu:exact_dist being symmetric in its operands): entry i -> j
+// is kept as (i, j) when i < j, and as (j, i) when i > j unless row j also
+// lists i (then row j keeps it).  Output order is arbitrary (msf_undirected
+// orders by (w_alt, a, b) explicitly).
+__global__ void knn_undirected_kernel(const int32_t *idx, const double *dist, int64_t n, int k, int32_t *oa,
+                                      int32_t *ob, double *ow, unsigned long long *count) {
+    const int lane = threadIdx.x & 31;
+    for (int64_t base = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) - lane; base < n * k;
+         base += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t e = base + lane;
+        bool keep = false;
+        int32_t a = 0, b = 0;
+        double w = 0.0;
+        if (e < n * k) {
+            const int32_t i = (int32_t)(e / k), j = idx[e];
+            w = dist[e];
+            if (j >= 0 && j != i) {
+                if (i < j) {
+                    a = i, b = j, keep = true;
+                } else {
+                    bool dup = false;
+                    for (int t = 0; t < k; t++) dup |= idx[(int64_t)j * k + t] == i;
+                    a = j, b = i, keep = !dup;
+                }
+            }
+        }
+        const unsigned m = __ballot_sync(0xffffffffu, keep);
+        unsigned long long at = 0;
+        if (lane == 0 && m) at = atomicAdd(count, (unsigned long long)__popc(m));
+        at = __shfl_sync(0xffffffffu, at, 0);
+        if (keep) {
+            const int64_t p = (int64_t)at + __popc(m & ((1u << lane) - 1u));
+            oa[p] = a;
+            ob[p] = b;
+            ow[p] = w;
+        }
+    }
+}
+
+// A spanning forest (canonical a < b, no duplicates) united with one
+// cross-colour bridge per point (i -> bdst[i], weight bw[i]): forest edges
+// join equal colours and bridges different ones, so only mutual bridge pairs
+// repeat (kept from the smaller endpoint).
+__global__ void union_bridges_kernel(const int32_t *bdst, const double *bw, int64_t n, int64_t ne, int32_t *oa,
+                                     int32_t *ob, double *ow, unsigned long long *count) {
+    const int lane = threadIdx.x & 31;
+    for (int64_t base = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) - lane; base < n;
+         base += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = base + lane;
+        bool keep = false;
+        int32_t a = 0, b = 0;
+        double w = 0.0;
+        if (i < n) {
+            const int32_t j = bdst[i];
+            w = bw[i];
+            if (j >= 0 && j != i) {
+                keep = (int32_t)i < j || bdst[j] != (int32_t)i;
+                a = min((int32_t)i, j);
+                b = max((int32_t)i, j);
+            }
+        }
+        const unsigned m = __ballot_sync(0xffffffffu, keep);
+        unsigned long long at = 0;
+        if (lane == 0 && m) at = atomicAdd(count, (unsigned long long)__popc(m));
+        at = __shfl_sync(0xffffffffu, at, 0);
+        if (keep) {
+            const int64_t p = ne + (int64_t)at + __popc(m & ((1u << lane) - 1u));
+            oa[p] = a;
+            ob[p] = b;
+            ow[p] = w;
+        }
+    }
+}
+
+// ------------------------------------- (w_alt, a, b) order with one sort
+// w_alt = w + hash * theta (1 - 2^-20) with theta the smallest gap between
+// distinct weights: for distinct w the w order IS the w_alt order (up to the
+// rounding case checked below), so one stable sort by w plus an explicit
+// (w_alt, a, b) sort of every run of equal w gives the solver's order.
+// alter_sorted_kernel: w_alt of the w-sorted list
+__global__ void alter_sorted_kernel(const int32_t *a, const int32_t *b, const double *ws, const int32_t *perm,
+                                    int64_t m, int64_t seed, double eps_max, double *alt) {
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < m; p += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t e = perm[p];
+        const uint32_t x = (uint32_t)a[e], y = (uint32_t)b[e];
+        // bit-identical to alter_kernel: hash of the canonical (min, max) pair
+        alt[p] = __dadd_rn(ws[p], __dmul_rn(hash_unit(x < y ? x : y, x < y ? y : x, seed), eps_max));
+    }
+}
+
+// (w_alt, a, b) order on canonical pairs (a = min, b = max of the endpoints)
+__device__ __forceinline__ bool alt_less(double x, int32_t xa, int32_t xb, double y, int32_t ya, int32_t yb) {
+    const int32_t xl = min(xa, xb), xh = max(xa, xb), yl = min(ya, yb), yh = max(ya, yb);
+    return x < y || (x == y && (xl < yl || (xl == yl && xh < yh)));
+}
+
+// runs of equal w: insertion sort by (w_alt, a, b); flag bit 0 = a run longer
+// than MAX_RUN (the caller then sorts by w_alt instead)
+constexpr int MAX_RUN = 64;
+__global__ void fixup_runs_kernel(const double *ws, double *alt, int32_t *perm, const int32_t *a, const int32_t *b,
+                                  int64_t m, int *flag) {
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < m; p += (int64_t)gridDim.x * blockDim.x) {
+        if (p > 0 && ws[p] == ws[p - 1]) continue;  // not a run start
+        int64_t e = p + 1;
+        while (e < m && ws[e] == ws[p] && e - p <= MAX_RUN) e++;
+        if (e - p == 1) continue;
+        if (e - p > MAX_RUN) {
+            atomicOr(flag, 1);
+            continue;
+        }
+        for (int64_t i = p + 1; i < e; i++) {
+            const double v = alt[i];
+            const int32_t pi = perm[i], va = a[pi], vb = b[pi];
+            int64_t j = i - 1;
+            while (j >= p && alt_less(v, va, vb, alt[j], a[perm[j]], b[perm[j]])) {
+                alt[j + 1] = alt[j];
+                perm[j + 1] = perm[j];
+                j--;
+            }
+            alt[j + 1] = v;
+            perm[j + 1] = pi;
+        }
+    }
+}
+
+// flag bit 1: the list is not strictly increasing in (w_alt, a, b)
+__global__ void check_order_kernel(const double *alt, const int32_t *perm, const int32_t *a, const int32_t *b,
+                                   int64_t m, int *flag) {
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < m; p += (int64_t)gridDim.x * blockDim.x) {
+        if (p == 0) continue;
+        const int32_t x = perm[p - 1], y = perm[p];
+        if (!alt_less(alt[p - 1], a[x], b[x], alt[p], a[y], b[y])) atomicOr(flag, 2);
+    }
+}
+
 EdgeSet dedup_undirected(int64_t n, const int32_t *src, const int32_t *dst, const double *w,
                          int64_t m, cudaStream_t s) {
     EdgeSet E;
@@ -627,6 +765,56 @@ EdgeSet dedup_undirected(int64_t n, const int32_t *src, const int32_t *dst, cons
     E.w.alloc(m, s);
     E.m = unique_min(keys.get(), w, m, 32 + bits_for(n), E.a.get(), E.b.get(), E.w.get(), s);
     return E;
+}
+
+EdgeSet knn_undirected(int64_t n, int k, const int32_t *idx, const double *dist, cudaStream_t s) {
+    EdgeSet E;
+    const int64_t m = n * k;
+    if (m == 0) return E;
+    E.a.alloc(m, s);
+    E.b.alloc(m, s);
+    E.w.alloc(m, s);
+    DevBuf<unsigned long long> cnt(1, s);
+    SLK_CUDA(cudaMemsetAsync(cnt.get(), 0, sizeof(unsigned long long), s));
+    LAUNCH(knn_undirected_kernel, m, idx, dist, n, k, E.a.get(), E.b.get(), E.w.get(), cnt.get());
+    E.m = (int64_t)read_scalar(cnt.get(), s);
+    return E;
+}
+
+EdgeSet forest_plus_bridges(int64_t n, const int32_t *fa, const int32_t *fb, const double *fw, int64_t ne,
+                            const int32_t *bdst, const double *bw, cudaStream_t s) {
+    EdgeSet E;
+    E.a.alloc(ne + n, s);
+    E.b.alloc(ne + n, s);
+    E.w.alloc(ne + n, s);
+    if (ne > 0) {
+        SLK_CUDA(cudaMemcpyAsync(E.a.get(), fa, ne * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+        SLK_CUDA(cudaMemcpyAsync(E.b.get(), fb, ne * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+        SLK_CUDA(cudaMemcpyAsync(E.w.get(), fw, ne * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    }
+    DevBuf<unsigned long long> cnt(1, s);
+    SLK_CUDA(cudaMemsetAsync(cnt.get(), 0, sizeof(unsigned long long), s));
+    LAUNCH(union_bridges_kernel, n, bdst, bw, n, ne, E.a.get(), E.b.get(), E.w.get(), cnt.get());
+    E.m = ne + (int64_t)read_scalar(cnt.get(), s);
+    return E;
+}
+
+// theta from weights already sorted ascending; m > 0.
+static double theta_of_sorted(const double *sorted, int64_t m, cudaStream_t s) {
+    DevBuf<unsigned long long> gap(1, s);
+    unsigned long long init = (unsigned long long)0x7ff0000000000000ull;  // +inf bits
+    SLK_CUDA(cudaMemcpyAsync(gap.get(), &init, sizeof(init), cudaMemcpyHostToDevice, s));
+    min_gap_kernel<<<grid_for(m, 256, 2048), 256, 0, s>>>(sorted, m, gap.get());
+    SLK_CHECK_LAUNCH();
+    unsigned long long g = read_scalar(gap.get(), s);
+    if (g != init) {
+        double theta;
+        memcpy(&theta, &g, sizeof theta);
+        return theta;
+    }
+    double first = read_scalar(sorted, s);
+    double a = fabs(first);
+    return (a > 1.0 ? a : 1.0) * 0x1p-20;  // single distinct weight (mst.py:219)
 }
 
 // theta (mst.py:215-219) of the given weights; m > 0.
@@ -671,7 +859,32 @@ void msf_undirected(int64_t n, const int32_t *a_in, const int32_t *b_in, const d
     const double *w = w_in;
     DevBuf<int32_t> sa, sb;
     DevBuf<double> sw;
-    if (!presorted && m > 0) {
+    // --- rank order (w_alt, a, b) with ONE stable sort by w (see
+    // fixup_runs_kernel), for unsorted input (the pipeline's sort-free
+    // dedups).  Falls back to sorting by w_alt over the (a, b)-sorted list when
+    // a run of equal weights is long or rounding breaks the order; (a, b)-
+    // sorted input (CSR graphs, integer road weights with long runs of equal
+    // weights) takes that path directly.
+    DevBuf<int32_t> fperm;
+    bool fast = false;
+    if (m > 0 && !presorted && !getenv("SLK_MSF_TWO_SORTS")) {
+        DevBuf<double> ww(m, s), ws(m, s), alt(m, s);
+        DevBuf<int32_t> iota(m, s);
+        fperm.alloc(m, s);
+        LAUNCH(negate_kernel, m, w_in, m, ww.get(), negate);
+        LAUNCH(iota_kernel, m, iota.get(), m);
+        sort_pairs(ww.get(), ws.get(), iota.get(), fperm.get(), m, s);
+        const double theta = theta_of_sorted(ws.get(), m, s);
+        LAUNCH(alter_sorted_kernel, m, a_in, b_in, ws.get(), fperm.get(), m, seed, theta * (1.0 - 0x1p-20),
+               alt.get());
+        DevBuf<int> flag(1, s);
+        SLK_CUDA(cudaMemsetAsync(flag.get(), 0, sizeof(int), s));
+        LAUNCH(fixup_runs_kernel, m, ws.get(), alt.get(), fperm.get(), a_in, b_in, m, flag.get());
+        LAUNCH(check_order_kernel, m, alt.get(), fperm.get(), a_in, b_in, m, flag.get());
+        fast = read_scalar(flag.get(), s) == 0;
+        if (!fast) fperm.release();
+    }
+    if (!presorted && m > 0 && !fast) {
         // the (w_alt, a, b) tie-break needs the list in (a, b) order first
         DevBuf<uint64_t> keys(m, s), ks(m, s);
         DevBuf<int32_t> iota(m, s), perm(m, s);
@@ -691,26 +904,29 @@ void msf_undirected(int64_t n, const int32_t *a_in, const int32_t *b_in, const d
     LAUNCH(iota_kernel, n, color.get(), n);
     int64_t accepted_count = 0;
     if (m > 0) {
-        // --- order: w_alt (mst.py:198-222), ties by (a, b) via a stable sort
-        DevBuf<double> ww(m, s), alt(m, s);
-        LAUNCH(negate_kernel, m, w, m, ww.get(), negate);
-        double theta = compute_theta(ww.get(), m, s);
-        double eps_max = theta * (1.0 - 0x1p-20);
-        LAUNCH(alter_kernel, m, a, b, ww.get(), m, seed, eps_max, alt.get());
-        DevBuf<int32_t> iota(m, s), perm(m, s);
-        DevBuf<double> alt_sorted(m, s);
-        LAUNCH(iota_kernel, m, iota.get(), m);
-        // (a, b) order of the input is required for the tie-break: callers pass
-        // edge lists sorted by (a, b) (dedup_undirected / CSR order).
-        sort_pairs(alt.get(), alt_sorted.get(), iota.get(), perm.get(), m, s);
+        // --- order: w_alt (mst.py:198-222), ties by (a, b)
+        DevBuf<int32_t> perm;
+        if (fast) {
+            perm = std::move(fperm);
+        } else {
+            // stable sort by w_alt over the (a, b)-sorted list
+            DevBuf<double> ww(m, s), alt(m, s);
+            LAUNCH(negate_kernel, m, w, m, ww.get(), negate);
+            double theta = compute_theta(ww.get(), m, s);
+            double eps_max = theta * (1.0 - 0x1p-20);
+            LAUNCH(alter_kernel, m, a, b, ww.get(), m, seed, eps_max, alt.get());
+            DevBuf<int32_t> iota(m, s);
+            DevBuf<double> alt_sorted(m, s);
+            perm.alloc(m, s);
+            LAUNCH(iota_kernel, m, iota.get(), m);
+            sort_pairs(alt.get(), alt_sorted.get(), iota.get(), perm.get(), m, s);
+        }
         DevBuf<int32_t> ra(m, s), rb(m, s);
         DevBuf<double> rw(m, s);
         LAUNCH(gather_kernel<int32_t>, m, a, perm.get(), m, ra.get());
         LAUNCH(gather_kernel<int32_t>, m, b, perm.get(), m, rb.get());
         LAUNCH(gather_kernel<double>, m, w, perm.get(), m, rw.get());
-        alt.release();
-        alt_sorted.release();
-        ww.release();
+        perm.release();
 
         // --- Boruvka rounds on ranks: one persistent cooperative launch
         DevBuf<int32_t> ea2(m, s), eb2(m, s), flag(m, s), pos(m, s);

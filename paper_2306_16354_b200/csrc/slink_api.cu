@@ -119,18 +119,6 @@ int num_sms() {
 
 namespace {
 
-__global__ void repeat_rows_kernel(int64_t n, int k, int32_t *src) {
-    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n * k;
-         e += (int64_t)gridDim.x * blockDim.x)
-        src[e] = (int32_t)(e / k);
-}
-
-__global__ void iota32_kernel(int64_t n, int32_t *v) {
-    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
-         e += (int64_t)gridDim.x * blockDim.x)
-        v[e] = (int32_t)e;
-}
-
 // The library's own stream for host-buffer entry points: one per device,
 // created once and kept, so the stream-ordered pool reuses the previous
 // call's scratch (a fresh stream per call made the pool map new memory:
@@ -405,17 +393,13 @@ void single_linkage_device(const float *x32, const double *x64, int64_t n, int d
     trace_mark("knn synced");
     double t1 = now_ms();
     // --- symmetrise + spanning forest (linkage.py:289-290)
-    DevBuf<int32_t> src(n * k, s);
-    repeat_rows_kernel<<<grid_for(n * k, 256), 256, 0, s>>>(n, k, src);
-    SLK_CHECK_LAUNCH();
-    EdgeSet E = dedup_undirected(n, src, idx, dist, n * k, s);
-    src.release();
+    EdgeSet E = knn_undirected(n, k, idx, dist, s);
     idx.release();
     dist.release();
     DevBuf<int32_t> ts(n, s), td(n, s), colors(n, s);
     DevBuf<double> tw(n, s);
     int64_t ne = 0, nc = 0;
-    msf_undirected(n, E.a, E.b, E.w, E.m, true, false, seed, ts, td, tw, colors, &ne, &nc, s);
+    msf_undirected(n, E.a, E.b, E.w, E.m, false, false, seed, ts, td, tw, colors, &ne, &nc, s);
     E = EdgeSet{};
     double t2 = now_ms();
     // --- connect loop (linkage.py:222-254)
@@ -428,7 +412,7 @@ void single_linkage_device(const float *x32, const double *x64, int64_t n, int d
         base_colors.alloc(n, s);
         SLK_CUDA(cudaMemcpyAsync(base_colors.get(), colors.get(), n * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
         if (P) P->block_hint = base_colors.get();
-        DevBuf<int32_t> usrc(2 * n, s), udst(2 * n, s);
+        DevBuf<int32_t> udst(2 * n, s);
         DevBuf<double> uw(2 * n, s);
         while (nc > 1) {
             if (iters >= budget) {
@@ -440,13 +424,7 @@ void single_linkage_device(const float *x32, const double *x64, int64_t n, int d
                                 " iterations: " + std::to_string(nc) +
                                 " components remain (largest sizes " + largest_sizes(hc) + ")"};
             }
-            // bridges: one per point (neighbors.py:375-391)
-            int64_t m = ne + n;
-            SLK_CUDA(cudaMemcpyAsync(usrc.get(), ts.get(), ne * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
-            SLK_CUDA(cudaMemcpyAsync(udst.get(), td.get(), ne * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
-            SLK_CUDA(cudaMemcpyAsync(uw.get(), tw.get(), ne * sizeof(double), cudaMemcpyDeviceToDevice, s));
-            iota32_kernel<<<grid_for(n, 256), 256, 0, s>>>(n, usrc.get() + ne);
-            SLK_CHECK_LAUNCH();
+            // bridges: one per point (neighbors.py:375-391), rows ne .. ne + n of udst / uw
             if (shards) {
                 // every shard scans its chunks against the replicated index
                 // with this iteration's colours; bridges come back by rows
@@ -472,8 +450,8 @@ void single_linkage_device(const float *x32, const double *x64, int64_t n, int d
             } else {
                 nn1_ps(*P, *P, 2, nullptr, colors, colors, 0, n, udst.get() + ne, uw.get() + ne, s);
             }
-            EdgeSet U = dedup_undirected(n, usrc, udst, uw, m, s);
-            msf_undirected(n, U.a, U.b, U.w, U.m, true, false, seed, ts, td, tw, colors, &ne, &nc, s);
+            EdgeSet U = forest_plus_bridges(n, ts, td, tw, ne, udst.get() + ne, uw.get() + ne, s);
+            msf_undirected(n, U.a, U.b, U.w, U.m, false, false, seed, ts, td, tw, colors, &ne, &nc, s);
             iters++;
         }
     }
