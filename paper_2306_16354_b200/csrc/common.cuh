@@ -301,6 +301,9 @@ struct FoldInput {
     const int64_t *off = nullptr;
     int64_t ngroups = 0;
     int threads = 1;
+    // flat cut taken on the device (dendro.cu): int32 labels in pinned host
+    // memory, valid once the stream has synchronised after the fold
+    const int32_t *labels = nullptr;
 };
 // cut: merges before the flat cut ((n-1) - (n_clusters-1)), < 0 for none
 FoldInput dendrogram_device_sort(const int32_t *src, const int32_t *dst, const double *w, int64_t n,

@@ -114,8 +114,36 @@ __global__ void group_gather_kernel(const int32_t *rank, int64_t t, const int32_
     }
 }
 
+// ---- the flat cut on the device (linkage.py:184-213): after the first `cut`
+// merges the clusters are the components of the forest of those edges; a
+// component's cluster id is n + (its last merge), a point alone keeps its own
+// id; labels rank the ids ascending (the roots are exactly those ids).
+__global__ void cut_max_kernel(const int32_t *a, int64_t cut, int32_t *parent, int32_t *cmax) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < cut; e += (int64_t)gridDim.x * blockDim.x)
+        atomicMax(&cmax[cc_find(parent, a[e])], (int32_t)e);
+}
+
+__global__ void cut_rid_kernel(int64_t n, int32_t *parent, const int32_t *cmax, int32_t *rid, int32_t *flag) {
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t r = cc_find(parent, (int32_t)v);
+        const int32_t id = cmax[r] >= 0 ? (int32_t)(n + cmax[r]) : (int32_t)v;
+        rid[v] = id;
+        flag[id] = 1;
+    }
+}
+
+__global__ void cut_label_kernel(int64_t n, const int32_t *rid, const int32_t *pos, int32_t *lab) {
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x)
+        lab[v] = pos[rid[v]];
+}
+
+__global__ void fill_minus1_kernel(int32_t *v, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        v[i] = -1;
+}
+
 struct FoldStaging {
-    PinnedBuf<int32_t> a, b, rank;
+    PinnedBuf<int32_t> a, b, rank, labels;
     PinnedBuf<double> w;
     std::vector<int64_t> off;
 };
@@ -204,6 +232,29 @@ FoldInput dendrogram_device_sort(const int32_t *src, const int32_t *dst, const d
     in.b = hb;
     in.w = hw;
     in.t = t;
+    if (cut >= 0 && !getenv("SLK_HOST_CUT")) {
+        // enqueued after the fold input is on the host: runs while the host
+        // folds; the caller synchronises the stream before reading labels
+        DevBuf<int32_t> parent(n, s), cmax(n, s), rid(n, s), flag(n + cut, s), pos(n + cut, s), lab(n, s);
+        cc_init_kernel<<<grid_for(n, 256), 256, 0, s>>>(parent, n);
+        fill_minus1_kernel<<<grid_for(n, 256), 256, 0, s>>>(cmax, n);
+        SLK_CUDA(cudaMemsetAsync(flag.get(), 0, (n + cut) * sizeof(int32_t), s));
+        if (cut > 0) {
+            cc_hook_kernel<<<grid_for(cut, 256), 256, 0, s>>>(a, b, cut, parent);
+            cut_max_kernel<<<grid_for(cut, 256), 256, 0, s>>>(a, cut, parent, cmax);
+        }
+        cut_rid_kernel<<<grid_for(n, 256), 256, 0, s>>>(n, parent, cmax, rid, flag);
+        SLK_CHECK_LAUNCH();
+        size_t tmp = 0;
+        SLK_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, flag.get(), pos.get(), (int)(n + cut), s));
+        DevBuf<unsigned char> tb(tmp, s);
+        SLK_CUDA(cub::DeviceScan::ExclusiveSum(tb.get(), tmp, flag.get(), pos.get(), (int)(n + cut), s));
+        cut_label_kernel<<<grid_for(n, 256), 256, 0, s>>>(n, rid, pos, lab);
+        SLK_CHECK_LAUNCH();
+        int32_t *hl = staging.labels.get(n);
+        SLK_CUDA(cudaMemcpyAsync(hl, lab.get(), n * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+        in.labels = hl;
+    }
     return in;
 }
 

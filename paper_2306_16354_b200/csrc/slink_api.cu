@@ -298,8 +298,25 @@ static void finish_tree(const int32_t *ts, const int32_t *td, const double *tw, 
         SLK_CUDA(cudaMemcpyAsync(st_w.get(n - 1), tw, (n - 1) * sizeof(double), cudaMemcpyDeviceToHost, s));
     }
     double extract_ms = 0.0;
-    dendrogram_fold(fin, h_merges, n_clusters, h_labels, &extract_ms);
+    // the flat cut: on the device when dendrogram_device_sort took it (labels
+    // in pinned staging after the stream syncs), else during the host fold
+    dendrogram_fold(fin, h_merges, n_clusters, fin.labels ? nullptr : h_labels, &extract_ms);
     trace_mark("dendrogram folded");
+    if (fin.labels) {
+        const double te = now_ms();
+        SLK_CUDA(cudaStreamSynchronize(s));
+        const int32_t *hl = fin.labels;
+        const int nt = (int)std::max<int64_t>(1, std::min<int64_t>(fin.threads, n / 65536 + 1));
+        auto widen = [&](int k) {
+            const int64_t lo = n * k / nt, hi = n * (k + 1) / nt;
+            for (int64_t i = lo; i < hi; i++) h_labels[i] = hl[i];
+        };
+        std::vector<std::thread> pool;
+        for (int k = 1; k < nt; k++) pool.emplace_back(widen, k);
+        widen(0);
+        for (auto &t : pool) t.join();
+        extract_ms = now_ms() - te;
+    }
     const double t5 = now_ms();
     if (want_tree) {
         SLK_CUDA(cudaStreamSynchronize(s));
