@@ -840,8 +840,29 @@ __device__ double certified_floor_bc(float T, float rho_s, double scale, int d, 
     return dlo - ev;
 }
 
+// exact_dist with the query row already in float64 (shared memory, one copy
+// per warp) and the candidate row read as float4: same products and the same
+// sequential sum as exact_dist (ref neighbors.py:80-89,132-137)
+__device__ __forceinline__ double exact_dist_sq(const double *sq, const float *x32, int64_t j, int d, double nq,
+                                                double nx) {
+    const float4 *xr = reinterpret_cast<const float4 *>(x32 + j * d);
+    double dot = 0.0;
+    for (int t = 0; t < d / 4; t++) {
+        const float4 b = __ldg(xr + t);
+        dot = __dadd_rn(dot, __dmul_rn(sq[4 * t + 0], (double)b.x));
+        dot = __dadd_rn(dot, __dmul_rn(sq[4 * t + 1], (double)b.y));
+        dot = __dadd_rn(dot, __dmul_rn(sq[4 * t + 2], (double)b.z));
+        dot = __dadd_rn(dot, __dmul_rn(sq[4 * t + 3], (double)b.w));
+    }
+    double v = __dsub_rn(__dadd_rn(nq, nx), __dmul_rn(2.0, dot));
+    return v < 0.0 ? 0.0 : v;
+}
+
+constexpr int REFINE_SQ_MAXD = 128;  // query rows staged in float64 up to this many dims
+
 template <int R>
 __global__ void refine_kernel(RefineArgs a) {
+    __shared__ double s_q[8][REFINE_SQ_MAXD];  // 256-thread blocks: one row per warp
     const int lane = threadIdx.x & 31;
     const int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int64_t nrows = a.row1 - a.row0;
@@ -850,13 +871,24 @@ __global__ void refine_kernel(RefineArgs a) {
     if (a.qid && a.qid[gi] < 0) return;  // padding row of a gathered query set
     const int32_t *cand = a.cand + wid * (32 * R);
     const double nq = a.qnorm[gi];
+    // cross-colour passes (k = 1, few candidates a row): the query row is
+    // converted to float64 once per warp instead of once per candidate (the
+    // conversions bound that refine on the XU pipe: 2.1 -> 1.5 ms at C3); the
+    // k-NN refine is load-bound and keeps the per-candidate form
+    const bool staged = a.k == 1 && !a.q64 && !a.x64 && (a.d & 3) == 0 && a.d <= REFINE_SQ_MAXD;
+    double *sq = s_q[(threadIdx.x >> 5) & 7];
+    if (staged) {
+        for (int t = lane; t < a.d; t += 32) sq[t] = (double)a.q32[gi * a.d + t];
+        __syncwarp();
+    }
     double lv[R];
     int li[R];
 #pragma unroll
     for (int r = 0; r < R; r++) {
         int j = cand[r * 32 + lane];
         if (j >= 0) {
-            lv[r] = exact_dist(a.q32, a.q64, a.x32, a.x64, gi, j, a.d, nq, a.xnorm[j]);
+            lv[r] = staged ? exact_dist_sq(sq, a.x32, j, a.d, nq, a.xnorm[j])
+                           : exact_dist(a.q32, a.q64, a.x32, a.x64, gi, j, a.d, nq, a.xnorm[j]);
             li[r] = j;
         } else {
             lv[r] = INFINITY;
