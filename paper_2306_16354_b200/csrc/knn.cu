@@ -1539,7 +1539,7 @@ int tc_pass(const PointSet &Q, const PointSet &X, const int32_t *qid, int k, int
             int64_t q1, float scale, float inv_scale2, int32_t *out_idx, double *out_dist,
             DevBuf<int> &fail, DevBuf<float> &kth, cudaStream_t s, const PointSet *Xscan = nullptr,
             const int32_t *xid = nullptr, bool self_pos = false, bool rerun = false, bool bc_ok = true,
-            const int32_t *xpos = nullptr) {
+            const int32_t *xpos = nullptr, bool unprunable = false) {
     ScanStats &st = scan_stats();
     const PointSet &XS = Xscan ? *Xscan : X;
     const int64_t rows = q1 - q0;
@@ -1550,7 +1550,9 @@ int tc_pass(const PointSet &Q, const PointSet &X, const int32_t *qid, int k, int
     // launch still fills the GPU with them
     // block-centred one-product kernel for the first pass (tc_bc.cu); the
     // re-blocked rerun keeps the query-centred three-product kernel
-    const bool bc = !rerun && bc_ok && tc::bc_supported(mode, d, kp);
+    // bc_ok: the caller's decision (search), which also accounts for how
+    // much the data prunes; here only the kernel's own limits
+    const bool bc = !rerun && bc_ok && tc::bc_supported(mode, d, kp, true);
     int qbn = bc ? 1 : tc::group_blocks(d, kp);
     // pairs pay in the 1-NN passes (conversion-bound); the k-NN pass is
     // insertion-bound and only sees the extra tiles (C3: +18 %)
@@ -1611,7 +1613,10 @@ int tc_pass(const PointSet &Q, const PointSet &X, const int32_t *qid, int k, int
                   Q.nb, scale, inv_scale2, mask, qcolor, xcolp.get() ? xcolp.get() : xcolor,
                   cand, kth_split, qhat, q0, q1,
                   V.sb_order, V.sb_lb, V.flat_lb, V.nvalid, XS.nsb, tiles, qid, nsplit, xid, self_pos ? 1 : 0,
-                  bc ? 1 : tc::nprod_for(rerun), bc ? ensure_bcpack(XS, scale, s) : nullptr, xpos};
+                  // chunked large-d kernel over data that does not prune: one fp16
+                  // product (measured C4 d = 512: 4.4 -> 3.3 s incl. the reruns)
+                  bc ? 1 : (!rerun && unprunable && tc::chunked(d) ? 1 : tc::nprod_for(rerun)),
+                  bc ? ensure_bcpack(XS, scale, s) : nullptr, xpos};
     if (bc) tc::bc_timeline_arm(s);
     else tc::timeline_arm(s);
     ev_scan.start(s);
@@ -1900,6 +1905,58 @@ __global__ void __launch_bounds__(BM) two_means_kernel(const float *__restrict__
     }
     (void)seed;
     part[blockIdx.x * (int64_t)BM + j] = ok ? (int8_t)my : (int8_t)2;
+}
+
+// Does the index prune at all?  Its blocks overlap everywhere when their mean
+// radius is comparable to the extent of the whole set (one Gaussian, or
+// clusters in random order): then every tile is computed and the scan is
+// paced by its tensor / operand side, where the block-centred kernel wins.
+__global__ void block_extent_kernel(const float *__restrict__ centroid, const float *__restrict__ radius, int64_t nb,
+                                    int d, float *out) {
+    __shared__ float cbar[512];
+    __shared__ float red[2][256];
+    const int tid = threadIdx.x;
+    for (int t = tid; t < d && t < 512; t += blockDim.x) {
+        double acc = 0.0;
+        for (int64_t b = 0; b < nb; b++) acc += centroid[(int64_t)t * nb + b];
+        cbar[t] = (float)(acc / nb);
+    }
+    __syncthreads();
+    float ext = 0.0f, rsum = 0.0f;
+    for (int64_t b = tid; b < nb; b += blockDim.x) {
+        float s2 = 0.0f;
+        for (int t = 0; t < d && t < 512; t++) {
+            const float df = centroid[(int64_t)t * nb + b] - cbar[t];
+            s2 = fmaf(df, df, s2);
+        }
+        ext = fmaxf(ext, sqrtf(s2) + radius[b]);
+        rsum += radius[b];
+    }
+    red[0][tid] = ext;
+    red[1][tid] = rsum;
+    __syncthreads();
+    for (int w = blockDim.x / 2; w; w >>= 1) {
+        if (tid < w) {
+            red[0][tid] = fmaxf(red[0][tid], red[0][tid + w]);
+            red[1][tid] += red[1][tid + w];
+        }
+        __syncthreads();
+    }
+    if (tid == 0) {
+        out[0] = red[1][0] / (float)nb;  // mean block radius
+        out[1] = red[0][0];              // extent: farthest block sphere from the mean centroid
+    }
+}
+
+bool blocks_overlap(const PointSet &X, cudaStream_t s) {
+    if (X.nb < 64) return false;
+    DevBuf<float> out(2, s);
+    block_extent_kernel<<<1, 256, 0, s>>>(X.centroid, X.radius, X.nb, X.d, out);
+    SLK_CHECK_LAUNCH();
+    float h[2];
+    SLK_CUDA(cudaMemcpyAsync(h, out.get(), sizeof(h), cudaMemcpyDeviceToHost, s));
+    SLK_CUDA(cudaStreamSynchronize(s));
+    return h[0] > 0.5f * h[1];
 }
 
 // blocks whose radius exceeds twice the median radius
@@ -2237,7 +2294,8 @@ void search(const PointSet &Q, const PointSet &X, int k, int mode, const uint8_t
         }
         if (nfail < 0) {
             // block-centred scan: its index blocks must be tight (split_index)
-            const int st = tc::bc_supported(mode, d, tc_kp(k, false)) ? split_index(X, s) : 2;
+            const bool unpr = mode == MODE_SELF && (d < 96 || tc::chunked(d)) && blocks_overlap(X, s);
+            const int st = tc::bc_supported(mode, d, tc_kp(k, false), unpr) ? split_index(X, s) : 2;
             if (st == 1) {
                 SplitIndex &SI = *X.split;
                 const int64_t m = SI.P.n;
@@ -2253,7 +2311,8 @@ void search(const PointSet &Q, const PointSet &X, int k, int mode, const uint8_t
                                 out_idx, out_dist, fail, kth, s, &SI.P, SI.xid, false, false, true, SI.xpos);
             } else {
                 nfail = tc_pass(Q, X, nullptr, k, tc_kp(k, false), mode, mask, qcolor, xcolor, q0, q1, scale,
-                                inv_scale2, out_idx, out_dist, fail, kth, s, nullptr, nullptr, false, false, st == 0);
+                                inv_scale2, out_idx, out_dist, fail, kth, s, nullptr, nullptr, false, false, st == 0,
+                                nullptr, unpr);
             }
         }
         (void)Rsel;

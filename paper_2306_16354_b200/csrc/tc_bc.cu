@@ -631,18 +631,22 @@ int bc_dk(int d) { return d <= 16 ? 16 : d <= 32 ? 32 : d <= 64 ? 64 : d <= 128 
 
 size_t bc_record_bytes(int d) { return bc_dk(d) ? rec_bytes(bc_dk(d)) : 0; }
 
-// Measured at the bench configs (round 2): the block-centred kernel wins on
-// the cross-colour passes at d >= 64 (C3 -20 %, C2 -25 %); the k-NN pass is
-// bound by its insertion epilogue either way (C3 +6 % here) and at d = 32
-// (C5) the query-centred kernel is faster.  SLK_TC_BC=0 disables it,
-// SLK_TC_BC=2 allows it for every supported pass.
-bool bc_supported(int mode, int d, int kp) {
+// Measured at the bench configs (round 2): the block-centred kernel wins
+// wherever the tensor / operand side paces the scan — the cross-colour passes
+// at d >= 64 (C3 -30 %, C2 -25 %), the k-NN pass at d = 128 (C2 -25 %), and
+// every k-NN pass over data whose blocks overlap so much that nothing prunes
+// (C4: d = 32 0.42 -> 0.29 s, d = 128 1.06 -> 0.52 s).  The k-NN pass over
+// well-separated clusters at d = 64 (C3) is bound by its insertion epilogue
+// either way and 6 % slower here, and at d = 32 the query-centred kernel wins
+// the cross-colour passes (C5).  `unprunable`: the caller's measure
+// (knn.cu:blocks_overlap).  SLK_TC_BC=0 disables the kernel, =2 allows it for
+// every supported pass.
+bool bc_supported(int mode, int d, int kp, bool unprunable) {
     int lvl = 1;
     if (const char *e = getenv("SLK_TC_BC")) lvl = atoi(e);
     if (lvl == 0 || !bc_dk(d)) return false;
-    if (lvl == 1 && (mode != MODE_COLOR || d <= 32)) return false;
-    if (mode == MODE_COLOR) return kp <= 8;
-    if (mode == MODE_SELF) return kp <= 16;
+    if (mode == MODE_COLOR) return kp <= 8 && (lvl == 2 || d > 32);
+    if (mode == MODE_SELF) return kp <= 16 && (lvl == 2 || d >= 96 || unprunable);
     return false;
 }
 

@@ -49,7 +49,7 @@ int nprod_for(bool rerun);
 // queries re-centred per tile into tensor memory; two column-half lists per
 // row, the refine's certificate takes the largest visited block radius from
 // qhat (float bits, zero-initialised).
-bool bc_supported(int mode, int d, int kp);
+bool bc_supported(int mode, int d, int kp, bool unprunable = false);
 size_t bc_record_bytes(int d);
 // rowmap (optional): position p of the index is row rowmap[p] of x32
 void bc_pack(const float *x32, const int32_t *rowmap, int64_t n, int d, int64_t nb, const float *centroid,
