@@ -603,7 +603,7 @@ __global__ void superblock_lb_kernel(const float *__restrict__ qc, const float *
                                      int64_t nqb, const int2 *__restrict__ qcol,
                                      const int2 *__restrict__ scol, float *__restrict__ key,
                                      float *__restrict__ lb, int32_t *__restrict__ ids,
-                                     int32_t *__restrict__ seg) {
+                                     int32_t *__restrict__ seg, bool common_order) {
     const int64_t total = nqb * nsb;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
          e += (int64_t)gridDim.x * blockDim.x) {
@@ -614,7 +614,9 @@ __global__ void superblock_lb_kernel(const float *__restrict__ qc, const float *
             s += df * df;
         }
         const bool same = same_colour(qcol, scol, q, b);
-        key[e] = same ? INFINITY : (float)s;
+        // common_order: every query group walks the superblocks in id order,
+        // so the CTAs resident together stream the same index tiles through L2
+        key[e] = same ? INFINITY : (common_order ? (float)b : (float)s);
         lb[e] = same ? INFINITY : sphere_lb(qc, qr, nqb_total, q, sc, sr, nsb, b, d);
         ids[e] = (int32_t)b;
         if (b == 0) seg[ql] = (int32_t)(ql * nsb);
@@ -1267,7 +1269,13 @@ void sort_segments(const float *key, const int32_t *ids, int64_t nseg, int64_t n
     SLK_CHECK_LAUNCH();
 }
 
-VisitOrder visit_order(const QueryGroups &G, const PointSet &X, int d, const int32_t *xcolor, cudaStream_t s) {
+// common_order (data that does not prune, knn.cu:blocks_overlap): one visit
+// order for every query group instead of centroid-distance order — every
+// block is computed anyway, and a shared order lets the CTAs resident at the
+// same time reuse each index tile from L2 (C4 d = 512: the 2 GB index is
+// streamed by every CTA otherwise).
+VisitOrder visit_order(const QueryGroups &G, const PointSet &X, int d, const int32_t *xcolor, cudaStream_t s,
+                       bool common_order = false) {
     const int64_t nqb = G.ng, qb0 = 0;
     const int64_t nxb = X.nb, nsb = X.nsb, stotal = nqb * nsb;
     if (stotal >= (1ll << 31)) throw_invalid("too many (query block, superblock) pairs: %lld", (long long)stotal);
@@ -1286,7 +1294,7 @@ VisitOrder visit_order(const QueryGroups &G, const PointSet &X, int d, const int
     DevBuf<int32_t> ids(stotal, s), seg(nqb + 1, s);
     superblock_lb_kernel<<<grid_for(stotal, 256), 256, 0, s>>>(
         G.cent, G.rad, G.ng, X.sb_centroid, X.sb_radius, nsb, d, qb0, nqb, qrange,
-        srange.get(), key, sblb_id, ids, seg);
+        srange.get(), key, sblb_id, ids, seg, common_order);
     SLK_CHECK_LAUNCH();
     V.sb_order.alloc(stotal, s);
     sort_segments(key, ids, nqb, nsb, seg, skey, V.sb_order, s);
@@ -1597,7 +1605,8 @@ int tc_pass(const PointSet &Q, const PointSet &X, const int32_t *qid, int k, int
     SLK_CUDA(cudaMemsetAsync(counters, 0, sizeof(int), s));
     EventPair ev_order, ev_scan, ev_refine;
     ev_order.start(s);
-    VisitOrder V = visit_order(G, XS, d, mode == MODE_COLOR ? xcolor : nullptr, s);
+    VisitOrder V = visit_order(G, XS, d, mode == MODE_COLOR ? xcolor : nullptr, s,
+                               unprunable && !getenv("SLK_NO_COMMON_ORDER"));
     ev_order.stop(s);
     trace_mark("visit_order enqueued");
     // colours of the index padded to whole blocks (one bulk copy per block)
