@@ -20,6 +20,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "host_pool.h"
 
 namespace slk {
 
@@ -86,10 +87,7 @@ inline void fold_run(Node *nd, const FoldInput &in, const int32_t *rank, int64_t
 template <class F>
 void parallel_slices(int64_t n, int threads, F body) {
     threads = (int)std::max<int64_t>(1, std::min<int64_t>(threads, n / 65536 + 1));
-    std::vector<std::thread> pool;
-    for (int k = 1; k < threads; k++) pool.emplace_back(body, n * k / threads, n * (k + 1) / threads);
-    body(0, n / threads);
-    for (auto &t : pool) t.join();
+    pool_slices(n, threads, body);  // persistent host workers (host_pool.h)
 }
 
 // Flat cut from the union-find state after the first `cut` merges
@@ -103,15 +101,11 @@ void cut_labels(const Node *nd, int64_t n, int64_t n_clusters, int64_t *labels, 
         // roots found per slice in parallel, concatenated (sorted below)
         const int nt = (int)std::max<int64_t>(1, std::min<int64_t>(threads, n / 65536 + 1));
         std::vector<std::vector<std::pair<int32_t, int32_t>>> part(nt);
-        std::vector<std::thread> pool;
-        auto scan = [&](int k) {
+        HostPool::get().run(nt, [&](int k) {
             const int64_t lo = n * k / nt, hi = n * (k + 1) / nt;
             for (int64_t v = lo; v < hi; v++)
                 if (nd[v].parent == (int32_t)v) part[k].emplace_back(nd[v].cid, (int32_t)v);
-        };
-        for (int k = 1; k < nt; k++) pool.emplace_back(scan, k);
-        scan(0);
-        for (auto &t : pool) t.join();
+        });
         roots.reserve(n_clusters);
         for (auto &p : part) roots.insert(roots.end(), p.begin(), p.end());
     }
@@ -182,10 +176,7 @@ void dendrogram_fold(const FoldInput &in, double *merges, int64_t n_clusters, in
             }
         };
         const int nt = (int)std::max<int64_t>(1, std::min<int64_t>(in.threads, ng));
-        std::vector<std::thread> pool;
-        for (int k = 1; k < nt; k++) pool.emplace_back(worker);
-        worker();
-        for (auto &t : pool) t.join();
+        HostPool::get().run(nt, [&](int) { worker(); });
         if (failed) throw_invalid("edges contain a cycle: not a spanning tree");
         start = in.t;
     }
