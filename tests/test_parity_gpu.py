@@ -491,3 +491,27 @@ def test_huge_float64_points_match_oracle(slk, oracle):
     e = slk.cross_color_1nn(x, colors)
     ci, cd = oracle.cross_color_1nn(x, colors.colors, rows=(0, 500))
     assert np.array_equal(e.dst[:500], ci) and np.array_equal(e.weight[:500], cd)
+
+
+@pytest.mark.parametrize("two_sorts", ["0", "1"])
+def test_single_linkage_tied_distances_match_oracle(slk, oracle, monkeypatch, two_sorts):
+    """Points on a small integer lattice (with a few duplicates removed):
+    thousands of exactly equal squared distances, so the forest solver's
+    (w_alt, a, b) order comes from long runs of equal weights.  The pipeline's
+    one-sort path must fall back (or fix up) to exactly the reference's
+    order; SLK_MSF_TWO_SORTS=1 forces the two-sort path for comparison.
+    Reference: mst.py:198-222,292-344."""
+    if two_sorts == "1":
+        monkeypatch.setenv("SLK_MSF_TWO_SORTS", "1")
+    else:
+        monkeypatch.delenv("SLK_MSF_TWO_SORTS", raising=False)
+    rng = np.random.default_rng(21)
+    pts = np.unique(rng.integers(0, 9, size=(2600, 3)), axis=0).astype(np.float32)
+    pts = pts[rng.permutation(len(pts))][:700]
+    cfg = slk.LinkageConfig(n_clusters=5, k=6, seed=3)
+    res = slk.single_linkage_result(pts, cfg)
+    ref = oracle.single_linkage(pts, 5, k=6, seed=3)
+    assert np.array_equal(res.tree.src, ref["tree_src"]) and np.array_equal(res.tree.dst, ref["tree_dst"])
+    assert np.array_equal(res.tree.weight, ref["tree_w"])
+    assert np.array_equal(res.dendrogram.merges, ref["merges"])
+    assert np.array_equal(res.labels.labels, ref["labels"])
