@@ -312,5 +312,19 @@ FoldInput dendrogram_device_sort(const int32_t *src, const int32_t *dst, const d
 void dendrogram_fold(const FoldInput &in, double *merges, int64_t n_clusters = 0, int64_t *labels = nullptr,
                      double *extract_ms = nullptr);
 void extract_labels(const double *merges, int64_t n, int64_t n_clusters, int64_t *labels);
+// The merge table built on the device (dendro.cu:krt_kernel): row i of the
+// reference's table is (rows[3i], rows[3i+1], w[i], rows[3i+2]) (children
+// a < b, height, size), and labels[n] (int32) is the flat cut when cut >= 0.
+struct DeviceMerges {
+    DevBuf<int32_t> rows;  // [n-1][3]
+    DevBuf<double> w;      // [n-1] merge heights (sqrt taken when requested)
+    DevBuf<int32_t> labels;
+};
+// Enqueued on s (the cut on `side` when given, joined back into s); the
+// returned pinned int is nonzero once s has synchronised if the edges contain
+// a cycle.
+const int *dendrogram_device(const int32_t *src, const int32_t *dst, const double *w, int64_t n,
+                             bool take_sqrt, int64_t cut, DeviceMerges &out, cudaStream_t s,
+                             cudaStream_t side = nullptr);
 
 }  // namespace slk

@@ -5,10 +5,11 @@
 // (:184-213, _inherit_labels :132-148).
 //
 // The (w, a, b) ordering of the N-1 tree edges is a device radix sort (two
-// stable passes: by canonical key, then by weight).  The merge fold is the
-// reference's sequential union-find (union by rank + path compression); like
-// the paper it runs on the host, in native code, over the
-// sorted arrays.  Its cost is O(N α(N)) and it is timed in the pipeline.
+// stable passes: by canonical key, then by weight).  The merge table is then
+// built on the device (krt_kernel, below): the reference's sequential
+// union-find fold is restated as a time-split recursion of polylog depth.
+// The host fold (fold.cu, the paper's choice: PAPER.md:355) stays as the
+// SLK_HOST_FOLD=1 alternative.
 #include <cub/cub.cuh>
 #include <cuda_runtime.h>
 #include <math.h>
@@ -16,6 +17,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cooperative_groups.h>
 #include <thread>
 #include <vector>
 
@@ -52,6 +54,39 @@ __global__ void dendro_final_kernel(const uint64_t *keys_sorted, const int32_t *
         uint64_t k = keys_sorted[perm2[e]];
         a[e] = (int32_t)(k >> 32);
         b[e] = (int32_t)(k & 0xffffffffu);
+    }
+}
+
+// After the sort by w': ks = the canonical keys in w' order with every run
+// of equal w' sorted by key (insertion sort, one thread per run); flag = 1 if
+// a run is longer than RUN_MAX (the caller re-sorts).
+constexpr int RUN_MAX = 64;
+__global__ void dendro_runs_kernel(const uint64_t *keys, const int32_t *perm, const double *ws, int64_t m,
+                                   uint64_t *ks, int *flag) {
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < m; p += (int64_t)gridDim.x * blockDim.x) {
+        if (p > 0 && ws[p] == ws[p - 1]) continue;  // not a run start
+        int64_t e = p + 1;
+        while (e < m && ws[e] == ws[p] && e - p <= RUN_MAX) e++;
+        if (e - p > RUN_MAX) {
+            atomicOr(flag, 1);
+            continue;
+        }
+        for (int64_t i = p; i < e; i++) {
+            const uint64_t v = keys[perm[i]];
+            int64_t j = i - 1;
+            while (j >= p && ks[j] > v) {
+                ks[j + 1] = ks[j];
+                j--;
+            }
+            ks[j + 1] = v;
+        }
+    }
+}
+
+__global__ void dendro_split_kernel(const uint64_t *ks, int64_t m, int32_t *a, int32_t *b) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m; e += (int64_t)gridDim.x * blockDim.x) {
+        a[e] = (int32_t)(ks[e] >> 32);
+        b[e] = (int32_t)(ks[e] & 0xffffffffu);
     }
 }
 
@@ -142,6 +177,267 @@ __global__ void fill_minus1_kernel(int32_t *v, int64_t n) {
         v[i] = -1;
 }
 
+// ---- the merge table on the device: Kruskal reconstruction tree (KRT)
+//
+// Row i of the reference's fold (linkage.py:103-129) records the cluster ids
+// of the two components that edge i joins in the forest F_{<i} of the edges
+// before it: a point alone keeps its own id, a component formed by merges
+// keeps n + (its largest merge).  Those ids are the KRT nodes of the
+// components, so row i only needs, for both endpoints, the KRT node of
+// their component in F_{<i}, and its size.
+//
+// Time-split recursion: a window [lo, hi) of merge ranks sees the components
+// of F_{<lo} as super-vertices, labelled by their KRT node ids.  Splitting it
+// at mid, the left half [lo, mid) keeps those labels; the right half needs
+// the components of F_{<mid}: the connected components of the left half's
+// edges over the super-vertices, each labelled n + (its largest edge), which
+// is exactly the KRT node the fold would give it.  After log2(m) levels every
+// window is one edge whose two labels are the row's children.  All windows of
+// one level are solved together with one union-find over node ids: a label
+// names a component of F_{<lo} for the windows that see it, and an edge of
+// any window touching it merges it away, so no label occurs in the left
+// halves of two windows of a level (nothing to separate).  The per-level
+// union-find state is tagged with its level instead of being reset: a node
+// whose entry carries an older level is a root with no largest edge and no
+// accumulated size.  Windows of KRT_LEAF edges are folded in order by one
+// warp each (labels deduplicated across the lanes, the fold itself on a
+// shared-memory union-find of at most 2 * KRT_LEAF slots).  Depth:
+// log2(m / KRT_LEAF) levels of three grid-wide phases, ONE cooperative launch.
+constexpr int KRT_LEAF_LOG = 5, KRT_LEAF = 1 << KRT_LEAF_LOG;  // = warp size: lane j folds rank i0 + j
+constexpr int KRT_THREADS = 256, KRT_WARPS = KRT_THREADS / 32;
+
+struct KrtArgs {
+    int64_t m, n;
+    int levels, top;  // levels with windows above KRT_LEAF; windows at level D hold 2^(top - D) ranks
+    const int32_t *a, *b;  // endpoints in merge order
+    const double *w;       // merge heights in merge order
+    int32_t *la, *lb;      // endpoint labels (KRT node ids) at the current level
+    int32_t *size;         // [2n-1] KRT node sizes (leaves 1; a merge node once it is a label)
+    // [2n-1] per-level state, tagged with the level in the high 32 bits:
+    // uf = (level, parent) (an older level: a root), cmax = (level, largest
+    // edge of the component), acc = (level, size of the component);
+    // seen = 2 * level + 1 once the node's size went into acc
+    unsigned long long *uf[2], *cmax, *acc;  // uf: one buffer per level parity
+    int32_t *seen;
+    int32_t *rows;   // [m][3] output: child a, child b (a < b), size; size -1 marks a cycle
+    int *cycle;
+    unsigned long long *stamps;  // SLK_TRACE: %globaltimer after each grid-wide phase (or null)
+};
+
+__device__ __forceinline__ void krt_stamp(const KrtArgs &k, int idx) {
+    if (k.stamps && blockIdx.x == 0 && threadIdx.x == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        k.stamps[idx] = t;
+    }
+}
+
+// level D is stored as D + 1, so the zero entry is "older than every level"
+// and tagged maxima compare level first
+__device__ __forceinline__ unsigned long long tag(int D, int32_t v) {
+    return ((unsigned long long)(uint32_t)(D + 1) << 32) | (uint32_t)v;
+}
+__device__ __forceinline__ int tag_level(unsigned long long t) { return (int)(t >> 32) - 1; }
+__device__ __forceinline__ int32_t tag_value(unsigned long long t) { return (int32_t)(uint32_t)t; }
+
+// root of x in the level-D forest (path halving; a stale halving write still
+// points at an ancestor); *rv = the root's entry, the CAS operand of a hook
+__device__ __forceinline__ int32_t krt_find(unsigned long long *uf, int D, int32_t x, unsigned long long *rv) {
+    unsigned long long v = uf[x];
+    while (tag_level(v) == D) {
+        const int32_t p = tag_value(v);
+        const unsigned long long vp = uf[p];
+        if (tag_level(vp) != D) {
+            x = p;
+            v = vp;
+            break;
+        }
+        uf[x] = vp;  // x -> grandparent
+        x = tag_value(vp);
+        v = uf[x];
+    }
+    *rv = v;
+    return x;
+}
+
+// the root with the SMALLER id hooks under the other: the labels of large
+// components are recent KRT nodes (large ids), so the many small labels
+// joining one of them hook under it, each CAS on its own entry
+__device__ __forceinline__ void krt_union(unsigned long long *uf, int D, int32_t u, int32_t v) {
+    while (true) {
+        unsigned long long ru, rv;
+        u = krt_find(uf, D, u, &ru);
+        v = krt_find(uf, D, v, &rv);
+        if (u == v) return;
+        if (u < v) {
+            if (atomicCAS(&uf[u], ru, tag(D, v)) == ru) return;
+        } else {
+            if (atomicCAS(&uf[v], rv, tag(D, u)) == rv) return;
+        }
+    }
+}
+
+// a left edge's share of its component: the sizes of its labels not yet
+// counted at this level, added to the component root's tagged accumulator
+__device__ __forceinline__ void krt_acc_add(unsigned long long *acc, int D, int32_t r, int32_t add) {
+    unsigned long long v = acc[r];
+    while (tag_level(v) != D) {  // first add of this level: replace the stale entry
+        const unsigned long long old = atomicCAS(&acc[r], v, tag(D, add));
+        if (old == v) return;
+        v = old;
+    }
+    atomicAdd(&acc[r], (unsigned long long)(uint32_t)add);
+}
+
+__global__ void __launch_bounds__(KRT_THREADS) krt_kernel(KrtArgs k) {
+    namespace cg = cooperative_groups;
+    cg::grid_group grid = cg::this_grid();
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int64_t nth = (int64_t)gridDim.x * blockDim.x;
+    const int64_t m = k.m, n = k.n, nodes = 2 * n - 1;
+    int32_t *la = k.la, *lb = k.lb, *size = k.size, *seen = k.seen;
+    unsigned long long *cmax = k.cmax, *acc = k.acc;
+    // every rank loop gives a warp 32 consecutive ranks
+    const int64_t tid0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    for (int64_t i = tid0; i < m; i += nth) {
+        la[i] = k.a[i];
+        lb[i] = k.b[i];
+    }
+    const unsigned long long stale = 0ull;  // level -1
+    for (int64_t v = tid0; v < nodes; v += nth) {
+        k.uf[0][v] = stale;
+        k.uf[1][v] = stale;
+        cmax[v] = stale;
+        acc[v] = stale;
+        seen[v] = -1;
+        if (v < n) size[v] = 1;
+    }
+    grid.sync();
+    krt_stamp(k, 0);
+    // (1) components of the left halves' edges, level 0 (later levels: in (3))
+    if (k.levels > 0) {
+        const int sh = k.top - 1;
+        for (int64_t i = tid0; i < m; i += nth)
+            if (!((i >> sh) & 1)) krt_union(k.uf[0], 0, la[i], lb[i]);
+    }
+    grid.sync();
+    krt_stamp(k, 1);
+    for (int D = 0; D < k.levels; D++) {
+        const int sh = k.top - D - 1;  // rank bit of the half within the window
+        const int32_t mark = 2 * D + 1;
+        unsigned long long *uf = k.uf[D & 1];
+        // (2) per component: its largest edge and its size (each label counted
+        // once), one pair of atomics per component per warp
+        for (int64_t base = tid0 - lane; base < m; base += nth) {  // warp-uniform
+            const int64_t i = base + lane;
+            const bool left = i < m && !((i >> sh) & 1);
+            int32_t r = -1, add = 0;
+            if (left) {
+                unsigned long long rv;
+                const int32_t x = la[i], y = lb[i];
+                r = krt_find(uf, D, x, &rv);
+                if (atomicExch(&seen[x], mark) != mark) add += size[x];
+                if (atomicExch(&seen[y], mark) != mark) add += size[y];
+            }
+            const unsigned grp = __match_any_sync(0xffffffffu, r);
+            const unsigned gmax = __reduce_max_sync(grp, left ? (unsigned)i : 0u);
+            const unsigned gsum = __reduce_add_sync(grp, (unsigned)add);
+            if (left && lane == __ffs(grp) - 1) {
+                atomicMax(&cmax[r], tag(D, (int32_t)gmax));
+                if (gsum) krt_acc_add(acc, D, r, (int32_t)gsum);
+            }
+        }
+        grid.sync();
+        krt_stamp(k, 2 + 2 * D);
+        // (3) new KRT nodes take their sizes; the right halves move to F_{<mid};
+        // then (1) of level D + 1 on the other union-find buffer (the same
+        // thread owns rank i in both loops, so its labels are final)
+        const bool next = D + 1 < k.levels;
+        unsigned long long *uf_next = k.uf[(D + 1) & 1];
+        for (int64_t i = tid0; i < m; i += nth) {
+            unsigned long long rv;
+            if (!((i >> sh) & 1)) {
+                const int32_t r = krt_find(uf, D, la[i], &rv);
+                if (tag_value(cmax[r]) == (int32_t)i) size[n + i] = tag_value(acc[r]);
+            } else {
+                const int32_t x = la[i], y = lb[i];
+                if (seen[x] == mark) la[i] = (int32_t)(n + tag_value(cmax[krt_find(uf, D, x, &rv)]));
+                if (seen[y] == mark) lb[i] = (int32_t)(n + tag_value(cmax[krt_find(uf, D, y, &rv)]));
+            }
+            if (next && !((i >> (sh - 1)) & 1)) krt_union(uf_next, D + 1, la[i], lb[i]);
+        }
+        grid.sync();
+        krt_stamp(k, 3 + 2 * D);
+    }
+    // leaf windows of L <= 32 ranks, one warp each: lane j holds rank i0 + j.
+    // Slots: 0..31 the x labels, 32..63 the y labels; a label's slot is its
+    // first occurrence (x half first), the fold runs on lane 0 over the
+    // slots' shared-memory union-find, and every lane writes its own row.
+    __shared__ int32_t s_val[KRT_WARPS][64], s_par[KRT_WARPS][64], s_cid[KRT_WARPS][64], s_sz[KRT_WARPS][64];
+    __shared__ int32_t s_slot[KRT_WARPS][32][2], s_res[KRT_WARPS][32][3];
+    const int64_t L = (int64_t)1 << (k.top - k.levels);
+    const int64_t nwin = (m + L - 1) / L;
+    const int64_t nwarps = (int64_t)gridDim.x * KRT_WARPS;
+    for (int64_t win = blockIdx.x * (int64_t)KRT_WARPS + wib; win < nwin; win += nwarps) {
+        const int64_t i0 = win * L;
+        const int cnt = (int)(m - i0 < L ? m - i0 : L);
+        const bool valid = lane < cnt;
+        const int64_t i = i0 + lane;
+        const int32_t x = valid ? la[i] : -1 - lane, y = valid ? lb[i] : -33 - lane;  // dummies never match
+        s_val[wib][lane] = x;
+        s_val[wib][32 + lane] = y;
+        const unsigned mx = __match_any_sync(0xffffffffu, x), my = __match_any_sync(0xffffffffu, y);
+        __syncwarp();
+        int sy = -1;
+        for (int q = 0; q < 32 && sy < 0; q++)
+            if (s_val[wib][q] == y) sy = q;
+        const int sx = __ffs(mx) - 1;
+        if (sy < 0) sy = 32 + __ffs(my) - 1;
+        s_slot[wib][lane][0] = sx;
+        s_slot[wib][lane][1] = sy;
+        s_par[wib][lane] = lane;
+        s_par[wib][32 + lane] = 32 + lane;
+        s_cid[wib][lane] = x;
+        s_cid[wib][32 + lane] = y;
+        s_sz[wib][lane] = valid ? size[x] : 0;
+        s_sz[wib][32 + lane] = valid ? size[y] : 0;
+        __syncwarp();
+        if (lane == 0) {
+            int32_t *par = s_par[wib], *cid = s_cid[wib], *sz = s_sz[wib];
+            for (int j = 0; j < cnt; j++) {
+                int rx = s_slot[wib][j][0], ry = s_slot[wib][j][1];
+                while (par[rx] != rx) rx = par[rx];
+                while (par[ry] != ry) ry = par[ry];
+                if (rx == ry) {
+                    s_res[wib][j][2] = -1;
+                    continue;
+                }
+                const int32_t ca = cid[rx], cb = cid[ry], tot = sz[rx] + sz[ry];
+                s_res[wib][j][0] = ca < cb ? ca : cb;
+                s_res[wib][j][1] = ca < cb ? cb : ca;
+                s_res[wib][j][2] = tot;
+                par[ry] = rx;
+                cid[rx] = (int32_t)(n + i0 + j);
+                sz[rx] = tot;
+            }
+        }
+        __syncwarp();
+        if (valid) {
+            int32_t *row = k.rows + 3 * i;
+            const int32_t tot = s_res[wib][lane][2];
+            if (tot < 0) *k.cycle = 1;
+            row[0] = s_res[wib][lane][0];
+            row[1] = s_res[wib][lane][1];
+            row[2] = tot;
+        }
+        __syncwarp();
+    }
+    if (k.stamps) {
+        grid.sync();
+        krt_stamp(k, 2 + 2 * k.levels);
+    }
+}
+
 struct FoldStaging {
     PinnedBuf<int32_t> a, b, rank, labels;
     PinnedBuf<double> w;
@@ -160,12 +456,84 @@ int fold_threads() {
 
 }  // namespace
 
-// Sorts the n-1 tree edges by (w', a, b) with w' = sqrt(w) when requested
-// (linkage.py:177, 295-297) and stages them on the host for the fold.  When
-// the tree is large, the first t = min(n-1-FOLD_TOP, cut) merges are grouped
-// by the component of the forest they form (device hook + pointer jumping,
-// stable radix sort by component root, gather), so the host folds the groups
-// in parallel (fold.cu).  cut < 0: no flat cut requested.
+namespace {
+
+struct SortedTree {
+    DevBuf<int32_t> a, b;  // canonical endpoints in merge order
+    DevBuf<double> w;      // merge heights w' in merge order
+};
+
+// The n-1 tree edges sorted by (w', a, b) with w' = sqrt(w) when requested
+// (linkage.py:177, 295-297): stable radix sort by the canonical key, then a
+// stable one by w'.
+SortedTree sort_tree(const int32_t *src, const int32_t *dst, const double *w, int64_t m, bool take_sqrt,
+                     cudaStream_t s) {
+    SortedTree T;
+    DevBuf<uint64_t> keys(m, s), ks(m, s);
+    DevBuf<double> wt(m, s);
+    DevBuf<int32_t> iota(m, s), perm(m, s);
+    T.a.alloc(m, s);
+    T.b.alloc(m, s);
+    T.w.alloc(m, s);
+    const int grid = grid_for(m, 256);
+    dendro_keys_kernel<<<grid, 256, 0, s>>>(src, dst, w, m, take_sqrt, keys, wt, iota);
+    SLK_CHECK_LAUNCH();
+    // One radix sort by w', then each run of equal w' put in (a, b) order in
+    // place (tree weights rarely tie); a run longer than RUN_MAX falls back
+    // to two stable sorts, by (a, b) and then by w'.
+    sort_pairs(wt.get(), T.w.get(), iota.get(), perm.get(), m, s);
+    DevBuf<int> flag(1, s);
+    SLK_CUDA(cudaMemsetAsync(flag.get(), 0, sizeof(int), s));
+    dendro_runs_kernel<<<grid, 256, 0, s>>>(keys, perm, T.w, m, ks, flag);
+    SLK_CHECK_LAUNCH();
+    if (read_scalar<int>(flag.get(), s)) {
+        DevBuf<double> w1(m, s);
+        DevBuf<int32_t> perm1(m, s);
+        sort_pairs(keys.get(), ks.get(), iota.get(), perm1.get(), m, s);  // by (a, b)
+        dendro_gather_kernel<<<grid, 256, 0, s>>>(ks, perm1, wt, m, w1);
+        SLK_CHECK_LAUNCH();
+        // stable by w' → (w', a, b); iota indexes the (a, b)-sorted list
+        sort_pairs(w1.get(), T.w.get(), iota.get(), perm.get(), m, s);
+        dendro_final_kernel<<<grid, 256, 0, s>>>(ks, perm, m, T.a, T.b);
+        SLK_CHECK_LAUNCH();
+        return T;
+    }
+    dendro_split_kernel<<<grid, 256, 0, s>>>(ks, m, T.a, T.b);
+    SLK_CHECK_LAUNCH();
+    return T;
+}
+
+// The flat cut on the device (linkage.py:184-213) from the merge-ordered
+// endpoints: int32 labels into lab[n].
+void device_cut(const int32_t *a, const int32_t *b, int64_t n, int64_t cut, int32_t *lab, cudaStream_t s) {
+    DevBuf<int32_t> parent(n, s), cmax(n, s), rid(n, s), flag(n + cut, s), pos(n + cut, s);
+    cc_init_kernel<<<grid_for(n, 256), 256, 0, s>>>(parent, n);
+    fill_minus1_kernel<<<grid_for(n, 256), 256, 0, s>>>(cmax, n);
+    SLK_CUDA(cudaMemsetAsync(flag.get(), 0, (n + cut) * sizeof(int32_t), s));
+    if (cut > 0) {
+        cc_hook_kernel<<<grid_for(cut, 256), 256, 0, s>>>(a, b, cut, parent);
+        cut_max_kernel<<<grid_for(cut, 256), 256, 0, s>>>(a, cut, parent, cmax);
+    }
+    cut_rid_kernel<<<grid_for(n, 256), 256, 0, s>>>(n, parent, cmax, rid, flag);
+    SLK_CHECK_LAUNCH();
+    size_t tmp = 0;
+    SLK_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, flag.get(), pos.get(), (int)(n + cut), s));
+    DevBuf<unsigned char> tb(tmp, s);
+    SLK_CUDA(cub::DeviceScan::ExclusiveSum(tb.get(), tmp, flag.get(), pos.get(), (int)(n + cut), s));
+    cut_label_kernel<<<grid_for(n, 256), 256, 0, s>>>(n, rid, pos, lab);
+    SLK_CHECK_LAUNCH();
+}
+
+thread_local PinnedBuf<int> cycle_flag;
+
+}  // namespace
+
+// Sorts the tree edges (sort_tree) and stages them on the host for the host
+// fold (fold.cu, SLK_HOST_FOLD=1).  When the tree is large, the first
+// t = min(n-1-FOLD_TOP, cut) merges are grouped by the component of the
+// forest they form (device hook + pointer jumping, stable radix sort by
+// component root, gather), so the host folds the groups in parallel.  cut < 0:
+// no flat cut requested.
 FoldInput dendrogram_device_sort(const int32_t *src, const int32_t *dst, const double *w, int64_t n,
                                  bool take_sqrt, int64_t cut, cudaStream_t s) {
     FoldInput in;
@@ -173,21 +541,10 @@ FoldInput dendrogram_device_sort(const int32_t *src, const int32_t *dst, const d
     in.threads = fold_threads();
     const int64_t m = n - 1;
     if (m <= 0) return in;
-    DevBuf<uint64_t> keys(m, s), ks(m, s);
-    DevBuf<double> wt(m, s), w1(m, s), w2(m, s);
-    DevBuf<int32_t> iota(m, s), perm1(m, s), iota2(m, s), perm2(m, s), a(m, s), b(m, s);
-    int grid = grid_for(m, 256);
-    dendro_keys_kernel<<<grid, 256, 0, s>>>(src, dst, w, m, take_sqrt, keys, wt, iota);
-    SLK_CHECK_LAUNCH();
-    sort_pairs(keys.get(), ks.get(), iota.get(), perm1.get(), m, s);  // by (a, b)
-    dendro_gather_kernel<<<grid, 256, 0, s>>>(ks, perm1, wt, m, w1);
-    SLK_CHECK_LAUNCH();
-    // stable by w' → (w', a, b); iota2 indexes the (a, b)-sorted list
-    SLK_CUDA(cudaMemcpyAsync(iota2.get(), iota.get(), m * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
-    sort_pairs(w1.get(), w2.get(), iota2.get(), perm2.get(), m, s);
-    dendro_final_kernel<<<grid, 256, 0, s>>>(ks, perm2, m, a, b);
-    SLK_CHECK_LAUNCH();
-
+    SortedTree T = sort_tree(src, dst, w, m, take_sqrt, s);
+    const int32_t *a = T.a.get(), *b = T.b.get();
+    const double *w2 = T.w.get();
+    DevBuf<int32_t> iota(m, s);
     int64_t t = std::min(m - FOLD_TOP, cut >= 0 ? cut : m);
     if (m < FOLD_MIN_PARALLEL || in.threads < 2 || t < FOLD_MIN_PARALLEL / 2) t = 0;
     int32_t *ha = staging.a.get(m), *hb = staging.b.get(m);
@@ -224,9 +581,9 @@ FoldInput dendrogram_device_sort(const int32_t *src, const int32_t *dst, const d
         in.off = staging.off.data();
         in.ngroups = ng;
     }
-    SLK_CUDA(cudaMemcpyAsync(ha + t, a.get() + t, (m - t) * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-    SLK_CUDA(cudaMemcpyAsync(hb + t, b.get() + t, (m - t) * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-    SLK_CUDA(cudaMemcpyAsync(hw + t, w2.get() + t, (m - t) * sizeof(double), cudaMemcpyDeviceToHost, s));
+    SLK_CUDA(cudaMemcpyAsync(ha + t, a + t, (m - t) * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    SLK_CUDA(cudaMemcpyAsync(hb + t, b + t, (m - t) * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    SLK_CUDA(cudaMemcpyAsync(hw + t, w2 + t, (m - t) * sizeof(double), cudaMemcpyDeviceToHost, s));
     SLK_CUDA(cudaStreamSynchronize(s));
     in.a = ha;
     in.b = hb;
@@ -235,27 +592,88 @@ FoldInput dendrogram_device_sort(const int32_t *src, const int32_t *dst, const d
     if (cut >= 0 && !getenv("SLK_HOST_CUT")) {
         // enqueued after the fold input is on the host: runs while the host
         // folds; the caller synchronises the stream before reading labels
-        DevBuf<int32_t> parent(n, s), cmax(n, s), rid(n, s), flag(n + cut, s), pos(n + cut, s), lab(n, s);
-        cc_init_kernel<<<grid_for(n, 256), 256, 0, s>>>(parent, n);
-        fill_minus1_kernel<<<grid_for(n, 256), 256, 0, s>>>(cmax, n);
-        SLK_CUDA(cudaMemsetAsync(flag.get(), 0, (n + cut) * sizeof(int32_t), s));
-        if (cut > 0) {
-            cc_hook_kernel<<<grid_for(cut, 256), 256, 0, s>>>(a, b, cut, parent);
-            cut_max_kernel<<<grid_for(cut, 256), 256, 0, s>>>(a, cut, parent, cmax);
-        }
-        cut_rid_kernel<<<grid_for(n, 256), 256, 0, s>>>(n, parent, cmax, rid, flag);
-        SLK_CHECK_LAUNCH();
-        size_t tmp = 0;
-        SLK_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, flag.get(), pos.get(), (int)(n + cut), s));
-        DevBuf<unsigned char> tb(tmp, s);
-        SLK_CUDA(cub::DeviceScan::ExclusiveSum(tb.get(), tmp, flag.get(), pos.get(), (int)(n + cut), s));
-        cut_label_kernel<<<grid_for(n, 256), 256, 0, s>>>(n, rid, pos, lab);
-        SLK_CHECK_LAUNCH();
+        DevBuf<int32_t> lab(n, s);
+        device_cut(a, b, n, cut, lab, s);
         int32_t *hl = staging.labels.get(n);
         SLK_CUDA(cudaMemcpyAsync(hl, lab.get(), n * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
         in.labels = hl;
     }
     return in;
+}
+
+// The merge table on the device (krt_kernel) and, when cut >= 0, the flat
+// cut (linkage.py:103-129, 184-213), see DeviceMerges.  Enqueued only; the
+// returned pinned flag is nonzero after the stream synchronises if the edges
+// contain a cycle (the caller raises).
+const int *dendrogram_device(const int32_t *src, const int32_t *dst, const double *w, int64_t n,
+                             bool take_sqrt, int64_t cut, DeviceMerges &out, cudaStream_t s,
+                             cudaStream_t side) {
+    int *flag = cycle_flag.get(1);
+    *flag = 0;
+    const int64_t m = n - 1;
+    if (m <= 0) return flag;
+    if (n >= (1ll << 30)) throw_invalid("n=%lld too large for the dendrogram", (long long)n);
+    EventPair ev_sort;
+    ev_sort.start(s);
+    SortedTree T = sort_tree(src, dst, w, m, take_sqrt, s);
+    out.rows.alloc(3 * m, s);
+    if (cut >= 0) out.labels.alloc(n, s);  // before the event the side stream waits on
+    const int64_t nodes = 2 * n - 1;
+    DevBuf<int32_t> la(m, s), lb(m, s), size(nodes, s), seen(nodes, s);
+    DevBuf<unsigned long long> uf0(nodes, s), uf1(nodes, s), cmax(nodes, s), acc(nodes, s);
+    DevBuf<int> dcycle(1, s);
+    SLK_CUDA(cudaMemsetAsync(dcycle.get(), 0, sizeof(int), s));
+    int top = 0;
+    while (((int64_t)1 << top) < m) top++;
+    KrtArgs ka{m, n, std::max(0, top - KRT_LEAF_LOG), top, T.a.get(), T.b.get(), T.w.get(), la.get(), lb.get(),
+               size.get(), {uf0.get(), uf1.get()}, cmax.get(), acc.get(), seen.get(), out.rows.get(), dcycle.get(),
+               nullptr};
+    static int coop_blocks = 0;
+    if (!coop_blocks) {
+        int per_sm = 0;
+        SLK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, krt_kernel, KRT_THREADS, 0));
+        coop_blocks = std::max(1, per_sm) * num_sms();
+    }
+    const bool trace = getenv("SLK_TRACE") != nullptr;
+    DevBuf<unsigned long long> stamps(trace ? 2 * ka.levels + 3 : 0, s);
+    ka.stamps = trace ? stamps.get() : nullptr;
+    EventPair ev_krt, ev_cut;
+    ev_sort.stop(s);
+    ev_krt.start(s);
+    void *kargs[] = {&ka};
+    SLK_CUDA(cudaLaunchCooperativeKernel((void *)krt_kernel, dim3(coop_blocks), dim3(KRT_THREADS), kargs, 0, s));
+    SLK_CHECK_LAUNCH();
+    ev_krt.stop(s);
+    if (cut >= 0) {
+        // the cut only needs the sorted endpoints: on the side stream, next to
+        // the table; s waits for it before the sorted arrays are freed
+        cudaStream_t cs = side ? side : s;
+        if (side) SLK_CUDA(cudaStreamWaitEvent(side, ev_sort.b, 0));  // recorded right after the sort
+        ev_cut.start(cs);
+        device_cut(T.a.get(), T.b.get(), n, cut, out.labels.get(), cs);
+        ev_cut.stop(cs);
+        if (side) SLK_CUDA(cudaStreamWaitEvent(s, ev_cut.b, 0));
+    } else {
+        ev_cut.start(s);
+        ev_cut.stop(s);
+    }
+    if (trace) {
+        std::vector<unsigned long long> h(2 * ka.levels + 3);
+        SLK_CUDA(cudaMemcpyAsync(h.data(), stamps.get(), h.size() * sizeof(unsigned long long),
+                                 cudaMemcpyDeviceToHost, s));
+        SLK_CUDA(cudaStreamSynchronize(s));
+        const double cut_ms = ev_cut.ms();
+        fprintf(stderr, "[slk] krt: sort %.3f ms; %d blocks, %d levels (leaf windows %lld): kernel %.3f ms, cut %.3f ms; "
+                        "union(0) %.1f us, per level (us, max+size / relabel+next union):", ev_sort.ms(), coop_blocks,
+                ka.levels, (long long)1 << (ka.top - ka.levels), ev_krt.ms(), cut_ms, (h[1] - h[0]) * 1e-3);
+        for (int D = 0; D < ka.levels; D++)
+            fprintf(stderr, " [%d] %.1f %.1f", D, (h[2 + 2 * D] - h[1 + 2 * D]) * 1e-3,
+                    (h[3 + 2 * D] - h[2 + 2 * D]) * 1e-3);
+        fprintf(stderr, " leaf %.1f\n", (h[2 + 2 * ka.levels] - h[1 + 2 * ka.levels]) * 1e-3);
+    }
+    SLK_CUDA(cudaMemcpyAsync(flag, dcycle.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
+    out.w = std::move(T.w);
+    return flag;
 }
 
 // linkage.py:184-213

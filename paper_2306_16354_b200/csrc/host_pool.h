@@ -33,6 +33,14 @@ class HostPool {
       public:
         explicit Batch(HostPool *p) : p_(p) {}
         Batch(Batch &&o) noexcept : p_(o.p_) { o.p_ = nullptr; }
+        Batch &operator=(Batch &&o) noexcept {
+            if (this != &o) {
+                wait();
+                p_ = o.p_;
+                o.p_ = nullptr;
+            }
+            return *this;
+        }
         Batch(const Batch &) = delete;
         ~Batch() { wait(); }
         void wait() {

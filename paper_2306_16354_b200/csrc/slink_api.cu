@@ -276,11 +276,9 @@ struct ShardSet {
 
 }  // namespace
 
-// Dendrogram + cut + spanning-tree copy-out of a device spanning tree
-// (linkage.py:295-311): device sort, parallel host fold, cut; returns the
-// dendrogram and extract milliseconds.  Shared by the single-process driver
-// and slk_finish_tree (the torchrun driver's rank 0).
-static void finish_tree(const int32_t *ts, const int32_t *td, const double *tw, int64_t n, int metric,
+// finish_tree with the host fold (SLK_HOST_FOLD=1; fold.cu): device sort,
+// parallel host fold, device cut.
+static void finish_tree_host_fold(const int32_t *ts, const int32_t *td, const double *tw, int64_t n, int metric,
                         int64_t n_clusters, double *h_merges, int64_t *h_labels, int64_t *h_tree_src,
                         int64_t *h_tree_dst, double *h_tree_w, double *dendro_ms, double *extract_ms_out,
                         cudaStream_t s) {
@@ -352,6 +350,164 @@ static void finish_tree(const int32_t *ts, const int32_t *td, const double *tw, 
     if (extract_ms_out) *extract_ms_out = extract_ms;
 }
 
+// Faults in the pages of the caller's output arrays (one write per 4 KB page,
+// pool threads) while the device works: they are usually fresh allocations,
+// and first touches inside the copy-out made it jitter between steps.
+static HostPool::Batch prefault_outputs(int64_t n, double *h_merges, int64_t *h_labels, int64_t *h_tree_src,
+                                        int64_t *h_tree_dst, double *h_tree_w) {
+    const int pf_parts = (int)std::min<int64_t>(16, std::max<int64_t>(1, n / 65536));
+    auto touch = [](void *base, size_t bytes, int k, int nt) {
+        char *c = static_cast<char *>(base);
+        const size_t pages = (bytes + 4095) / 4096, lo = pages * k / nt, hi = pages * (k + 1) / nt;
+        for (size_t pg = lo; pg < hi; pg++) c[pg * 4096] = 0;
+    };
+    return HostPool::get().submit(pf_parts, [=](int k) {
+        if (h_merges) touch(h_merges, (size_t)(n - 1) * 4 * sizeof(double), k, pf_parts);
+        if (h_labels) touch(h_labels, (size_t)n * sizeof(int64_t), k, pf_parts);
+        if (h_tree_src) touch(h_tree_src, (size_t)(n - 1) * sizeof(int64_t), k, pf_parts);
+        if (h_tree_dst) touch(h_tree_dst, (size_t)(n - 1) * sizeof(int64_t), k, pf_parts);
+        if (h_tree_w) touch(h_tree_w, (size_t)(n - 1) * sizeof(double), k, pf_parts);
+    });
+}
+
+static int copy_threads(int64_t count) {
+    const unsigned hc = std::max(1u, std::thread::hardware_concurrency());
+    return (int)std::max<int64_t>(1, std::min<int64_t>({(int64_t)std::min(16u, hc), count / 65536 + 1}));
+}
+
+// Enqueues the copies of a device merge table to pinned staging in chunks
+// (an event after each); merges_expand then widens each chunk into the
+// caller's float64 rows as soon as it lands, overlapping the next chunk's copy.
+struct MergeCopies {
+    static constexpr int MAX_CHUNKS = 4;
+    int64_t m = 0;
+    int chunks = 0;
+    cudaEvent_t ev[MAX_CHUNKS] = {};
+    int32_t *rows = nullptr;
+    double *w = nullptr;
+    ~MergeCopies() {
+        for (int k = 0; k < chunks; k++) cudaEventDestroy(ev[k]);
+    }
+};
+
+static void merges_enqueue(const DeviceMerges &dm, int64_t m, MergeCopies &mc, cudaStream_t s) {
+    static thread_local PinnedBuf<int32_t> st_rows;
+    static thread_local PinnedBuf<double> st_w;
+    mc.m = m;
+    mc.rows = st_rows.get(3 * m);
+    mc.w = st_w.get(m);
+    mc.chunks = m >= (1 << 18) ? MergeCopies::MAX_CHUNKS : 1;
+    for (int k = 0; k < mc.chunks; k++) {
+        const int64_t lo = m * k / mc.chunks, hi = m * (k + 1) / mc.chunks;
+        SLK_CUDA(cudaEventCreateWithFlags(&mc.ev[k], cudaEventDisableTiming));
+        SLK_CUDA(cudaMemcpyAsync(mc.rows + 3 * lo, dm.rows.get() + 3 * lo, (hi - lo) * 3 * sizeof(int32_t),
+                                 cudaMemcpyDeviceToHost, s));
+        SLK_CUDA(cudaMemcpyAsync(mc.w + lo, dm.w.get() + lo, (hi - lo) * sizeof(double), cudaMemcpyDeviceToHost,
+                                 s));
+        SLK_CUDA(cudaEventRecord(mc.ev[k], s));
+    }
+}
+
+static void merges_expand(const MergeCopies &mc, double *h_merges) {
+    const int32_t *hr = mc.rows;
+    const double *hw = mc.w;
+    for (int k = 0; k < mc.chunks; k++) {
+        const int64_t lo = mc.m * k / mc.chunks, hi = mc.m * (k + 1) / mc.chunks;
+        SLK_CUDA(cudaEventSynchronize(mc.ev[k]));
+        if (!h_merges) continue;
+        pool_slices(hi - lo, copy_threads(hi - lo), [&](int64_t a, int64_t b) {
+            for (int64_t i = lo + a; i < lo + b; i++) {
+                double *row = h_merges + 4 * i;
+                row[0] = (double)hr[3 * i];
+                row[1] = (double)hr[3 * i + 1];
+                row[2] = hw[i];
+                row[3] = (double)hr[3 * i + 2];
+            }
+        });
+    }
+}
+
+// Dendrogram + cut + spanning-tree copy-out of a device spanning tree
+// (linkage.py:295-311): device sort, device merge table (dendro.cu:krt_kernel)
+// and device cut; the spanning tree is copied out on a side stream while the
+// device builds the table, the table in chunks that the host widens as they
+// land.  Returns the dendrogram and extract milliseconds.  Shared by the
+// single-process driver and slk_finish_tree (the torchrun driver's rank 0).
+static void finish_tree(const int32_t *ts, const int32_t *td, const double *tw, int64_t n, int metric,
+                        int64_t n_clusters, double *h_merges, int64_t *h_labels, int64_t *h_tree_src,
+                        int64_t *h_tree_dst, double *h_tree_w, double *dendro_ms, double *extract_ms_out,
+                        cudaStream_t s, bool prefaulted = false) {
+    if (getenv("SLK_HOST_FOLD")) {
+        finish_tree_host_fold(ts, td, tw, n, metric, n_clusters, h_merges, h_labels, h_tree_src, h_tree_dst,
+                              h_tree_w, dendro_ms, extract_ms_out, s);
+        return;
+    }
+    const double t3 = now_ms();
+    trace_mark("dendrogram start");
+    HostPool::Batch prefault(nullptr);
+    if (!prefaulted) prefault = prefault_outputs(n, h_merges, h_labels, h_tree_src, h_tree_dst, h_tree_w);
+    const int64_t m = n - 1;
+    // the spanning tree: side stream, overlapping the device work below
+    static thread_local PinnedBuf<int32_t> st_src, st_dst, st_lab;
+    static thread_local PinnedBuf<double> st_w;
+    const bool want_tree = h_tree_src || h_tree_dst || h_tree_w;
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_ready = nullptr, ev_tree = nullptr;
+    SLK_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+    if (want_tree) {
+        SLK_CUDA(cudaEventCreateWithFlags(&ev_ready, cudaEventDisableTiming));
+        SLK_CUDA(cudaEventCreateWithFlags(&ev_tree, cudaEventDisableTiming));
+        SLK_CUDA(cudaEventRecord(ev_ready, s));
+        SLK_CUDA(cudaStreamWaitEvent(side, ev_ready, 0));
+        SLK_CUDA(cudaMemcpyAsync(st_src.get(m), ts, m * sizeof(int32_t), cudaMemcpyDeviceToHost, side));
+        SLK_CUDA(cudaMemcpyAsync(st_dst.get(m), td, m * sizeof(int32_t), cudaMemcpyDeviceToHost, side));
+        SLK_CUDA(cudaMemcpyAsync(st_w.get(m), tw, m * sizeof(double), cudaMemcpyDeviceToHost, side));
+        SLK_CUDA(cudaEventRecord(ev_tree, side));
+    }
+    DeviceMerges dm;
+    // (the cut stays on s: next to the cooperative table kernel it only slowed both)
+    const int *cycle = dendrogram_device(ts, td, tw, n, metric == 0, (n - 1) - (n_clusters - 1), dm, s);
+    MergeCopies mc;
+    merges_enqueue(dm, m, mc, s);
+    int32_t *hl = h_labels ? st_lab.get(n) : nullptr;
+    if (hl) SLK_CUDA(cudaMemcpyAsync(hl, dm.labels.get(), n * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    prefault.wait();
+    double t_tree = 0.0;
+    if (want_tree) {
+        SLK_CUDA(cudaEventSynchronize(ev_tree));
+        const double tt = now_ms();
+        const int32_t *hs = st_src.p, *hd = st_dst.p;
+        const double *hw = st_w.p;
+        pool_slices(m, copy_threads(m), [&](int64_t lo, int64_t hi) {
+            for (int64_t i = lo; i < hi; i++) {
+                if (h_tree_src) h_tree_src[i] = hs[i];
+                if (h_tree_dst) h_tree_dst[i] = hd[i];
+            }
+            if (h_tree_w) memcpy(h_tree_w + lo, hw + lo, (hi - lo) * sizeof(double));
+        });
+        t_tree = now_ms() - tt;
+        SLK_CUDA(cudaEventDestroy(ev_ready));
+        SLK_CUDA(cudaEventDestroy(ev_tree));
+    }
+    const double t4 = now_ms();
+    merges_expand(mc, h_merges);
+    SLK_CUDA(cudaStreamSynchronize(s));
+    SLK_CUDA(cudaStreamDestroy(side));  // its work is joined into s
+    if (*cycle) throw_invalid("edges contain a cycle: not a spanning tree");
+    const double t5 = now_ms();
+    if (hl)
+        pool_slices(n, copy_threads(n), [&](int64_t lo, int64_t hi) {
+            for (int64_t i = lo; i < hi; i++) h_labels[i] = hl[i];
+        });
+    const double t6 = now_ms();
+    trace_mark("dendrogram copied out");
+    if (getenv("SLK_TRACE"))
+        fprintf(stderr, "[slk] dendrogram: tree copy-out %.2f ms (overlapped), merges landed+widened %.2f ms after, "
+                        "labels %.2f ms; total %.2f ms\n", t_tree, t5 - t4, t6 - t5, t6 - t3);
+    if (dendro_ms) *dendro_ms = t5 - t3;
+    if (extract_ms_out) *extract_ms_out = t6 - t5;
+}
+
 // Pipeline state on one device (used by slk_single_linkage); n_gpus > 1
 // shards the two neighbour searches (ShardSet above).
 void single_linkage_device(const float *x32, const double *x64, int64_t n, int d, int k,
@@ -368,6 +524,9 @@ void single_linkage_device(const float *x32, const double *x64, int64_t n, int d
         reserve_pool((size_t)(2.0 * est), s);
     }
     double t0 = now_ms();
+    // the caller's output arrays are fresh allocations: fault their pages in
+    // on the host pool while the device computes (off the critical path)
+    HostPool::Batch prefault = prefault_outputs(n, h_merges, h_labels, h_tree_src, h_tree_dst, h_tree_w);
     // --- k-NN graph (linkage.py:287)
     std::unique_ptr<ShardSet> shards;
     std::shared_ptr<PointSet> P;
@@ -484,8 +643,9 @@ void single_linkage_device(const float *x32, const double *x64, int64_t n, int d
     SLK_CUDA(cudaStreamSynchronize(s));
     double t3 = now_ms();
     double dendro_ms = 0.0, extract_ms = 0.0;
+    prefault.wait();
     finish_tree(ts, td, tw, n, metric, n_clusters, h_merges, h_labels, h_tree_src, h_tree_dst, h_tree_w,
-                &dendro_ms, &extract_ms, s);
+                &dendro_ms, &extract_ms, s, true);
     const double t4 = t3 + dendro_ms, t5 = t4 + extract_ms;
     if (n_iters) *n_iters = iters;
     if (timings) {
@@ -720,8 +880,18 @@ int slk_build_dendrogram(const int32_t *d_src, const int32_t *d_dst, const doubl
     STREAM(s);
     return guarded([&] {
         if (n < 2) throw_invalid("dendrogram needs at least 2 points");
-        const FoldInput in = dendrogram_device_sort(d_src, d_dst, d_w, n, false, -1, s);
-        dendrogram_fold(in, h_merges);
+        if (getenv("SLK_HOST_FOLD")) {
+            const FoldInput in = dendrogram_device_sort(d_src, d_dst, d_w, n, false, -1, s);
+            dendrogram_fold(in, h_merges);
+            return;
+        }
+        DeviceMerges dm;
+        const int *cycle = dendrogram_device(d_src, d_dst, d_w, n, false, -1, dm, s);
+        MergeCopies mc;
+        merges_enqueue(dm, n - 1, mc, s);
+        merges_expand(mc, h_merges);
+        SLK_CUDA(cudaStreamSynchronize(s));
+        if (*cycle) throw_invalid("edges contain a cycle: not a spanning tree");
     });
 }
 

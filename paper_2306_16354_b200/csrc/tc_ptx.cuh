@@ -11,6 +11,11 @@
 #ifdef SLK_TIMELINE
 constexpr int TL_CTAS = 16, TL_EV = 16, TL_IT = 512;
 __device__ unsigned long long *g_tl;  // one per translation unit
+// epilogue counters of the same build: [0] 32-column chunks read per warp,
+// [1] chunks with a passing column, [2] insertion-loop iterations per warp
+// (divergent: max over lanes), [3] candidates examined per thread, [4] inserted
+__device__ unsigned long long g_cnt[8];
+#define TLC(i, v) atomicAdd(&g_cnt[i], (unsigned long long)(v))
 #define TL(ev, it)                                                                                  \
     do {                                                                                            \
         if (g_tl && blockIdx.x < TL_CTAS && (it) < TL_IT)                                           \
@@ -19,6 +24,9 @@ __device__ unsigned long long *g_tl;  // one per translation unit
 #else
 #define TL(ev, it) \
     do {           \
+    } while (0)
+#define TLC(i, v) \
+    do {          \
     } while (0)
 #endif
 
@@ -211,6 +219,8 @@ static void tl_arm(cudaStream_t s) {
     const size_t bytes = sizeof(unsigned long long) * TL_CTAS * TL_EV * TL_IT;
     if (!tl_buf) SLK_CUDA(cudaMalloc(&tl_buf, bytes));
     SLK_CUDA(cudaMemsetAsync(tl_buf, 0, bytes, s));
+    const unsigned long long zc[8] = {};
+    SLK_CUDA(cudaMemcpyToSymbolAsync(g_cnt, zc, sizeof(zc), 0, cudaMemcpyHostToDevice, s));
     SLK_CUDA(cudaMemcpyToSymbolAsync(g_tl, &tl_buf, sizeof(tl_buf), 0, cudaMemcpyHostToDevice, s));
 }
 static void tl_dump(int mode, int64_t rows, cudaStream_t s) {
@@ -222,6 +232,10 @@ static void tl_dump(int mode, int64_t rows, cudaStream_t s) {
     SLK_CUDA(cudaStreamSynchronize(s));
     unsigned long long *z = nullptr;
     SLK_CUDA(cudaMemcpyToSymbol(g_tl, &z, sizeof(z)));
+    unsigned long long c[8];
+    SLK_CUDA(cudaMemcpyFromSymbol(c, g_cnt, sizeof(c)));
+    fprintf(stderr, "[slk] epilogue counters mode %d rows %lld: chunks %llu hit %llu loop_iters %llu examined %llu inserted %llu\n",
+            mode, (long long)rows, c[0], c[1], c[2], c[3], c[4]);
     FILE *f = fopen(path, "ab");
     if (f) {
         const long long hdr[5] = {mode, rows, TL_CTAS, TL_EV, TL_IT};

@@ -565,6 +565,9 @@ __global__ void __launch_bounds__(Cfg<QB * HS>::NTHREADS, 1) tc_scan_kernel(TcAr
             li[p] = -1;
         }
         float thr = row_ok ? INFINITY : -INFINITY;
+#ifdef SLK_TIMELINE
+        unsigned long long n_chunk = 0, n_hit = 0, n_iter = 0, n_exam = 0, n_ins = 0;
+#endif
 
         for (int it = 0;; it++) {
             const int ts = it % NT;
@@ -619,6 +622,9 @@ __global__ void __launch_bounds__(Cfg<QB * HS>::NTHREADS, 1) tc_scan_kernel(TcAr
 #pragma unroll
                     for (int i = 0; i < w; i++) mx[i] = AUG ? fmaxf(mx[i], mx[i + w]) : fminf(mx[i], mx[i + w]);
                 const bool hit = AUG ? mx[0] > -0.5f * thr : mx[0] < thr;
+#ifdef SLK_TIMELINE
+                n_chunk++;
+#endif
                 if (!__any_sync(FULL, hit)) continue;  // warp-uniform: nothing to insert
                 uint32_t pass = 0;
                 if (hit) {
@@ -655,11 +661,19 @@ __global__ void __launch_bounds__(Cfg<QB * HS>::NTHREADS, 1) tc_scan_kernel(TcAr
                         }
                     }
                 }
+#ifdef SLK_TIMELINE
+                n_hit++;
+                n_iter += __reduce_max_sync(FULL, (unsigned)__popc(pass));
+                n_exam += __popc(pass);
+#endif
                 while (pass) {
                     const int i = __ffs(pass) - 1;
                     pass &= pass - 1;
                     const float v = AUG ? -2.0f * stg[i] : stg[i];
                     if (!(v < thr)) continue;  // the threshold may have dropped
+#ifdef SLK_TIMELINE
+                    n_ins++;
+#endif
                     const int id = (int)(col0 + c0 + i);
                     // shift-insert: new[p] = v < old[p-1] ? old[p-1] : (v < old[p] ? v : old[p])
                     bool c_next = v < lv[KP - 1];
@@ -686,6 +700,19 @@ __global__ void __launch_bounds__(Cfg<QB * HS>::NTHREADS, 1) tc_scan_kernel(TcAr
             for (int o = 16; o; o >>= 1) wm = fmaxf(wm, __shfl_xor_sync(FULL, wm, o));
             if (lane == 0) atomicExch(&misc->part[grp * 4 + ew], wm);
         }
+#ifdef SLK_TIMELINE
+        for (int o = 16; o; o >>= 1) {
+            n_exam += __shfl_xor_sync(FULL, n_exam, o);
+            n_ins += __shfl_xor_sync(FULL, n_ins, o);
+        }
+        if (lane == 0) {
+            TLC(0, n_chunk);
+            TLC(1, n_hit);
+            TLC(2, n_iter);
+            TLC(3, n_exam);
+            TLC(4, n_ins);
+        }
+#endif
         // write this row's candidate list (slots >= KP hold -1)
         if (gi >= a.row0 && gi < a.row1 && row_ok) {
             const int64_t slot = ((gi - a.row0) * a.nsplit + split) * HS + half;

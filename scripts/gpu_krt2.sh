@@ -1,0 +1,4 @@
+O=gpurun_out/${TAG:-krt2}
+mkdir -p $O
+SLK_TRACE=1 timeout 300 python scripts/bench_dendro.py 1000000 > $O/bench_dendro.log 2>&1
+SLK_TRACE=1 timeout 300 python bench.py --config C3 --no-cpu-baseline --steps 3 --warmup 3 > $O/bench_C3.log 2>&1

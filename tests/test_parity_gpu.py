@@ -314,22 +314,82 @@ def test_single_linkage_large_d_matches_oracle(slk, oracle):
 
 
 @pytest.mark.parametrize("n_clusters", [1, 30, 5000])
-def test_parallel_fold_matches_sequential(slk, monkeypatch, n_clusters):
-    """Large trees fold their first merges per forest component on several
-    host threads (dendro.cu grouping + fold.cu); the merge table and the cut
-    must equal the single-threaded in-order fold bit for bit."""
+def test_device_fold_matches_host_folds(slk, monkeypatch, n_clusters):
+    """The merge table is built on the device (dendro.cu:krt_kernel); the
+    host fold (SLK_HOST_FOLD=1: parallel per forest component, or one thread
+    in order) must give the same merge table and cut bit for bit."""
     from paper_2306_16354_b200.synthetic import make_blobs
 
     x = make_blobs(np.random.default_rng(3), 300_000, 8, 30).astype(np.float32)
     cfg = slk.LinkageConfig(n_clusters=n_clusters, k=5)
+    dev = slk.single_linkage_result(x, cfg)
+    monkeypatch.setenv("SLK_HOST_FOLD", "1")
     monkeypatch.setenv("SLK_FOLD_THREADS", "1")
     seq = slk.single_linkage_result(x, cfg)
     monkeypatch.setenv("SLK_FOLD_THREADS", "8")
     par = slk.single_linkage_result(x, cfg)
-    assert np.array_equal(seq.dendrogram.merges, par.dendrogram.merges)
-    assert np.array_equal(seq.labels.labels, par.labels.labels)
+    for other in (seq, par):
+        assert np.array_equal(dev.dendrogram.merges, other.dendrogram.merges)
+        assert np.array_equal(dev.labels.labels, other.labels.labels)
+    monkeypatch.delenv("SLK_HOST_FOLD")
     d = slk.build_dendrogram(par.tree, len(x))  # standalone entry (no cut), squared weights
     assert d.merges.shape == (len(x) - 1, 4)
+
+
+def _random_tree(rng, n, shape):
+    if shape == "chain":
+        src = np.arange(1, n)
+        dst = src - 1
+    elif shape == "star":
+        src = np.arange(1, n)
+        dst = np.zeros(n - 1, dtype=np.int64)
+    elif shape == "caterpillar":
+        src = np.arange(1, n)
+        dst = np.where(src % 2 == 1, np.maximum(src - 2, 0), src - 1)
+    else:  # random attachment
+        src = np.arange(1, n)
+        dst = (rng.random(n - 1) * src).astype(np.int64)
+    perm = rng.permutation(n)  # random vertex ids
+    return perm[src], perm[dst]
+
+
+@pytest.mark.parametrize("n", [2, 3, 33, 34, 65, 1025, 4097, 200_001])
+@pytest.mark.parametrize("shape", ["chain", "star", "caterpillar", "random"])
+def test_dendrogram_shapes_match_oracle(slk, oracle, n, shape):
+    """Device merge table vs the oracle's in-order fold on trees whose
+    dendrograms are as deep (chain, caterpillar) or as flat (star) as they
+    get, at sizes around the leaf windows (32) and not powers of two, with
+    many tied heights (ties resolve by the canonical (a, b) key)."""
+    rng = np.random.default_rng(n + len(shape))
+    src, dst = _random_tree(rng, n, shape)
+    w = rng.integers(0, max(2, n // 8), size=n - 1).astype(np.float64) + 0.5
+    d = slk.build_dendrogram(slk.EdgeList(n, src, dst, w), n)
+    assert np.array_equal(d.merges, oracle.build_dendrogram(src, dst, w, n))
+
+
+@pytest.mark.parametrize("levels", [1, 3, 50])
+def test_dendrogram_long_ties_match_oracle(slk, oracle, levels):
+    """Heights with runs of equal values far longer than the sort's in-place
+    run fix-up handles (dendro.cu:RUN_MAX): the (a, b) order inside a run
+    comes from the two-sort fallback and must still match the reference."""
+    rng = np.random.default_rng(levels)
+    n = 5000
+    src, dst = _random_tree(rng, n, "random")
+    w = rng.integers(0, levels, size=n - 1).astype(np.float64) + 1.0
+    d = slk.build_dendrogram(slk.EdgeList(n, src, dst, w), n)
+    assert np.array_equal(d.merges, oracle.build_dendrogram(src, dst, w, n))
+
+
+def test_dendrogram_cycle_large(slk):
+    """A cycle in a large edge list raises the reference's error."""
+    n = 100_000
+    src = np.arange(1, n)
+    dst = src - 1
+    dst[-1] = 5  # edge (n-1, 5) closes nothing...
+    src[-2], dst[-2] = 7, 3  # ...(7, 3) closes the cycle 3-4-5-6-7 and leaves n-2 disconnected
+    w = np.arange(n - 1, dtype=np.float64) + 1.0
+    with pytest.raises(slk.ValidationError, match="cycle"):
+        slk.build_dendrogram(slk.EdgeList(n, src, dst, w), n)
 
 
 def _ref_is_symmetric(g):
