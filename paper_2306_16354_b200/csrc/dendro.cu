@@ -101,10 +101,13 @@ void sort_pairs(const K *kin, K *kout, const V *vin, V *vout, int64_t m, cudaStr
 }
 
 // ---- components of the forest of the first t merges (hook + pointer jumping)
+// Union-find entries that other SMs update during the same launch are read
+// with ld.global.cg (L2, never a stale L1 line): the hook loops retry until
+// a CAS sees the current root, so a stale cached read could spin.
 __device__ __forceinline__ int32_t cc_find(int32_t *parent, int32_t x) {
-    int32_t p = parent[x];
+    int32_t p = __ldcg(parent + x);
     while (p != x) {
-        const int32_t g = parent[p];
+        const int32_t g = __ldcg(parent + p);
         if (g != p) parent[x] = g;  // halving; a stale write still points at an ancestor
         x = p;
         p = g;
@@ -243,10 +246,10 @@ __device__ __forceinline__ int32_t tag_value(unsigned long long t) { return (int
 // root of x in the level-D forest (path halving; a stale halving write still
 // points at an ancestor); *rv = the root's entry, the CAS operand of a hook
 __device__ __forceinline__ int32_t krt_find(unsigned long long *uf, int D, int32_t x, unsigned long long *rv) {
-    unsigned long long v = uf[x];
+    unsigned long long v = __ldcg(uf + x);  // L2: see cc_find
     while (tag_level(v) == D) {
         const int32_t p = tag_value(v);
-        const unsigned long long vp = uf[p];
+        const unsigned long long vp = __ldcg(uf + p);
         if (tag_level(vp) != D) {
             x = p;
             v = vp;
@@ -254,7 +257,7 @@ __device__ __forceinline__ int32_t krt_find(unsigned long long *uf, int D, int32
         }
         uf[x] = vp;  // x -> grandparent
         x = tag_value(vp);
-        v = uf[x];
+        v = __ldcg(uf + x);
     }
     *rv = v;
     return x;
@@ -280,7 +283,7 @@ __device__ __forceinline__ void krt_union(unsigned long long *uf, int D, int32_t
 // a left edge's share of its component: the sizes of its labels not yet
 // counted at this level, added to the component root's tagged accumulator
 __device__ __forceinline__ void krt_acc_add(unsigned long long *acc, int D, int32_t r, int32_t add) {
-    unsigned long long v = acc[r];
+    unsigned long long v = __ldcg(acc + r);
     while (tag_level(v) != D) {  // first add of this level: replace the stale entry
         const unsigned long long old = atomicCAS(&acc[r], v, tag(D, add));
         if (old == v) return;

@@ -562,6 +562,91 @@ __global__ void __launch_bounds__(256) pair_lb_kernel(const float *__restrict__ 
     }
 }
 
+// The same bounds written straight into the flat visit order (no nqb x nxb
+// intermediate, no gather): the CTA's 32 index blocks are superblock
+// blockIdx.x, whose position in query block ql's order is rank[ql][sb].
+// Register tiles of 4 query blocks x 2 index blocks per thread (two shared-
+// memory loads per 8 pairs per dimension instead of nine); every pair's sum
+// runs over the dimensions in the same order as pair_lb_kernel, so the bounds
+// are the same floats.  Padding blocks past nxb get +inf.
+__global__ void __launch_bounds__(256) pair_flat_lb_kernel(
+    const float *__restrict__ qc, const float *__restrict__ qr, int64_t nqb_total, const float *__restrict__ xc,
+    const float *__restrict__ xr, int64_t nxb, int d, int64_t qb0, int64_t nqb, const int2 *__restrict__ qcol,
+    const int2 *__restrict__ xcol, const int32_t *__restrict__ rank, int64_t nsb, float *__restrict__ flat) {
+    __shared__ __align__(16) float sq[32][64];
+    __shared__ __align__(16) float sx[32][32];
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;  // blocks 2tx, 2tx+1; queries 4ty .. 4ty+3
+    const int64_t sb = blockIdx.x;
+    const int64_t ql0 = (int64_t)blockIdx.y * 64;
+    float acc[4][2] = {{0.0f, 0.0f}, {0.0f, 0.0f}, {0.0f, 0.0f}, {0.0f, 0.0f}};
+    for (int t0 = 0; t0 < d; t0 += 32) {
+        const int tn = min(32, d - t0);
+        __syncthreads();
+        for (int e = threadIdx.x; e < tn * 64; e += 256) {
+            const int t = e >> 6, j = e & 63;
+            const int64_t qg = qb0 + ql0 + j;
+            sq[t][j] = ql0 + j < nqb ? qc[(int64_t)(t0 + t) * nqb_total + qg] : 0.0f;
+        }
+        for (int e = threadIdx.x; e < tn * 32; e += 256) {
+            const int t = e >> 5, j = e & 31;
+            const int64_t xg = sb * 32 + j;
+            sx[t][j] = xg < nxb ? xc[(int64_t)(t0 + t) * nxb + xg] : 0.0f;
+        }
+        __syncthreads();
+        for (int t = 0; t < tn; t++) {
+            const float4 q4 = *reinterpret_cast<const float4 *>(&sq[t][4 * ty]);
+            const float2 x2 = *reinterpret_cast<const float2 *>(&sx[t][2 * tx]);
+            const float qv[4] = {q4.x, q4.y, q4.z, q4.w}, xv[2] = {x2.x, x2.y};
+#pragma unroll
+            for (int i = 0; i < 4; i++)
+#pragma unroll
+                for (int j = 0; j < 2; j++) {
+                    const float df = qv[i] - xv[j];
+                    acc[i][j] = __fmaf_rn(df, df, acc[i][j]);
+                }
+        }
+    }
+    const float shrink = 1.0f - (float)(d + 8) * 0x1p-23f;
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+        const int64_t ql = ql0 + 4 * ty + i;
+        if (ql >= nqb) continue;
+        const int64_t q = qb0 + ql;
+        float *dst = flat + ((int64_t)ql * nsb + rank[ql * nsb + sb]) * 32;
+#pragma unroll
+        for (int j = 0; j < 2; j++) {
+            const int m = 2 * tx + j;
+            const int64_t b = sb * 32 + m;
+            float v = INFINITY;
+            if (b < nxb && !same_colour(qcol, xcol, q, b)) {
+                const float g = __fsub_rd(__fsub_rd(__fsqrt_rd(__fmul_rd(acc[i][j], shrink)), qr[q]), xr[b]);
+                v = g > 0.0f ? __fmul_rd(__fmul_rd(g, g), 1.0f - 0x1p-22f) : 0.0f;
+            }
+            dst[m] = v;
+        }
+    }
+}
+
+// Per (query block, position in its order): rank of each superblock, the
+// superblock bounds in visit order, and nvalid (superblocks with a finite key
+// sort first).
+__global__ void visit_meta_kernel(const int32_t *__restrict__ sb_order, const float *__restrict__ sb_key,
+                                  const float *__restrict__ sb_lb_id, int64_t nqb, int64_t nsb,
+                                  int32_t *__restrict__ rank, float *__restrict__ sblb, int32_t *__restrict__ nvalid) {
+    const int64_t total = nqb * nsb;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t ql = e / nsb, sp = e - ql * nsb;
+        const int32_t sb = sb_order[e];
+        rank[ql * nsb + sb] = (int32_t)sp;
+        const bool fin = sb_key[e] != INFINITY;
+        sblb[e] = fin ? sb_lb_id[ql * nsb + sb] : INFINITY;
+        const bool next_inf = sp + 1 == nsb || sb_key[e + 1] == INFINITY;
+        if (fin && next_inf) nvalid[ql] = (int32_t)(sp + 1);
+        if (sp == 0 && !fin) nvalid[ql] = 0;
+    }
+}
+
 // Flat visit order: for query block ql and the s-th superblock of its sorted
 // order, the superblock's bound and the bounds of its 32 member blocks (+inf
 // past the last block, for same-coloured pairs and for superblocks with an
@@ -1298,16 +1383,26 @@ VisitOrder visit_order(const QueryGroups &G, const PointSet &X, int d, const int
     SLK_CHECK_LAUNCH();
     V.sb_order.alloc(stotal, s);
     sort_segments(key, ids, nqb, nsb, seg, skey, V.sb_order, s);
-    DevBuf<float> blk_lb(nqb * nxb, s);
-    pair_lb_kernel<<<dim3((unsigned)((nxb + 31) / 32), (unsigned)((nqb + 63) / 64)), 256, 0, s>>>(
-        G.cent, G.rad, G.ng, X.centroid, X.radius, nxb, d, qb0, nqb, qrange, xrange.get(), blk_lb);
-    SLK_CHECK_LAUNCH();
     V.flat_lb.alloc(stotal * 32, s);
     V.sb_lb.alloc(stotal, s);
     V.nvalid.alloc(nqb, s);
-    flat_lb_kernel<<<grid_for(stotal * 32, 256), 256, 0, s>>>(
-        G.cent, G.rad, G.ng, X.centroid, X.radius, nxb, d, qb0, nqb, qrange,
-        xrange.get(), V.sb_order, skey, nsb, sblb_id, blk_lb, V.flat_lb, V.sb_lb, V.nvalid);
+    if (getenv("SLK_FLAT_GATHER")) {  // the two-step version (bounds, then the reordering gather)
+        DevBuf<float> blk_lb(nqb * nxb, s);
+        pair_lb_kernel<<<dim3((unsigned)((nxb + 31) / 32), (unsigned)((nqb + 63) / 64)), 256, 0, s>>>(
+            G.cent, G.rad, G.ng, X.centroid, X.radius, nxb, d, qb0, nqb, qrange, xrange.get(), blk_lb);
+        SLK_CHECK_LAUNCH();
+        flat_lb_kernel<<<grid_for(stotal * 32, 256), 256, 0, s>>>(
+            G.cent, G.rad, G.ng, X.centroid, X.radius, nxb, d, qb0, nqb, qrange,
+            xrange.get(), V.sb_order, skey, nsb, sblb_id, blk_lb, V.flat_lb, V.sb_lb, V.nvalid);
+        SLK_CHECK_LAUNCH();
+        return V;
+    }
+    DevBuf<int32_t> rank(stotal, s);
+    visit_meta_kernel<<<grid_for(stotal, 256), 256, 0, s>>>(V.sb_order, skey, sblb_id, nqb, nsb, rank, V.sb_lb,
+                                                           V.nvalid);
+    SLK_CHECK_LAUNCH();
+    pair_flat_lb_kernel<<<dim3((unsigned)nsb, (unsigned)((nqb + 63) / 64)), 256, 0, s>>>(
+        G.cent, G.rad, G.ng, X.centroid, X.radius, nxb, d, qb0, nqb, qrange, xrange.get(), rank, nsb, V.flat_lb);
     SLK_CHECK_LAUNCH();
     return V;
 }
@@ -1920,21 +2015,32 @@ __global__ void __launch_bounds__(BM) two_means_kernel(const float *__restrict__
 // radius is comparable to the extent of the whole set (one Gaussian, or
 // clusters in random order): then every tile is computed and the scan is
 // paced by its tensor / operand side, where the block-centred kernel wins.
-__global__ void block_extent_kernel(const float *__restrict__ centroid, const float *__restrict__ radius, int64_t nb,
-                                    int d, float *out) {
-    __shared__ float cbar[512];
+// blocks_overlap statistics in three short kernels (one CTA per dimension
+// for the mean centroid, a grid over the blocks, one CTA to combine the
+// per-CTA partials in a fixed order); a single-CTA version took 0.6 ms at C3.
+__global__ void centroid_mean_kernel(const float *__restrict__ centroid, int64_t nb, float *__restrict__ cbar) {
+    __shared__ double red[256];
+    const int t = blockIdx.x, tid = threadIdx.x;
+    double acc = 0.0;
+    for (int64_t b = tid; b < nb; b += blockDim.x) acc += centroid[(int64_t)t * nb + b];
+    red[tid] = acc;
+    __syncthreads();
+    for (int w = blockDim.x / 2; w; w >>= 1) {
+        if (tid < w) red[tid] += red[tid + w];
+        __syncthreads();
+    }
+    if (tid == 0) cbar[t] = (float)(red[0] / nb);
+}
+
+__global__ void block_extent_part_kernel(const float *__restrict__ centroid, const float *__restrict__ radius,
+                                         int64_t nb, int d, const float *__restrict__ cbar,
+                                         float2 *__restrict__ part) {
     __shared__ float red[2][256];
     const int tid = threadIdx.x;
-    for (int t = tid; t < d && t < 512; t += blockDim.x) {
-        double acc = 0.0;
-        for (int64_t b = 0; b < nb; b++) acc += centroid[(int64_t)t * nb + b];
-        cbar[t] = (float)(acc / nb);
-    }
-    __syncthreads();
     float ext = 0.0f, rsum = 0.0f;
-    for (int64_t b = tid; b < nb; b += blockDim.x) {
+    for (int64_t b = blockIdx.x * (int64_t)blockDim.x + tid; b < nb; b += (int64_t)gridDim.x * blockDim.x) {
         float s2 = 0.0f;
-        for (int t = 0; t < d && t < 512; t++) {
+        for (int t = 0; t < d; t++) {
             const float df = centroid[(int64_t)t * nb + b] - cbar[t];
             s2 = fmaf(df, df, s2);
         }
@@ -1951,16 +2057,28 @@ __global__ void block_extent_kernel(const float *__restrict__ centroid, const fl
         }
         __syncthreads();
     }
-    if (tid == 0) {
-        out[0] = red[1][0] / (float)nb;  // mean block radius
-        out[1] = red[0][0];              // extent: farthest block sphere from the mean centroid
+    if (tid == 0) part[blockIdx.x] = make_float2(red[0][0], red[1][0]);
+}
+
+__global__ void block_extent_final_kernel(const float2 *__restrict__ part, int np, int64_t nb, float *out) {
+    if (threadIdx.x != 0) return;
+    float ext = 0.0f, rsum = 0.0f;
+    for (int i = 0; i < np; i++) {
+        ext = fmaxf(ext, part[i].x);
+        rsum += part[i].y;
     }
+    out[0] = rsum / (float)nb;  // mean block radius
+    out[1] = ext;               // extent: farthest block sphere from the mean centroid
 }
 
 bool blocks_overlap(const PointSet &X, cudaStream_t s) {
     if (X.nb < 64) return false;
-    DevBuf<float> out(2, s);
-    block_extent_kernel<<<1, 256, 0, s>>>(X.centroid, X.radius, X.nb, X.d, out);
+    const int np = (int)std::min<int64_t>(148, (X.nb + 255) / 256);
+    DevBuf<float> out(2, s), cbar(X.d, s);
+    DevBuf<float2> part(np, s);
+    centroid_mean_kernel<<<X.d, 256, 0, s>>>(X.centroid, X.nb, cbar);
+    block_extent_part_kernel<<<np, 256, 0, s>>>(X.centroid, X.radius, X.nb, X.d, cbar, part);
+    block_extent_final_kernel<<<1, 32, 0, s>>>(part, np, X.nb, out);
     SLK_CHECK_LAUNCH();
     float h[2];
     SLK_CUDA(cudaMemcpyAsync(h, out.get(), sizeof(h), cudaMemcpyDeviceToHost, s));
