@@ -211,7 +211,8 @@ constexpr int KRT_THREADS = 256, KRT_WARPS = KRT_THREADS / 32;
 
 struct KrtArgs {
     int64_t m, n;
-    int levels, top;  // levels with windows above KRT_LEAF; windows at level D hold 2^(top - D) ranks
+    int levels, top;  // grid-wide levels; windows at level D hold 2^(top - D) ranks
+    bool block_tail;  // the windows left after the grid levels go to krt_block_kernel
     const int32_t *a, *b;  // endpoints in merge order
     const double *w;       // merge heights in merge order
     int32_t *la, *lb;      // endpoint labels (KRT node ids) at the current level
@@ -372,6 +373,13 @@ __global__ void __launch_bounds__(KRT_THREADS) krt_kernel(KrtArgs k) {
         grid.sync();
         krt_stamp(k, 3 + 2 * D);
     }
+    if (k.block_tail) {
+        if (k.stamps) {
+            grid.sync();
+            krt_stamp(k, 2 + 2 * k.levels);
+        }
+        return;  // uniform
+    }
     // leaf windows of L <= 32 ranks, one warp each: lane j holds rank i0 + j.
     // Slots: 0..31 the x labels, 32..63 the y labels; a label's slot is its
     // first occurrence (x half first), the fold runs on lane 0 over the
@@ -438,6 +446,169 @@ __global__ void __launch_bounds__(KRT_THREADS) krt_kernel(KrtArgs k) {
     if (k.stamps) {
         grid.sync();
         krt_stamp(k, 2 + 2 * k.levels);
+    }
+}
+
+// ---- the lower levels of the recursion, one CTA per window of up to
+// KB ranks (block-local, shared memory, block barriers instead of grid-wide
+// ones).  The window's labels go into a shared-memory hash table (slot =
+// table position); per level the slots' union-find, largest edge and size
+// are reset and recomputed exactly as in krt_kernel, the new labels
+// (n + largest edge) are inserted with their sizes, and the right halves
+// move to them; windows of 32 ranks are then folded in order by lane 0 of a
+// warp on the slots (labels are unique to a 32-rank window, so the warps of
+// a CTA never touch the same slot).
+constexpr int KB_LOG = 10, KB = 1 << KB_LOG, KB_T = 4 * KB, KB_THREADS = 256, KB_PER = KB / KB_THREADS;
+constexpr size_t KB_SMEM = 5 * KB_T * sizeof(int32_t) + (KB_T / 32) * sizeof(uint32_t) + KB * 5 * sizeof(int32_t);
+
+__device__ __forceinline__ int kb_insert(int32_t *keys, int32_t *ssz, int32_t label, int32_t sz_if_new,
+                                         const int32_t *gsize) {
+    uint32_t h = ((uint32_t)label * 2654435761u) >> (32 - (KB_LOG + 2));
+    while (true) {
+        const int32_t old = atomicCAS(&keys[h], -1, label);
+        if (old == -1) {
+            ssz[h] = gsize ? gsize[label] : sz_if_new;
+            return (int)h;
+        }
+        if (old == label) return (int)h;
+        h = (h + 1) & (KB_T - 1);
+    }
+}
+
+// read-only walk (no path halving: concurrent halving writes in shared memory
+// are benign but racecheck cannot tell; hash-slot ids link at random, so the
+// trees stay shallow)
+__device__ __forceinline__ int kb_find(const int32_t *uf, int x) {
+    int p = uf[x];
+    while (p != x) {
+        x = p;
+        p = uf[x];
+    }
+    return x;
+}
+
+__global__ void __launch_bounds__(KB_THREADS) krt_block_kernel(KrtArgs k) {
+    extern __shared__ __align__(16) unsigned char kb_smem[];
+    int32_t *keys = reinterpret_cast<int32_t *>(kb_smem), *uf = keys + KB_T, *cmx = uf + KB_T, *acc = cmx + KB_T,
+            *ssz = acc + KB_T;
+    uint32_t *sbits = reinterpret_cast<uint32_t *>(ssz + KB_T);
+    int32_t(*s_slot)[2] = reinterpret_cast<int32_t(*)[2]>(sbits + KB_T / 32);
+    int32_t(*s_res)[3] = reinterpret_cast<int32_t(*)[3]>(s_slot + KB);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int wlog = k.top - k.levels;  // <= KB_LOG
+    const int64_t m = k.m, n = k.n;
+    const int64_t i0 = (int64_t)blockIdx.x << wlog;
+    const int cnt = (int)(m - i0 < ((int64_t)1 << wlog) ? m - i0 : ((int64_t)1 << wlog));
+    for (int e = tid; e < KB_T; e += KB_THREADS) keys[e] = -1;
+    __syncthreads();
+    int sx[KB_PER], sy[KB_PER];  // slots of my ranks r = j * KB_THREADS + tid
+#pragma unroll
+    for (int j = 0; j < KB_PER; j++) {
+        const int r = j * KB_THREADS + tid;
+        sx[j] = sy[j] = -1;
+        if (r < cnt) {
+            sx[j] = kb_insert(keys, ssz, k.la[i0 + r], 0, k.size);
+            sy[j] = kb_insert(keys, ssz, k.lb[i0 + r], 0, k.size);
+        }
+    }
+    for (int L = 0; L < wlog - KRT_LEAF_LOG; L++) {
+        const int sh = wlog - L - 1;
+        __syncthreads();
+        for (int e = tid; e < KB_T; e += KB_THREADS) {
+            uf[e] = e;
+            cmx[e] = -1;
+            acc[e] = 0;
+        }
+        for (int e = tid; e < KB_T / 32; e += KB_THREADS) sbits[e] = 0;
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < KB_PER; j++) {  // (1) union of the left halves' edges
+            const int r = j * KB_THREADS + tid;
+            if (r >= cnt || ((r >> sh) & 1)) continue;
+            int u = sx[j], v = sy[j];
+            while (true) {
+                u = kb_find(uf, u);
+                v = kb_find(uf, v);
+                if (u == v) break;
+                const int hi = u > v ? u : v, lo = u > v ? v : u;
+                if (atomicCAS(&uf[lo], lo, hi) == lo) break;
+            }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < KB_PER; j++) {  // (2) largest edge, sizes (each slot once)
+            const int r = j * KB_THREADS + tid;
+            if (r >= cnt || ((r >> sh) & 1)) continue;
+            const int rt = kb_find(uf, sx[j]);
+            atomicMax(&cmx[rt], r);
+            int add = 0;
+            const uint32_t bx = 1u << (sx[j] & 31), by = 1u << (sy[j] & 31);
+            if (!(atomicOr(&sbits[sx[j] >> 5], bx) & bx)) add += ssz[sx[j]];
+            if (!(atomicOr(&sbits[sy[j] >> 5], by) & by)) add += ssz[sy[j]];
+            if (add) atomicAdd(&acc[rt], add);
+        }
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < KB_PER; j++) {  // (3a) the component's new label n + (largest edge)
+            const int r = j * KB_THREADS + tid;
+            if (r >= cnt || ((r >> sh) & 1)) continue;
+            const int rt = kb_find(uf, sx[j]);
+            if (atomicAdd(&cmx[rt], 0) == r) {  // atomic read: the creator rewrites it below
+                const int h = kb_insert(keys, ssz, (int32_t)(n + i0 + r), acc[rt], nullptr);
+                atomicExch(&cmx[rt], -(h + 2));  // never equal to a rank
+            }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < KB_PER; j++) {  // (3b) right halves move to F_{<mid}
+            const int r = j * KB_THREADS + tid;
+            if (r >= cnt || !((r >> sh) & 1)) continue;
+            if (sbits[sx[j] >> 5] & (1u << (sx[j] & 31))) sx[j] = -cmx[kb_find(uf, sx[j])] - 2;
+            if (sbits[sy[j] >> 5] & (1u << (sy[j] & 31))) sy[j] = -cmx[kb_find(uf, sy[j])] - 2;
+        }
+    }
+    // fold the 32-rank windows in order: slot state = union-find, cluster id, size
+    __syncthreads();
+    for (int e = tid; e < KB_T; e += KB_THREADS) {
+        uf[e] = e;
+        acc[e] = keys[e];  // cluster id
+    }
+#pragma unroll
+    for (int j = 0; j < KB_PER; j++) {
+        const int r = j * KB_THREADS + tid;
+        s_slot[r][0] = sx[j];
+        s_slot[r][1] = sy[j];
+    }
+    __syncthreads();
+    if (lane == 0) {
+        for (int j = 0; j < KB_PER; j++) {
+            const int r0 = j * KB_THREADS + warp * 32;
+            for (int r = r0; r < r0 + 32 && r < cnt; r++) {
+                int rx = s_slot[r][0], ry = s_slot[r][1];
+                while (uf[rx] != rx) rx = uf[rx];
+                while (uf[ry] != ry) ry = uf[ry];
+                if (rx == ry) {
+                    s_res[r][2] = -1;
+                    continue;
+                }
+                const int32_t ca = acc[rx], cb = acc[ry], tot = ssz[rx] + ssz[ry];
+                s_res[r][0] = ca < cb ? ca : cb;
+                s_res[r][1] = ca < cb ? cb : ca;
+                s_res[r][2] = tot;
+                uf[ry] = rx;
+                acc[rx] = (int32_t)(n + i0 + r);
+                ssz[rx] = tot;
+            }
+        }
+    }
+    __syncthreads();
+    for (int r = tid; r < cnt; r += KB_THREADS) {
+        int32_t *row = k.rows + 3 * (i0 + r);
+        const int32_t tot = s_res[r][2];
+        if (tot < 0) *k.cycle = 1;
+        row[0] = s_res[r][0];
+        row[1] = s_res[r][1];
+        row[2] = tot;
     }
 }
 
@@ -628,7 +799,9 @@ const int *dendrogram_device(const int32_t *src, const int32_t *dst, const doubl
     SLK_CUDA(cudaMemsetAsync(dcycle.get(), 0, sizeof(int), s));
     int top = 0;
     while (((int64_t)1 << top) < m) top++;
-    KrtArgs ka{m, n, std::max(0, top - KRT_LEAF_LOG), top, T.a.get(), T.b.get(), T.w.get(), la.get(), lb.get(),
+    const bool block_tail = !getenv("SLK_KRT_GRID_ONLY");
+    KrtArgs ka{m, n, std::max(0, top - (block_tail ? KB_LOG : KRT_LEAF_LOG)), top, block_tail, T.a.get(), T.b.get(),
+               T.w.get(), la.get(), lb.get(),
                size.get(), {uf0.get(), uf1.get()}, cmax.get(), acc.get(), seen.get(), out.rows.get(), dcycle.get(),
                nullptr};
     static int coop_blocks = 0;
@@ -646,6 +819,19 @@ const int *dendrogram_device(const int32_t *src, const int32_t *dst, const doubl
     void *kargs[] = {&ka};
     SLK_CUDA(cudaLaunchCooperativeKernel((void *)krt_kernel, dim3(coop_blocks), dim3(KRT_THREADS), kargs, 0, s));
     SLK_CHECK_LAUNCH();
+    EventPair ev_blk;
+    ev_blk.start(s);
+    if (block_tail) {
+        static bool attr = false;
+        if (!attr) {
+            SLK_CUDA(cudaFuncSetAttribute(krt_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)KB_SMEM));
+            attr = true;
+        }
+        const int64_t nwin = (m + ((int64_t)1 << (top - ka.levels)) - 1) >> (top - ka.levels);
+        krt_block_kernel<<<(unsigned)nwin, KB_THREADS, KB_SMEM, s>>>(ka);
+        SLK_CHECK_LAUNCH();
+    }
+    ev_blk.stop(s);
     ev_krt.stop(s);
     if (cut >= 0) {
         // the cut only needs the sorted endpoints: on the side stream, next to
@@ -672,7 +858,8 @@ const int *dendrogram_device(const int32_t *src, const int32_t *dst, const doubl
         for (int D = 0; D < ka.levels; D++)
             fprintf(stderr, " [%d] %.1f %.1f", D, (h[2 + 2 * D] - h[1 + 2 * D]) * 1e-3,
                     (h[3 + 2 * D] - h[2 + 2 * D]) * 1e-3);
-        fprintf(stderr, " leaf %.1f\n", (h[2 + 2 * ka.levels] - h[1 + 2 * ka.levels]) * 1e-3);
+        fprintf(stderr, " leaf %.1f; block-local tail %.3f ms\n", (h[2 + 2 * ka.levels] - h[1 + 2 * ka.levels]) * 1e-3,
+                block_tail ? ev_blk.ms() : 0.0);
     }
     SLK_CUDA(cudaMemcpyAsync(flag, dcycle.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
     out.w = std::move(T.w);
