@@ -320,11 +320,9 @@ struct DeviceMerges {
     DevBuf<double> w;      // [n-1] merge heights (sqrt taken when requested)
     DevBuf<int32_t> labels;
 };
-// Enqueued on s (the cut on `side` when given, joined back into s); the
-// returned pinned int is nonzero once s has synchronised if the edges contain
-// a cycle.
+// Enqueued on s; the returned pinned int is nonzero once s has synchronised
+// if the edges contain a cycle.
 const int *dendrogram_device(const int32_t *src, const int32_t *dst, const double *w, int64_t n,
-                             bool take_sqrt, int64_t cut, DeviceMerges &out, cudaStream_t s,
-                             cudaStream_t side = nullptr);
+                             bool take_sqrt, int64_t cut, DeviceMerges &out, cudaStream_t s);
 
 }  // namespace slk

@@ -18,6 +18,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cooperative_groups.h>
+#include <memory>
 #include <thread>
 #include <vector>
 
@@ -780,18 +781,20 @@ FoldInput dendrogram_device_sort(const int32_t *src, const int32_t *dst, const d
 // returned pinned flag is nonzero after the stream synchronises if the edges
 // contain a cycle (the caller raises).
 const int *dendrogram_device(const int32_t *src, const int32_t *dst, const double *w, int64_t n,
-                             bool take_sqrt, int64_t cut, DeviceMerges &out, cudaStream_t s,
-                             cudaStream_t side) {
+                             bool take_sqrt, int64_t cut, DeviceMerges &out, cudaStream_t s) {
     int *flag = cycle_flag.get(1);
     *flag = 0;
     const int64_t m = n - 1;
     if (m <= 0) return flag;
     if (n >= (1ll << 30)) throw_invalid("n=%lld too large for the dendrogram", (long long)n);
-    EventPair ev_sort;
-    ev_sort.start(s);
+    // timing events only under SLK_TRACE (no per-call event churn otherwise)
+    const bool trace = getenv("SLK_TRACE") != nullptr;
+    std::unique_ptr<EventPair> ev_sort(trace ? new EventPair : nullptr), ev_krt(trace ? new EventPair : nullptr),
+        ev_cut(trace ? new EventPair : nullptr), ev_blk(trace ? new EventPair : nullptr);
+    if (trace) ev_sort->start(s);
     SortedTree T = sort_tree(src, dst, w, m, take_sqrt, s);
     out.rows.alloc(3 * m, s);
-    if (cut >= 0) out.labels.alloc(n, s);  // before the event the side stream waits on
+    if (cut >= 0) out.labels.alloc(n, s);
     const int64_t nodes = 2 * n - 1;
     DevBuf<int32_t> la(m, s), lb(m, s), size(nodes, s), seen(nodes, s);
     DevBuf<unsigned long long> uf0(nodes, s), uf1(nodes, s), cmax(nodes, s), acc(nodes, s);
@@ -810,17 +813,16 @@ const int *dendrogram_device(const int32_t *src, const int32_t *dst, const doubl
         SLK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, krt_kernel, KRT_THREADS, 0));
         coop_blocks = std::max(1, per_sm) * num_sms();
     }
-    const bool trace = getenv("SLK_TRACE") != nullptr;
     DevBuf<unsigned long long> stamps(trace ? 2 * ka.levels + 3 : 0, s);
     ka.stamps = trace ? stamps.get() : nullptr;
-    EventPair ev_krt, ev_cut;
-    ev_sort.stop(s);
-    ev_krt.start(s);
+    if (trace) {
+        ev_sort->stop(s);
+        ev_krt->start(s);
+    }
     void *kargs[] = {&ka};
     SLK_CUDA(cudaLaunchCooperativeKernel((void *)krt_kernel, dim3(coop_blocks), dim3(KRT_THREADS), kargs, 0, s));
     SLK_CHECK_LAUNCH();
-    EventPair ev_blk;
-    ev_blk.start(s);
+    if (trace) ev_blk->start(s);
     if (block_tail) {
         static bool attr = false;
         if (!attr) {
@@ -831,35 +833,27 @@ const int *dendrogram_device(const int32_t *src, const int32_t *dst, const doubl
         krt_block_kernel<<<(unsigned)nwin, KB_THREADS, KB_SMEM, s>>>(ka);
         SLK_CHECK_LAUNCH();
     }
-    ev_blk.stop(s);
-    ev_krt.stop(s);
-    if (cut >= 0) {
-        // the cut only needs the sorted endpoints: on the side stream, next to
-        // the table; s waits for it before the sorted arrays are freed
-        cudaStream_t cs = side ? side : s;
-        if (side) SLK_CUDA(cudaStreamWaitEvent(side, ev_sort.b, 0));  // recorded right after the sort
-        ev_cut.start(cs);
-        device_cut(T.a.get(), T.b.get(), n, cut, out.labels.get(), cs);
-        ev_cut.stop(cs);
-        if (side) SLK_CUDA(cudaStreamWaitEvent(s, ev_cut.b, 0));
-    } else {
-        ev_cut.start(s);
-        ev_cut.stop(s);
+    if (trace) {
+        ev_blk->stop(s);
+        ev_krt->stop(s);
     }
+    if (trace) ev_cut->start(s);
+    if (cut >= 0) device_cut(T.a.get(), T.b.get(), n, cut, out.labels.get(), s);
+    if (trace) ev_cut->stop(s);
     if (trace) {
         std::vector<unsigned long long> h(2 * ka.levels + 3);
         SLK_CUDA(cudaMemcpyAsync(h.data(), stamps.get(), h.size() * sizeof(unsigned long long),
                                  cudaMemcpyDeviceToHost, s));
         SLK_CUDA(cudaStreamSynchronize(s));
-        const double cut_ms = ev_cut.ms();
+        const double cut_ms = ev_cut->ms();
         fprintf(stderr, "[slk] krt: sort %.3f ms; %d blocks, %d levels (leaf windows %lld): kernel %.3f ms, cut %.3f ms; "
-                        "union(0) %.1f us, per level (us, max+size / relabel+next union):", ev_sort.ms(), coop_blocks,
-                ka.levels, (long long)1 << (ka.top - ka.levels), ev_krt.ms(), cut_ms, (h[1] - h[0]) * 1e-3);
+                        "union(0) %.1f us, per level (us, max+size / relabel+next union):", ev_sort->ms(), coop_blocks,
+                ka.levels, (long long)1 << (ka.top - ka.levels), ev_krt->ms(), cut_ms, (h[1] - h[0]) * 1e-3);
         for (int D = 0; D < ka.levels; D++)
             fprintf(stderr, " [%d] %.1f %.1f", D, (h[2 + 2 * D] - h[1 + 2 * D]) * 1e-3,
                     (h[3 + 2 * D] - h[2 + 2 * D]) * 1e-3);
         fprintf(stderr, " leaf %.1f; block-local tail %.3f ms\n", (h[2 + 2 * ka.levels] - h[1 + 2 * ka.levels]) * 1e-3,
-                block_tail ? ev_blk.ms() : 0.0);
+                block_tail ? ev_blk->ms() : 0.0);
     }
     SLK_CUDA(cudaMemcpyAsync(flag, dcycle.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
     out.w = std::move(T.w);

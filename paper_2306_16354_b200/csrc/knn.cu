@@ -383,11 +383,14 @@ __global__ void __launch_bounds__(128) block_sphere_kernel(const float *__restri
                                                            int64_t nb, float *__restrict__ centroid,
                                                            float *__restrict__ radius,
                                                            const int32_t *__restrict__ rowmap = nullptr) {
-    // one CTA of 128 threads per block.  Centroid: thread t sums dim t % 64 of
-    // every other row (a warp reads 32 consecutive floats of one row), float64;
-    // radius: thread j = point j, its distance to the float centroid in float64.
+    // one CTA of 128 threads per block; the block's rows are staged in shared
+    // memory 64 dimensions at a time (coalesced 16-byte loads, one pass over
+    // the points).  Centroid: thread t sums dim t of every other row (two
+    // interleaved float64 sums); radius: thread j = point j accumulates its
+    // float64 squared distance to the float centroid dimension by dimension.
+    __shared__ float xs[BN][65];
     __shared__ double part[2][64];
-    __shared__ float cent[512];
+    __shared__ float cent[64];
     __shared__ double r2w[4];
     const int64_t b = blockIdx.x;
     if (b >= nb) return;
@@ -395,28 +398,47 @@ __global__ void __launch_bounds__(128) block_sphere_kernel(const float *__restri
     const int cnt = (int)(n - b * BN < BN ? n - b * BN : BN);
     // row-major points of the block (through rowmap for a virtual re-blocked index)
     auto row = [&](int j) { return xp + (rowmap ? (int64_t)rowmap[b * BN + j] : b * BN + j) * d; };
+    const bool vec = (d & 3) == 0;
+    double acc = 0.0;
     for (int t0 = 0; t0 < d; t0 += 64) {
-        const int t = t0 + (tid & 63), par = tid >> 6;
-        double s = 0.0;
-        if (t < d)
-            for (int j = par; j < cnt; j += 2) s += (double)row(j)[t];
-        part[par][tid & 63] = s;
+        const int tn = min(64, d - t0);
         __syncthreads();
-        if (tid < 64 && t0 + tid < d) {
+        if (vec) {
+            const int per = tn / 4;
+            for (int e = tid; e < cnt * per; e += blockDim.x) {
+                const int j = e / per, v = e - j * per;
+                const float4 x4 = __ldg(reinterpret_cast<const float4 *>(row(j) + t0) + v);
+                xs[j][4 * v] = x4.x;
+                xs[j][4 * v + 1] = x4.y;
+                xs[j][4 * v + 2] = x4.z;
+                xs[j][4 * v + 3] = x4.w;
+            }
+        } else {
+            for (int e = tid; e < cnt * tn; e += blockDim.x) {
+                const int j = e / tn, v = e - j * tn;
+                xs[j][v] = row(j)[t0 + v];
+            }
+        }
+        __syncthreads();
+        {
+            const int t = tid & 63, par = tid >> 6;
+            double sum = 0.0;
+            if (t < tn)
+                for (int j = par; j < cnt; j += 2) sum += (double)xs[j][t];
+            part[par][t] = sum;
+        }
+        __syncthreads();
+        if (tid < tn) {
             const float c = (float)((part[0][tid] + part[1][tid]) / cnt);
             centroid[(int64_t)(t0 + tid) * nb + b] = c;
-            if (t0 + tid < 512) cent[t0 + tid] = c;
+            cent[tid] = c;
         }
         __syncthreads();
-    }
-    double acc = 0.0;
-    if (tid < cnt) {
-        const float *xr = row(tid);
-        for (int t = 0; t < d; t++) {
-            const double c = t < 512 ? (double)cent[t] : (double)centroid[(int64_t)t * nb + b];
-            const double df = (double)xr[t] - c;
-            acc += df * df;
-        }
+        if (tid < cnt)
+            for (int t = 0; t < tn; t++) {
+                const double df = (double)xs[tid][t] - (double)cent[t];
+                acc += df * df;
+            }
     }
     for (int o = 16; o; o >>= 1) acc = fmax(acc, __shfl_xor_sync(FULL, acc, o));
     if ((tid & 31) == 0) r2w[tid >> 5] = acc;
@@ -486,15 +508,9 @@ __global__ void group_sphere_kernel(const float *__restrict__ bc, const float *_
 // Lower bound on the squared distance between any point of query block q and
 // any point of a sphere (c, r): (|c_q - c| - r_q - r)^2 by the triangle
 // inequality, rounded down.
-__device__ __forceinline__ float sphere_lb(const float *qc, const float *qr, int64_t nqb_total,
-                                           int64_t q, const float *xc, const float *xr,
-                                           int64_t nx_total, int64_t b, int d) {
-    double s = 0.0;
-    for (int t = 0; t < d; t++) {
-        double df = (double)qc[(int64_t)t * nqb_total + q] - (double)xc[(int64_t)t * nx_total + b];
-        s += df * df;
-    }
-    double g = sqrt(s) * (1.0 - 1e-12) - (double)qr[q] - (double)xr[b];
+// s = the float64 sum of squared centre differences, in dimension order
+__device__ __forceinline__ float sphere_lb_of(double s, float rq, float rb) {
+    double g = sqrt(s) * (1.0 - 1e-12) - (double)rq - (double)rb;
     return g > 0.0 ? (float)(g * g * (1.0 - 1e-6)) : 0.0f;
 }
 
@@ -702,7 +718,7 @@ __global__ void superblock_lb_kernel(const float *__restrict__ qc, const float *
         // common_order: every query group walks the superblocks in id order,
         // so the CTAs resident together stream the same index tiles through L2
         key[e] = same ? INFINITY : (common_order ? (float)b : (float)s);
-        lb[e] = same ? INFINITY : sphere_lb(qc, qr, nqb_total, q, sc, sr, nsb, b, d);
+        lb[e] = same ? INFINITY : sphere_lb_of(s, qr[q], sr[b]);  // the same sum as sphere_lb
         ids[e] = (int32_t)b;
         if (b == 0) seg[ql] = (int32_t)(ql * nsb);
         if (e == total - 1) seg[nqb] = (int32_t)total;

@@ -382,13 +382,31 @@ struct MergeCopies {
     static constexpr int MAX_CHUNKS = 4;
     int64_t m = 0;
     int chunks = 0;
-    cudaEvent_t ev[MAX_CHUNKS] = {};
+    cudaEvent_t *ev = nullptr;
     int32_t *rows = nullptr;
     double *w = nullptr;
-    ~MergeCopies() {
-        for (int k = 0; k < chunks; k++) cudaEventDestroy(ev[k]);
-    }
 };
+
+// Per host thread and device: the side stream and the events finish_tree
+// reuses (created once: per-call creation showed up as rare multi-ms stalls).
+struct TreeCopyRes {
+    cudaStream_t side = nullptr;
+    cudaEvent_t ready = nullptr, tree = nullptr, chunk[MergeCopies::MAX_CHUNKS] = {};
+};
+static TreeCopyRes &tree_copy_res() {
+    static thread_local std::vector<TreeCopyRes> res;
+    int dev = 0;
+    SLK_CUDA(cudaGetDevice(&dev));
+    if ((int)res.size() <= dev) res.resize(dev + 1);
+    TreeCopyRes &r = res[dev];
+    if (!r.side) {
+        SLK_CUDA(cudaStreamCreateWithFlags(&r.side, cudaStreamNonBlocking));
+        SLK_CUDA(cudaEventCreateWithFlags(&r.ready, cudaEventDisableTiming));
+        SLK_CUDA(cudaEventCreateWithFlags(&r.tree, cudaEventDisableTiming));
+        for (auto &e : r.chunk) SLK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    return r;
+}
 
 static void merges_enqueue(const DeviceMerges &dm, int64_t m, MergeCopies &mc, cudaStream_t s) {
     static thread_local PinnedBuf<int32_t> st_rows;
@@ -397,9 +415,9 @@ static void merges_enqueue(const DeviceMerges &dm, int64_t m, MergeCopies &mc, c
     mc.rows = st_rows.get(3 * m);
     mc.w = st_w.get(m);
     mc.chunks = m >= (1 << 18) ? MergeCopies::MAX_CHUNKS : 1;
+    mc.ev = tree_copy_res().chunk;
     for (int k = 0; k < mc.chunks; k++) {
         const int64_t lo = m * k / mc.chunks, hi = m * (k + 1) / mc.chunks;
-        SLK_CUDA(cudaEventCreateWithFlags(&mc.ev[k], cudaEventDisableTiming));
         SLK_CUDA(cudaMemcpyAsync(mc.rows + 3 * lo, dm.rows.get() + 3 * lo, (hi - lo) * 3 * sizeof(int32_t),
                                  cudaMemcpyDeviceToHost, s));
         SLK_CUDA(cudaMemcpyAsync(mc.w + lo, dm.w.get() + lo, (hi - lo) * sizeof(double), cudaMemcpyDeviceToHost,
@@ -451,12 +469,10 @@ static void finish_tree(const int32_t *ts, const int32_t *td, const double *tw, 
     static thread_local PinnedBuf<int32_t> st_src, st_dst, st_lab;
     static thread_local PinnedBuf<double> st_w;
     const bool want_tree = h_tree_src || h_tree_dst || h_tree_w;
-    cudaStream_t side = nullptr;
-    cudaEvent_t ev_ready = nullptr, ev_tree = nullptr;
-    SLK_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+    TreeCopyRes &res = tree_copy_res();
+    cudaStream_t side = res.side;
+    cudaEvent_t ev_ready = res.ready, ev_tree = res.tree;
     if (want_tree) {
-        SLK_CUDA(cudaEventCreateWithFlags(&ev_ready, cudaEventDisableTiming));
-        SLK_CUDA(cudaEventCreateWithFlags(&ev_tree, cudaEventDisableTiming));
         SLK_CUDA(cudaEventRecord(ev_ready, s));
         SLK_CUDA(cudaStreamWaitEvent(side, ev_ready, 0));
         SLK_CUDA(cudaMemcpyAsync(st_src.get(m), ts, m * sizeof(int32_t), cudaMemcpyDeviceToHost, side));
@@ -486,13 +502,10 @@ static void finish_tree(const int32_t *ts, const int32_t *td, const double *tw, 
             if (h_tree_w) memcpy(h_tree_w + lo, hw + lo, (hi - lo) * sizeof(double));
         });
         t_tree = now_ms() - tt;
-        SLK_CUDA(cudaEventDestroy(ev_ready));
-        SLK_CUDA(cudaEventDestroy(ev_tree));
     }
     const double t4 = now_ms();
     merges_expand(mc, h_merges);
     SLK_CUDA(cudaStreamSynchronize(s));
-    SLK_CUDA(cudaStreamDestroy(side));  // its work is joined into s
     if (*cycle) throw_invalid("edges contain a cycle: not a spanning tree");
     const double t5 = now_ms();
     if (hl)
