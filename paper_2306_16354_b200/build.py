@@ -28,7 +28,7 @@ FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxe
 # Diagnostic variants (never loaded unless SLK_LIB_VARIANT names one):
 # "timeline" stamps the scan's warp-role hand-offs (tc_scan.cu, SLK_TIMELINE).
 VARIANTS = {"timeline": ["-DSLK_TIMELINE"], "nomma": ["-DSLK_ABL_NOMMA"], "noconv": ["-DSLK_ABL_NOCONV"],
-            "noepi": ["-DSLK_ABL_NOEPI"]}
+            "noepi": ["-DSLK_ABL_NOEPI"], "ncg2": ["-DSLK_BC_NCG2_MIN_DK=64"]}
 
 
 def variant_path(name: str) -> Path:

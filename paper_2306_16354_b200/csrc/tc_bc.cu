@@ -232,9 +232,12 @@ __global__ void __launch_bounds__(128) bcpack_kernel(const float *__restrict__ x
 // would not fit one thread's registers (DK = 128).  The register file is
 // split over the four SM sub-partitions: 14 warps allow 128 registers per
 // thread, 18 warps 96.
+#ifndef SLK_BC_NCG2_MIN_DK
+#define SLK_BC_NCG2_MIN_DK 128
+#endif
 template <int DK, int KP>
 struct Shape {
-    static constexpr int NCG = DK >= 128 ? 2 : 1;  // convert warp groups
+    static constexpr int NCG = DK >= SLK_BC_NCG2_MIN_DK ? 2 : 1;  // convert warp groups
     static constexpr int DC = DK / NCG;           // dims per convert thread
     static constexpr int NTHREADS = (14 + 4 * (NCG - 1)) * 32;
     static constexpr int NA = DK <= 64 ? 3 : 2;   // A slots in TMEM (NT * 128 + NA * DK / 2 <= 512)
