@@ -320,9 +320,12 @@ struct DeviceMerges {
     DevBuf<double> w;      // [n-1] merge heights (sqrt taken when requested)
     DevBuf<int32_t> labels;
 };
-// Enqueued on s; the returned pinned int is nonzero once s has synchronised
-// if the edges contain a cycle.
+// Enqueued on s (the cut on cut_stream after table_done when both are
+// given: the caller reads labels after synchronising cut_stream); the
+// returned pinned int is nonzero once s has synchronised if the edges
+// contain a cycle.
 const int *dendrogram_device(const int32_t *src, const int32_t *dst, const double *w, int64_t n,
-                             bool take_sqrt, int64_t cut, DeviceMerges &out, cudaStream_t s);
+                             bool take_sqrt, int64_t cut, DeviceMerges &out, cudaStream_t s,
+                             cudaStream_t cut_stream = nullptr, cudaEvent_t table_done = nullptr);
 
 }  // namespace slk

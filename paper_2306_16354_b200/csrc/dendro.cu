@@ -781,7 +781,8 @@ FoldInput dendrogram_device_sort(const int32_t *src, const int32_t *dst, const d
 // returned pinned flag is nonzero after the stream synchronises if the edges
 // contain a cycle (the caller raises).
 const int *dendrogram_device(const int32_t *src, const int32_t *dst, const double *w, int64_t n,
-                             bool take_sqrt, int64_t cut, DeviceMerges &out, cudaStream_t s) {
+                             bool take_sqrt, int64_t cut, DeviceMerges &out, cudaStream_t s,
+                             cudaStream_t cut_stream, cudaEvent_t table_done) {
     int *flag = cycle_flag.get(1);
     *flag = 0;
     const int64_t m = n - 1;
@@ -837,9 +838,18 @@ const int *dendrogram_device(const int32_t *src, const int32_t *dst, const doubl
         ev_blk->stop(s);
         ev_krt->stop(s);
     }
-    if (trace) ev_cut->start(s);
-    if (cut >= 0) device_cut(T.a.get(), T.b.get(), n, cut, out.labels.get(), s);
-    if (trace) ev_cut->stop(s);
+    // the cut after the table (next to the cooperative kernel both slowed
+    // down); on cut_stream when given, so the table's copies on s overlap it
+    cudaStream_t cs = s;
+    if (cut >= 0 && cut_stream && table_done) {
+        SLK_CUDA(cudaEventRecord(table_done, s));
+        SLK_CUDA(cudaStreamWaitEvent(cut_stream, table_done, 0));
+        cs = cut_stream;
+        T.a.stream = T.b.stream = cut_stream;  // freed after the cut has read them
+    }
+    if (trace) ev_cut->start(cs);
+    if (cut >= 0) device_cut(T.a.get(), T.b.get(), n, cut, out.labels.get(), cs);
+    if (trace) ev_cut->stop(cs);
     if (trace) {
         std::vector<unsigned long long> h(2 * ka.levels + 3);
         SLK_CUDA(cudaMemcpyAsync(h.data(), stamps.get(), h.size() * sizeof(unsigned long long),

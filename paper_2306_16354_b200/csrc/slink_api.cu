@@ -391,7 +391,7 @@ struct MergeCopies {
 // reuses (created once: per-call creation showed up as rare multi-ms stalls).
 struct TreeCopyRes {
     cudaStream_t side = nullptr;
-    cudaEvent_t ready = nullptr, tree = nullptr, chunk[MergeCopies::MAX_CHUNKS] = {};
+    cudaEvent_t ready = nullptr, tree = nullptr, table = nullptr, chunk[MergeCopies::MAX_CHUNKS] = {};
 };
 static TreeCopyRes &tree_copy_res() {
     static thread_local std::vector<TreeCopyRes> res;
@@ -403,6 +403,7 @@ static TreeCopyRes &tree_copy_res() {
         SLK_CUDA(cudaStreamCreateWithFlags(&r.side, cudaStreamNonBlocking));
         SLK_CUDA(cudaEventCreateWithFlags(&r.ready, cudaEventDisableTiming));
         SLK_CUDA(cudaEventCreateWithFlags(&r.tree, cudaEventDisableTiming));
+        SLK_CUDA(cudaEventCreateWithFlags(&r.table, cudaEventDisableTiming));
         for (auto &e : r.chunk) SLK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     }
     return r;
@@ -481,12 +482,13 @@ static void finish_tree(const int32_t *ts, const int32_t *td, const double *tw, 
         SLK_CUDA(cudaEventRecord(ev_tree, side));
     }
     DeviceMerges dm;
-    // (the cut stays on s: next to the cooperative table kernel it only slowed both)
-    const int *cycle = dendrogram_device(ts, td, tw, n, metric == 0, (n - 1) - (n_clusters - 1), dm, s);
+    // the cut runs on the side stream after the table, next to the table's copies on s
+    const int *cycle = dendrogram_device(ts, td, tw, n, metric == 0, (n - 1) - (n_clusters - 1), dm, s, side,
+                                         res.table);
     MergeCopies mc;
     merges_enqueue(dm, m, mc, s);
     int32_t *hl = h_labels ? st_lab.get(n) : nullptr;
-    if (hl) SLK_CUDA(cudaMemcpyAsync(hl, dm.labels.get(), n * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    if (hl) SLK_CUDA(cudaMemcpyAsync(hl, dm.labels.get(), n * sizeof(int32_t), cudaMemcpyDeviceToHost, side));
     prefault.wait();
     double t_tree = 0.0;
     if (want_tree) {
@@ -506,6 +508,7 @@ static void finish_tree(const int32_t *ts, const int32_t *td, const double *tw, 
     const double t4 = now_ms();
     merges_expand(mc, h_merges);
     SLK_CUDA(cudaStreamSynchronize(s));
+    SLK_CUDA(cudaStreamSynchronize(side));  // the cut and its labels
     if (*cycle) throw_invalid("edges contain a cycle: not a spanning tree");
     const double t5 = now_ms();
     if (hl)
