@@ -1833,21 +1833,20 @@ struct Gathered {
     int64_t n = 0;
 };
 
-Gathered gather_queries(const PointSet &Q, const std::vector<int32_t> &src,
-                        const std::vector<int32_t> &qid, int mode, const int32_t *qcolor,
-                        const uint8_t *mask, int64_t nx, cudaStream_t s) {
+// Gathered copy of Q's rows dsrc[0, nout) (device ids); G.qid takes dqid
+// (moved in: the caller's buffer becomes the set's query ids).
+Gathered gather_queries_dev(const PointSet &Q, const int32_t *dsrc, DevBuf<int32_t> &&dqid, int64_t nout, int mode,
+                            const int32_t *qcolor, const uint8_t *mask, int64_t nx, cudaStream_t s) {
     Gathered G;
-    G.n = (int64_t)src.size();
+    G.n = nout;
     const int d = Q.d;
-    DevBuf<int32_t> dsrc(G.n, s);
-    G.qid.alloc(G.n, s);
-    SLK_CUDA(cudaMemcpyAsync(dsrc.get(), src.data(), G.n * sizeof(int32_t), cudaMemcpyHostToDevice, s));
-    SLK_CUDA(cudaMemcpyAsync(G.qid.get(), qid.data(), G.n * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+    G.qid = std::move(dqid);
     G.x32.alloc(G.n * d, s);
     if (Q.x64) G.x64.alloc(G.n * d, s);
     gather_rows_kernel<<<grid_for(G.n * d, 256), 256, 0, s>>>(Q.x32, Q.x64, dsrc, G.n, d, G.x32,
                                                                G.x64.get());
     SLK_CHECK_LAUNCH();
+    trace_mark("gather: rows gathered");
     if (mode == MODE_COLOR) G.qcolor.alloc(G.n, s);
     if (mode == MODE_MASK) G.mask.alloc(G.n * nx, s);
     if (mode == MODE_COLOR || mode == MODE_MASK) {
@@ -1858,7 +1857,132 @@ Gathered gather_queries(const PointSet &Q, const std::vector<int32_t> &src,
         SLK_CHECK_LAUNCH();
     }
     G.P = make_pointset(G.x32, G.x64.get(), G.n, d, s);
+    trace_mark("gather: point set");
     return G;
+}
+
+Gathered gather_queries(const PointSet &Q, const std::vector<int32_t> &src,
+                        const std::vector<int32_t> &qid, int mode, const int32_t *qcolor,
+                        const uint8_t *mask, int64_t nx, cudaStream_t s) {
+    const int64_t nout = (int64_t)src.size();
+    DevBuf<int32_t> dsrc(nout, s), dqid(nout, s);
+    SLK_CUDA(cudaMemcpyAsync(dsrc.get(), src.data(), nout * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+    SLK_CUDA(cudaMemcpyAsync(dqid.get(), qid.data(), nout * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+    return gather_queries_dev(Q, dsrc.get(), std::move(dqid), nout, mode, qcolor, mask, nx, s);
+}
+
+// ---- segment blocking on the device (colour / pivot re-blocking below)
+// Points sorted by a segment key; every segment of >= BM/2 points (except
+// the first) starts on a fresh BM-row block, the gap padded with repeats of
+// the previous segment's first point (query id -1, index mark -1).  The
+// output offset of a segment is a scan over the segments with the
+// associative step  x -> (len >= BM/2 ? align(x + a) : x) + b  (closed under
+// composition: align(align(x + a1) + b1 + a2) = align(x + a1) + align(b1 + a2)).
+struct SegStep {
+    int32_t align;  // 1: align(x + a) + b, 0: x + b
+    int64_t a, b;
+};
+struct SegStepCompose {  // apply l then r
+    __host__ __device__ SegStep operator()(const SegStep &l, const SegStep &r) const {
+        if (!r.align) return SegStep{l.align, l.a, l.b + r.b};
+        if (!l.align) return SegStep{1, l.b + r.a, r.b};
+        const int64_t c = l.b + r.a;
+        return SegStep{1, l.a, ((c + BM - 1) / BM) * BM + r.b};
+    }
+};
+
+template <class K>
+__global__ void seg_flags_kernel(const K *keys, int64_t n, int32_t *flag) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        flag[i] = (i == 0 || keys[i] != keys[i - 1]) ? 1 : 0;
+}
+__global__ void seg_starts_kernel(const int32_t *flag, const int32_t *segid, int64_t n, int64_t *start) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        if (flag[i]) start[segid[i] - 1] = i;
+}
+__global__ void seg_steps_kernel(const int64_t *start, int64_t nseg, int64_t n, SegStep *step) {
+    for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < nseg; g += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t len = (g + 1 < nseg ? start[g + 1] : n) - start[g];
+        step[g] = SegStep{(len >= BM / 2 && g > 0) ? 1 : 0, 0, len};
+    }
+}
+// off[g] = output offset of segment g = (exclusive composition up to g) applied
+// to 0, then segment g's own alignment
+__global__ void seg_offsets_kernel(const SegStep *excl, const SegStep *step, int64_t nseg, int64_t *off) {
+    for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < nseg; g += (int64_t)gridDim.x * blockDim.x) {
+        const SegStep e = excl[g];
+        int64_t x = g == 0 ? 0 : (e.align ? ((e.a + BM - 1) / BM) * BM + e.b : e.b);  // end of segment g-1
+        if (step[g].align) x = ((x + BM - 1) / BM) * BM;
+        off[g] = x;
+    }
+}
+__global__ void seg_scatter_kernel(const int32_t *ids, const int32_t *segid, const int64_t *start, const int64_t *off,
+                                   int64_t n, int32_t *src, int32_t *qid, int32_t *mark) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t g = segid[i] - 1;
+        const int64_t p = off[g] + (i - start[g]);
+        src[p] = ids[i];
+        qid[p] = ids[i];
+        if (mark) mark[p] = 0;
+    }
+}
+__global__ void seg_pad_kernel(const int32_t *ids, const int64_t *start, const int64_t *off, int64_t nseg, int64_t n,
+                               int32_t *src, int32_t *qid, int32_t *mark) {
+    for (int64_t g = 1 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < nseg; g += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t prev_end = off[g - 1] + (start[g] - start[g - 1]);
+        const int32_t fill = ids[start[g - 1]];  // the previous segment's first point
+        for (int64_t p = prev_end; p < off[g]; p++) {
+            src[p] = fill;
+            qid[p] = -1;
+            if (mark) mark[p] = -1;
+        }
+    }
+}
+
+// Device segment blocking of sorted (keys, ids): fills dsrc / dqid / dmark
+// (dmark optional) and returns the padded length.
+template <class K>
+int64_t segment_blocks(const K *keys, const int32_t *ids, int64_t n, DevBuf<int32_t> &dsrc,
+                       DevBuf<int32_t> &dqid, DevBuf<int32_t> *dmark, cudaStream_t s) {
+    DevBuf<int32_t> flag(n, s), segid(n, s);
+    seg_flags_kernel<K><<<grid_for(n, 256), 256, 0, s>>>(keys, n, flag);
+    SLK_CHECK_LAUNCH();
+    // segid = inclusive count of segment starts (segment index + 1)
+    size_t tmp = 0;
+    SLK_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tmp, flag.get(), segid.get(), (int)n, s));
+    DevBuf<unsigned char> tb(tmp, s);
+    SLK_CUDA(cub::DeviceScan::InclusiveSum(tb.get(), tmp, flag.get(), segid.get(), (int)n, s));
+    int32_t last_id = 0;
+    SLK_CUDA(cudaMemcpyAsync(&last_id, segid.get() + n - 1, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    SLK_CUDA(cudaStreamSynchronize(s));
+    const int64_t nseg = (int64_t)last_id;
+    DevBuf<int64_t> start(nseg, s), off(nseg, s);
+    DevBuf<SegStep> step(nseg, s), excl(nseg, s);
+    seg_starts_kernel<<<grid_for(n, 256), 256, 0, s>>>(flag, segid, n, start);
+    seg_steps_kernel<<<grid_for(nseg, 256), 256, 0, s>>>(start, nseg, n, step);
+    SLK_CHECK_LAUNCH();
+    tmp = 0;
+    const SegStep ident{0, 0, 0};
+    SLK_CUDA(cub::DeviceScan::ExclusiveScan(nullptr, tmp, step.get(), excl.get(), SegStepCompose(), ident, (int)nseg, s));
+    DevBuf<unsigned char> tb2(tmp, s);
+    SLK_CUDA(cub::DeviceScan::ExclusiveScan(tb2.get(), tmp, step.get(), excl.get(), SegStepCompose(), ident, (int)nseg,
+                                            s));
+    seg_offsets_kernel<<<grid_for(nseg, 256), 256, 0, s>>>(excl, step, nseg, off);
+    SLK_CHECK_LAUNCH();
+    int64_t last_off = 0, last_start = 0;
+    SLK_CUDA(cudaMemcpyAsync(&last_off, off.get() + nseg - 1, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    SLK_CUDA(cudaMemcpyAsync(&last_start, start.get() + nseg - 1, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    SLK_CUDA(cudaStreamSynchronize(s));
+    const int64_t nout = last_off + (n - last_start);
+    dsrc.alloc(nout, s);
+    dqid.alloc(nout, s);
+    if (dmark) dmark->alloc(nout, s);
+    seg_scatter_kernel<<<grid_for(n, 256), 256, 0, s>>>(ids, segid, start, off, n, dsrc, dqid,
+                                                        dmark ? dmark->get() : nullptr);
+    seg_pad_kernel<<<grid_for(nseg, 256), 256, 0, s>>>(ids, start, off, nseg, n, dsrc, dqid,
+                                                       dmark ? dmark->get() : nullptr);
+    SLK_CHECK_LAUNCH();
+    return nout;
 }
 
 // ---------------------------------------------------------------- split index
@@ -2234,8 +2358,8 @@ __global__ void map_failed_kernel(const int *gfail, const float *gkth, int nfail
 // colour) in which every colour segment of >= 64 points starts a fresh
 // block; pad rows repeat the previous segment's first point (query id -1).
 // Returns false when few blocks straddle (C3: 49 boundaries in 7813 blocks).
-bool plan_colour_blocks(const PointSet &Q, const int32_t *colors, std::vector<int32_t> &src,
-                        std::vector<int32_t> &qid, cudaStream_t s) {
+bool plan_colour_blocks(const PointSet &Q, const int32_t *colors, DevBuf<int32_t> &dsrc, DevBuf<int32_t> &dqid,
+                        int64_t &nout, cudaStream_t s) {
     const int64_t n = Q.n;
     DevBuf<unsigned long long> changes(1, s);
     SLK_CUDA(cudaMemsetAsync(changes, 0, sizeof(unsigned long long), s));
@@ -2254,31 +2378,9 @@ bool plan_colour_blocks(const PointSet &Q, const int32_t *colors, std::vector<in
     SLK_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, key.get(), keys.get(), iota.get(), ids.get(), (int)n, 0, 64, s));
     DevBuf<unsigned char> t(tmp, s);
     SLK_CUDA(cub::DeviceRadixSort::SortPairs(t.get(), tmp, key.get(), keys.get(), iota.get(), ids.get(), (int)n, 0, 64, s));
-    std::vector<uint64_t> hk(n);
-    std::vector<int32_t> hi(n);
-    SLK_CUDA(cudaMemcpyAsync(hk.data(), keys.get(), n * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
-    SLK_CUDA(cudaMemcpyAsync(hi.data(), ids.get(), n * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-    SLK_CUDA(cudaStreamSynchronize(s));
-    src.clear();
-    qid.clear();
-    src.reserve(n + n / 4);
-    qid.reserve(n + n / 4);
-    int32_t prev_first = hi[0];
-    for (int64_t i = 0; i < n;) {
-        int64_t j = i + 1;
-        while (j < n && hk[j] == hk[i]) j++;
-        if (j - i >= BM / 2 && !src.empty())
-            while (src.size() % BM) {
-                src.push_back(prev_first);
-                qid.push_back(-1);
-            }
-        for (int64_t r = i; r < j; r++) {
-            src.push_back(hi[r]);
-            qid.push_back(hi[r]);
-        }
-        prev_first = hi[i];
-        i = j;
-    }
+    trace_mark("colour: sorted");
+    nout = segment_blocks<uint64_t>(keys.get(), ids.get(), n, dsrc, dqid, nullptr, s);
+    trace_mark("colour: blocked on the device");
     return true;
 }
 
@@ -2293,8 +2395,8 @@ void search(const PointSet &Q, const PointSet &X, int k, int mode, const uint8_t
 // >= 64 points on a fresh block, so blocks stay inside one cell.  Pad rows
 // repeat the previous cell's first point: query id -1, index mark -1 (the
 // scan never takes them).  Returns false when few blocks are oversized (C3).
-bool plan_pivot_blocks(const PointSet &X, std::vector<int32_t> &src, std::vector<int32_t> &qid,
-                       std::vector<int32_t> &mark, cudaStream_t s) {
+bool plan_pivot_blocks(const PointSet &X, DevBuf<int32_t> &dsrc, DevBuf<int32_t> &dqid, DevBuf<int32_t> &dmark,
+                       int64_t &nout, cudaStream_t s) {
     const int64_t n = X.n, nb = X.nb;
     if (nb < 64 || getenv("SLK_NO_PIVOT_REBLOCK")) return false;
     std::vector<float> r(nb);
@@ -2320,34 +2422,9 @@ bool plan_pivot_blocks(const PointSet &X, std::vector<int32_t> &src, std::vector
     SLK_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, near.get(), keys.get(), iota.get(), ids.get(), (int)n, 0, 32, s));
     DevBuf<unsigned char> t(tmp, s);
     SLK_CUDA(cub::DeviceRadixSort::SortPairs(t.get(), tmp, near.get(), keys.get(), iota.get(), ids.get(), (int)n, 0, 32, s));
-    std::vector<int32_t> hk(n), hi(n);
-    SLK_CUDA(cudaMemcpyAsync(hk.data(), keys.get(), n * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-    SLK_CUDA(cudaMemcpyAsync(hi.data(), ids.get(), n * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-    SLK_CUDA(cudaStreamSynchronize(s));
-    src.clear();
-    qid.clear();
-    mark.clear();
-    src.reserve(n + n / 2);
-    qid.reserve(n + n / 2);
-    mark.reserve(n + n / 2);
-    int32_t prev_first = hi[0];
-    for (int64_t i = 0; i < n;) {
-        int64_t j = i + 1;
-        while (j < n && hk[j] == hk[i]) j++;
-        if (j - i >= BM / 2 && !src.empty())
-            while (src.size() % BM) {
-                src.push_back(prev_first);
-                qid.push_back(-1);
-                mark.push_back(-1);
-            }
-        for (int64_t q = i; q < j; q++) {
-            src.push_back(hi[q]);
-            qid.push_back(hi[q]);
-            mark.push_back(0);
-        }
-        prev_first = hi[i];
-        i = j;
-    }
+    trace_mark("pivot: nearest pivots sorted");
+    nout = segment_blocks<int32_t>(keys.get(), ids.get(), n, dsrc, dqid, &dmark, s);
+    trace_mark("pivot: blocked on the device");
     return true;
 }
 
@@ -2374,14 +2451,14 @@ void search(const PointSet &Q, const PointSet &X, int k, int mode, const uint8_t
         DevBuf<int> fail;
         DevBuf<float> kth;
         int nfail = -1;
-        std::vector<int32_t> csrc, cqid;
+        DevBuf<int32_t> csrc, cqid;
+        int64_t cn = 0;
         if (mode == MODE_COLOR && k == 1 && &Q == &X && qcolor == xcolor && q0 == 0 && q1 == Q.n &&
-            !getenv("SLK_NO_COLOUR_REBLOCK") && plan_colour_blocks(Q, qcolor, csrc, cqid, s)) {
+            !getenv("SLK_NO_COLOUR_REBLOCK") && plan_colour_blocks(Q, qcolor, csrc, cqid, cn, s)) {
             // scan the colour-blocked copy against itself (candidates mapped back to
             // X ids in the kernel), refine against X, scatter rows back
-            Gathered CG = gather_queries(Q, csrc, cqid, mode, qcolor, nullptr, nx, s);
-            DevBuf<int32_t> xid(CG.n, s);
-            SLK_CUDA(cudaMemcpyAsync(xid.get(), csrc.data(), CG.n * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+            Gathered CG = gather_queries_dev(Q, csrc.get(), std::move(cqid), cn, mode, qcolor, nullptr, nx, s);
+            DevBuf<int32_t> xid = std::move(csrc);  // position -> X id
             DevBuf<int32_t> gidx(CG.n * k, s);
             DevBuf<double> gdist(CG.n * k, s);
             DevBuf<int> gfail;
@@ -2404,16 +2481,15 @@ void search(const PointSet &Q, const PointSet &X, int k, int mode, const uint8_t
             }
             nfail = gn;
         }
-        std::vector<int32_t> psrc, pqid, pmark;
+        DevBuf<int32_t> psrc, pqid, pmark;
+        int64_t pn = 0;
         if (nfail < 0 && mode == MODE_SELF && &Q == &X && q0 == 0 && q1 == Q.n &&
-            plan_pivot_blocks(Q, psrc, pqid, pmark, s)) {
+            plan_pivot_blocks(Q, psrc, pqid, pmark, pn, s)) {
             // scan the pivot-ordered copy against itself; candidates map back to
             // X ids in the kernel, a row's own point sits at its own position,
             // pad entries (mark -1) are never taken
-            Gathered PG = gather_queries(Q, psrc, pqid, mode, nullptr, nullptr, nx, s);
-            DevBuf<int32_t> xid(PG.n, s), xmark(PG.n, s);
-            SLK_CUDA(cudaMemcpyAsync(xid.get(), psrc.data(), PG.n * sizeof(int32_t), cudaMemcpyHostToDevice, s));
-            SLK_CUDA(cudaMemcpyAsync(xmark.get(), pmark.data(), PG.n * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+            Gathered PG = gather_queries_dev(Q, psrc.get(), std::move(pqid), pn, mode, nullptr, nullptr, nx, s);
+            DevBuf<int32_t> xid = std::move(psrc), xmark = std::move(pmark);
             DevBuf<int32_t> gidx(PG.n * k, s);
             DevBuf<double> gdist(PG.n * k, s);
             DevBuf<int> gfail;
