@@ -1,14 +1,16 @@
 // fold.cu — host-side union-find fold of the sorted spanning tree into the
-// merge table (and the flat cut), native code.  Replaces the reference's
-// _dendrogram_merge / _uf_find (/root/reference/pkg/src/parlink/linkage.py:
-// 91-129) and, for the pipeline, _inherit_labels / extract_clusters
-// (:132-148, :184-213).
+// merge table (and the flat cut), native code: the SLK_HOST_FOLD=1
+// alternative to the device merge table (dendro.cu:krt_kernel), kept for
+// comparison.  Replaces the reference's _dendrogram_merge / _uf_find
+// (/root/reference/pkg/src/parlink/linkage.py:91-129) and, for the pipeline,
+// _inherit_labels / extract_clusters (:132-148, :184-213).
 //
-// The fold is inherently sequential (row i needs the cluster ids produced by
-// rows < i); like the paper it runs on the host.  It is bound by
-// cache misses on random vertex ids, so: one 16-byte node per vertex (parent,
-// cluster id, size, rank share a cache line), and the nodes of the endpoints
-// of edge i + D are prefetched while edge i is folded.
+// The fold is sequential in merge order; like the paper it
+// runs on the host, split over the components of the forest of its first
+// merges.  It is bound by cache misses on random vertex ids, so: one 16-byte
+// node per vertex (parent, cluster id, size, rank share a cache line), and
+// the nodes of the endpoints of edge i + D are prefetched while edge i is
+// folded.
 #include <stdint.h>
 #include <string.h>
 
