@@ -865,6 +865,10 @@ int group_blocks(int d, int kp) {
 bool halves_supported(int mode, int d, int kp) {
     if (chunked(d) || kp > 16 || (mode != MODE_SELF && mode != MODE_COLOR) || (mode == MODE_COLOR && kp > 8))
         return false;
+    // k-NN lists of K' = 8 (k < 8): one list per row is faster than two of 8
+    // (C5, k = 2: scan 8.2 -> 7.4 ms, refine 1.0 -> 0.6 ms); the halves pay
+    // off for K' = 16 (C3: scan 19.4 -> 17.6 ms)
+    if (mode == MODE_SELF && kp < 16) return false;
     if (const char *e = getenv("SLK_TC_HS"))
         if (atoi(e) == 1) return false;
     return make_plan(k_extent(d), use_aug(d), 1, 0, 2).nb >= (use_aug(d) ? 3 : 2);
