@@ -2419,9 +2419,11 @@ bool plan_pivot_blocks(const PointSet &X, DevBuf<int32_t> &dsrc, DevBuf<int32_t>
     iota_ids_kernel<<<grid_for(n, 256), 256, 0, s>>>(iota, n);
     SLK_CHECK_LAUNCH();
     size_t tmp = 0;
-    SLK_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, near.get(), keys.get(), iota.get(), ids.get(), (int)n, 0, 32, s));
+    int pbits = 1;  // pivot ids < np: only their low bits need sorting
+    while (((int64_t)1 << pbits) < np) pbits++;
+    SLK_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, near.get(), keys.get(), iota.get(), ids.get(), (int)n, 0, pbits, s));
     DevBuf<unsigned char> t(tmp, s);
-    SLK_CUDA(cub::DeviceRadixSort::SortPairs(t.get(), tmp, near.get(), keys.get(), iota.get(), ids.get(), (int)n, 0, 32, s));
+    SLK_CUDA(cub::DeviceRadixSort::SortPairs(t.get(), tmp, near.get(), keys.get(), iota.get(), ids.get(), (int)n, 0, pbits, s));
     trace_mark("pivot: nearest pivots sorted");
     nout = segment_blocks<int32_t>(keys.get(), ids.get(), n, dsrc, dqid, &dmark, s);
     trace_mark("pivot: blocked on the device");
